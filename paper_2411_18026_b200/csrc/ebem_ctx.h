@@ -1,0 +1,56 @@
+// Plain-data structures shared by the host runtime (C++) and the sm_100a
+// kernels (CUDA).  No torch types, no STL.
+#pragma once
+
+#include <stdint.h>
+
+namespace ebem_gpu {
+
+constexpr int kMaxSeriesPow = 48;  // dense power tables r^0 .. r^47
+constexpr int kMaxGauss = 40;      // Gauss-Legendre orders 1 .. 40 on device
+constexpr int kGaussSlots = kMaxGauss * (kMaxGauss + 1) / 2;
+
+// Medium constants (proj/include/ebem/medium.hpp, kernel_scalars.cpp:123-131,
+// assembly.cpp:42-50).
+struct DevMedium {
+  double kL, kT, lam, mu;
+  double aratio;         // lam / (lam + 2 mu)
+  double cconst;         // (lam + mu) / (8 pi (lam + 2 mu))
+  double qfactor;        // 8 mu cconst
+  double series_radius;  // 0.25 / kT
+  double kappa;          // mu / (2 pi (lam + 2 mu))
+  double ccon;           // (lam + mu) / (8 pi (lam + 2 mu))
+  double alpha_re, alpha_im;
+};
+
+// Element geometry, structure of arrays over the N elements (element e runs
+// from node e to node (e+1) mod N): p = start node, d = end - start, t = unit
+// tangent, n = unit normal (+90 deg rotation of t), h = length.
+enum ElemField { EPX = 0, EPY, EDX, EDY, ETX, ETY, ENX, ENY, EH, kElemFields };
+
+struct DevCtx {
+  DevMedium med;
+  int n_nodes;
+  int series_maxq;
+  // Remainder series of the ten scalars: series[(k * kMaxSeriesPow + q) * 4 +
+  // {0,1,2,3}] = {Re a_q, Im a_q, Re b_q, Im b_q} of sum (a_q + b_q ln r) r^q.
+  double series[10 * kMaxSeriesPow * 4];
+  // Gauss-Legendre rules on [0,1]; order n occupies [n(n-1)/2, n(n+1)/2).
+  double gx[kGaussSlots];
+  double gw[kGaussSlots];
+  // Quadrature knobs (AssemblyConfig, proj/include/ebem/assembly.hpp:21-30).
+  int far_nodes;
+  int corner_n;   // scaled corner_nodes
+  int proxy_n;    // ProxyConfig::n_gauss
+  int m_prime;    // ProxyConfig::m_prime
+  double refine;
+  // cos/sin of 2 pi j / m' (host libm), for the proxy polygons.
+  double poly_cs[2 * 512];
+  // Element geometry (device pointer, kElemFields * n_nodes doubles).
+  const double* elem;
+  const double* node_xy;  // 2 * n_nodes, interleaved x, y
+};
+
+__host__ __device__ inline int gauss_offset(int n) { return n * (n - 1) / 2; }
+
+}  // namespace ebem_gpu

@@ -1,0 +1,613 @@
+// Batched complex-double dense linear algebra for the skeletonization and the
+// merges (sm_100a).  One CTA per small matrix; matrices live in shared memory
+// when they fit (<= kSmemCap bytes) and are worked on in place in global
+// memory (L2/L1 resident) otherwise.
+//
+//   k_qr_reduce  unpivoted Householder QR of a row block -> R (n x n); tall
+//                interaction matrices are reduced block by block (TSQR) before
+//                the pivoted factorization, which keeps the column norms and
+//                therefore the pivot sequence of the full matrix.
+//   k_cpqr       column-pivoted Householder QR with LAPACK zlaqp2 pivoting
+//                (first index of the largest partial norm, norm downdating
+//                with recomputation below sqrt(eps)), stopping at the first
+//                |R_kk| <= stop_rel |R_00| (Cpqr, proj/src/lapack.cpp:101-138;
+//                kPivotFloor, proj/src/compression.cpp:15,93-99)
+//   k_interp     [I, R11^-1 R12] scattered by pivot (Cpqr::interpolation,
+//                proj/src/lapack.cpp:140-158), optionally conj-transposed
+//   k_getrf      partial-pivoted LU, pivot = first max |Re|+|Im| (zgetrf as
+//                called by LuFactor, proj/src/lapack.cpp:31-53)
+//   k_getrs      row swaps + unit-lower + upper triangular solves
+//                (LuFactor::solve, proj/src/lapack.cpp:73-89)
+//   k_gemm       C = alpha op(A) op(B) + beta C, ragged batch
+//   k_copy       batched block copies (optionally conjugated)
+#include <cuda_runtime.h>
+
+#include "ebem_dense.h"
+
+namespace ebem_gpu {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 zconj(double2 a) { return make_double2(a.x, -a.y); }
+// a - b*c
+__device__ __forceinline__ double2 zfms(double2 a, double2 b, double2 c) {
+  return make_double2(fma(-b.y, -c.y, fma(-b.x, c.x, a.x)),
+                      fma(-b.y, c.x, fma(-b.x, c.y, a.y)));
+}
+// a + b*c
+__device__ __forceinline__ double2 zfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(-b.y, c.y, fma(b.x, c.x, a.x)),
+                      fma(b.y, c.x, fma(b.x, c.y, a.y)));
+}
+// a + conj(b)*c
+__device__ __forceinline__ double2 zfmac(double2 a, double2 b, double2 c) {
+  return make_double2(fma(b.y, c.y, fma(b.x, c.x, a.x)),
+                      fma(-b.y, c.x, fma(b.x, c.y, a.y)));
+}
+__device__ __forceinline__ double2 zdiv(double2 a, double2 b) {
+  // Smith's algorithm
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double r = b.y / b.x, d = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / d, (a.y - a.x * r) / d);
+  }
+  const double r = b.x / b.y, d = b.y + b.x * r;
+  return make_double2((a.x * r + a.y) / d, (a.y * r - a.x) / d);
+}
+__device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double2 warp_sum2(double2 v) {
+  return make_double2(warp_sum(v.x), warp_sum(v.y));
+}
+
+// Block-wide sum of one double per thread (all threads must call).
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < kWarps ? red[threadIdx.x] : 0.0;
+    s = warp_sum(s);
+    if (threadIdx.x == 0) red[0] = s;
+  }
+  __syncthreads();
+  s = red[0];
+  __syncthreads();
+  return s;
+}
+
+// Load an m x n block (ld) into a dense workspace (ld m).
+__device__ void load_block(const double2* __restrict__ src, int m, int n, int ld,
+                           double2* __restrict__ dst) {
+  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
+    const int j = idx / m, i = idx - j * m;
+    dst[idx] = src[(size_t)j * ld + i];
+  }
+}
+
+// Generate the Householder reflector of column `col` rows [i, m) of A (ld m):
+// returns tau, overwrites A[i,col] with beta and A[i+1:,col] with v.
+// Semantics of zlarfg (beta = -sign(alpha_r) ||(alpha, x)||).
+__device__ double2 householder(double2* A, int m, int ld, int i, int col,
+                               double* red, double* beta_out) {
+  double2* c = A + (size_t)col * ld;
+  double part = 0.0;
+  for (int r = i + 1 + threadIdx.x; r < m; r += blockDim.x) {
+    const double2 v = c[r];
+    part = fma(v.x, v.x, fma(v.y, v.y, part));
+  }
+  const double xnorm2 = block_sum(part, red);
+  const double2 alpha = c[i];
+  double2 tau = make_double2(0.0, 0.0);
+  double beta;
+  if (xnorm2 == 0.0 && alpha.y == 0.0) {
+    beta = alpha.x;  // H = I
+  } else {
+    const double nrm = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2);
+    beta = alpha.x >= 0.0 ? -nrm : nrm;
+    tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+    const double2 scal = zdiv(make_double2(1.0, 0.0),
+                              make_double2(alpha.x - beta, alpha.y));
+    for (int r = i + 1 + threadIdx.x; r < m; r += blockDim.x) c[r] = zmul(scal, c[r]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) c[i] = make_double2(beta, 0.0);
+  __syncthreads();
+  *beta_out = beta;
+  return tau;
+}
+
+// Apply H^H = I - conj(tau) v v^H (v_i = 1, v stored below A[i,col]) to the
+// columns cols [c0, n) of A, rows [i, m).  One warp per column.
+__device__ void apply_reflector(double2* A, int m, int ld, int i, int col,
+                                double2 tau, int c0, int n) {
+  if (tau.x == 0.0 && tau.y == 0.0) return;
+  const double2 ctau = zconj(tau);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const double2* v = A + (size_t)col * ld;
+  for (int j = c0 + w; j < n; j += kWarps) {
+    double2* cj = A + (size_t)j * ld;
+    // s = v^H c_j
+    double2 s = make_double2(0.0, 0.0);
+    for (int r = i + l; r < m; r += 32) {
+      const double2 vr = (r == i) ? make_double2(1.0, 0.0) : v[r];
+      s = zfmac(s, vr, cj[r]);
+    }
+    s = warp_sum2(s);
+    const double2 f = zmul(ctau, s);
+    for (int r = i + l; r < m; r += 32) {
+      const double2 vr = (r == i) ? make_double2(1.0, 0.0) : v[r];
+      cj[r] = zfms(cj[r], vr, f);
+    }
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ QR reduction
+__global__ void __launch_bounds__(kThreads)
+k_qr_reduce(const QrTask* __restrict__ tasks, double2* __restrict__ gws) {
+  extern __shared__ double2 smem[];
+  __shared__ double red[kWarps + 1];
+  const QrTask T = tasks[blockIdx.x];
+  const int m = T.rows, n = T.n;
+  double2* A = T.in_smem ? smem : gws + T.ws_off;
+  load_block(reinterpret_cast<const double2*>(T.src), m, n, T.ld, A);
+  __syncthreads();
+  const int steps = m < n ? m : n;
+  for (int i = 0; i < steps; ++i) {
+    double beta;
+    const double2 tau = householder(A, m, m, i, i, red, &beta);
+    apply_reflector(A, m, m, i, i, tau, i + 1, n);
+    __syncthreads();
+  }
+  double2* R = reinterpret_cast<double2*>(T.dst);
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int j = idx / n, i = idx - j * n;
+    R[(size_t)j * T.dst_ld + i] = (i <= j && i < m) ? A[(size_t)j * m + i]
+                                                    : make_double2(0.0, 0.0);
+  }
+}
+
+// --------------------------------------------------------------------- CPQR
+__global__ void __launch_bounds__(kThreads)
+k_cpqr(const CpqrTask* __restrict__ tasks, double2* __restrict__ gws) {
+  extern __shared__ double2 smem[];
+  __shared__ double red[kWarps + 1];
+  __shared__ double vn1[kMaxCpqrCols], vn2[kMaxCpqrCols];
+  __shared__ int jp[kMaxCpqrCols];
+  __shared__ int s_pvt;
+  __shared__ double s_r00;
+  const CpqrTask T = tasks[blockIdx.x];
+  const int m = T.rows, n = T.n;
+  double2* A = T.in_smem ? smem : gws + T.ws_off;
+  load_block(reinterpret_cast<const double2*>(T.src), m, n, T.ld, A);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) jp[j] = j;
+  __syncthreads();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  // initial column norms
+  for (int j = w; j < n; j += kWarps) {
+    const double2* c = A + (size_t)j * m;
+    double s = 0.0;
+    for (int r = l; r < m; r += 32) s = fma(c[r].x, c[r].x, fma(c[r].y, c[r].y, s));
+    s = warp_sum(s);
+    if (l == 0) vn1[j] = vn2[j] = sqrt(s);
+  }
+  __syncthreads();
+  const double tol3z = 1.0536712127723509e-08;  // sqrt(2^-53)
+  const int mn = m < n ? m : n;
+  int steps = mn;
+  double* rdiag = T.rdiag;
+  for (int i = 0; i < mn; ++i) {
+    // pivot: first index of the largest partial norm (idamax)
+    if (w == 0) {
+      double best = -1.0;
+      int bi = i;
+      for (int j = i + l; j < n; j += 32) {
+        const double v = vn1[j];
+        if (v > best) { best = v; bi = j; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (l == 0) s_pvt = bi;
+    }
+    __syncthreads();
+    const int pvt = s_pvt;
+    if (pvt != i) {
+      double2* a = A + (size_t)pvt * m;
+      double2* b = A + (size_t)i * m;
+      for (int r = threadIdx.x; r < m; r += blockDim.x) {
+        const double2 t = a[r];
+        a[r] = b[r];
+        b[r] = t;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int t = jp[pvt];
+        jp[pvt] = jp[i];
+        jp[i] = t;
+        vn1[pvt] = vn1[i];
+        vn2[pvt] = vn2[i];
+      }
+      __syncthreads();
+    }
+    double beta;
+    const double2 tau = householder(A, m, m, i, i, red, &beta);
+    const double rii = fabs(beta);
+    if (threadIdx.x == 0) {
+      rdiag[i] = rii;
+      if (i == 0) s_r00 = rii;
+    }
+    __syncthreads();
+    const double r00 = s_r00;
+    if (r00 == 0.0 || rii <= T.stop_rel * r00) {
+      steps = i;
+      break;
+    }
+    apply_reflector(A, m, m, i, i, tau, i + 1, n);
+    __syncthreads();
+    // partial norm downdate (zlaqp2)
+    for (int j = i + 1 + w; j < n; j += kWarps) {
+      const double v1 = vn1[j];
+      if (v1 == 0.0) continue;
+      const double2 aij = A[(size_t)j * m + i];
+      double temp = hypot(aij.x, aij.y) / v1;
+      temp = 1.0 - temp * temp;
+      temp = temp > 0.0 ? temp : 0.0;
+      const double ratio = v1 / vn2[j];
+      const double temp2 = temp * ratio * ratio;
+      if (temp2 <= tol3z) {
+        double nv = 0.0;
+        if (i + 1 < m) {
+          const double2* c = A + (size_t)j * m;
+          double s = 0.0;
+          for (int r = i + 1 + l; r < m; r += 32) s = fma(c[r].x, c[r].x, fma(c[r].y, c[r].y, s));
+          nv = sqrt(warp_sum(s));
+        }
+        if (l == 0) vn1[j] = vn2[j] = nv;
+      } else {
+        if (l == 0) vn1[j] = v1 * sqrt(temp);
+      }
+    }
+    __syncthreads();
+  }
+  // outputs: pivots, steps, R rows [0, steps) in pivoted order (ld n)
+  for (int j = threadIdx.x; j < n; j += blockDim.x) T.jpvt[j] = jp[j];
+  if (threadIdx.x == 0) *T.steps = steps;
+  double2* R = reinterpret_cast<double2*>(T.r_out);
+  for (int idx = threadIdx.x; idx < steps * n; idx += blockDim.x) {
+    const int j = idx / steps, i = idx - j * steps;
+    R[(size_t)j * T.r_ld + i] = (i <= j) ? A[(size_t)j * m + i] : make_double2(0.0, 0.0);
+  }
+}
+
+// ------------------------------------------------------------- interpolation
+// coeff = [I, R11^-1 R12] (k x n) with column jpvt[j] <- column j.  Output
+// (k x n, ld out_ld) or its conjugate transpose (n x k) when T.adjoint.
+__global__ void __launch_bounds__(kThreads)
+k_interp(const InterpTask* __restrict__ tasks) {
+  const InterpTask T = tasks[blockIdx.x];
+  const int k = T.k, n = T.n;
+  if (k == 0) return;
+  const double2* R = reinterpret_cast<const double2*>(T.r);
+  double2* out = reinterpret_cast<double2*>(T.out);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  // one warp per column j >= k of R12: back substitution, lanes over rows
+  extern __shared__ double2 col[];  // kWarps * k
+  double2* x = col + w * k;
+  for (int j = k + w; j < n; j += kWarps) {
+    for (int r = l; r < k; r += 32) x[r] = R[(size_t)j * T.r_ld + r];
+    __syncwarp();
+    for (int r = k - 1; r >= 0; --r) {
+      if (l == 0) x[r] = zdiv(x[r], R[(size_t)r * T.r_ld + r]);
+      __syncwarp();
+      const double2 xr = x[r];
+      for (int q = l; q < r; q += 32) x[q] = zfms(x[q], R[(size_t)r * T.r_ld + q], xr);
+      __syncwarp();
+    }
+    const int dc = T.jpvt[j];
+    for (int r = l; r < k; r += 32) {
+      if (T.adjoint) out[(size_t)r * T.out_ld + dc] = zconj(x[r]);
+      else out[(size_t)dc * T.out_ld + r] = x[r];
+    }
+    __syncwarp();
+  }
+  // identity part
+  for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
+    const int j = idx / k, r = idx - j * k;
+    const int dc = T.jpvt[j];
+    const double2 v = make_double2(r == j ? 1.0 : 0.0, 0.0);
+    if (T.adjoint) out[(size_t)r * T.out_ld + dc] = v;
+    else out[(size_t)dc * T.out_ld + r] = v;
+  }
+}
+
+// ----------------------------------------------------------------------- LU
+__global__ void __launch_bounds__(kThreads)
+k_getrf(const LuTask* __restrict__ tasks, double2* __restrict__ gws) {
+  extern __shared__ double2 smem[];
+  __shared__ int s_p;
+  __shared__ int s_info;
+  const LuTask T = tasks[blockIdx.x];
+  const int n = T.n;
+  double2* G = reinterpret_cast<double2*>(T.a);
+  double2* A = T.in_smem ? smem : gws + T.ws_off;
+  load_block(G, n, n, T.ld, A);
+  if (threadIdx.x == 0) s_info = 0;
+  __syncthreads();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int k = 0; k < n; ++k) {
+    if (w == 0) {
+      double best = -1.0;
+      int bi = k;
+      for (int r = k + l; r < n; r += 32) {
+        const double v = cabs1(A[(size_t)k * n + r]);
+        if (v > best) { best = v; bi = r; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (l == 0) {
+        s_p = bi;
+        T.ipiv[k] = bi;
+        if (best == 0.0 && s_info == 0) s_info = k + 1;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p != k) {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const double2 t = A[(size_t)j * n + k];
+        A[(size_t)j * n + k] = A[(size_t)j * n + p];
+        A[(size_t)j * n + p] = t;
+      }
+      __syncthreads();
+    }
+    const double2 piv = A[(size_t)k * n + k];
+    if (piv.x != 0.0 || piv.y != 0.0) {
+      const double2 rp = zdiv(make_double2(1.0, 0.0), piv);
+      for (int r = k + 1 + threadIdx.x; r < n; r += blockDim.x)
+        A[(size_t)k * n + r] = zmul(A[(size_t)k * n + r], rp);
+    }
+    __syncthreads();
+    // rank-1 update of the trailing block, one warp per column
+    for (int j = k + 1 + w; j < n; j += kWarps) {
+      const double2 akj = A[(size_t)j * n + k];
+      for (int r = k + 1 + l; r < n; r += 32)
+        A[(size_t)j * n + r] = zfms(A[(size_t)j * n + r], A[(size_t)k * n + r], akj);
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int j = idx / n, i = idx - j * n;
+    G[(size_t)j * T.ld + i] = A[idx];
+  }
+  if (threadIdx.x == 0) *T.info = s_info;
+}
+
+// ---------------------------------------------------------------- LU solve
+// One warp per right-hand-side column.  grid = (task, column group).
+__global__ void __launch_bounds__(kThreads)
+k_getrs(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off,
+        int n_tasks) {
+  // find task
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const LuSolveTask T = tasks[lo];
+  const int n = T.n;
+  const double2* A = reinterpret_cast<const double2*>(T.lu);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int col = (blockIdx.x - block_off[lo]) * kWarps + w;
+  if (col >= T.nrhs) return;
+  double2* b = reinterpret_cast<double2*>(T.b) + (size_t)col * T.ldb;
+  // row interchanges in order
+  if (l == 0) {
+    for (int k = 0; k < n; ++k) {
+      const int p = T.ipiv[k];
+      if (p != k) {
+        const double2 t = b[k];
+        b[k] = b[p];
+        b[p] = t;
+      }
+    }
+  }
+  __syncwarp();
+  // L y = b (unit lower)
+  for (int k = 0; k < n; ++k) {
+    const double2 bk = b[k];
+    for (int r = k + 1 + l; r < n; r += 32) b[r] = zfms(b[r], A[(size_t)k * T.ld + r], bk);
+    __syncwarp();
+  }
+  // U x = y
+  for (int k = n - 1; k >= 0; --k) {
+    if (l == 0) b[k] = zdiv(b[k], A[(size_t)k * T.ld + k]);
+    __syncwarp();
+    const double2 xk = b[k];
+    for (int r = l; r < k; r += 32) b[r] = zfms(b[r], A[(size_t)k * T.ld + r], xk);
+    __syncwarp();
+  }
+}
+
+// --------------------------------------------------------------------- GEMM
+// C = alpha op(A) op(B) + beta C; 32x32 output tile per CTA, 256 threads,
+// each thread 4 outputs; K staged through shared memory in chunks of 16.
+constexpr int kTile = 32;
+constexpr int kKc = 16;
+
+__global__ void __launch_bounds__(kThreads)
+k_gemm(const GemmTask* __restrict__ tasks, const int* __restrict__ block_off,
+       int n_tasks) {
+  __shared__ double2 As[kKc][kTile + 1];
+  __shared__ double2 Bs[kKc][kTile + 1];
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmTask T = tasks[lo];
+  const int tiles_m = (T.m + kTile - 1) / kTile;
+  const int tile = blockIdx.x - block_off[lo];
+  const int tm = tile % tiles_m, tn = tile / tiles_m;
+  const int r0 = tm * kTile, c0 = tn * kTile;
+  const double2* A = reinterpret_cast<const double2*>(T.a);
+  const double2* B = reinterpret_cast<const double2*>(T.b);
+  double2* C = reinterpret_cast<double2*>(T.c);
+  const int tr = threadIdx.x & 31;        // row in tile
+  const int tc = (threadIdx.x >> 5) * 4;  // 4 columns per thread
+  double2 acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < T.k; k0 += kKc) {
+    // stage A tile (rows r0.., k k0..) and B tile (k k0.., cols c0..)
+    for (int idx = threadIdx.x; idx < kKc * kTile; idx += kThreads) {
+      const int kk = idx / kTile, rr = idx - kk * kTile;
+      const int gr = r0 + rr, gk = k0 + kk;
+      double2 va = make_double2(0.0, 0.0);
+      if (gr < T.m && gk < T.k) {
+        va = T.trans_a ? A[(size_t)gr * T.lda + gk] : A[(size_t)gk * T.lda + gr];
+        if (T.trans_a == 2) va = zconj(va);
+      }
+      As[kk][rr] = va;
+      const int gc = c0 + rr;
+      double2 vb = make_double2(0.0, 0.0);
+      if (gc < T.n && gk < T.k) {
+        vb = T.trans_b ? B[(size_t)gk * T.ldb + gc] : B[(size_t)gc * T.ldb + gk];
+        if (T.trans_b == 2) vb = zconj(vb);
+      }
+      Bs[kk][rr] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kKc; ++kk) {
+      const double2 a = As[kk][tr];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = zfma(acc[q], a, Bs[kk][tc + q]);
+    }
+    __syncthreads();
+  }
+  const double2 alpha = make_double2(T.alpha_re, T.alpha_im);
+  const double2 beta = make_double2(T.beta_re, T.beta_im);
+  const int gr = r0 + tr;
+  if (gr >= T.m) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int gc = c0 + tc + q;
+    if (gc >= T.n) continue;
+    double2* cp = C + (size_t)gc * T.ldc + gr;
+    double2 v = zmul(alpha, acc[q]);
+    if (beta.x != 0.0 || beta.y != 0.0) v = zfma(v, beta, *cp);
+    *cp = v;
+  }
+}
+
+// --------------------------------------------------------------------- copy
+__global__ void __launch_bounds__(kThreads)
+k_copy(const CopyTask* __restrict__ tasks, const int* __restrict__ block_off,
+       int n_tasks) {
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const CopyTask T = tasks[lo];
+  const long long base = (long long)(blockIdx.x - block_off[lo]) * kThreads * 4;
+  const double2* S = reinterpret_cast<const double2*>(T.src);
+  double2* D = reinterpret_cast<double2*>(T.dst);
+  const long long total = (long long)T.rows * T.cols;
+  for (int q = 0; q < 4; ++q) {
+    const long long idx = base + q * kThreads + threadIdx.x;
+    if (idx >= total) break;
+    const int j = int(idx / T.rows), i = int(idx - (long long)j * T.rows);
+    double2 v = T.src ? S[(size_t)j * T.src_ld + i] : make_double2(0.0, 0.0);
+    if (T.transpose == 2) v = make_double2(i == j ? 1.0 : 0.0, 0.0);  // identity
+    if (T.conj) v = zconj(v);
+    if (T.transpose == 1) D[(size_t)i * T.dst_ld + j] = v;
+    else D[(size_t)j * T.dst_ld + i] = v;
+  }
+}
+
+// ----------------------------------------------------------- host wrappers
+static void set_smem_attr(const void* f) {
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
+}
+
+void dense_init() {
+  static bool done = false;
+  if (done) return;
+  set_smem_attr((const void*)k_qr_reduce);
+  set_smem_attr((const void*)k_cpqr);
+  set_smem_attr((const void*)k_getrf);
+  done = true;
+}
+
+void launch_qr_reduce(const QrTask* tasks, int n, size_t smem, double2* gws,
+                      cudaStream_t st) {
+  if (n <= 0) return;
+  k_qr_reduce<<<n, kThreads, smem, st>>>(tasks, gws);
+}
+void launch_cpqr(const CpqrTask* tasks, int n, size_t smem, double2* gws,
+                 cudaStream_t st) {
+  if (n <= 0) return;
+  k_cpqr<<<n, kThreads, smem, st>>>(tasks, gws);
+}
+void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st) {
+  if (n <= 0) return;
+  k_interp<<<n, kThreads, size_t(kWarps) * (max_k > 0 ? max_k : 1) * sizeof(double2),
+             st>>>(tasks);
+}
+void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
+                  cudaStream_t st) {
+  if (n <= 0) return;
+  k_getrf<<<n, kThreads, smem, st>>>(tasks, gws);
+}
+int getrs_blocks(int nrhs) { return (nrhs + kWarps - 1) / kWarps; }
+void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
+                  int n_blocks, cudaStream_t st) {
+  if (n_blocks <= 0) return;
+  k_getrs<<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+}
+int gemm_blocks(int m, int n) {
+  return ((m + kTile - 1) / kTile) * ((n + kTile - 1) / kTile);
+}
+void launch_gemm(const GemmTask* tasks, const int* block_off, int n_tasks,
+                 int n_blocks, cudaStream_t st) {
+  if (n_blocks <= 0) return;
+  k_gemm<<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+}
+int copy_blocks(int rows, int cols) {
+  const long long t = (long long)rows * cols;
+  return int((t + kThreads * 4 - 1) / (kThreads * 4));
+}
+void launch_copy(const CopyTask* tasks, const int* block_off, int n_tasks,
+                 int n_blocks, cudaStream_t st) {
+  if (n_blocks <= 0) return;
+  k_copy<<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+}
+
+}  // namespace ebem_gpu

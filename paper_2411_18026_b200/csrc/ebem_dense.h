@@ -1,0 +1,99 @@
+// Task descriptors and launch wrappers of the batched dense kernels
+// (ebem_dense.cu).  Complex matrices are column-major interleaved doubles.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace ebem_gpu {
+
+constexpr int kSmemCap = 200 * 1024;  // dynamic shared memory per CTA
+constexpr int kMaxCpqrCols = 256;
+
+struct QrTask {  // R (n x n, dst_ld) of the rows x n block at src (ld)
+  const double* src;
+  double* dst;
+  int rows, n, ld, dst_ld;
+  int in_smem;
+  int pad;
+  long long ws_off;  // global workspace offset (complex) when !in_smem
+};
+
+struct CpqrTask {
+  const double* src;  // rows x n, ld
+  int rows, n, ld;
+  int in_smem;
+  double stop_rel;  // stop at the first |R_ii| <= stop_rel |R_00|
+  int* jpvt;        // n, zero-based pivot order
+  double* rdiag;    // |R_ii| of the computed steps (+ the stopping one)
+  int* steps;       // number of completed steps (= eps_rank(stop_rel))
+  double* r_out;    // steps x n, ld r_ld (upper trapezoid, pivoted order)
+  int r_ld;
+  int pad;
+  long long ws_off;
+};
+
+struct InterpTask {
+  const double* r;  // k x n upper trapezoid, ld r_ld
+  const int* jpvt;
+  double* out;      // k x n (ld out_ld) or n x k when adjoint
+  int k, n, r_ld, out_ld;
+  int adjoint;
+  int pad;
+};
+
+struct LuTask {
+  double* a;  // n x n, ld, factored in place
+  int* ipiv;  // zero-based row interchanges
+  int* info;  // 0, or 1 + index of the first exactly-zero pivot
+  int n, ld;
+  int in_smem;
+  int pad;
+  long long ws_off;
+};
+
+struct LuSolveTask {
+  const double* lu;
+  const int* ipiv;
+  double* b;
+  int n, ld, nrhs, ldb;
+};
+
+// trans: 0 = N, 1 = T, 2 = C (conjugate transpose)
+struct GemmTask {
+  const double* a;
+  const double* b;
+  double* c;
+  int m, n, k;
+  int lda, ldb, ldc;
+  int trans_a, trans_b;
+  double alpha_re, alpha_im, beta_re, beta_im;
+};
+
+struct CopyTask {  // dst(i, j) = src(i, j) (0 when src is null; transpose 1:
+                   // dst(j, i); 2: identity)
+  const double* src;
+  double* dst;
+  int rows, cols, src_ld, dst_ld;
+  int conj, transpose;
+};
+
+void dense_init();
+void launch_qr_reduce(const QrTask* tasks, int n, size_t smem, double2* gws,
+                      cudaStream_t st);
+void launch_cpqr(const CpqrTask* tasks, int n, size_t smem, double2* gws,
+                 cudaStream_t st);
+void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st);
+void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
+                  cudaStream_t st);
+int getrs_blocks(int nrhs);
+void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
+                  int n_blocks, cudaStream_t st);
+int gemm_blocks(int m, int n);
+void launch_gemm(const GemmTask* tasks, const int* block_off, int n_tasks,
+                 int n_blocks, cudaStream_t st);
+int copy_blocks(int rows, int cols);
+void launch_copy(const CopyTask* tasks, const int* block_off, int n_tasks,
+                 int n_blocks, cudaStream_t st);
+
+}  // namespace ebem_gpu

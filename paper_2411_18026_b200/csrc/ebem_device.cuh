@@ -1,0 +1,336 @@
+// Device-side FP64 building blocks of the Galerkin fill: complex arithmetic,
+// the H0/H1 Hankel pair, the ten radial kernel scalars, and the 2x2 kernel
+// combiners.  Everything lives in registers; the per-medium tables (log-power
+// series, Gauss rules) are read from a per-handle context in global memory
+// with warp-uniform addresses (L1 broadcast).
+//
+// Reference formulas followed (behaviour, not code):
+//   hankel1_01                proj/src/hankel.cpp:34-71
+//   KernelScalars::full       proj/src/kernel_scalars.cpp:214-281
+//   KernelScalars::static_part proj/src/kernel_scalars.cpp:283-299
+//   KernelScalars::split      proj/src/kernel_scalars.cpp:301-331
+//   KernelScalars::remainder  proj/src/kernel_scalars.cpp:346-379
+//   integrated_remainder      proj/src/kernel_scalars.cpp:333-344 (+ LogSeries
+//                             ::integrate_scaled :108-121)
+//   combine_D / combine_N     proj/src/kernels.cpp:22-68
+//   q0_kernel                 proj/src/kernels.cpp:70-78
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "ebem_ctx.h"
+#include "hankel_tables.cuh"
+
+namespace ebem_gpu {
+
+// ----------------------------------------------------------------- complex
+struct cplx {
+  double re, im;
+};
+__device__ __forceinline__ cplx mk(double r, double i = 0.0) { return {r, i}; }
+__device__ __forceinline__ cplx operator+(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
+__device__ __forceinline__ cplx operator-(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
+__device__ __forceinline__ cplx operator-(cplx a) { return {-a.re, -a.im}; }
+__device__ __forceinline__ cplx operator*(cplx a, cplx b) {
+  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+__device__ __forceinline__ cplx operator*(double s, cplx a) { return {s * a.re, s * a.im}; }
+__device__ __forceinline__ cplx operator*(cplx a, double s) { return {s * a.re, s * a.im}; }
+__device__ __forceinline__ cplx operator/(cplx a, double s) { return {a.re / s, a.im / s}; }
+__device__ __forceinline__ cplx& operator+=(cplx& a, cplx b) { a.re += b.re; a.im += b.im; return a; }
+__device__ __forceinline__ cplx& operator-=(cplx& a, cplx b) { a.re -= b.re; a.im -= b.im; return a; }
+__device__ __forceinline__ cplx conj(cplx a) { return {a.re, -a.im}; }
+// a += s * b  (s real)
+__device__ __forceinline__ void axpy(cplx& a, double s, cplx b) {
+  a.re = fma(s, b.re, a.re);
+  a.im = fma(s, b.im, a.im);
+}
+// a += b * c (complex)
+__device__ __forceinline__ void cfma(cplx& a, cplx b, cplx c) {
+  a.re = fma(b.re, c.re, a.re);
+  a.re = fma(-b.im, c.im, a.re);
+  a.im = fma(b.re, c.im, a.im);
+  a.im = fma(b.im, c.re, a.im);
+}
+
+// ----------------------------------------------------------------- Hankel
+template <int N>
+__device__ __forceinline__ double clenshaw01(const double (&c)[N], double u) {
+  const double y = 2.0 * u - 1.0;
+  const double y2 = 2.0 * y;
+  double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+  for (int j = N - 1; j >= 1; --j) {
+    const double t = fma(y2, b1, c[j] - b2);
+    b2 = b1;
+    b1 = t;
+  }
+  return fma(y, b1, c[0] - b2);
+}
+
+constexpr double kTwoOverPi = 0.63661977236758134308;
+constexpr double kEulerGamma = 0.57721566490153286061;
+constexpr double kPio4Hi = 0.78539816339744827900;
+constexpr double kPio4Lo = 3.06161699786838301793e-17;
+constexpr double kPi = 3.14159265358979323846;
+
+// H0^(1)(x), H1^(1)(x) for real x > 0 (Chebyshev in (x/8)^2 below 8,
+// Hankel asymptotic factors in (8/x)^2 above, phase x - pi/4 kept exact with
+// a two-sum as in proj/src/hankel.cpp:53-65).
+__device__ __forceinline__ void hankel01(double x, cplx& h0, cplx& h1) {
+  if (x <= 8.0) {
+    const double q = x * 0.125;
+    const double t = q * q;
+    const double j0 = clenshaw01(kJ0Small, t);
+    const double j1 = clenshaw01(kJ1Small, t) * x;
+    const double lg = kTwoOverPi * (log(0.5 * x) + kEulerGamma);
+    const double y0 = fma(lg, j0, clenshaw01(kV0Small, t));
+    const double y1 = clenshaw01(kV1Small, t) * x + lg * j1 - kTwoOverPi / x;
+    h0 = mk(j0, y0);
+    h1 = mk(j1, y1);
+    return;
+  }
+  const double q = 8.0 / x;
+  const double v = q * q;
+  const double p0 = clenshaw01(kP0Large, v);
+  const double q0 = clenshaw01(kQ0Large, v) / x;
+  const double p1 = clenshaw01(kP1Large, v);
+  const double q1 = clenshaw01(kQ1Large, v) / x;
+  const double amp = sqrt(kTwoOverPi / x);
+  const double chi0 = x - kPio4Hi;
+  const double resid = (x - chi0) - kPio4Hi;
+  const double corr = resid - kPio4Lo;
+  double s0, c0;
+  sincos(chi0, &s0, &c0);
+  const double s0c = fma(corr, c0, s0);
+  const double c0c = fma(-corr, s0, c0);
+  s0 = s0c;
+  c0 = c0c;
+  const double c1 = s0;
+  const double s1 = -c0;
+  h0 = mk(amp * (p0 * c0 - q0 * s0), amp * (p0 * s0 + q0 * c0));
+  h1 = mk(amp * (p1 * c1 - q1 * s1), amp * (p1 * s1 + q1 * c1));
+}
+
+// ----------------------------------------------------------------- scalars
+// Order everywhere: gpsi, gchi, d1, d2, d3, n1, n2, n4, n5, n7.
+struct Scalars {
+  cplx s[10];
+};
+struct StaticScalars {
+  double s[10];
+};
+
+__device__ __forceinline__ void static_part(const DevMedium& m, double r,
+                                            StaticScalars& o) {
+  const double logr = log(r);
+  const double lp2m = m.lam + 2.0 * m.mu;
+  o.s[0] = -logr / (2.0 * kPi) + m.cconst * (2.0 * logr + 1.0);
+  o.s[1] = 2.0 * m.cconst;
+  o.s[2] = m.mu / (2.0 * kPi * lp2m * r);
+  o.s[3] = -o.s[2];
+  o.s[4] = -8.0 * m.cconst / r;
+  const double r2 = r * r;
+  o.s[5] = m.mu * m.mu / (kPi * lp2m * r2);
+  o.s[6] = m.mu * m.lam / (kPi * lp2m * r2);
+  o.s[7] = -8.0 * m.qfactor / r2;
+  o.s[8] = m.mu * (m.lam - m.mu) / (kPi * lp2m * r2);
+  o.s[9] = 2.0 * m.mu * m.mu / (kPi * lp2m * r2);
+}
+
+// {Re a, Im a, Re b, Im b} of power q of series k (warp-uniform address).
+__device__ __forceinline__ double4 ld_series(const DevCtx* __restrict__ ctx,
+                                             int k, int q) {
+  const double2* p = reinterpret_cast<const double2*>(ctx->series) +
+                     2 * (k * kMaxSeriesPow + q);
+  const double2 a = __ldg(p), b = __ldg(p + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// Remainder series below the series radius: sum_q (a_q + b_q ln r) r^q, dense
+// power tables (zeros where the series has no term).
+__device__ __forceinline__ void series_eval(const DevCtx* __restrict__ ctx,
+                                            double r, Scalars& o) {
+  const double logr = log(r);
+  const int maxq = ctx->series_maxq;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) o.s[k] = mk(0.0, 0.0);
+  double rp = 1.0;
+  for (int q = 0; q <= maxq; ++q) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      const double4 c = ld_series(ctx, k, q);
+      // (a + b ln r) r^q
+      const cplx t = mk(fma(c.z, logr, c.x), fma(c.w, logr, c.y));
+      axpy(o.s[k], rp, t);
+    }
+    rp *= r;
+  }
+}
+
+// Full dynamic scalars at r (> 0), proj/src/kernel_scalars.cpp:214-281.
+__device__ __forceinline__ void scalars_full(const DevCtx* __restrict__ ctx,
+                                             double r, Scalars& o) {
+  const DevMedium& m = ctx->med;
+  if (r < m.series_radius) {
+    series_eval(ctx, r, o);
+    StaticScalars s0;
+    static_part(m, r, s0);
+#pragma unroll
+    for (int k = 0; k < 10; ++k) o.s[k].re += s0.s[k];
+    return;
+  }
+  const double kT = m.kT, kL = m.kL;
+  const double zT = kT * r;
+  const double zL = kL * r;
+  cplx h0T, h1T, h0L, h1L;
+  hankel01(zT, h0T, h1T);
+  hankel01(zL, h0L, h1L);
+  // chi = (i/4) H0; multiplying by i/4: (a+ib) i/4 = (-b/4, a/4)
+  auto i4 = [](cplx z) { return mk(-0.25 * z.im, 0.25 * z.re); };
+  const cplx chiT = i4(h0T);
+  const cplx chiL = i4(h0L);
+  const cplx chiT1 = -(kT * i4(h1T));
+  const cplx chiL1 = -(kL * i4(h1L));
+  const double izT = 1.0 / zT, izL = 1.0 / zL;
+  const cplx chiT2 = -(kT * kT) * i4(h0T - h1T * izT);
+  const cplx chiL2 = -(kL * kL) * i4(h0L - h1L * izL);
+  const cplx chiT3 = -(kT * kT * kT) *
+                     i4(-h1T - h0T * izT + (2.0 * izT * izT) * h1T);
+  const cplx chiL3 = -(kL * kL * kL) *
+                     i4(-h1L - h0L * izL + (2.0 * izL * izL) * h1L);
+  const cplx chiT4 = -(kT * kT * kT * kT) *
+                     i4(-h0T + (2.0 * izT) * h1T + (3.0 * izT * izT) * h0T -
+                        (6.0 * izT * izT * izT) * h1T);
+  const cplx chiL4 = -(kL * kL * kL * kL) *
+                     i4(-h0L + (2.0 * izL) * h1L + (3.0 * izL * izL) * h0L -
+                        (6.0 * izL * izL * izL) * h1L);
+  const double ikT2 = 1.0 / (kT * kT);
+  const cplx psi1 = (chiT1 - chiL1) * ikT2;
+  const cplx psi2 = (chiT2 - chiL2) * ikT2;
+  const cplx psi3 = (chiT3 - chiL3) * ikT2;
+  const cplx psi4 = (chiT4 - chiL4) * ikT2;
+  const double ir = 1.0 / r;
+  const double mu = m.mu;
+  o.s[0] = chiT + psi1 * ir;
+  o.s[1] = psi2 - psi1 * ir;
+  const cplx w = o.s[1] * ir;
+  const cplx gam = o.s[1] * (ir * ir);
+  const cplx bet = (psi3 - 3.0 * w) * ir;
+  const cplx alf = psi4 - (6.0 * ir) * psi3 + 15.0 * gam;
+  o.s[2] = m.aratio * chiL1 + 2.0 * w;
+  o.s[3] = chiT1 + 2.0 * w;
+  o.s[4] = 2.0 * (psi3 - 3.0 * w);
+  o.s[5] = (-2.0 * mu * ir) * chiT1 - (4.0 * mu) * gam;
+  o.s[6] = (-mu) * (chiT2 - chiT1 * ir) - (4.0 * mu) * bet;
+  o.s[7] = (-4.0 * mu) * alf;
+  o.s[8] = (m.lam * m.aratio * kL * kL) * chiL -
+           (4.0 * mu * m.aratio * ir) * chiL1 - (4.0 * mu) * gam;
+  o.s[9] = (-2.0 * mu * m.aratio) * (chiL2 - chiL1 * ir) - (4.0 * mu) * bet;
+}
+
+// full and remainder together, proj/src/kernel_scalars.cpp:301-331.
+__device__ __forceinline__ void scalars_split(const DevCtx* __restrict__ ctx,
+                                              double r, Scalars& full,
+                                              Scalars& rem) {
+  StaticScalars s0;
+  static_part(ctx->med, r, s0);
+  if (r < ctx->med.series_radius) {
+    series_eval(ctx, r, rem);
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      full.s[k] = rem.s[k];
+      full.s[k].re += s0.s[k];
+    }
+    return;
+  }
+  scalars_full(ctx, r, full);
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    rem.s[k] = full.s[k];
+    rem.s[k].re -= s0.s[k];
+  }
+}
+
+// Closed form of int_0^1 u^upow rem(scale*u) du per scalar,
+// proj/src/kernel_scalars.cpp:108-121,333-344.  Sets *bad when the element is
+// too long for the frequency (the reference throws std::domain_error).
+__device__ __forceinline__ void integrated_remainder(
+    const DevCtx* __restrict__ ctx, double scale, int upow, Scalars& o,
+    int* bad) {
+  if (!(ctx->med.kT * scale < 2.5)) atomicExch(bad, 1);
+  const double logc = log(scale);
+  const int maxq = ctx->series_maxq;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) o.s[k] = mk(0.0, 0.0);
+  double cp = 1.0;
+  for (int q = 0; q <= maxq; ++q) {
+    const double inv = 1.0 / double(q + upow + 1);
+    const double inv2 = inv * inv;
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      const double4 c = ld_series(ctx, k, q);
+      // c^q [ (a + b ln c) inv - b inv^2 ]
+      const cplx t = mk(fma(c.z, logc, c.x) * inv - c.z * inv2,
+                        fma(c.w, logc, c.y) * inv - c.w * inv2);
+      axpy(o.s[k], cp, t);
+    }
+    cp *= scale;
+  }
+}
+
+// ----------------------------------------------------------------- combiners
+// 2x2 complex tensor, row-major a11 a12 a21 a22.
+struct CMat2 {
+  cplx a[4];
+};
+
+// D_ij = -(d1 n_j zh_i + d2 ((n.zh) d_ij + n_i zh_j) + d3 (n.zh) zh_i zh_j)
+__device__ __forceinline__ void combine_D(const Scalars& s, double zx,
+                                          double zy, double nyx, double nyy,
+                                          CMat2& m) {
+  const double nz = nyx * zx + nyy * zy;
+  const cplx d1 = s.s[2], d2 = s.s[3], d3 = s.s[4];
+  m.a[0] = -(d1 * (nyx * zx) + d2 * (nz + nyx * zx) + d3 * (nz * zx * zx));
+  m.a[1] = -(d1 * (nyy * zx) + d2 * (nyx * zy) + d3 * (nz * zx * zy));
+  m.a[2] = -(d1 * (nyx * zy) + d2 * (nyy * zx) + d3 * (nz * zy * zx));
+  m.a[3] = -(d1 * (nyy * zy) + d2 * (nz + nyy * zy) + d3 * (nz * zy * zy));
+}
+
+// Hypersingular kernel, m = observation normal (nx), n = source normal (ny).
+__device__ __forceinline__ void combine_N(const Scalars& s, double zx,
+                                          double zy, double mx, double my,
+                                          double nx, double ny, CMat2& out) {
+  const double mn = mx * nx + my * ny;
+  const double mz = mx * zx + my * zy;
+  const double nz = nx * zx + ny * zy;
+  const double mv[2] = {mx, my}, nv[2] = {nx, ny}, zv[2] = {zx, zy};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double dij = (i == j) ? 1.0 : 0.0;
+      const double c1 = mn * dij + nv[i] * mv[j];
+      const double c2 = mn * zv[i] * zv[j] + mz * nz * dij + mz * nv[i] * zv[j] +
+                        nz * zv[i] * mv[j];
+      const double c4 = mz * nz * zv[i] * zv[j];
+      const double c5 = mv[i] * nv[j];
+      const double c7 = mz * zv[i] * nv[j] + nz * mv[i] * zv[j];
+      out.a[2 * i + j] = s.s[5] * c1 + s.s[6] * c2 + s.s[7] * c4 +
+                         s.s[8] * c5 + s.s[9] * c7;
+    }
+  }
+}
+
+// Integrated-by-parts static hypersingular kernel (real).
+__device__ __forceinline__ void q0_kernel(double qfactor, double r, double zx,
+                                          double zy, double q[4]) {
+  const double lr = qfactor * log(r);
+  q[0] = lr - qfactor * (zx * zx);
+  q[1] = -qfactor * (zx * zy);
+  q[2] = q[1];
+  q[3] = lr - qfactor * (zy * zy);
+}
+
+}  // namespace ebem_gpu

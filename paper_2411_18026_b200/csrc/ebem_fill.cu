@@ -1,0 +1,597 @@
+// Galerkin fill kernels (sm_100a, FP64):
+//   k_proxy_pairs     proxy polygon <-> curve element pairs, n_g x n_g Gauss,
+//                     full kernel, both orientations from one scalar
+//                     evaluation (kernel_cross_block, proj/src/assembly.cpp:424-509)
+//   k_near_separated  exact Galerkin pairs, tiered tensor Gauss with the
+//                     static hypersingular part integrated by parts
+//                     (PairIntegrator::separated, proj/src/assembly.cpp:248-286)
+//   k_near_singular   coincident (closed form + integrated series) and
+//                     adjacent (Duffy) pairs (proj/src/assembly.cpp:70-246)
+//   k_gather          ordered scatter of bundles into output blocks
+//                     (proj/src/assembly.cpp:373-407, :493-506)
+#include <cuda_runtime.h>
+
+#include "ebem_device.cuh"
+#include "ebem_jobs.h"
+#include "ebem_kernels.h"
+
+namespace ebem_gpu {
+
+namespace {
+
+__device__ __forceinline__ double ef(const DevCtx* __restrict__ c, int f, int e) {
+  return __ldg(c->elem + size_t(f) * c->n_nodes + e);
+}
+
+// Largest j in [0, n) with off[j] <= x (off ascending, off[0] == 0).
+template <class T>
+__device__ __forceinline__ int find_job(const T* __restrict__ off, int n, T x) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(off + mid) <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ double pt_seg_dist(double px, double py, double ax,
+                                              double ay, double bx, double by) {
+  const double abx = bx - ax, aby = by - ay;
+  const double len2 = abx * abx + aby * aby;
+  double t = len2 > 0.0 ? ((px - ax) * abx + (py - ay) * aby) / len2 : 0.0;
+  t = fmin(fmax(t, 0.0), 1.0);
+  return hypot(px - (ax + t * abx), py - (ay + t * aby));
+}
+
+// Mesh::element_distance, proj/src/geometry.cpp:83-96.
+__device__ __forceinline__ double element_distance(const DevCtx* __restrict__ c,
+                                                   int ea, int eb) {
+  const double a0x = ef(c, EPX, ea), a0y = ef(c, EPY, ea);
+  const double a1x = a0x + ef(c, EDX, ea), a1y = a0y + ef(c, EDY, ea);
+  const double b0x = ef(c, EPX, eb), b0y = ef(c, EPY, eb);
+  const double b1x = b0x + ef(c, EDX, eb), b1y = b0y + ef(c, EDY, eb);
+  double d = pt_seg_dist(a0x, a0y, b0x, b0y, b1x, b1y);
+  d = fmin(d, pt_seg_dist(a1x, a1y, b0x, b0y, b1x, b1y));
+  d = fmin(d, pt_seg_dist(b0x, b0y, a0x, a0y, a1x, a1y));
+  d = fmin(d, pt_seg_dist(b1x, b1y, a0x, a0y, a1x, a1y));
+  return d;
+}
+
+// tier_nodes, proj/src/assembly.cpp:27-38.
+__device__ __forceinline__ int tier_nodes(double q, int far, double refine) {
+  int n = far;
+  if (q >= 8.0) {
+  } else if (q >= 4.0) {
+    n += 2;
+  } else if (q >= 2.0) {
+    n += 5;
+  } else {
+    n += 9;
+  }
+  return int(n * refine + 0.5);
+}
+
+__device__ __forceinline__ void store_bundle(double* __restrict__ out, long long p,
+                                             const cplx (&v)[kBundle]) {
+  double2* o = reinterpret_cast<double2*>(out) + p * kBundle;
+#pragma unroll
+  for (int k = 0; k < kBundle; ++k) o[k] = make_double2(v[k].re, v[k].im);
+}
+
+// bundle index: ((la * 2 + lb) * 2 + i) * 2 + j
+__device__ __forceinline__ int bidx(int la, int lb, int i, int j) {
+  return ((la * 2 + lb) * 2 + i) * 2 + j;
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- separated
+// One thread per element pair.  Pairs that touch (coincident / adjacent) are
+// skipped here and produced by k_near_singular.
+__global__ void __launch_bounds__(128)
+k_near_separated(const DevCtx* __restrict__ ctx, const NearJob* __restrict__ jobs,
+                 const long long* __restrict__ job_pair_off, int n_jobs,
+                 const int* __restrict__ elems, long long n_pairs,
+                 double* __restrict__ bundles) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= n_pairs) return;
+  const int jb = find_job(job_pair_off, n_jobs, p);
+  const NearJob J = jobs[jb];
+  const long long local = p - J.pair_off;
+  const int ra = int(local / J.nces);
+  const int cb = int(local - (long long)ra * J.nces);
+  const int ea = __ldg(elems + J.res_off + ra);
+  const int eb = __ldg(elems + J.ces_off + cb);
+  const int N = ctx->n_nodes;
+  const int na = ea + 1 == N ? 0 : ea + 1;
+  const int nb = eb + 1 == N ? 0 : eb + 1;
+  if (ea == eb || na == eb || nb == ea) return;  // singular pair
+
+  const double hx = ef(ctx, EH, ea), hy = ef(ctx, EH, eb);
+  const int n = tier_nodes(element_distance(ctx, ea, eb) / fmax(hx, hy),
+                           ctx->far_nodes, ctx->refine);
+  const double* gx = ctx->gx + gauss_offset(n);
+  const double* gw = ctx->gw + gauss_offset(n);
+  const double pax = ef(ctx, EPX, ea), pay = ef(ctx, EPY, ea);
+  const double dax = ef(ctx, EDX, ea), day = ef(ctx, EDY, ea);
+  const double pbx = ef(ctx, EPX, eb), pby = ef(ctx, EPY, eb);
+  const double dbx = ef(ctx, EDX, eb), dby = ef(ctx, EDY, eb);
+  const double nxx = ef(ctx, ENX, ea), nxy = ef(ctx, ENY, ea);
+  const double nyx = ef(ctx, ENX, eb), nyy = ef(ctx, ENY, eb);
+  const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
+  const double qfac = ctx->med.qfactor;
+
+  cplx acc[kBundle];
+#pragma unroll
+  for (int k = 0; k < kBundle; ++k) acc[k] = mk(0.0, 0.0);
+
+  for (int is = 0; is < n; ++is) {
+    const double s = __ldg(gx + is);
+    const double ws = __ldg(gw + is);
+    const double xx = pax + s * dax, xy = pay + s * day;
+    for (int it = 0; it < n; ++it) {
+      const double t = __ldg(gx + it);
+      const double wt = __ldg(gw + it);
+      const double zx = xx - (pbx + t * dbx);
+      const double zy = xy - (pby + t * dby);
+      const double r = hypot(zx, zy);
+      const double ir = 1.0 / r;
+      const double zhx = ir * zx, zhy = ir * zy;
+      Scalars fs, rs;
+      scalars_split(ctx, r, fs, rs);
+      CMat2 dm, nm;
+      combine_D(fs, zhx, zhy, nyx, nyy, dm);
+      combine_N(rs, zhx, zhy, nxx, nxy, nyx, nyy, nm);
+      double qm[4];
+      q0_kernel(qfac, r, zhx, zhy, qm);
+      const double ww = ws * wt;
+      const double wgt = ww * hx * hy;
+      // K = D + alpha N (the reference adds alpha N at scatter time)
+      cplx km[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) km[e] = dm.a[e] + alpha * nm.a[e];
+      const double ps[2] = {1.0 - s, s};
+      const double pt[2] = {1.0 - t, t};
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const double f = wgt * ps[a] * pt[b];
+          const double g = ww * ((a == b) ? 1.0 : -1.0);  // slope_a * slope_b
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            cplx& o = acc[(a * 2 + b) * 4 + e];
+            axpy(o, f, km[e]);
+            axpy(o, g * qm[e], alpha);
+          }
+        }
+      }
+    }
+  }
+  store_bundle(bundles, p, acc);
+}
+
+// ---------------------------------------------------------------- singular
+namespace {
+
+__device__ void coincident_bundle(const DevCtx* __restrict__ ctx, int e,
+                                  cplx (&v)[kBundle], int* bad) {
+  const double h = ef(ctx, EH, e);
+  const double tx = ef(ctx, ETX, e), ty = ef(ctx, ETY, e);
+  const double nx = ef(ctx, ENX, e), ny = ef(ctx, ENY, e);
+  const double logh = log(h);
+  const double qfac = ctx->med.qfactor;
+  const double kappa = ctx->med.kappa;
+  const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
+  cplx D[kBundle], Nn[kBundle];
+#pragma unroll
+  for (int k = 0; k < kBundle; ++k) D[k] = Nn[k] = mk(0.0, 0.0);
+  const double M[2][2] = {{h / 3.0, h / 6.0}, {h / 6.0, h / 3.0}};
+
+  // traction, static: principal values -+ 1/2 on the off-diagonal shapes
+  const double dcoef = 0.5 * kappa * h;
+  D[bidx(0, 1, 0, 1)] += mk(dcoef);
+  D[bidx(0, 1, 1, 0)] += mk(-dcoef);
+  D[bidx(1, 0, 0, 1)] += mk(-dcoef);
+  D[bidx(1, 0, 1, 0)] += mk(dcoef);
+
+  Scalars f0, f1, f2, f3;
+  integrated_remainder(ctx, h, 1, f1, bad);
+  integrated_remainder(ctx, h, 2, f2, bad);
+  const cplx i1 = f2.s[2] - f1.s[2];
+  const cplx i2 = f2.s[3] - f1.s[3];
+  const double h2 = h * h;
+  const double tv[2] = {tx, ty}, nv[2] = {nx, ny};
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const cplx val = (-h2) * (i1 * (tv[i] * nv[j]) + i2 * (nv[i] * tv[j]));
+      D[bidx(0, 1, i, j)] += val;
+      D[bidx(1, 0, i, j)] -= val;
+    }
+  // hypersingular, static part by parts
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const double sgn = (a == b) ? 1.0 : -1.0;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const double dij = (i == j) ? 1.0 : 0.0;
+          Nn[bidx(a, b, i, j)] += mk(sgn * qfac * ((logh - 1.5) * dij - tv[i] * tv[j]));
+        }
+    }
+  // hypersingular remainder: even reduction weights
+  integrated_remainder(ctx, h, 0, f0, bad);
+  integrated_remainder(ctx, h, 3, f3, bad);
+  Scalars sdiag, soff;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    sdiag.s[k] = f3.s[k] / 3.0 - f1.s[k] + (2.0 * f0.s[k]) / 3.0;
+    soff.s[k] = (f0.s[k] - f3.s[k]) / 3.0;
+  }
+  CMat2 nd, no;
+  combine_N(sdiag, tx, ty, nx, ny, nx, ny, nd);
+  combine_N(soff, tx, ty, nx, ny, nx, ny, no);
+#pragma unroll
+  for (int e4 = 0; e4 < 4; ++e4) {
+    Nn[bidx(0, 0, 0, 0) + e4] += h2 * nd.a[e4];
+    Nn[bidx(1, 1, 0, 0) + e4] += h2 * nd.a[e4];
+    Nn[bidx(0, 1, 0, 0) + e4] += h2 * no.a[e4];
+    Nn[bidx(1, 0, 0, 0) + e4] += h2 * no.a[e4];
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int k = bidx(a, b, i, j);
+          cplx val = D[k] + alpha * Nn[k];
+          if (i == j) val.re += 0.5 * M[a][b];
+          v[k] = val;
+        }
+}
+
+__device__ void adjacent_bundle(const DevCtx* __restrict__ ctx, int ea, int eb,
+                                bool end_start, cplx (&v)[kBundle], int* bad) {
+  const double hx = ef(ctx, EH, ea), hy = ef(ctx, EH, eb);
+  double txx, txy, tyx, tyy;
+  double bx0[2], bx1[2], by0[2], by1[2];
+  if (end_start) {
+    txx = -ef(ctx, ETX, ea); txy = -ef(ctx, ETY, ea);
+    bx0[0] = 0.0; bx1[0] = 1.0; bx0[1] = 1.0; bx1[1] = -1.0;
+    tyx = ef(ctx, ETX, eb); tyy = ef(ctx, ETY, eb);
+    by0[0] = 1.0; by1[0] = -1.0; by0[1] = 0.0; by1[1] = 1.0;
+  } else {
+    txx = ef(ctx, ETX, ea); txy = ef(ctx, ETY, ea);
+    bx0[0] = 1.0; bx1[0] = -1.0; bx0[1] = 0.0; bx1[1] = 1.0;
+    tyx = -ef(ctx, ETX, eb); tyy = -ef(ctx, ETY, eb);
+    by0[0] = 0.0; by1[0] = 1.0; by0[1] = 1.0; by1[1] = -1.0;
+  }
+  const double nxx = ef(ctx, ENX, ea), nxy = ef(ctx, ENY, ea);
+  const double nyx = ef(ctx, ENX, eb), nyy = ef(ctx, ENY, eb);
+  const double qfac = ctx->med.qfactor;
+  const double hxy = hx * hy;
+  const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
+  Scalars dhat;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) dhat.s[k] = mk(0.0);
+  dhat.s[2] = mk(ctx->med.kappa);
+  dhat.s[3] = mk(-ctx->med.kappa);
+  dhat.s[4] = mk(-8.0 * ctx->med.ccon);
+
+  cplx acc[kBundle];
+#pragma unroll
+  for (int k = 0; k < kBundle; ++k) acc[k] = mk(0.0);
+  const int n = ctx->corner_n;
+  const double* gx = ctx->gx + gauss_offset(n);
+  const double* gw = ctx->gw + gauss_offset(n);
+  for (int tri = 0; tri < 2; ++tri) {
+    for (int wi = 0; wi < n; ++wi) {
+      const double w = gx[wi];
+      const double wt = gw[wi];
+      double zvx, zvy;
+      if (tri == 0) {
+        zvx = hx * txx - (w * hy) * tyx;
+        zvy = hx * txy - (w * hy) * tyy;
+      } else {
+        zvx = (w * hx) * txx - hy * tyx;
+        zvy = (w * hx) * txy - hy * tyy;
+      }
+      const double g = hypot(zvx, zvy);
+      const double ig = 1.0 / g;
+      const double zhx = ig * zvx, zhy = ig * zvy;
+      const double logg = log(g);
+      CMat2 dmat[3], nmat[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        Scalars s;
+        integrated_remainder(ctx, g, j + 1, s, bad);
+        combine_D(s, zhx, zhy, nyx, nyy, dmat[j]);
+        combine_N(s, zhx, zhy, nxx, nxy, nyx, nyy, nmat[j]);
+      }
+      CMat2 dstat;
+      combine_D(dhat, zhx, zhy, nyx, nyy, dstat);
+      const double ql = qfac * (logg * 0.5 - 0.25);
+      const double qz = qfac * 0.5;
+      const double qm[4] = {ql - qz * zhx * zhx, -qz * zhx * zhy,
+                            -qz * zhy * zhx, ql - qz * zhy * zhy};
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const double t0 = bx0[a], u0 = by0[b];
+          const double t1 = (tri == 0) ? bx1[a] : bx1[a] * w;
+          const double u1 = (tri == 0) ? by1[b] * w : by1[b];
+          const double c[3] = {t0 * u0, t0 * u1 + t1 * u0, t1 * u1};
+          const double cint = c[0] / 1.0 + c[1] / 2.0 + c[2] / 3.0;
+          const double fs = wt * hxy * cint / g;
+          const double sgn = (a == b) ? 1.0 : -1.0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            cplx d = fs * dstat.a[e];
+            cplx nn = mk(wt * sgn * qm[e]);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const double f = wt * hxy * c[j];
+              axpy(d, f, dmat[j].a[e]);
+              axpy(nn, f, nmat[j].a[e]);
+            }
+            acc[(a * 2 + b) * 4 + e] += d + alpha * nn;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kBundle; ++k) v[k] = acc[k];
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(64)
+k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pairs,
+                const int* __restrict__ pair_elems, int n, double* __restrict__ bundles,
+                int* bad) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int ea = pair_elems[2 * t], eb = pair_elems[2 * t + 1];
+  const int N = ctx->n_nodes;
+  cplx v[kBundle];
+  if (ea == eb) {
+    coincident_bundle(ctx, ea, v, bad);
+  } else {
+    const bool end_start = (ea + 1 == N ? 0 : ea + 1) == eb;
+    adjacent_bundle(ctx, ea, eb, end_start, v, bad);
+  }
+  store_bundle(bundles, pairs[t], v);
+}
+
+// ------------------------------------------------------------------- proxy
+// CTA = kProxyPairs element pairs x n_g threads; thread (pair, i) fixes the
+// polygon quadrature point s_i and sweeps the curve points t_j.  The row sums
+// of both orientations go through shared memory and are reduced over i.
+constexpr int kProxyThreads = 256;
+
+__global__ void __launch_bounds__(kProxyThreads)
+k_proxy_pairs(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ jobs,
+              const int* __restrict__ job_block_off, int n_jobs,
+              const int* __restrict__ elems, double* __restrict__ bundles,
+              int kProxyPairs) {
+  extern __shared__ double2 sh[];  // [kProxyPairs * ng][2 orient][2][4]
+  const int ng = ctx->proxy_n;
+  const int m = ctx->m_prime;
+  const int jb = find_job(job_block_off, n_jobs, (int)blockIdx.x);
+  const ProxyJob J = jobs[jb];
+  const int npairs = m * J.nE;
+  const int pair0 = (blockIdx.x - J.block_off) * kProxyPairs;
+  const int lp = threadIdx.x / ng;
+  const int i = threadIdx.x - lp * ng;
+  const int pair = pair0 + lp;
+  const bool active = lp < kProxyPairs && pair < npairs;
+  const double* gx = ctx->gx + gauss_offset(ng);
+  const double* gw = ctx->gw + gauss_offset(ng);
+
+  if (active) {
+    const int pe = pair / J.nE;
+    const int q = pair - pe * J.nE;
+    const int eb = __ldg(elems + J.e_off + q);
+    // polygon element pe: node pe -> node (pe+1) mod m (Mesh ctor, geometry.cpp:15-37)
+    const int pn = pe + 1 == m ? 0 : pe + 1;
+    const double p0x = J.cx + J.radius * ctx->poly_cs[2 * pe];
+    const double p0y = J.cy + J.radius * ctx->poly_cs[2 * pe + 1];
+    const double p1x = J.cx + J.radius * ctx->poly_cs[2 * pn];
+    const double p1y = J.cy + J.radius * ctx->poly_cs[2 * pn + 1];
+    const double pdx = p1x - p0x, pdy = p1y - p0y;
+    const double hp = hypot(pdx, pdy);
+    const double ptx = pdx / hp, pty = pdy / hp;
+    const double pnx = -pty, pny = ptx;
+    const double mpx = ef(ctx, EPX, eb), mpy = ef(ctx, EPY, eb);
+    const double mdx = ef(ctx, EDX, eb), mdy = ef(ctx, EDY, eb);
+    const double mnx = ef(ctx, ENX, eb), mny = ef(ctx, ENY, eb);
+    const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
+
+    const double s = __ldg(gx + i);
+    const double xx = p0x + s * pdx, xy = p0y + s * pdy;
+    cplx rv[2][4], ru[2][4];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) rv[b][e] = ru[b][e] = mk(0.0);
+    for (int j = 0; j < ng; ++j) {
+      const double t = __ldg(gx + j);
+      const double wj = __ldg(gw + j);
+      const double zx = xx - (mpx + t * mdx);
+      const double zy = xy - (mpy + t * mdy);
+      const double r = hypot(zx, zy);
+      const double ir = 1.0 / r;
+      const double zhx = ir * zx, zhy = ir * zy;
+      Scalars fs;
+      scalars_full(ctx, r, fs);
+      CMat2 dm, nm;
+      // V: test on the polygon (normal pn), trial on the curve (normal mn)
+      combine_D(fs, zhx, zhy, mnx, mny, dm);
+      combine_N(fs, zhx, zhy, pnx, pny, mnx, mny, nm);
+      const double pt[2] = {wj * (1.0 - t), wj * t};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const cplx k = dm.a[e] + alpha * nm.a[e];
+        axpy(rv[0][e], pt[0], k);
+        axpy(rv[1][e], pt[1], k);
+      }
+      // U: test on the curve, trial on the polygon, zh reversed
+      combine_D(fs, -zhx, -zhy, pnx, pny, dm);
+      combine_N(fs, -zhx, -zhy, mnx, mny, pnx, pny, nm);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const cplx k = dm.a[e] + alpha * nm.a[e];
+        axpy(ru[0][e], pt[0], k);
+        axpy(ru[1][e], pt[1], k);
+      }
+    }
+    double2* my = sh + threadIdx.x * 16;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        my[b * 4 + e] = make_double2(rv[b][e].re, rv[b][e].im);
+        my[8 + b * 4 + e] = make_double2(ru[b][e].re, ru[b][e].im);
+      }
+  }
+  __syncthreads();
+  // Reduction over i: thread handles (pair lp2, orientation, 16 outputs / 2).
+  const int nthreads = blockDim.x;
+  for (int o = threadIdx.x; o < kProxyPairs * 2 * kBundle; o += nthreads) {
+    const int lp2 = o / (2 * kBundle);
+    const int rem = o - lp2 * 2 * kBundle;
+    const int orient = rem / kBundle;
+    const int k = rem - orient * kBundle;  // bidx(la, lb, i, j)
+    const int p2 = pair0 + lp2;
+    if (p2 >= npairs) continue;
+    const int la = k >> 3, lb = (k >> 2) & 1, e = k & 3;
+    const int pe = p2 / J.nE;
+    const int q = p2 - pe * J.nE;
+    const int pn = pe + 1 == m ? 0 : pe + 1;
+    double2 accv = make_double2(0.0, 0.0);
+    for (int ii = 0; ii < ng; ++ii) {
+      const double s = __ldg(gx + ii);
+      const double wi = __ldg(gw + ii);
+      // V: poly test shape la at s_i, curve trial shape lb summed in row sums
+      // U: curve test shape la in the row sums, poly trial shape lb at s_i
+      const double shape = orient == 0 ? (la == 0 ? 1.0 - s : s)
+                                       : (lb == 0 ? 1.0 - s : s);
+      const int slot = orient == 0 ? (lb * 4 + e) : (8 + la * 4 + e);
+      const double2 v = sh[(lp2 * ng + ii) * 16 + slot];
+      accv.x = fma(wi * shape, v.x, accv.x);
+      accv.y = fma(wi * shape, v.y, accv.y);
+    }
+    // element lengths: recompute (cheap) to scale by h_poly * h_curve
+    const int eb = __ldg(elems + J.e_off + q);
+    const double p0x = J.cx + J.radius * ctx->poly_cs[2 * pe];
+    const double p0y = J.cy + J.radius * ctx->poly_cs[2 * pe + 1];
+    const double p1x = J.cx + J.radius * ctx->poly_cs[2 * pn];
+    const double p1y = J.cy + J.radius * ctx->poly_cs[2 * pn + 1];
+    const double hh = hypot(p1x - p0x, p1y - p0y) * ef(ctx, EH, eb);
+    const long long dst = orient == 0 ? J.v_off + p2 : J.u_off + (long long)q * m + pe;
+    reinterpret_cast<double2*>(bundles)[dst * kBundle + k] =
+        make_double2(hh * accv.x, hh * accv.y);
+  }
+}
+
+// ------------------------------------------------------------------ gather
+__global__ void __launch_bounds__(256)
+k_gather(const GatherJob* __restrict__ jobs, const long long* __restrict__ job_entry_off,
+         int n_jobs, const NodeDesc* __restrict__ desc, long long n_entries,
+         const double* __restrict__ bundles) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= n_entries) return;
+  const int jb = find_job(job_entry_off, n_jobs, t);
+  const GatherJob& J = jobs[jb];
+  const long long local = t - J.entry_off;
+  // column-major sweep: consecutive threads -> consecutive rows
+  const int c = int(local / J.nrows);
+  const int r = int(local - (long long)c * J.nrows);
+  const NodeDesc rd = desc[J.rdesc_off + r];
+  const NodeDesc cd = desc[J.cdesc_off + c];
+  const int i = rd.bits >> 2, j = cd.bits >> 2;
+  const int ra[2] = {rd.e1, rd.e2}, la[2] = {rd.bits & 1, (rd.bits >> 1) & 1};
+  const int cb[2] = {cd.e1, cd.e2}, lb[2] = {cd.bits & 1, (cd.bits >> 1) & 1};
+  const double2* B = reinterpret_cast<const double2*>(bundles);
+  double re = 0.0, im = 0.0;
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y) {
+      const long long pidx = J.pair_off + (long long)ra[x] * J.nces + cb[y];
+      const double2 v = __ldg(B + pidx * kBundle + bidx(la[x], lb[y], i, j));
+      re += v.x;
+      im += v.y;
+    }
+  double2* D = reinterpret_cast<double2*>(J.dest);
+  if (J.trans) D[rd.dest * (long long)J.ld + cd.dest] = make_double2(re, -im);
+  else D[cd.dest * (long long)J.ld + rd.dest] = make_double2(re, im);
+}
+
+// ------------------------------------------------------------ host wrappers
+void launch_near_separated(const DevCtx* ctx, const NearJob* jobs,
+                           const long long* job_pair_off, int n_jobs,
+                           const int* elems, long long n_pairs, double* bundles,
+                           cudaStream_t st) {
+  if (n_pairs <= 0) return;
+  const int bs = 128;
+  k_near_separated<<<(unsigned)((n_pairs + bs - 1) / bs), bs, 0, st>>>(
+      ctx, jobs, job_pair_off, n_jobs, elems, n_pairs, bundles);
+}
+
+void launch_near_singular(const DevCtx* ctx, const long long* pairs,
+                          const int* pair_elems, int n, double* bundles, int* bad,
+                          cudaStream_t st) {
+  if (n <= 0) return;
+  const int bs = 64;
+  k_near_singular<<<(n + bs - 1) / bs, bs, 0, st>>>(ctx, pairs, pair_elems, n,
+                                                     bundles, bad);
+}
+
+int proxy_pairs_per_block(int n_gauss) {
+  return n_gauss >= kProxyThreads ? 1 : (kProxyThreads / n_gauss < 32 ? kProxyThreads / n_gauss : 32);
+}
+
+int proxy_blocks_for(int m_prime, int nE, int n_gauss) {
+  const int p = proxy_pairs_per_block(n_gauss);
+  return (m_prime * nE + p - 1) / p;
+}
+
+void launch_proxy_pairs(const DevCtx* ctx, int n_gauss, const ProxyJob* jobs,
+                        const int* job_block_off, int n_jobs, int n_blocks,
+                        const int* elems, double* bundles, cudaStream_t st) {
+  if (n_blocks <= 0) return;
+  const int p = proxy_pairs_per_block(n_gauss);
+  const int threads = p * n_gauss;
+  const size_t shmem = size_t(threads) * 16 * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_proxy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kProxyThreads * 16 * (int)sizeof(double2));
+    attr = true;
+  }
+  k_proxy_pairs<<<n_blocks, threads, shmem, st>>>(ctx, jobs, job_block_off,
+                                                  n_jobs, elems, bundles, p);
+}
+
+void launch_gather(const GatherJob* jobs, const long long* job_entry_off,
+                   int n_jobs, const NodeDesc* desc, long long n_entries,
+                   const double* bundles, cudaStream_t st) {
+  if (n_entries <= 0) return;
+  const int bs = 256;
+  k_gather<<<(unsigned)((n_entries + bs - 1) / bs), bs, 0, st>>>(
+      jobs, job_entry_off, n_jobs, desc, n_entries, bundles);
+}
+
+}  // namespace ebem_gpu

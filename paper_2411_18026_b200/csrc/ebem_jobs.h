@@ -1,0 +1,58 @@
+// Work descriptors the host runtime plans per tree level and the fill
+// kernels consume.  Plain data, shared by host C++ and device code.
+//
+// The Galerkin fill is split the way the reference's scatter is organised
+// (proj/src/assembly.cpp:373-407, :460-507): every (test element, trial
+// element) pair produces a bundle of 16 complex numbers V[la][lb][i][j] =
+// D + alpha N (+ M/2 on coincident diagonals); every output entry is then the
+// sum of the (at most 2 x 2) bundles of the elements supporting its row and
+// column hat functions, added in ascending (test element, trial element)
+// order.
+#pragma once
+
+namespace ebem_gpu {
+
+constexpr int kBundle = 16;  // complex numbers per element-pair bundle
+
+// One row (or column) of an output block: the hat function of a node in one
+// component.  e1 < e2 are the indices (into the job's element list) of the
+// two supporting elements in ascending element order; la1/la2 are the local
+// shape indices of the node on them (1 on element g-1, 0 on element g).
+struct NodeDesc {
+  int dest;  // destination row (column) index in the output matrix
+  int e1, e2;
+  int bits;  // la1 | la2 << 1 | comp << 2
+};
+
+// Element pairs of one true_block evaluation (res x ces, row-major).
+struct NearJob {
+  long long pair_off;
+  int res_off, nres;  // element ids in the level's element pool
+  int ces_off, nces;
+};
+
+// One proxy interaction job per cell: m' polygon elements x nE curve
+// elements, both orientations from the same scalar evaluations.
+// V bundle (polygon test, curve trial) at v_off + pe * nE + q,
+// U bundle (curve test, polygon trial) at u_off + q * m' + pe.
+struct ProxyJob {
+  long long v_off, u_off;
+  int e_off, nE;
+  int block_off;  // first CTA of this job in the proxy launch
+  int pad;
+  double cx, cy, radius;
+};
+
+// Scatter of bundles into one output block.
+struct GatherJob {
+  long long pair_off;   // bundle index of (row element 0, col element 0)
+  long long entry_off;  // first entry of this job in the gather launch
+  int nces;             // bundle row stride (column elements)
+  int rdesc_off, nrows;
+  int cdesc_off, ncols;
+  int trans;  // 1: write conj(v) at (col dest, row dest)
+  int ld;
+  double* dest;  // interleaved complex, column-major
+};
+
+}  // namespace ebem_gpu

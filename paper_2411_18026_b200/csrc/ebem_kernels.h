@@ -1,0 +1,37 @@
+// Host-callable launch wrappers of the sm_100a kernels (defined in *.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "ebem_ctx.h"
+#include "ebem_jobs.h"
+
+namespace ebem_gpu {
+
+// ---- fill (ebem_fill.cu)
+void launch_near_separated(const DevCtx* ctx, const NearJob* jobs,
+                           const long long* job_pair_off, int n_jobs,
+                           const int* elems, long long n_pairs, double* bundles,
+                           cudaStream_t st);
+void launch_near_singular(const DevCtx* ctx, const long long* pairs,
+                          const int* pair_elems, int n, double* bundles, int* bad,
+                          cudaStream_t st);
+int proxy_blocks_for(int m_prime, int nE, int n_gauss);
+void launch_proxy_pairs(const DevCtx* ctx, int n_gauss, const ProxyJob* jobs,
+                        const int* job_block_off, int n_jobs, int n_blocks,
+                        const int* elems, double* bundles, cudaStream_t st);
+void launch_gather(const GatherJob* jobs, const long long* job_entry_off,
+                   int n_jobs, const NodeDesc* desc, long long n_entries,
+                   const double* bundles, cudaStream_t st);
+
+// ---- incident-field right-hand sides (ebem_rhs.cu)
+void launch_rhs_plane(const DevCtx* ctx, int n_nodes, int kind,
+                      const double* angles, int m, double amplitude, int rhs_n,
+                      double* out, cudaStream_t st);
+
+// ---- special functions, exposed for parity tests (ebem_rhs.cu)
+void launch_eval_hankel(const double* x, int n, double* out, cudaStream_t st);
+void launch_eval_scalars(const DevCtx* ctx, const double* r, int n, int which,
+                         double* out, cudaStream_t st);
+
+}  // namespace ebem_gpu

@@ -1,0 +1,154 @@
+// Incident-field right-hand sides and point evaluations of the special
+// functions (the latter only back the parity tests of the device math).
+//
+//   k_rhs_plane   BlockAssembler::rhs with a plane P wave (PlanePWave,
+//                 proj/src/kernels.cpp:99-118; proj/include/ebem/assembly.hpp:94-119)
+//                 or a plane SV wave (config 4; not in the reference, derived
+//                 from the same constitutive law).  One thread per
+//                 node sums its two supporting elements in ascending element
+//                 order, Gauss points in rule order, as the reference loop does.
+#include <cuda_runtime.h>
+
+#include "ebem_device.cuh"
+#include "ebem_kernels.h"
+
+namespace ebem_gpu {
+
+namespace {
+
+__device__ __forceinline__ double efr(const DevCtx* __restrict__ c, int f, int e) {
+  return __ldg(c->elem + size_t(f) * c->n_nodes + e);
+}
+
+// Plane wave with unit direction d: P (kind 0) u = A d e^{-i kL d.x};
+// SV (kind 1) u = A p e^{-i kT d.x} with p = (-d_y, d_x).
+__device__ __forceinline__ void wave_at(const DevMedium& m, int kind, double dx,
+                                        double dy, double amp, double x,
+                                        double y, double nx, double ny,
+                                        cplx& ux, cplx& uy, cplx& tx, cplx& ty) {
+  const double k = kind == 0 ? m.kL : m.kT;
+  double sn, cs;
+  sincos(-k * (dx * x + dy * y), &sn, &cs);
+  const cplx ph = mk(amp * cs, amp * sn);
+  const cplx f = mk(0.0, -k) * ph;  // -i k A e^{...}
+  const double nd = nx * dx + ny * dy;
+  if (kind == 0) {
+    ux = ph * dx;
+    uy = ph * dy;
+    tx = f * (m.lam * nx + 2.0 * m.mu * nd * dx);
+    ty = f * (m.lam * ny + 2.0 * m.mu * nd * dy);
+  } else {
+    const double px = -dy, py = dx;
+    const double np = nx * px + ny * py;
+    ux = ph * px;
+    uy = ph * py;
+    tx = f * (m.mu * (nd * px + np * dx));
+    ty = f * (m.mu * (nd * py + np * dy));
+  }
+}
+
+}  // namespace
+
+// out: 2N x m complex, column-major (component-major rows).
+__global__ void k_rhs_plane(const DevCtx* __restrict__ ctx, int kind,
+                            const double* __restrict__ angles, int m,
+                            double amp, int rhs_n, double* __restrict__ out) {
+  const int N = ctx->n_nodes;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)N * m) return;
+  const int col = int(t / N);
+  const int g = int(t - (long long)col * N);
+  const double ang = angles[col];
+  double dys, dxs;
+  sincos(ang, &dys, &dxs);
+  const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
+  const double* gx = ctx->gx + gauss_offset(rhs_n);
+  const double* gw = ctx->gw + gauss_offset(rhs_n);
+  // supporting elements of node g in ascending order, with local shape index
+  int es[2], as[2];
+  if (g == 0) {
+    es[0] = 0; as[0] = 0; es[1] = N - 1; as[1] = 1;
+  } else {
+    es[0] = g - 1; as[0] = 1; es[1] = g; as[1] = 0;
+  }
+  cplx b1 = mk(0.0), b2 = mk(0.0);
+  for (int q = 0; q < 2; ++q) {
+    const int e = es[q];
+    const double h = efr(ctx, EH, e);
+    const double px = efr(ctx, EPX, e), py = efr(ctx, EPY, e);
+    const double ddx = efr(ctx, EDX, e), ddy = efr(ctx, EDY, e);
+    const double nx = efr(ctx, ENX, e), ny = efr(ctx, ENY, e);
+    for (int k = 0; k < rhs_n; ++k) {
+      const double s = gx[k];
+      cplx ux, uy, tx, ty;
+      wave_at(ctx->med, kind, dxs, dys, amp, px + s * ddx, py + s * ddy, nx, ny,
+              ux, uy, tx, ty);
+      const cplx v1 = ux + alpha * tx;
+      const cplx v2 = uy + alpha * ty;
+      const double wh = gw[k] * h;
+      const double p = as[q] == 0 ? (1.0 - s) * wh : s * wh;
+      axpy(b1, p, v1);
+      axpy(b2, p, v2);
+    }
+  }
+  double2* o = reinterpret_cast<double2*>(out) + (long long)col * 2 * N;
+  o[g] = make_double2(b1.re, b1.im);
+  o[N + g] = make_double2(b2.re, b2.im);
+}
+
+__global__ void k_eval_hankel(const double* __restrict__ x, int n,
+                              double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  cplx h0, h1;
+  hankel01(x[t], h0, h1);
+  out[4 * t] = h0.re;
+  out[4 * t + 1] = h0.im;
+  out[4 * t + 2] = h1.re;
+  out[4 * t + 3] = h1.im;
+}
+
+__global__ void k_eval_scalars(const DevCtx* __restrict__ ctx,
+                               const double* __restrict__ r, int n, int which,
+                               double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  Scalars s;
+  if (which == 0) {
+    scalars_full(ctx, r[t], s);
+  } else if (which == 1) {
+    Scalars f;
+    scalars_split(ctx, r[t], f, s);
+  } else {
+    StaticScalars s0;
+    static_part(ctx->med, r[t], s0);
+    for (int k = 0; k < 10; ++k) s.s[k] = mk(s0.s[k]);
+  }
+  for (int k = 0; k < 10; ++k) {
+    out[20 * t + 2 * k] = s.s[k].re;
+    out[20 * t + 2 * k + 1] = s.s[k].im;
+  }
+}
+
+void launch_rhs_plane(const DevCtx* ctx, int n_nodes, int kind,
+                        const double* angles, int m, double amplitude,
+                        int rhs_n, double* out, cudaStream_t st) {
+  const long long total = (long long)n_nodes * m;
+  if (total <= 0) return;
+  const int bs = 128;
+  k_rhs_plane<<<(unsigned)((total + bs - 1) / bs), bs, 0, st>>>(
+      ctx, kind, angles, m, amplitude, rhs_n, out);
+}
+
+void launch_eval_hankel(const double* x, int n, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_eval_hankel<<<(n + 127) / 128, 128, 0, st>>>(x, n, out);
+}
+
+void launch_eval_scalars(const DevCtx* ctx, const double* r, int n, int which,
+                         double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_eval_scalars<<<(n + 127) / 128, 128, 0, st>>>(ctx, r, n, which, out);
+}
+
+}  // namespace ebem_gpu

@@ -1,0 +1,1315 @@
+// Native host runtime: planning and driving the batched sm_100a kernels.
+//
+// Reference behaviour mirrored here (the arithmetic itself runs on device):
+//   build_proxy                   proj/src/compression.cpp:25-69
+//   AssemblerSource::cell_basis   proj/src/compression.cpp:132-169
+//   basis_from_interactions       proj/src/compression.cpp:71-118
+//   BlockAssembler::true_block    proj/src/assembly.cpp:332-409 (element sets,
+//                                 scatter order)
+//   FdsSolver::build / solve      proj/src/fds.cpp:56-263
+#include "runtime.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
+
+#include "ebem_kernels.h"
+#include "host_setup.h"
+
+namespace ebem_gpu {
+
+std::atomic<long long> g_launches{0};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(EBEM_CUDA_ERROR, std::string("CUDA error in ") + what + ": " +
+                                     cudaGetErrorString(e));
+}
+
+void Pack::upload(DBuf<char>& dev, cudaStream_t st) {
+  if (buf_.empty()) return;
+  dev.ensure(buf_.size());
+  CK(cudaMemcpyAsync(dev.get(), buf_.data(), buf_.size(), cudaMemcpyHostToDevice, st));
+}
+
+namespace {
+
+double now() {
+  return std::chrono::duration<double>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+constexpr long long kMaxBundlesPerWave = 8ll << 20;  // 2 GiB of bundles
+
+}  // namespace
+
+// ------------------------------------------------------------ NodeBoxTree
+int NodeBoxTree::make(const double* xy, int lo, int hi) {
+  Box b{lo, hi, -1, -1, 0, 0, 0, 0};
+  if (hi - lo <= 16) {
+    b.x0 = b.y0 = std::numeric_limits<double>::infinity();
+    b.x1 = b.y1 = -std::numeric_limits<double>::infinity();
+    for (int g = lo; g < hi; ++g) {
+      b.x0 = std::min(b.x0, xy[2 * g]);
+      b.x1 = std::max(b.x1, xy[2 * g]);
+      b.y0 = std::min(b.y0, xy[2 * g + 1]);
+      b.y1 = std::max(b.y1, xy[2 * g + 1]);
+    }
+  } else {
+    const int mid = lo + (hi - lo) / 2;
+    b.left = make(xy, lo, mid);
+    b.right = make(xy, mid, hi);
+    const Box& L = boxes_[b.left];
+    const Box& R = boxes_[b.right];
+    b.x0 = std::min(L.x0, R.x0);
+    b.x1 = std::max(L.x1, R.x1);
+    b.y0 = std::min(L.y0, R.y0);
+    b.y1 = std::max(L.y1, R.y1);
+  }
+  boxes_.push_back(b);
+  return int(boxes_.size()) - 1;
+}
+
+void NodeBoxTree::build(const double* xy, int n) {
+  boxes_.clear();
+  boxes_.reserve(size_t(n / 8 + 4));
+  root_ = make(xy, 0, n);
+}
+
+void NodeBoxTree::enclosed(const double* xy, double cx, double cy,
+                           double radius, int begin, int end,
+                           std::vector<int>& out) const {
+  out.clear();
+  // explicit stack, left before right -> ascending node order
+  int stack[128];
+  int sp = 0;
+  stack[sp++] = root_;
+  const double slack = radius * (1.0 + 1e-9) + 1e-300;
+  while (sp) {
+    const Box& b = boxes_[stack[--sp]];
+    const double dx = std::max(std::max(b.x0 - cx, cx - b.x1), 0.0);
+    const double dy = std::max(std::max(b.y0 - cy, cy - b.y1), 0.0);
+    if (std::hypot(dx, dy) > slack) continue;
+    if (b.left < 0) {
+      for (int g = b.lo; g < b.hi; ++g) {
+        if (g >= begin && g < end) continue;
+        // exactly the reference predicate: (node - center).norm() < radius
+        if (std::hypot(xy[2 * g] - cx, xy[2 * g + 1] - cy) < radius)
+          out.push_back(g);
+      }
+    } else {
+      stack[sp++] = b.right;
+      stack[sp++] = b.left;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- Problem
+Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
+                 double omega, double are, double aim,
+                 const ebem_assembly_config& a, const ebem_proxy_config& p)
+    : n_(n), acfg_(a), pcfg_(p) {
+  if (n < 4) throw Error(EBEM_INVALID_ARGUMENT, "Mesh: needs at least 4 nodes");
+  if (n < 8) throw Error(EBEM_INVALID_ARGUMENT, "PairIntegrator: mesh too coarse");
+  xy_.assign(xy, xy + 2 * size_t(n));
+  elem_.resize(size_t(kElemFields) * n);
+  try {
+    build_elements(xy_.data(), n, elem_.data(), &hmin_, &hmax_);
+  } catch (const std::invalid_argument& e) {
+    throw Error(EBEM_INVALID_ARGUMENT, e.what());
+  }
+  DevMedium med;
+  try {
+    med = make_medium(lam, mu, rho, omega, are, aim);
+  } catch (const std::invalid_argument& e) {
+    throw Error(EBEM_INVALID_ARGUMENT, e.what());
+  }
+  auto scaled = [&](int q) { return int(q * a.refine + 0.5); };
+  hctx_.med = med;
+  hctx_.n_nodes = n;
+  try {
+    hctx_.series_maxq = build_series(med, hctx_.series, kMaxSeriesPow);
+  } catch (const std::logic_error& e) {
+    throw Error(EBEM_LOGIC_ERROR, e.what());
+  }
+  for (int q = 1; q <= kMaxGauss; ++q)
+    gauss_rule(q, hctx_.gx + gauss_offset(q), hctx_.gw + gauss_offset(q));
+  hctx_.far_nodes = a.far_nodes;
+  hctx_.refine = a.refine;
+  hctx_.corner_n = scaled(a.corner_nodes);
+  hctx_.proxy_n = p.n_gauss;
+  hctx_.m_prime = p.m_prime;
+  const int max_tier = scaled(a.far_nodes + 9);
+  if (hctx_.corner_n < 1 || hctx_.corner_n > kMaxGauss || max_tier > kMaxGauss ||
+      scaled(a.far_nodes) < 1 || scaled(a.rhs_nodes) < 1 ||
+      scaled(a.rhs_nodes) > kMaxGauss)
+    throw Error(EBEM_INVALID_ARGUMENT, "gauss_rule: order out of range");
+  if (p.n_gauss < 1 || p.n_gauss > kMaxGauss)
+    throw Error(EBEM_INVALID_ARGUMENT, "gauss_rule: order out of range");
+  if (p.radius_factor <= 1.0)
+    throw Error(EBEM_INVALID_ARGUMENT,
+                "build_proxy: radius_factor must exceed 1 so the circle "
+                "encloses the cell");
+  if (p.m_prime < 3)
+    throw Error(EBEM_INVALID_ARGUMENT, "build_proxy: polygon needs >= 3 nodes");
+  if (p.m_prime > 512)
+    throw Error(EBEM_INVALID_ARGUMENT, "build_proxy: m_prime above 512 unsupported");
+  for (int j = 0; j < p.m_prime; ++j) {
+    const double t = 2.0 * 3.14159265358979323846 * j / p.m_prime;
+    hctx_.poly_cs[2 * j] = std::cos(t);
+    hctx_.poly_cs[2 * j + 1] = std::sin(t);
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(EBEM_CUDA_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
+  CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  delem_.alloc(elem_.size());
+  dxy_.alloc(xy_.size());
+  CK(cudaMemcpyAsync(delem_.get(), elem_.data(), elem_.size() * 8, cudaMemcpyHostToDevice, st_));
+  CK(cudaMemcpyAsync(dxy_.get(), xy_.data(), xy_.size() * 8, cudaMemcpyHostToDevice, st_));
+  hctx_.elem = delem_.get();
+  hctx_.node_xy = dxy_.get();
+  dctx_.alloc(1);
+  CK(cudaMemcpyAsync(dctx_.get(), &hctx_, sizeof(DevCtx), cudaMemcpyHostToDevice, st_));
+  bad.alloc(1);
+  CK(cudaMemsetAsync(bad.get(), 0, sizeof(int), st_));
+  CK(cudaStreamSynchronize(st_));
+  dense_init();
+  tree_.build(xy_.data(), n);
+}
+
+Problem::~Problem() {
+  if (st_) {
+    cudaStreamSynchronize(st_);
+    cudaStreamDestroy(st_);
+  }
+}
+
+ProxyGeom Problem::build_proxy(int begin, int end) const {
+  const int n = n_;
+  if (begin < 0 || end > n || begin >= end)
+    throw Error(EBEM_INVALID_ARGUMENT, "build_proxy: bad node range");
+  double xmin = std::numeric_limits<double>::infinity(), xmax = -xmin;
+  double ymin = xmin, ymax = -xmin;
+  for (int g = begin - 1; g <= end; ++g) {
+    const int w = (g % n + n) % n;
+    xmin = std::min(xmin, xy_[2 * w]);
+    xmax = std::max(xmax, xy_[2 * w]);
+    ymin = std::min(ymin, xy_[2 * w + 1]);
+    ymax = std::max(ymax, xy_[2 * w + 1]);
+  }
+  ProxyGeom g;
+  g.cx = 0.5 * (xmin + xmax);
+  g.cy = 0.5 * (ymin + ymax);
+  const double half_diag = 0.5 * std::hypot(xmax - xmin, ymax - ymin);
+  g.radius = pcfg_.radius_factor * std::max(half_diag, 1e-300);
+  tree_.enclosed(xy_.data(), g.cx, g.cy, g.radius, begin, end, g.enclosed);
+  return g;
+}
+
+void Problem::check_domain() {
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+  if (h) {
+    CK(cudaMemsetAsync(bad.get(), 0, sizeof(int), st_));
+    throw Error(EBEM_DOMAIN_ERROR,
+                "KernelScalars: element too long for this frequency (needs "
+                "several elements per wavelength)");
+  }
+}
+
+// ---------------------------------------------------------------- FillPlan
+void FillPlan::clear() {
+  bundles_ = near_pairs_ = entries_ = 0;
+  proxy_blocks_ = 0;
+  poly_desc_off_ = -1;
+  elems_.clear();
+  near_.clear();
+  near_local_.clear();
+  sing_pair_.clear();
+  sing_elems_.clear();
+  proxy_.clear();
+  proxy_boff_.clear();
+  gather_.clear();
+  gather_off_.clear();
+  desc_.clear();
+}
+
+// Elements supporting the hat functions of the listed nodes (node g owns
+// elements g-1 and g), ascending and unique (proj/src/assembly.cpp:342-368).
+void FillPlan::elements_of(const Lists& nodes, std::vector<int>& out) const {
+  out.clear();
+  for (int p = 0; p < 2; ++p)
+    for (int g : nodes[p]) {
+      out.push_back(g);
+      out.push_back(g == 0 ? N_ - 1 : g - 1);
+    }
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+}
+
+void FillPlan::node_descs(const Lists& nodes, const std::vector<int>& elems,
+                          const int dest_off[2],
+                          std::vector<NodeDesc>& out) const {
+  auto idx = [&](int e) {
+    return int(std::lower_bound(elems.begin(), elems.end(), e) - elems.begin());
+  };
+  for (int p = 0; p < 2; ++p) {
+    for (size_t k = 0; k < nodes[p].size(); ++k) {
+      const int g = nodes[p][k];
+      NodeDesc d;
+      d.dest = dest_off[p] + int(k);
+      int la1, la2;
+      if (g == 0) {  // elements 0 (shape 0) and N-1 (shape 1)
+        d.e1 = idx(0);
+        d.e2 = idx(N_ - 1);
+        la1 = 0;
+        la2 = 1;
+      } else {  // elements g-1 (shape 1) and g (shape 0)
+        d.e1 = idx(g - 1);
+        d.e2 = idx(g);
+        la1 = 1;
+        la2 = 0;
+      }
+      d.bits = la1 | (la2 << 1) | (p << 2);
+      out.push_back(d);
+    }
+  }
+}
+
+void FillPlan::add_true_block(const Lists& rows, const Lists& cols,
+                              double* dest, int ld, const int drow[2],
+                              const int dcol[2], int trans) {
+  const int nr = int(rows[0].size() + rows[1].size());
+  const int nc = int(cols[0].size() + cols[1].size());
+  if (nr == 0 || nc == 0) return;
+  std::vector<int> res, ces;
+  elements_of(rows, res);
+  elements_of(cols, ces);
+  NearJob J;
+  J.pair_off = bundles_;
+  J.res_off = int(elems_.size());
+  J.nres = int(res.size());
+  elems_.insert(elems_.end(), res.begin(), res.end());
+  J.ces_off = int(elems_.size());
+  J.nces = int(ces.size());
+  elems_.insert(elems_.end(), ces.begin(), ces.end());
+  near_.push_back(J);
+  near_local_.push_back(near_pairs_);
+  const long long np = (long long)J.nres * J.nces;
+  near_pairs_ += np;
+  // touching pairs (coincident / adjacent) go to the singular kernel
+  for (int ra = 0; ra < J.nres; ++ra) {
+    const int ea = res[ra];
+    const int cand[3] = {ea == 0 ? N_ - 1 : ea - 1, ea, ea + 1 == N_ ? 0 : ea + 1};
+    for (int c : cand) {
+      auto it = std::lower_bound(ces.begin(), ces.end(), c);
+      if (it != ces.end() && *it == c) {
+        const int cb = int(it - ces.begin());
+        sing_pair_.push_back(J.pair_off + (long long)ra * J.nces + cb);
+        sing_elems_.push_back(ea);
+        sing_elems_.push_back(c);
+      }
+    }
+  }
+  GatherJob G;
+  G.pair_off = J.pair_off;
+  G.entry_off = entries_;
+  G.nces = J.nces;
+  G.rdesc_off = int(desc_.size());
+  node_descs(rows, res, drow, desc_);
+  G.nrows = nr;
+  G.cdesc_off = int(desc_.size());
+  node_descs(cols, ces, dcol, desc_);
+  G.ncols = nc;
+  G.trans = trans;
+  G.ld = ld;
+  G.dest = dest;
+  gather_.push_back(G);
+  gather_off_.push_back(entries_);
+  entries_ += (long long)nr * nc;
+  bundles_ += np;
+}
+
+// Descriptors of the 2 m' polygon hat functions (both components); the
+// polygon element list is 0..m'-1 itself.
+int FillPlan::poly_descs() {
+  if (poly_desc_off_ >= 0) return poly_desc_off_;
+  poly_desc_off_ = int(desc_.size());
+  for (int p = 0; p < 2; ++p)
+    for (int j = 0; j < m_; ++j) {
+      NodeDesc d;
+      d.dest = p * m_ + j;
+      int la1, la2;
+      if (j == 0) {
+        d.e1 = 0;
+        d.e2 = m_ - 1;
+        la1 = 0;
+        la2 = 1;
+      } else {
+        d.e1 = j - 1;
+        d.e2 = j;
+        la1 = 1;
+        la2 = 0;
+      }
+      d.bits = la1 | (la2 << 1) | (p << 2);
+      desc_.push_back(d);
+    }
+  return poly_desc_off_;
+}
+
+void FillPlan::add_proxy(double cx, double cy, double radius, const Lists& rows,
+                         const Lists& cols, double* tv, int ld_v, double* tu,
+                         int ld_u) {
+  Lists both;
+  both[0] = rows[0];
+  both[0].insert(both[0].end(), rows[1].begin(), rows[1].end());
+  both[1] = cols[0];
+  both[1].insert(both[1].end(), cols[1].begin(), cols[1].end());
+  std::vector<int> E;
+  elements_of(both, E);
+  ProxyJob J;
+  J.e_off = int(elems_.size());
+  J.nE = int(E.size());
+  elems_.insert(elems_.end(), E.begin(), E.end());
+  J.v_off = bundles_;
+  J.u_off = bundles_ + (long long)m_ * J.nE;
+  J.block_off = proxy_blocks_;
+  J.pad = 0;
+  J.cx = cx;
+  J.cy = cy;
+  J.radius = radius;
+  proxy_.push_back(J);
+  proxy_boff_.push_back(proxy_blocks_);
+  proxy_blocks_ += proxy_blocks_for(m_, J.nE, ng_);
+  bundles_ += 2ll * m_ * J.nE;
+  const int pd = poly_descs();
+  const int nr = int(rows[0].size() + rows[1].size());
+  const int nc = int(cols[0].size() + cols[1].size());
+  // T_V poly rows: M_V(poly (i, pj), col (j, c))
+  if (nc > 0) {
+    GatherJob G;
+    G.pair_off = J.v_off;
+    G.entry_off = entries_;
+    G.nces = J.nE;
+    G.rdesc_off = pd;
+    G.nrows = 2 * m_;
+    G.cdesc_off = int(desc_.size());
+    const int dcol[2] = {0, int(cols[0].size())};
+    node_descs(cols, E, dcol, desc_);
+    G.ncols = nc;
+    G.trans = 0;
+    G.ld = ld_v;
+    G.dest = tv;
+    gather_.push_back(G);
+    gather_off_.push_back(entries_);
+    entries_ += (long long)G.nrows * G.ncols;
+  }
+  // T_U poly rows: conj(M_U(row (i, r), poly (j, pj)))
+  if (nr > 0) {
+    GatherJob G;
+    G.pair_off = J.u_off;
+    G.entry_off = entries_;
+    G.nces = m_;
+    G.rdesc_off = int(desc_.size());
+    const int drow[2] = {0, int(rows[0].size())};
+    node_descs(rows, E, drow, desc_);
+    G.nrows = nr;
+    G.cdesc_off = pd;
+    G.ncols = 2 * m_;
+    G.trans = 1;
+    G.ld = ld_u;
+    G.dest = tu;
+    gather_.push_back(G);
+    gather_off_.push_back(entries_);
+    entries_ += (long long)G.nrows * G.ncols;
+  }
+}
+
+void Problem::execute(FillPlan& plan) {
+  if (plan.empty()) return;
+  Pack pk;
+  const size_t o_el = pk.add(plan.elems_);
+  const size_t o_nj = pk.add(plan.near_);
+  const size_t o_nl = pk.add(plan.near_local_);
+  const size_t o_sp = pk.add(plan.sing_pair_);
+  const size_t o_se = pk.add(plan.sing_elems_);
+  const size_t o_pj = pk.add(plan.proxy_);
+  const size_t o_pb = pk.add(plan.proxy_boff_);
+  const size_t o_gj = pk.add(plan.gather_);
+  const size_t o_go = pk.add(plan.gather_off_);
+  const size_t o_de = pk.add(plan.desc_);
+  pk.upload(plan_dev, st_);
+  bundles.ensure(size_t(plan.bundles_) * kBundle * 2);
+  const int* el = pk.at<int>(plan_dev, o_el);
+  if (!plan.proxy_.empty()) {
+    launch_proxy_pairs(dctx(), pcfg_.n_gauss, pk.at<ProxyJob>(plan_dev, o_pj),
+                       pk.at<int>(plan_dev, o_pb), int(plan.proxy_.size()),
+                       plan.proxy_blocks_, el, bundles.get(), st_);
+    ++g_launches;
+  }
+  if (plan.near_pairs_ > 0) {
+    launch_near_separated(dctx(), pk.at<NearJob>(plan_dev, o_nj),
+                          pk.at<long long>(plan_dev, o_nl), int(plan.near_.size()),
+                          el, plan.near_pairs_, bundles.get(), st_);
+    ++g_launches;
+  }
+  if (!plan.sing_pair_.empty()) {
+    launch_near_singular(dctx(), pk.at<long long>(plan_dev, o_sp),
+                         pk.at<int>(plan_dev, o_se), int(plan.sing_pair_.size()),
+                         bundles.get(), bad.get(), st_);
+    ++g_launches;
+  }
+  launch_gather(pk.at<GatherJob>(plan_dev, o_gj), pk.at<long long>(plan_dev, o_go),
+                int(plan.gather_.size()), pk.at<NodeDesc>(plan_dev, o_de),
+                plan.entries_, bundles.get(), st_);
+  ++g_launches;
+  CK(cudaGetLastError());
+  plan.clear();
+}
+
+void Problem::interaction(const std::vector<BasisReq>& req,
+                          std::vector<ProxyGeom>& geom,
+                          std::vector<size_t>& tv_off,
+                          std::vector<size_t>& tu_off, std::vector<int>& n_out,
+                          DBuf<double>& tbuf) {
+  const int m = pcfg_.m_prime;
+  const size_t nc_ = req.size();
+  geom.resize(nc_);
+  tv_off.resize(nc_);
+  tu_off.resize(nc_);
+  n_out.resize(nc_);
+  size_t run = 0;
+  for (size_t c = 0; c < nc_; ++c) {
+    geom[c] = build_proxy(req[c].begin, req[c].end);
+    n_out[c] = 2 * m + 2 * int(geom[c].enclosed.size());
+    const size_t ncol = (*req[c].cols)[0].size() + (*req[c].cols)[1].size();
+    const size_t nrow = (*req[c].rows)[0].size() + (*req[c].rows)[1].size();
+    tv_off[c] = run;
+    run += size_t(n_out[c]) * ncol;
+    tu_off[c] = run;
+    run += size_t(n_out[c]) * nrow;
+  }
+  tbuf.ensure(2 * run + 2);
+  FillPlan plan(n_, m, pcfg_.n_gauss);
+  double* base = tbuf.get();
+  for (size_t c = 0; c < nc_; ++c) {
+    const Lists& rows = *req[c].rows;
+    const Lists& cols = *req[c].cols;
+    double* tv = base + 2 * tv_off[c];
+    double* tu = base + 2 * tu_off[c];
+    const int no = n_out[c];
+    plan.add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv, no,
+                   tu, no);
+    if (!geom[c].enclosed.empty()) {
+      const Lists enc{geom[c].enclosed, geom[c].enclosed};
+      const int ne = int(geom[c].enclosed.size());
+      const int drow_v[2] = {2 * m, 2 * m + ne};
+      const int dcol_v[2] = {0, int(cols[0].size())};
+      plan.add_true_block(enc, cols, tv, no, drow_v, dcol_v, 0);
+      const int drow_u[2] = {0, int(rows[0].size())};
+      const int dcol_u[2] = {2 * m, 2 * m + ne};
+      plan.add_true_block(rows, enc, tu, no, drow_u, dcol_u, 1);
+    }
+    if (plan.bundles() > kMaxBundlesPerWave) execute(plan);
+  }
+  execute(plan);
+}
+
+void Problem::bases(const std::vector<BasisReq>& req, double eps,
+                    std::vector<BasisRes>& res, DBuf<double>& vbuf,
+                    DBuf<double>& ubuf, double* fill_seconds) {
+  const size_t ncell = req.size();
+  res.assign(ncell, BasisRes{});
+  if (ncell == 0) return;
+  std::vector<ProxyGeom> geom;
+  std::vector<size_t> tv_off, tu_off;
+  std::vector<int> n_out;
+  DBuf<double> tbuf;
+  const double t0 = now();
+  interaction(req, geom, tv_off, tu_off, n_out, tbuf);
+  if (fill_seconds) {
+    CK(cudaStreamSynchronize(st_));
+    *fill_seconds = now() - t0;
+  }
+  check_domain();
+
+  // ---- the four ID inputs per cell: column halves of T_V and T_U
+  struct QIn {
+    const double* p;
+    int rows, n, ld;
+  };
+  std::vector<QIn> q(4 * ncell);
+  for (size_t c = 0; c < ncell; ++c) {
+    const Lists& rows = *req[c].rows;
+    const Lists& cols = *req[c].cols;
+    const int nc0 = int(cols[0].size()), nc1 = int(cols[1].size());
+    const int nr0 = int(rows[0].size()), nr1 = int(rows[1].size());
+    if (nc0 == 0 || nc1 == 0 || nr0 == 0 || nr1 == 0)
+      throw Error(EBEM_INVALID_ARGUMENT, "Cpqr: empty matrix");
+    const int no = n_out[c];
+    const double* tv = tbuf.get() + 2 * tv_off[c];
+    const double* tu = tbuf.get() + 2 * tu_off[c];
+    q[4 * c + 0] = {tv, no, nc0, no};
+    q[4 * c + 1] = {tv + 2 * size_t(no) * nc0, no, nc1, no};
+    q[4 * c + 2] = {tu, no, nr0, no};
+    q[4 * c + 3] = {tu + 2 * size_t(no) * nr0, no, nr1, no};
+  }
+  // ---- TSQR rounds until each input fits one CTA's shared memory
+  std::vector<DBuf<double>> rounds;
+  for (;;) {
+    std::vector<QrTask> tasks;
+    std::vector<size_t> out_off(q.size(), 0);
+    size_t out_total = 0, ws_total = 0;
+    std::vector<int> pieces(q.size(), 0);
+    for (size_t i = 0; i < q.size(); ++i) {
+      const QIn& x = q[i];
+      const size_t bytes = size_t(x.rows) * x.n * 16;
+      if (bytes <= size_t(kSmemCap) || x.rows <= 2 * x.n) continue;
+      const int chunk = std::max(2 * x.n, int(kSmemCap / (16 * size_t(x.n))));
+      pieces[i] = (x.rows + chunk - 1) / chunk;
+      out_off[i] = out_total;
+      out_total += size_t(pieces[i]) * x.n * x.n;
+    }
+    if (out_total == 0) break;
+    rounds.emplace_back();
+    rounds.back().alloc(2 * out_total);
+    double* ob = rounds.back().get();
+    for (size_t i = 0; i < q.size(); ++i) {
+      if (!pieces[i]) continue;
+      const QIn& x = q[i];
+      const int chunk = (x.rows + pieces[i] - 1) / pieces[i];
+      const int ld_out = pieces[i] * x.n;
+      for (int pc = 0; pc < pieces[i]; ++pc) {
+        const int r0 = pc * chunk;
+        const int rr = std::min(chunk, x.rows - r0);
+        QrTask t{};
+        t.src = x.p + 2 * size_t(r0);
+        t.dst = ob + 2 * (out_off[i] + size_t(pc) * x.n);
+        t.rows = rr;
+        t.n = x.n;
+        t.ld = x.ld;
+        t.dst_ld = ld_out;
+        t.in_smem = size_t(rr) * x.n * 16 <= size_t(kSmemCap);
+        t.ws_off = (long long)ws_total;
+        if (!t.in_smem) ws_total += size_t(rr) * x.n;
+        tasks.push_back(t);
+      }
+    }
+    gws.ensure(ws_total + 1);
+    Pack pk;
+    const size_t o = pk.add(tasks);
+    pk.upload(task_dev, st_);
+    size_t smem = 0;
+    for (const QrTask& t : tasks)
+      if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
+    launch_qr_reduce(pk.at<QrTask>(task_dev, o), int(tasks.size()), smem,
+                     gws.get(), st_);
+    ++g_launches;
+    CK(cudaGetLastError());
+    for (size_t i = 0; i < q.size(); ++i) {
+      if (!pieces[i]) continue;
+      q[i].p = ob + 2 * out_off[i];
+      q[i].rows = pieces[i] * q[i].n;
+      q[i].ld = q[i].rows;
+    }
+    CK(cudaStreamSynchronize(st_));  // task_dev is reused next round
+  }
+  // ---- pivoted QR of every input
+  const size_t nq = q.size();
+  size_t jp_total = 0, r_total = 0, ws_total = 0;
+  std::vector<size_t> jp_off(nq), r_off(nq);
+  for (size_t i = 0; i < nq; ++i) {
+    jp_off[i] = jp_total;
+    jp_total += size_t(q[i].n) + 1;
+    r_off[i] = r_total;
+    r_total += size_t(q[i].n) * q[i].n;
+  }
+  DBuf<int> d_jp, d_steps;
+  DBuf<double> d_rd, d_r;
+  d_jp.alloc(jp_total);
+  d_steps.alloc(nq);
+  d_rd.alloc(jp_total);
+  d_r.alloc(2 * r_total);
+  std::vector<CpqrTask> ct(nq);
+  size_t smem = 0;
+  for (size_t i = 0; i < nq; ++i) {
+    if (q[i].n > kMaxCpqrCols)
+      throw Error(EBEM_INVALID_ARGUMENT, "Cpqr: more columns than supported");
+    CpqrTask& t = ct[i];
+    t.src = q[i].p;
+    t.rows = q[i].rows;
+    t.n = q[i].n;
+    t.ld = q[i].ld;
+    t.in_smem = size_t(t.rows) * t.n * 16 <= size_t(kSmemCap);
+    t.stop_rel = 1e-14;  // kPivotFloor, proj/src/compression.cpp:15
+    t.jpvt = d_jp.get() + jp_off[i];
+    t.rdiag = d_rd.get() + jp_off[i];
+    t.steps = d_steps.get() + i;
+    t.r_out = d_r.get() + 2 * r_off[i];
+    t.r_ld = t.n;
+    t.ws_off = (long long)ws_total;
+    if (!t.in_smem) ws_total += size_t(t.rows) * t.n;
+    else smem = std::max(smem, size_t(t.rows) * t.n * 16);
+  }
+  gws.ensure(ws_total + 1);
+  {
+    Pack pk;
+    const size_t o = pk.add(ct);
+    pk.upload(task_dev, st_);
+    launch_cpqr(pk.at<CpqrTask>(task_dev, o), int(nq), smem, gws.get(), st_);
+    ++g_launches;
+    CK(cudaGetLastError());
+  }
+  std::vector<int> h_jp(jp_total), h_steps(nq);
+  std::vector<double> h_rd(jp_total);
+  CK(cudaMemcpyAsync(h_jp.data(), d_jp.get(), jp_total * 4, cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(h_steps.data(), d_steps.get(), nq * 4, cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(h_rd.data(), d_rd.get(), jp_total * 8, cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+
+  // ---- shared rank (basis_from_interactions, compression.cpp:92-99)
+  size_t v_total = 0, u_total = 0;
+  for (size_t c = 0; c < ncell; ++c) {
+    int k = 0, cap = std::numeric_limits<int>::max();
+    for (int a = 0; a < 4; ++a) {
+      const size_t i = 4 * c + a;
+      const double* rd = h_rd.data() + jp_off[i];
+      const int steps = h_steps[i];
+      const int mn = std::min(q[i].rows, q[i].n);
+      // eps_rank(eps): first j with |R_jj| <= eps |R_00| (0 if R_00 == 0)
+      int er;
+      if (steps == 0 && mn > 0 && rd[0] == 0.0) {
+        er = 0;
+      } else {
+        er = std::min(steps, mn);
+        const int lim = std::min(steps + 1, mn);
+        for (int j = 0; j < lim; ++j)
+          if (rd[j] <= eps * rd[0]) { er = j; break; }
+      }
+      k = std::max(k, er);
+      cap = std::min(cap, steps);
+    }
+    k = std::min(k, cap);
+    const Lists& rows = *req[c].rows;
+    const Lists& cols = *req[c].cols;
+    BasisRes& r = res[c];
+    r.k = k;
+    r.saturated = k >= std::min(std::min(cols[0].size(), cols[1].size()),
+                                std::min(rows[0].size(), rows[1].size()));
+    for (int a = 0; a < 4; ++a) {
+      const int* jp = h_jp.data() + jp_off[4 * c + a];
+      const std::vector<int>& src = a == 0 ? cols[0] : a == 1 ? cols[1] : a == 2 ? rows[0] : rows[1];
+      std::vector<int>& dst = a == 0 ? r.scol[0] : a == 1 ? r.scol[1] : a == 2 ? r.srow[0] : r.srow[1];
+      dst.resize(k);
+      for (int j = 0; j < k; ++j) dst[j] = src[jp[j]];
+    }
+    r.v_off = v_total;
+    v_total += size_t(k) * (cols[0].size() + cols[1].size());
+    r.u_off = u_total;
+    u_total += size_t(k) * (rows[0].size() + rows[1].size());
+  }
+  // ---- interpolation coefficients
+  vbuf.ensure(2 * v_total + 2);
+  ubuf.ensure(2 * u_total + 2);
+  std::vector<InterpTask> it;
+  int max_k = 1;
+  for (size_t c = 0; c < ncell; ++c) {
+    const int k = res[c].k;
+    if (k == 0) continue;
+    max_k = std::max(max_k, k);
+    const Lists& rows = *req[c].rows;
+    const Lists& cols = *req[c].cols;
+    size_t vo = res[c].v_off, uo = res[c].u_off;
+    for (int a = 0; a < 4; ++a) {
+      const size_t i = 4 * c + a;
+      InterpTask t{};
+      t.r = d_r.get() + 2 * r_off[i];
+      t.jpvt = d_jp.get() + jp_off[i];
+      t.k = k;
+      t.n = q[i].n;
+      t.r_ld = q[i].n;
+      if (a < 2) {
+        t.out = vbuf.get() + 2 * vo;
+        t.out_ld = k;
+        t.adjoint = 0;
+        vo += size_t(k) * (a == 0 ? cols[0].size() : cols[1].size());
+      } else {
+        t.out = ubuf.get() + 2 * uo;
+        t.out_ld = t.n;
+        t.adjoint = 1;
+        uo += size_t(k) * (a == 2 ? rows[0].size() : rows[1].size());
+      }
+      it.push_back(t);
+    }
+  }
+  if (!it.empty()) {
+    Pack pk;
+    const size_t o = pk.add(it);
+    pk.upload(task_dev, st_);
+    launch_interp(pk.at<InterpTask>(task_dev, o), int(it.size()), max_k, st_);
+    ++g_launches;
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(st_));
+}
+
+void Problem::true_block_host(const Lists& rows, const Lists& cols, double* out) {
+  const int nr = int(rows[0].size() + rows[1].size());
+  const int nc = int(cols[0].size() + cols[1].size());
+  if (nr == 0 || nc == 0) return;
+  for (const auto& l : {rows[0], rows[1], cols[0], cols[1]})
+    for (int g : l)
+      if (g < 0 || g >= n_) throw Error(EBEM_INVALID_ARGUMENT, "true_block: node out of range");
+  DBuf<double> d;
+  d.alloc(2 * size_t(nr) * nc);
+  FillPlan plan(n_, pcfg_.m_prime, pcfg_.n_gauss);
+  const int drow[2] = {0, int(rows[0].size())};
+  const int dcol[2] = {0, int(cols[0].size())};
+  plan.add_true_block(rows, cols, d.get(), nr, drow, dcol, 0);
+  execute(plan);
+  check_domain();
+  CK(cudaMemcpyAsync(out, d.get(), 16 * size_t(nr) * nc, cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+}
+
+void Problem::rhs_plane(int kind, const double* angles, int m, double amp,
+                        double* out_host) {
+  if (m <= 0) return;
+  DBuf<double> da, dout;
+  da.alloc(m);
+  dout.alloc(4 * size_t(n_) * m);
+  CK(cudaMemcpyAsync(da.get(), angles, 8 * size_t(m), cudaMemcpyHostToDevice, st_));
+  const int rn = int(acfg_.rhs_nodes * acfg_.refine + 0.5);
+  launch_rhs_plane(dctx(), n_, kind, da.get(), m, amp, rn, dout.get(), st_);
+  ++g_launches;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_host, dout.get(), 32 * size_t(n_) * m, cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+}
+
+// ------------------------------------------------------------ batched LA
+namespace {
+template <class T, class F>
+void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
+                 void (*launch)(const T*, const int*, int, int, cudaStream_t)) {
+  if (t.empty()) return;
+  std::vector<int> boff(t.size());
+  int total = 0;
+  for (size_t i = 0; i < t.size(); ++i) {
+    boff[i] = total;
+    total += blocks_of(t[i]);
+  }
+  if (total == 0) return;
+  Pack pk;
+  const size_t o1 = pk.add(t);
+  const size_t o2 = pk.add(boff);
+  pk.upload(P.task_dev, P.stream());
+  launch(pk.at<T>(P.task_dev, o1), pk.at<int>(P.task_dev, o2), int(t.size()),
+         total, P.stream());
+  ++g_launches;
+  CK(cudaGetLastError());
+  // task_dev is reused by the next upload: keep the host from racing ahead
+  CK(cudaStreamSynchronize(P.stream()));
+}
+}  // namespace
+
+void run_copies(Problem& P, const std::vector<CopyTask>& t) {
+  run_blocked(P, t, [](const CopyTask& c) { return copy_blocks(c.rows, c.cols); },
+              launch_copy);
+}
+void run_gemms(Problem& P, const std::vector<GemmTask>& t) {
+  run_blocked(P, t, [](const GemmTask& g) { return g.k > 0 ? gemm_blocks(g.m, g.n) : 0; },
+              launch_gemm);
+}
+void run_getrs(Problem& P, const std::vector<LuSolveTask>& t) {
+  run_blocked(P, t, [](const LuSolveTask& s) { return s.n > 0 ? getrs_blocks(s.nrhs) : 0; },
+              launch_getrs);
+}
+std::vector<int> run_getrf(Problem& P, std::vector<LuTask> t) {
+  std::vector<int> info(t.size(), 0);
+  if (t.empty()) return info;
+  DBuf<int> dinfo;
+  dinfo.alloc(t.size());
+  size_t smem = 0, ws = 0;
+  for (size_t i = 0; i < t.size(); ++i) {
+    t[i].info = dinfo.get() + i;
+    const size_t bytes = size_t(t[i].n) * t[i].n * 16;
+    t[i].in_smem = bytes <= size_t(kSmemCap);
+    t[i].ws_off = (long long)ws;
+    if (t[i].in_smem) smem = std::max(smem, bytes);
+    else ws += size_t(t[i].n) * t[i].n;
+  }
+  P.gws.ensure(ws + 1);
+  Pack pk;
+  const size_t o = pk.add(t);
+  pk.upload(P.task_dev, P.stream());
+  launch_getrf(pk.at<LuTask>(P.task_dev, o), int(t.size()), smem, P.gws.get(), P.stream());
+  ++g_launches;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(info.data(), dinfo.get(), 4 * t.size(), cudaMemcpyDeviceToHost, P.stream()));
+  CK(cudaStreamSynchronize(P.stream()));
+  return info;
+}
+
+namespace {
+CopyTask copy_task(const double* src, int src_ld, double* dst, int dst_ld,
+                   int rows, int cols) {
+  CopyTask c{};
+  c.src = src;
+  c.dst = dst;
+  c.rows = rows;
+  c.cols = cols;
+  c.src_ld = src_ld;
+  c.dst_ld = dst_ld;
+  return c;
+}
+GemmTask gemm_task(const double* a, int lda, const double* b, int ldb, double* c,
+                   int ldc, int m, int n, int k, double beta) {
+  GemmTask g{};
+  g.a = a;
+  g.b = b;
+  g.c = c;
+  g.m = m;
+  g.n = n;
+  g.k = k;
+  g.lda = lda;
+  g.ldb = ldb;
+  g.ldc = ldc;
+  g.alpha_re = 1.0;
+  g.beta_re = beta;
+  return g;
+}
+void singular_error(int info, int n) {
+  throw Error(EBEM_RUNTIME_ERROR,
+              "LuFactor: matrix is singular, zero pivot at index " +
+                  std::to_string(info - 1) + " of " + std::to_string(n));
+}
+}  // namespace
+
+// -------------------------------------------------------------------- Fds
+Fds::Fds(Problem& p, int depth, const ebem_fds_config& cfg)
+    : P_(p), depth_(depth), cfg_(cfg) {
+  const int n = P_.n();
+  if (depth < 0) throw Error(EBEM_INVALID_ARGUMENT, "ClusterTree: negative depth");
+  if (depth >= EBEM_MAX_LEVELS - 1)
+    throw Error(EBEM_INVALID_ARGUMENT, "ClusterTree: depth too large");
+  const int leaves = 1 << depth;
+  if (n <= 0 || n % leaves != 0)
+    throw Error(EBEM_INVALID_ARGUMENT,
+                "ClusterTree: node count must be divisible by 2^depth (got " +
+                    std::to_string(n) + " nodes, depth " + std::to_string(depth) + ")");
+  if (cfg_.ell0 < 0 || cfg_.ell0 >= depth)
+    throw Error(EBEM_INVALID_ARGUMENT,
+                "FdsSolver: dense level must lie strictly above the leaves (got " +
+                    std::to_string(cfg_.ell0) + " with depth " + std::to_string(depth) + ")");
+  if (!(cfg_.epsilon > 0.0))
+    throw Error(EBEM_INVALID_ARGUMENT, "Cpqr: truncation epsilon must be positive");
+  build();
+}
+
+void Fds::reduced_diagonal(FillPlan& plan, std::vector<CopyTask>& copies,
+                           int cell, double* dest, int ld, int off) {
+  // proj/src/fds.cpp:33-54
+  const Cell& c1 = cells_[2 * cell + 1];
+  const Cell& c2 = cells_[2 * cell + 2];
+  const int k1 = c1.k, k2 = c2.k, np = k1 + k2;
+  for (int p = 0; p < 2; ++p)
+    for (int q = 0; q < 2; ++q) {
+      if (k1 > 0)
+        copies.push_back(copy_task(c1.atilde + 2 * (size_t(q) * k1 * 2 * k1 + size_t(p) * k1),
+                                   2 * k1,
+                                   dest + 2 * (size_t(off + q * np) * ld + off + p * np),
+                                   ld, k1, k1));
+      if (k2 > 0)
+        copies.push_back(copy_task(c2.atilde + 2 * (size_t(q) * k2 * 2 * k2 + size_t(p) * k2),
+                                   2 * k2,
+                                   dest + 2 * (size_t(off + q * np + k1) * ld + off + p * np + k1),
+                                   ld, k2, k2));
+    }
+  double* base = dest + 2 * (size_t(off) * ld + off);
+  const int drow12[2] = {0, np}, dcol12[2] = {k1, np + k1};
+  plan.add_true_block(c1.srow, c2.scol, base, ld, drow12, dcol12, 0);
+  const int drow21[2] = {k1, np + k1}, dcol21[2] = {0, np};
+  plan.add_true_block(c2.srow, c1.scol, base, ld, drow21, dcol21, 0);
+}
+
+void Fds::build() {
+  const double t_start = now();
+  const int n = P_.n();
+  const int ncells = (2 << depth_) - 1;
+  cells_.assign(ncells, Cell{});
+  store_.resize(depth_ + 1);
+  stats_ = ebem_fds_stats{};
+  stats_.depth = depth_;
+  const int leaf = n >> depth_;
+  for (int l = 0; l <= depth_; ++l)
+    for (int c = first(l); c <= last(l); ++c) {
+      cells_[c].begin = (c - first(l)) * (n >> l);
+      cells_[c].end = cells_[c].begin + (n >> l);
+    }
+  for (int c = first(depth_); c <= last(depth_); ++c) {
+    Cell& C = cells_[c];
+    std::vector<int> r(leaf);
+    for (int i = 0; i < leaf; ++i) r[i] = C.begin + i;
+    C.jrow = {r, r};
+    C.jcol = {r, r};
+    C.nloc = leaf;
+  }
+  double basis_seconds = 0.0;
+  const int m = P_.proxy_cfg().m_prime;
+  (void)m;
+  for (int level = depth_; level > cfg_.ell0; --level) {
+    const int f = first(level), L = last(level);
+    const int nlev = L - f + 1;
+    Store& S = store_[level];
+    // ---- bases of every cell of the level
+    std::vector<BasisReq> req(nlev);
+    for (int c = f; c <= L; ++c)
+      req[c - f] = BasisReq{&cells_[c].jrow, &cells_[c].jcol, cells_[c].begin, cells_[c].end};
+    std::vector<BasisRes> br;
+    DBuf<double> ubuf;
+    const double tb = now();
+    P_.bases(req, cfg_.epsilon, br, S.v, ubuf);
+    basis_seconds += now() - tb;
+    // ---- diagonal blocks (leaf: exact; above: reduced) into the LU arena
+    size_t lu_total = 0, piv_total = 0, au_total = 0, at_total = 0;
+    std::vector<size_t> lu_off(nlev), piv_off(nlev), au_off(nlev), at_off(nlev);
+    for (int i = 0; i < nlev; ++i) {
+      Cell& C = cells_[f + i];
+      C.k = br[i].k;
+      C.srow = br[i].srow;
+      C.scol = br[i].scol;
+      lu_off[i] = lu_total;
+      lu_total += size_t(2 * C.nloc) * (2 * C.nloc);
+      piv_off[i] = piv_total;
+      piv_total += 2 * C.nloc;
+      au_off[i] = au_total;
+      au_total += size_t(2 * C.nloc) * (2 * C.k);
+      at_off[i] = at_total;
+      at_total += size_t(2 * C.k) * (2 * C.k);
+      stats_.max_rank[level] = std::max(stats_.max_rank[level], C.k);
+      stats_.saturated = stats_.saturated || br[i].saturated;
+    }
+    S.lu.alloc(2 * lu_total + 2);
+    S.ipiv.alloc(piv_total + 1);
+    S.ainv_u.alloc(2 * au_total + 2);
+    S.atilde.alloc(2 * at_total + 2);
+    for (int i = 0; i < nlev; ++i) {
+      Cell& C = cells_[f + i];
+      C.lu = S.lu.get() + 2 * lu_off[i];
+      C.ipiv = S.ipiv.get() + piv_off[i];
+      C.ainv_u = S.ainv_u.get() + 2 * au_off[i];
+      C.atilde = S.atilde.get() + 2 * at_off[i];
+      C.v = S.v.get() + 2 * br[i].v_off;
+    }
+    {
+      FillPlan plan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
+      std::vector<CopyTask> copies;
+      for (int i = 0; i < nlev; ++i) {
+        Cell& C = cells_[f + i];
+        const int d = 2 * C.nloc;
+        if (level == depth_) {
+          const int drow[2] = {0, C.nloc}, dcol[2] = {0, C.nloc};
+          plan.add_true_block(C.jrow, C.jcol, C.lu, d, drow, dcol, 0);
+        } else {
+          reduced_diagonal(plan, copies, f + i, C.lu, d, 0);
+        }
+        if (plan.bundles() > kMaxBundlesPerWave) P_.execute(plan);
+      }
+      P_.execute(plan);
+      run_copies(P_, copies);
+      P_.check_domain();
+    }
+    // ---- LU of the diagonal blocks
+    {
+      std::vector<LuTask> lt;
+      for (int i = 0; i < nlev; ++i) {
+        Cell& C = cells_[f + i];
+        LuTask t{};
+        t.a = C.lu;
+        t.ipiv = C.ipiv;
+        t.n = 2 * C.nloc;
+        t.ld = 2 * C.nloc;
+        lt.push_back(t);
+      }
+      const std::vector<int> info = run_getrf(P_, lt);
+      for (int i = 0; i < nlev; ++i)
+        if (info[i]) singular_error(info[i], 2 * cells_[f + i].nloc);
+    }
+    // ---- A^-1 U with U = blockdiag(u0, u1)
+    {
+      std::vector<CopyTask> ct;
+      std::vector<LuSolveTask> st;
+      for (int i = 0; i < nlev; ++i) {
+        Cell& C = cells_[f + i];
+        const int nl = C.nloc, k = C.k;
+        if (k == 0) continue;
+        const int d = 2 * nl;
+        ct.push_back(copy_task(nullptr, 0, C.ainv_u, d, d, 2 * k));  // zero
+        const double* u = ubuf.get() + 2 * br[i].u_off;
+        ct.push_back(copy_task(u, nl, C.ainv_u, d, nl, k));
+        ct.push_back(copy_task(u + 2 * size_t(nl) * k, nl,
+                               C.ainv_u + 2 * (size_t(k) * d + nl), d, nl, k));
+        st.push_back(LuSolveTask{C.lu, C.ipiv, C.ainv_u, d, d, 2 * k, d});
+      }
+      run_copies(P_, ct);
+      run_getrs(P_, st);
+    }
+    // ---- W = [v0 A^-1U_top ; v1 A^-1U_bottom], atilde = W^-1
+    {
+      DBuf<double> wbuf;
+      DBuf<int> wpiv;
+      wbuf.alloc(2 * at_total + 2);
+      wpiv.alloc(2 * at_total / 1 + 1);
+      std::vector<GemmTask> gt;
+      std::vector<LuTask> lt;
+      std::vector<CopyTask> ct;
+      std::vector<LuSolveTask> st;
+      size_t poff = 0;
+      for (int i = 0; i < nlev; ++i) {
+        Cell& C = cells_[f + i];
+        const int nl = C.nloc, k = C.k;
+        if (k == 0) continue;
+        const int d = 2 * nl, kk = 2 * k;
+        double* w = wbuf.get() + 2 * at_off[i];
+        gt.push_back(gemm_task(C.v, k, C.ainv_u, d, w, kk, k, kk, nl, 0.0));
+        gt.push_back(gemm_task(C.v + 2 * size_t(k) * nl, k, C.ainv_u + 2 * size_t(nl), d,
+                               w + 2 * size_t(k), kk, k, kk, nl, 0.0));
+        LuTask t{};
+        t.a = w;
+        t.ipiv = wpiv.get() + poff;
+        t.n = kk;
+        t.ld = kk;
+        lt.push_back(t);
+        CopyTask id = copy_task(nullptr, 0, C.atilde, kk, kk, kk);
+        id.transpose = 2;  // identity
+        ct.push_back(id);
+        st.push_back(LuSolveTask{w, wpiv.get() + poff, C.atilde, kk, kk, kk, kk});
+        poff += kk;
+      }
+      run_gemms(P_, gt);
+      const std::vector<int> info = run_getrf(P_, lt);
+      for (size_t i = 0; i < info.size(); ++i)
+        if (info[i]) singular_error(info[i], lt[i].n);
+      run_copies(P_, ct);
+      run_getrs(P_, st);
+    }
+    // ---- parent sequences: concatenated child skeletons per component
+    for (int c = first(level - 1); c <= last(level - 1); ++c) {
+      Cell& Pc = cells_[c];
+      const Cell& c1 = cells_[2 * c + 1];
+      const Cell& c2 = cells_[2 * c + 2];
+      for (int comp = 0; comp < 2; ++comp) {
+        Pc.jrow[comp] = c1.srow[comp];
+        Pc.jrow[comp].insert(Pc.jrow[comp].end(), c2.srow[comp].begin(), c2.srow[comp].end());
+        Pc.jcol[comp] = c1.scol[comp];
+        Pc.jcol[comp].insert(Pc.jcol[comp].end(), c2.scol[comp].begin(), c2.scol[comp].end());
+      }
+      Pc.nloc = c1.k + c2.k;
+    }
+  }
+  CK(cudaStreamSynchronize(P_.stream()));
+  stats_.upward_seconds = now() - t_start;
+  stats_.basis_cpu_seconds = basis_seconds;
+
+  // ---- dense system over the cells of level ell0 (proj/src/fds.cpp:131-152)
+  const double t_top = now();
+  const int tf = first(cfg_.ell0), tl = last(cfg_.ell0);
+  top_off_.assign(tl - tf + 2, 0);
+  for (int i = 0; i <= tl - tf; ++i) top_off_[i + 1] = top_off_[i] + 2 * cells_[tf + i].nloc;
+  top_dim_ = top_off_.back();
+  stats_.top_dim = top_dim_;
+  top_lu_.alloc(2 * size_t(top_dim_) * top_dim_ + 2);
+  top_ipiv_.alloc(top_dim_ + 1);
+  {
+    FillPlan plan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
+    std::vector<CopyTask> copies;
+    for (int i = 0; i <= tl - tf; ++i) {
+      const Cell& ci = cells_[tf + i];
+      for (int j = 0; j <= tl - tf; ++j) {
+        const Cell& cj = cells_[tf + j];
+        if (i == j) {
+          reduced_diagonal(plan, copies, tf + i, top_lu_.get(), top_dim_, top_off_[i]);
+        } else {
+          const int drow[2] = {top_off_[i], top_off_[i] + ci.nloc};
+          const int dcol[2] = {top_off_[j], top_off_[j] + cj.nloc};
+          plan.add_true_block(ci.jrow, cj.jcol, top_lu_.get(), top_dim_, drow, dcol, 0);
+        }
+      }
+    }
+    P_.execute(plan);
+    run_copies(P_, copies);
+    P_.check_domain();
+    if (top_dim_ > 0) {
+      LuTask t{};
+      t.a = top_lu_.get();
+      t.ipiv = top_ipiv_.get();
+      t.n = top_dim_;
+      t.ld = top_dim_;
+      const std::vector<int> info = run_getrf(P_, {t});
+      if (info[0]) singular_error(info[0], top_dim_);
+    }
+  }
+  CK(cudaStreamSynchronize(P_.stream()));
+  stats_.top_factor_seconds = now() - t_top;
+}
+
+int Fds::rank_of(int cell) const {
+  if (cell < 0 || cell >= int(cells_.size())) return -1;
+  return cells_[cell].k;
+}
+
+void Fds::cell_info(int cell, int* sizes, int* skel) const {
+  if (cell < 0 || cell >= int(cells_.size()))
+    throw Error(EBEM_INVALID_ARGUMENT, "FdsSolver: cell out of range");
+  const Cell& C = cells_[cell];
+  sizes[0] = int(C.jrow[0].size());
+  sizes[1] = int(C.jrow[1].size());
+  sizes[2] = int(C.jcol[0].size());
+  sizes[3] = int(C.jcol[1].size());
+  sizes[4] = C.k;
+  if (skel) {
+    const int k = C.k;
+    for (int i = 0; i < k && i < int(C.srow[0].size()); ++i) {
+      skel[i] = C.srow[0][i];
+      skel[k + i] = C.srow[1][i];
+      skel[2 * k + i] = C.scol[0][i];
+      skel[3 * k + i] = C.scol[1][i];
+    }
+  }
+}
+
+void Fds::solve_device(const double* rhs, int m, double* x,
+                       ebem_fds_solve_timing* timing) {
+  const int n = P_.n();
+  const int ncells = int(cells_.size());
+  const int leaf = n >> depth_;
+  // per-cell row offsets of the f/x (2 nloc) and ftilde/t (2k) blocks
+  std::vector<size_t> fo(ncells, 0), ko(ncells, 0);
+  size_t ftot = 0, ktot = 0;
+  for (int c = 0; c < ncells; ++c) {
+    fo[c] = ftot;
+    ftot += 2 * size_t(cells_[c].nloc);
+    ko[c] = ktot;
+    ktot += 2 * size_t(cells_[c].k);
+  }
+  ws_f_.ensure(2 * ftot * m + 2);
+  ws_ft_.ensure(2 * ktot * m + 2);
+  ws_t_.ensure(2 * ktot * m + 2);
+  ws_x_.ensure(2 * size_t(top_dim_) * m + 2);
+  auto F = [&](int c) { return ws_f_.get() + 2 * fo[c] * m; };
+  auto FT = [&](int c) { return ws_ft_.get() + 2 * ko[c] * m; };
+  auto TT = [&](int c) { return ws_t_.get() + 2 * ko[c] * m; };
+  const double t0 = now();
+  // leaves: f = [rhs[a:a+s]; rhs[N+a:N+a+s]]
+  {
+    std::vector<CopyTask> ct;
+    for (int c = first(depth_); c <= last(depth_); ++c) {
+      const int a = cells_[c].begin;
+      ct.push_back(copy_task(rhs + 2 * size_t(a), 2 * n, F(c), 2 * leaf, leaf, m));
+      ct.push_back(copy_task(rhs + 2 * size_t(n + a), 2 * n, F(c) + 2 * size_t(leaf), 2 * leaf, leaf, m));
+    }
+    run_copies(P_, ct);
+  }
+  for (int level = depth_; level > cfg_.ell0; --level) {
+    std::vector<LuSolveTask> st;
+    std::vector<GemmTask> g1, g2;
+    for (int c = first(level); c <= last(level); ++c) {
+      const Cell& C = cells_[c];
+      const int nl = C.nloc, d = 2 * nl, k = C.k, kk = 2 * k;
+      st.push_back(LuSolveTask{C.lu, C.ipiv, F(c), d, d, m, d});  // ainvf in place
+      if (k == 0) continue;
+      g1.push_back(gemm_task(C.v, k, F(c), d, TT(c), kk, k, m, nl, 0.0));
+      g1.push_back(gemm_task(C.v + 2 * size_t(k) * nl, k, F(c) + 2 * size_t(nl), d,
+                             TT(c) + 2 * size_t(k), kk, k, m, nl, 0.0));
+      g2.push_back(gemm_task(C.atilde, kk, TT(c), kk, FT(c), kk, kk, m, kk, 0.0));
+    }
+    run_getrs(P_, st);
+    run_gemms(P_, g1);
+    run_gemms(P_, g2);
+    // parent f = [ft1 top; ft2 top; ft1 bottom; ft2 bottom]
+    std::vector<CopyTask> ct;
+    for (int c = first(level - 1); c <= last(level - 1); ++c) {
+      const int c1 = 2 * c + 1, c2 = 2 * c + 2;
+      const int k1 = cells_[c1].k, k2 = cells_[c2].k, np = k1 + k2;
+      const int ld = 2 * np;
+      if (ld == 0) continue;
+      if (k1) {
+        ct.push_back(copy_task(FT(c1), 2 * k1, F(c), ld, k1, m));
+        ct.push_back(copy_task(FT(c1) + 2 * size_t(k1), 2 * k1, F(c) + 2 * size_t(np), ld, k1, m));
+      }
+      if (k2) {
+        ct.push_back(copy_task(FT(c2), 2 * k2, F(c) + 2 * size_t(k1), ld, k2, m));
+        ct.push_back(copy_task(FT(c2) + 2 * size_t(k2), 2 * k2, F(c) + 2 * size_t(np + k1), ld, k2, m));
+      }
+    }
+    run_copies(P_, ct);
+  }
+  CK(cudaStreamSynchronize(P_.stream()));
+  const double t1 = now();
+  // top: stack, solve, unstack (x of the top cells lives in their f blocks)
+  {
+    const int tf = first(cfg_.ell0), tl = last(cfg_.ell0);
+    std::vector<CopyTask> ct, back;
+    for (int i = 0; i <= tl - tf; ++i) {
+      const int c = tf + i;
+      const int d = 2 * cells_[c].nloc;
+      if (d == 0) continue;
+      ct.push_back(copy_task(F(c), d, ws_x_.get() + 2 * size_t(top_off_[i]), top_dim_, d, m));
+      back.push_back(copy_task(ws_x_.get() + 2 * size_t(top_off_[i]), top_dim_, F(c), d, d, m));
+    }
+    run_copies(P_, ct);
+    if (top_dim_ > 0)
+      run_getrs(P_, {LuSolveTask{top_lu_.get(), top_ipiv_.get(), ws_x_.get(), top_dim_,
+                                 top_dim_, m, top_dim_}});
+    run_copies(P_, back);
+  }
+  CK(cudaStreamSynchronize(P_.stream()));
+  const double t2 = now();
+  // downward: x_child = ainvf + ainv_u (atilde y - ftilde)
+  for (int level = cfg_.ell0; level < depth_; ++level) {
+    std::vector<CopyTask> ct;
+    std::vector<GemmTask> g1, g2;
+    for (int c = first(level); c <= last(level); ++c) {
+      const int c1 = 2 * c + 1, c2 = 2 * c + 2;
+      const int k1 = cells_[c1].k, k2 = cells_[c2].k, np = k1 + k2;
+      for (int side = 0; side < 2; ++side) {
+        const int cc = side == 0 ? c1 : c2;
+        const Cell& C = cells_[cc];
+        const int k = C.k, kk = 2 * k, d = 2 * C.nloc;
+        if (k == 0) continue;
+        const int row0 = side == 0 ? 0 : k1;
+        ct.push_back(copy_task(F(c) + 2 * size_t(row0), 2 * np, TT(cc), kk, k, m));
+        ct.push_back(copy_task(F(c) + 2 * size_t(np + row0), 2 * np, TT(cc) + 2 * size_t(k), kk, k, m));
+        GemmTask a = gemm_task(C.atilde, kk, TT(cc), kk, FT(cc), kk, kk, m, kk, -1.0);
+        g1.push_back(a);
+        g2.push_back(gemm_task(C.ainv_u, d, FT(cc), kk, F(cc), d, d, m, kk, 1.0));
+      }
+    }
+    run_copies(P_, ct);
+    run_gemms(P_, g1);
+    run_gemms(P_, g2);
+  }
+  {
+    std::vector<CopyTask> ct;
+    for (int c = first(depth_); c <= last(depth_); ++c) {
+      const int a = cells_[c].begin;
+      ct.push_back(copy_task(F(c), 2 * leaf, x + 2 * size_t(a), 2 * n, leaf, m));
+      ct.push_back(copy_task(F(c) + 2 * size_t(leaf), 2 * leaf, x + 2 * size_t(n + a), 2 * n, leaf, m));
+    }
+    run_copies(P_, ct);
+  }
+  CK(cudaStreamSynchronize(P_.stream()));
+  const double t3 = now();
+  if (timing) {
+    timing->upward_seconds = t1 - t0;
+    timing->top_seconds = t2 - t1;
+    timing->downward_seconds = t3 - t2;
+  }
+}
+
+}  // namespace ebem_gpu

@@ -1,0 +1,286 @@
+// Native host runtime of the B200 solver path: device buffers, the per-level
+// work planner, the batched basis / merge / sweep drivers.  The C ABI
+// (capi.cpp) is a thin shell over the classes declared here.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <atomic>
+#include <cstddef>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ebem_ctx.h"
+#include "ebem_dense.h"
+#include "ebem_gpu.h"
+#include "ebem_jobs.h"
+
+namespace ebem_gpu {
+
+using Lists = std::array<std::vector<int>, 2>;
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+void cuda_check(cudaError_t e, const char* what);
+#define CK(x) ::ebem_gpu::cuda_check((x), #x)
+
+extern std::atomic<long long> g_launches;
+
+// ----------------------------------------------------------------- buffers
+template <class T>
+class DBuf {
+ public:
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t n) {
+    release();
+    if (n == 0) return;
+    CK(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    n_ = n;
+  }
+  // grow-only
+  void ensure(size_t n) {
+    if (n <= n_) return;
+    alloc(n + n / 4);
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+// Packs host arrays into one device upload (16-byte aligned segments).
+class Pack {
+ public:
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    return add_raw(v.data(), v.size() * sizeof(T));
+  }
+  size_t add_raw(const void* p, size_t bytes) {
+    const size_t off = (buf_.size() + 15) & ~size_t(15);
+    buf_.resize(off + bytes);
+    if (bytes) std::memcpy(buf_.data() + off, p, bytes);
+    return off;
+  }
+  void upload(DBuf<char>& dev, cudaStream_t st);
+  template <class T>
+  T* at(const DBuf<char>& dev, size_t off) const {
+    return reinterpret_cast<T*>(dev.get() + off);
+  }
+  size_t bytes() const { return buf_.size(); }
+
+ private:
+  std::vector<char> buf_;
+};
+
+// ------------------------------------------------------------ segment tree
+// Bounding boxes over node index ranges, for the enclosed-node search of
+// build_proxy (proj/src/compression.cpp:62-66): same predicate, node order
+// and result, visiting only boxes that can intersect the circle.
+class NodeBoxTree {
+ public:
+  void build(const double* xy, int n);
+  void enclosed(const double* xy, double cx, double cy, double radius,
+                int begin, int end, std::vector<int>& out) const;
+
+ private:
+  struct Box { int lo, hi, left, right; double x0, y0, x1, y1; };
+  int make(const double* xy, int lo, int hi);
+  std::vector<Box> boxes_;
+  int root_ = -1;
+};
+
+// ------------------------------------------------------------------ problem
+struct ProxyGeom {
+  double cx, cy, radius;
+  std::vector<int> enclosed;
+};
+
+struct BasisReq {  // one cell_basis call
+  const Lists* rows;
+  const Lists* cols;
+  int begin, end;
+};
+
+struct BasisRes {
+  int k = 0;
+  bool saturated = false;
+  Lists srow, scol;
+  size_t v_off = 0;  // V0 (k x nc0) then V1 (k x nc1) in the V buffer
+  size_t u_off = 0;  // U0 (nr0 x k) then U1 (nr1 x k) in the U buffer
+};
+
+class FillPlan;
+
+class Problem {
+ public:
+  Problem(const double* xy, int n, double lam, double mu, double rho,
+          double omega, double are, double aim, const ebem_assembly_config& a,
+          const ebem_proxy_config& p);
+  ~Problem();
+
+  int n() const { return n_; }
+  cudaStream_t stream() const { return st_; }
+  const ebem_proxy_config& proxy_cfg() const { return pcfg_; }
+  const ebem_assembly_config& asm_cfg() const { return acfg_; }
+  const DevCtx* dctx() const { return dctx_.get(); }
+  const double* xy() const { return xy_.data(); }
+
+  ProxyGeom build_proxy(int begin, int end) const;
+  // Runs a fill plan (bundles + gathers) on the stream.
+  void execute(FillPlan& plan);
+  // Raises std::domain_error semantics when a singular-pair series check
+  // failed since the last call.
+  void check_domain();
+  // Shared-rank bases of a batch of cells (AssemblerSource::cell_basis).
+  // V/U coefficient blocks land in vbuf/ubuf (device), offsets in res.
+  void bases(const std::vector<BasisReq>& req, double eps,
+             std::vector<BasisRes>& res, DBuf<double>& vbuf,
+             DBuf<double>& ubuf, double* fill_seconds = nullptr);
+  // Interaction matrices (device, column-major) of a batch of cells:
+  // T_V = M_V (n_out x ncols) and T_U = M_U^H (n_out x nrows).
+  void interaction(const std::vector<BasisReq>& req,
+                   std::vector<ProxyGeom>& geom, std::vector<size_t>& tv_off,
+                   std::vector<size_t>& tu_off, std::vector<int>& n_out,
+                   DBuf<double>& tbuf);
+  void true_block_host(const Lists& rows, const Lists& cols, double* out);
+  void rhs_plane(int kind, const double* angles, int m, double amp,
+                 double* out_host);
+
+  // scratch shared by the drivers
+  DBuf<char> plan_dev;
+  DBuf<double> bundles;
+  DBuf<double2> gws;
+  DBuf<char> task_dev;
+  DBuf<int> bad;
+
+ private:
+  int n_;
+  std::vector<double> xy_, elem_;
+  double hmin_ = 0, hmax_ = 0;
+  ebem_assembly_config acfg_;
+  ebem_proxy_config pcfg_;
+  DevCtx hctx_{};
+  DBuf<DevCtx> dctx_;
+  DBuf<double> delem_, dxy_;
+  cudaStream_t st_ = nullptr;
+  NodeBoxTree tree_;
+};
+
+// Work planner for one batch of Galerkin fills.
+class FillPlan {
+ public:
+  FillPlan(int n_nodes, int m_prime, int n_gauss)
+      : N_(n_nodes), m_(m_prime), ng_(n_gauss) {}
+  // true_block(rows, cols) into dest with per-component destination offsets;
+  // trans writes conj(v) at (col, row).
+  void add_true_block(const Lists& rows, const Lists& cols, double* dest,
+                      int ld, const int drow[2], const int dcol[2], int trans);
+  // Both proxy blocks of one cell: polygon rows -> T_V rows [0, 2m'),
+  // polygon cols of M_U -> T_U rows [0, 2m') (conj-transposed).
+  void add_proxy(double cx, double cy, double radius, const Lists& rows,
+                 const Lists& cols, double* tv, int ld_v, double* tu, int ld_u);
+  long long bundles() const { return bundles_; }
+  bool empty() const { return gather_.empty(); }
+  void clear();
+
+ private:
+  friend class Problem;
+  void elements_of(const Lists& nodes, std::vector<int>& out) const;
+  void node_descs(const Lists& nodes, const std::vector<int>& elems,
+                  const int dest_off[2], std::vector<NodeDesc>& out) const;
+  int poly_descs();
+  int N_, m_, ng_;
+  long long bundles_ = 0;
+  long long near_pairs_ = 0;
+  long long entries_ = 0;
+  int proxy_blocks_ = 0;
+  int poly_desc_off_ = -1;
+  std::vector<int> elems_;
+  std::vector<NearJob> near_;
+  std::vector<long long> near_local_;
+  std::vector<long long> sing_pair_;
+  std::vector<int> sing_elems_;
+  std::vector<ProxyJob> proxy_;
+  std::vector<int> proxy_boff_;
+  std::vector<GatherJob> gather_;
+  std::vector<long long> gather_off_;
+  std::vector<NodeDesc> desc_;
+};
+
+// ----------------------------------------------------------------- solver
+class Fds {
+ public:
+  Fds(Problem& p, int depth, const ebem_fds_config& cfg);
+  void solve_device(const double* rhs, int m, double* x, ebem_fds_solve_timing* t);
+  const ebem_fds_stats& stats() const { return stats_; }
+  int rank_of(int cell) const;
+  void cell_info(int cell, int* sizes, int* skel) const;
+  Problem& problem() { return P_; }
+
+ private:
+  struct Cell {
+    int begin = 0, end = 0;
+    Lists jrow, jcol, srow, scol;
+    int nloc = 0, k = 0;
+    // device factors
+    double* lu = nullptr;
+    int* ipiv = nullptr;
+    double* ainv_u = nullptr;  // 2n x 2k
+    double* v = nullptr;       // V0 (k x n) then V1 (k x n)
+    double* atilde = nullptr;  // 2k x 2k
+  };
+  struct Store {
+    DBuf<double> lu, ainv_u, v, atilde;
+    DBuf<int> ipiv;
+  };
+  void build();
+  void reduced_diagonal(FillPlan& plan, std::vector<CopyTask>& copies, int cell,
+                        double* dest, int ld, int off);
+  int first(int l) const { return (1 << l) - 1; }
+  int last(int l) const { return (2 << l) - 2; }
+
+  Problem& P_;
+  int depth_;
+  ebem_fds_config cfg_;
+  std::vector<Cell> cells_;
+  std::vector<Store> store_;
+  std::vector<int> top_off_;
+  DBuf<double> top_lu_;
+  DBuf<int> top_ipiv_;
+  int top_dim_ = 0;
+  ebem_fds_stats stats_{};
+  // solve workspaces (grow-only)
+  DBuf<double> ws_f_, ws_ainvf_, ws_ft_, ws_x_, ws_t_;
+};
+
+// ------------------------------------------------------------ batched LA
+// Thin host helpers that upload task arrays and launch the dense kernels.
+void run_copies(Problem& P, const std::vector<CopyTask>& t);
+void run_gemms(Problem& P, const std::vector<GemmTask>& t);
+void run_getrs(Problem& P, const std::vector<LuSolveTask>& t);
+// Factors in place; returns per-task info (0 ok).
+std::vector<int> run_getrf(Problem& P, std::vector<LuTask> t);
+
+}  // namespace ebem_gpu
