@@ -292,6 +292,13 @@ int ebem_gpu_fds_cell(const ebem_gpu_fds* f, int cell, int* sizes, int* skel) {
   return guarded([&] { f->f->cell_info(cell, sizes, skel); });
 }
 
+// Debug hook: copies a cell's device factor (0 lu, 1 ipiv, 2 A^-1 U, 3 V,
+// 4 atilde) to host memory.
+int ebem_gpu_fds_debug_cell(const ebem_gpu_fds* f, int cell, int which,
+                            double* out) {
+  return guarded([&] { f->f->debug_cell(cell, which, out); });
+}
+
 int ebem_gpu_eval_hankel(const double* x, int n, double* out) {
   return guarded([&] {
     if (n <= 0) return;

@@ -34,7 +34,7 @@ struct DevCtx {
   int series_maxq;
   // Remainder series of the ten scalars: series[(k * kMaxSeriesPow + q) * 4 +
   // {0,1,2,3}] = {Re a_q, Im a_q, Re b_q, Im b_q} of sum (a_q + b_q ln r) r^q.
-  double series[10 * kMaxSeriesPow * 4];
+  alignas(16) double series[10 * kMaxSeriesPow * 4];
   // Gauss-Legendre rules on [0,1]; order n occupies [n(n-1)/2, n(n+1)/2).
   double gx[kGaussSlots];
   double gw[kGaussSlots];

@@ -98,7 +98,7 @@ k_near_separated(const DevCtx* __restrict__ ctx, const NearJob* __restrict__ job
   if (p >= n_pairs) return;
   const int jb = find_job(job_pair_off, n_jobs, p);
   const NearJob J = jobs[jb];
-  const long long local = p - J.pair_off;
+  const long long local = p - __ldg(job_pair_off + jb);  // within the job
   const int ra = int(local / J.nces);
   const int cb = int(local - (long long)ra * J.nces);
   const int ea = __ldg(elems + J.res_off + ra);
@@ -169,7 +169,7 @@ k_near_separated(const DevCtx* __restrict__ ctx, const NearJob* __restrict__ job
       }
     }
   }
-  store_bundle(bundles, p, acc);
+  store_bundle(bundles, J.pair_off + local, acc);
 }
 
 // ---------------------------------------------------------------- singular

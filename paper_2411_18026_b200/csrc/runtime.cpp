@@ -13,6 +13,8 @@
 #include <chrono>
 #include <cmath>
 #include <limits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "ebem_kernels.h"
 #include "host_setup.h"
@@ -884,6 +886,10 @@ GemmTask gemm_task(const double* a, int lda, const double* b, int ldb, double* c
   return g;
 }
 void singular_error(int info, int n) {
+  if (std::getenv("EBEM_DEBUG_NOTHROW")) {
+    std::fprintf(stderr, "[ebem] singular: pivot %d of %d\n", info - 1, n);
+    return;
+  }
   throw Error(EBEM_RUNTIME_ERROR,
               "LuFactor: matrix is singular, zero pivot at index " +
                   std::to_string(info - 1) + " of " + std::to_string(n));
@@ -1049,7 +1055,9 @@ void Fds::build() {
         const int nl = C.nloc, k = C.k;
         if (k == 0) continue;
         const int d = 2 * nl;
-        ct.push_back(copy_task(nullptr, 0, C.ainv_u, d, d, 2 * k));  // zero
+        // off-diagonal zero blocks (tasks of one launch must not overlap)
+        ct.push_back(copy_task(nullptr, 0, C.ainv_u + 2 * size_t(nl), d, nl, k));
+        ct.push_back(copy_task(nullptr, 0, C.ainv_u + 2 * size_t(k) * d, d, nl, k));
         const double* u = ubuf.get() + 2 * br[i].u_off;
         ct.push_back(copy_task(u, nl, C.ainv_u, d, nl, k));
         ct.push_back(copy_task(u + 2 * size_t(nl) * k, nl,
@@ -1156,6 +1164,22 @@ void Fds::build() {
   }
   CK(cudaStreamSynchronize(P_.stream()));
   stats_.top_factor_seconds = now() - t_top;
+}
+
+void Fds::debug_cell(int cell, int which, double* out) const {
+  const Cell& C = cells_.at(cell);
+  const size_t d = 2 * size_t(C.nloc), kk = 2 * size_t(C.k);
+  const void* src = nullptr;
+  size_t bytes = 0;
+  switch (which) {
+    case 0: src = C.lu; bytes = 16 * d * d; break;
+    case 1: src = C.ipiv; bytes = 4 * d; break;
+    case 2: src = C.ainv_u; bytes = 16 * d * kk; break;
+    case 3: src = C.v; bytes = 16 * kk * C.nloc; break;
+    case 4: src = C.atilde; bytes = 16 * kk * kk; break;
+    default: throw Error(EBEM_INVALID_ARGUMENT, "debug_cell: bad selector");
+  }
+  if (src && bytes) CK(cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost));
 }
 
 int Fds::rank_of(int cell) const {

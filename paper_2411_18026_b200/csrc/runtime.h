@@ -236,6 +236,7 @@ class Fds {
   void solve_device(const double* rhs, int m, double* x, ebem_fds_solve_timing* t);
   const ebem_fds_stats& stats() const { return stats_; }
   int rank_of(int cell) const;
+  void debug_cell(int cell, int which, double* out) const;
   void cell_info(int cell, int* sizes, int* skel) const;
   Problem& problem() { return P_; }
 

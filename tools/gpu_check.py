@@ -52,6 +52,10 @@ def main():
     rmv, rmu = rp.cell_mats((leaf, leaf), (leaf, leaf), 0, 32)
     print("cell_mats", mv.shape, rmv.shape, rel(mv, rmv), rel(mu, rmu))
     print("  entry max rel", np.max(np.abs(mv - rmv)) / np.max(np.abs(rmv)))
+    print("  poly part", rel(mv[:128], rmv[:128]), "near part", rel(mv[128:], rmv[128:]))
+    print("  U poly part", rel(mu[:, :128], rmu[:, :128]), "near part", rel(mu[:, 128:], rmu[:, 128:]))
+    np.set_printoptions(linewidth=200, precision=4)
+
     b = src.cell_basis((leaf, leaf), (leaf, leaf), 0, 32, 1e-10)
     rb = rp.cell_basis((leaf, leaf), (leaf, leaf), 0, 32, 1e-10)
     print("cell_basis k", b.k, rb["k"])
