@@ -68,7 +68,8 @@ typedef struct ebem_fds_stats {
   int saturated;
   double upward_seconds;
   double top_factor_seconds;
-  double basis_cpu_seconds; /* device time of the basis phase (fill + ID) */
+  double basis_cpu_seconds; /* wall time of the basis phase (fill + ID) */
+  double factorize_device_seconds; /* CUDA events around the whole build */
 } ebem_fds_stats;
 
 /* FdsSolveTiming, proj/include/ebem/fds.hpp:38-42 */
@@ -76,6 +77,7 @@ typedef struct ebem_fds_solve_timing {
   double upward_seconds;
   double top_seconds;
   double downward_seconds;
+  double device_seconds; /* CUDA events around the whole solve */
 } ebem_fds_solve_timing;
 
 typedef struct ebem_gpu_problem ebem_gpu_problem;
@@ -170,6 +172,24 @@ int ebem_gpu_eval_scalars(ebem_gpu_problem* p, const double* r, int n,
 
 /* Number of kernel launches issued by the library since load (bench). */
 long long ebem_gpu_launch_count(void);
+
+/* Per-kernel device timing with CUDA events on the launching stream
+ * (measurement hooks for bench.py).  prof_read fills n entries of
+ * milliseconds, launch counts and algorithmic work units (point
+ * evaluations for the fill kernels, flops or bytes for the others). */
+int ebem_gpu_prof_enable(int on);
+int ebem_gpu_prof_read(int reset, double* ms, long long* count, double* units,
+                       int n);
+const char* ebem_gpu_prof_name(int id);
+int ebem_gpu_prof_kernels(void);
+/* Measured FP64 FMA throughput of the device (TFLOP/s), the roofline
+ * denominator of the fill kernels. */
+int ebem_gpu_fp64_peak(double* tflops);
+
+/* Debug hook: copies a cell's device factor (0 LU, 1 pivots, 2 A^-1 U,
+ * 3 V = [v0 v1], 4 atilde) into host memory. */
+int ebem_gpu_fds_debug_cell(const ebem_gpu_fds* f, int cell, int which,
+                            double* out);
 
 #ifdef __cplusplus
 }

@@ -102,13 +102,15 @@ class _FdsStats(ctypes.Structure):
                 ("top_dim", ctypes.c_int), ("saturated", ctypes.c_int),
                 ("upward_seconds", ctypes.c_double),
                 ("top_factor_seconds", ctypes.c_double),
-                ("basis_cpu_seconds", ctypes.c_double)]
+                ("basis_cpu_seconds", ctypes.c_double),
+                ("factorize_device_seconds", ctypes.c_double)]
 
 
 class _SolveTiming(ctypes.Structure):
     _fields_ = [("upward_seconds", ctypes.c_double),
                 ("top_seconds", ctypes.c_double),
-                ("downward_seconds", ctypes.c_double)]
+                ("downward_seconds", ctypes.c_double),
+                ("device_seconds", ctypes.c_double)]
 
 
 def lib():
@@ -357,6 +359,7 @@ class FdsStats:
     upward_seconds: float = 0.0
     top_factor_seconds: float = 0.0
     basis_cpu_seconds: float = 0.0
+    factorize_device_seconds: float = 0.0
 
 
 @dataclass
@@ -364,6 +367,7 @@ class FdsSolveTiming:
     upward_seconds: float = 0.0
     top_seconds: float = 0.0
     downward_seconds: float = 0.0
+    device_seconds: float = 0.0
 
 
 @dataclass
@@ -573,7 +577,8 @@ class FdsSolver:
             max_rank=list(st.max_rank)[: tree.depth() + 1], top_dim=st.top_dim,
             saturated=bool(st.saturated), upward_seconds=st.upward_seconds,
             top_factor_seconds=st.top_factor_seconds,
-            basis_cpu_seconds=st.basis_cpu_seconds)
+            basis_cpu_seconds=st.basis_cpu_seconds,
+            factorize_device_seconds=st.factorize_device_seconds)
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -596,6 +601,7 @@ class FdsSolver:
             timing.upward_seconds = t.upward_seconds
             timing.top_seconds = t.top_seconds
             timing.downward_seconds = t.downward_seconds
+            timing.device_seconds = t.device_seconds
         x = _from_cbuf(buf, 2 * n, m)
         return x[:, 0] if vec else x
 
@@ -622,3 +628,31 @@ class FdsSolver:
     @property
     def handle(self):
         return self._h
+
+
+# ------------------------------------------------------------- measurement
+
+
+def prof_enable(on: bool = True) -> None:
+    """Per-kernel CUDA-event timing on the launching stream (bench hooks)."""
+    _check(lib().ebem_gpu_prof_enable(1 if on else 0))
+
+
+def prof_read(reset: bool = False) -> dict:
+    """{kernel: (milliseconds, launches, work units)} since the last reset."""
+    L = lib()
+    L.ebem_gpu_prof_name.restype = ctypes.c_char_p
+    n = L.ebem_gpu_prof_kernels()
+    ms = np.zeros(n)
+    cnt = np.zeros(n, dtype=np.int64)
+    units = np.zeros(n)
+    _check(L.ebem_gpu_prof_read(1 if reset else 0, _p(ms), _p(cnt), _p(units), n))
+    return {L.ebem_gpu_prof_name(i).decode(): (float(ms[i]), int(cnt[i]), float(units[i]))
+            for i in range(n)}
+
+
+def fp64_peak_tflops() -> float:
+    """Measured FP64 FMA throughput (DFMA chains on every SM)."""
+    v = ctypes.c_double()
+    _check(lib().ebem_gpu_fp64_peak(ctypes.byref(v)))
+    return float(v.value)

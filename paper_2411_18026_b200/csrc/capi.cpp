@@ -77,6 +77,43 @@ const char* ebem_gpu_last_error(void) { return g_err.c_str(); }
 
 long long ebem_gpu_launch_count(void) { return g_launches.load(); }
 
+int ebem_gpu_prof_enable(int on) {
+  return guarded([&] {
+    g_prof.collect();
+    if (on && !g_prof.near_points) {
+      CK(cudaMalloc(reinterpret_cast<void**>(&g_prof.near_points), 8));
+      CK(cudaMemset(g_prof.near_points, 0, 8));
+    }
+    g_prof.on = on != 0;
+  });
+}
+
+int ebem_gpu_prof_read(int reset, double* ms, long long* count, double* units,
+                       int n) {
+  return guarded([&] {
+    g_prof.collect();
+    for (int i = 0; i < n && i < KP_COUNT; ++i) {
+      ms[i] = g_prof.ms[i];
+      count[i] = g_prof.count[i];
+      units[i] = g_prof.units[i];
+    }
+    if (reset) g_prof.reset();
+  });
+}
+
+const char* ebem_gpu_prof_name(int id) { return kernel_name(id); }
+
+int ebem_gpu_fp64_peak(double* tflops) {
+  return guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      throw Error(EBEM_CUDA_ERROR, "no CUDA device");
+    *tflops = measure_fp64_peak_tflops();
+    CK(cudaGetLastError());
+  });
+}
+int ebem_gpu_prof_kernels(void) { return KP_COUNT; }
+
 int ebem_gpu_device_info(char* buf, int len) {
   return guarded([&] {
     int n = 0;
@@ -307,7 +344,7 @@ int ebem_gpu_eval_hankel(const double* x, int n, double* out) {
     dout.alloc(4 * size_t(n));
     CK(cudaMemcpy(dx.get(), x, 8 * size_t(n), cudaMemcpyHostToDevice));
     launch_eval_hankel(dx.get(), n, dout.get(), 0);
-    ++g_launches;
+    ++g_launches;  // test hook
     CK(cudaGetLastError());
     CK(cudaMemcpy(out, dout.get(), 32 * size_t(n), cudaMemcpyDeviceToHost));
   });

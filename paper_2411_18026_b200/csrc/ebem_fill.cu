@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(128)
 k_near_separated(const DevCtx* __restrict__ ctx, const NearJob* __restrict__ jobs,
                  const long long* __restrict__ job_pair_off, int n_jobs,
                  const int* __restrict__ elems, long long n_pairs,
-                 double* __restrict__ bundles) {
+                 double* __restrict__ bundles, unsigned long long* points) {
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   const int jb = find_job(job_pair_off, n_jobs, p);
@@ -111,6 +111,11 @@ k_near_separated(const DevCtx* __restrict__ ctx, const NearJob* __restrict__ job
   const double hx = ef(ctx, EH, ea), hy = ef(ctx, EH, eb);
   const int n = tier_nodes(element_distance(ctx, ea, eb) / fmax(hx, hy),
                            ctx->far_nodes, ctx->refine);
+  if (points) {  // profiling: count point evaluations (warp-aggregated)
+    const unsigned act = __activemask();
+    const unsigned s = __reduce_add_sync(act, unsigned(n * n));
+    if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(points, (unsigned long long)s);
+  }
   const double* gx = ctx->gx + gauss_offset(n);
   const double* gw = ctx->gw + gauss_offset(n);
   const double pax = ef(ctx, EPX, ea), pay = ef(ctx, EPY, ea);
@@ -543,11 +548,11 @@ k_gather(const GatherJob* __restrict__ jobs, const long long* __restrict__ job_e
 void launch_near_separated(const DevCtx* ctx, const NearJob* jobs,
                            const long long* job_pair_off, int n_jobs,
                            const int* elems, long long n_pairs, double* bundles,
-                           cudaStream_t st) {
+                           unsigned long long* points, cudaStream_t st) {
   if (n_pairs <= 0) return;
   const int bs = 128;
   k_near_separated<<<(unsigned)((n_pairs + bs - 1) / bs), bs, 0, st>>>(
-      ctx, jobs, job_pair_off, n_jobs, elems, n_pairs, bundles);
+      ctx, jobs, job_pair_off, n_jobs, elems, n_pairs, bundles, points);
 }
 
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,

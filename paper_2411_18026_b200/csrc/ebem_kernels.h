@@ -12,7 +12,7 @@ namespace ebem_gpu {
 void launch_near_separated(const DevCtx* ctx, const NearJob* jobs,
                            const long long* job_pair_off, int n_jobs,
                            const int* elems, long long n_pairs, double* bundles,
-                           cudaStream_t st);
+                           unsigned long long* points, cudaStream_t st);
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,
                           const int* pair_elems, int n, double* bundles, int* bad,
                           cudaStream_t st);
@@ -30,6 +30,7 @@ void launch_rhs_plane(const DevCtx* ctx, int n_nodes, int kind,
                       double* out, cudaStream_t st);
 
 // ---- special functions, exposed for parity tests (ebem_rhs.cu)
+double measure_fp64_peak_tflops();
 void launch_eval_hankel(const double* x, int n, double* out, cudaStream_t st);
 void launch_eval_scalars(const DevCtx* ctx, const double* r, int n, int which,
                          double* out, cudaStream_t st);

@@ -130,6 +130,47 @@ __global__ void k_eval_scalars(const DevCtx* __restrict__ ctx,
   }
 }
 
+// FP64 FMA throughput probe: 8 independent dependency chains per thread.
+__global__ void __launch_bounds__(256) k_fp64_peak(int iters, double seed,
+                                                   double* sink) {
+  double a[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a[q] = seed + q + threadIdx.x;
+  const double b = 1.0 - 1e-9, c = 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = fma(a[q], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += a[q];
+  if (s == 12345.678) sink[0] = s;
+}
+
+double measure_fp64_peak_tflops() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* sink = nullptr;
+  cudaMalloc(&sink, 8);
+  const int blocks = sms * 8, threads = 256, iters = 1 << 14;
+  k_fp64_peak<<<blocks, threads>>>(64, 1.0, sink);  // warm-up
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k_fp64_peak<<<blocks, threads>>>(iters, 1.0, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  const double flops = 2.0 * 8.0 * double(iters) * blocks * threads;
+  return ms > 0 ? flops / (1e-3 * ms) / 1e12 : 0.0;
+}
+
 void launch_rhs_plane(const DevCtx* ctx, int n_nodes, int kind,
                         const double* angles, int m, double amplitude,
                         int rhs_n, double* out, cudaStream_t st) {

@@ -22,6 +22,67 @@
 namespace ebem_gpu {
 
 std::atomic<long long> g_launches{0};
+Profiler g_prof;
+
+const char* kernel_name(int id) {
+  static const char* names[KP_COUNT] = {
+      "k_proxy_pairs", "k_near_separated", "k_near_singular", "k_gather",
+      "k_qr_reduce", "k_cpqr", "k_interp", "k_getrf", "k_getrs", "k_gemm",
+      "k_copy", "k_rhs_plane"};
+  return (id >= 0 && id < KP_COUNT) ? names[id] : "?";
+}
+
+cudaEvent_t Profiler::ev() {
+  if (!pool_.empty()) {
+    cudaEvent_t e = pool_.back();
+    pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+
+void Profiler::begin(cudaStream_t st) {
+  if (!on) return;
+  cur_ = ev();
+  CK(cudaEventRecord(cur_, st));
+}
+
+void Profiler::end(int id, cudaStream_t st, double u) {
+  ++g_launches;
+  if (!on || !cur_) return;
+  cudaEvent_t b = ev();
+  CK(cudaEventRecord(b, st));
+  pending_.push_back(Rec{id, cur_, b, u});
+  cur_ = nullptr;
+}
+
+void Profiler::collect() {
+  if (pending_.empty() && !near_points) return;
+  CK(cudaDeviceSynchronize());
+  for (const Rec& r : pending_) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.id] += t;
+    count[r.id] += 1;
+    units[r.id] += r.units;
+    pool_.push_back(r.a);
+    pool_.push_back(r.b);
+  }
+  pending_.clear();
+  if (near_points) {
+    unsigned long long h = 0;
+    CK(cudaMemcpy(&h, near_points, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(near_points, 0, 8));
+    units[KP_NEAR_SEP] += double(h);
+  }
+}
+
+void Profiler::reset() {
+  collect();
+  for (int i = 0; i < KP_COUNT; ++i) ms[i] = 0.0, count[i] = 0, units[i] = 0.0;
+}
 
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -448,27 +509,36 @@ void Problem::execute(FillPlan& plan) {
   bundles.ensure(size_t(plan.bundles_) * kBundle * 2);
   const int* el = pk.at<int>(plan_dev, o_el);
   if (!plan.proxy_.empty()) {
+    double pts = 0.0;
+    for (const ProxyJob& j : plan.proxy_)
+      pts += double(pcfg_.m_prime) * j.nE * pcfg_.n_gauss * pcfg_.n_gauss;
+    g_prof.begin(st_);
     launch_proxy_pairs(dctx(), pcfg_.n_gauss, pk.at<ProxyJob>(plan_dev, o_pj),
                        pk.at<int>(plan_dev, o_pb), int(plan.proxy_.size()),
                        plan.proxy_blocks_, el, bundles.get(), st_);
-    ++g_launches;
+    g_prof.end(KP_PROXY, st_, pts);
   }
   if (plan.near_pairs_ > 0) {
+    g_prof.begin(st_);
     launch_near_separated(dctx(), pk.at<NearJob>(plan_dev, o_nj),
                           pk.at<long long>(plan_dev, o_nl), int(plan.near_.size()),
-                          el, plan.near_pairs_, bundles.get(), st_);
-    ++g_launches;
+                          el, plan.near_pairs_, bundles.get(),
+                          g_prof.on ? g_prof.near_points : nullptr, st_);
+    g_prof.end(KP_NEAR_SEP, st_, 0.0);
   }
   if (!plan.sing_pair_.empty()) {
+    g_prof.begin(st_);
     launch_near_singular(dctx(), pk.at<long long>(plan_dev, o_sp),
                          pk.at<int>(plan_dev, o_se), int(plan.sing_pair_.size()),
                          bundles.get(), bad.get(), st_);
-    ++g_launches;
+    g_prof.end(KP_NEAR_SING, st_, double(plan.sing_pair_.size()));
   }
+  g_prof.begin(st_);
   launch_gather(pk.at<GatherJob>(plan_dev, o_gj), pk.at<long long>(plan_dev, o_go),
                 int(plan.gather_.size()), pk.at<NodeDesc>(plan_dev, o_de),
                 plan.entries_, bundles.get(), st_);
-  ++g_launches;
+  // bytes: 4 bundle reads (16 B each) + one 16 B store per entry
+  g_prof.end(KP_GATHER, st_, 80.0 * double(plan.entries_));
   CK(cudaGetLastError());
   plan.clear();
 }
@@ -608,9 +678,15 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     size_t smem = 0;
     for (const QrTask& t : tasks)
       if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
+    double fl = 0.0;  // complex Householder QR: 8 m n^2 - 8 n^3 / 3
+    for (const QrTask& t : tasks) {
+      const double mm = t.rows, nn = std::min(t.rows, t.n);
+      fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
+    }
+    g_prof.begin(st_);
     launch_qr_reduce(pk.at<QrTask>(task_dev, o), int(tasks.size()), smem,
                      gws.get(), st_);
-    ++g_launches;
+    g_prof.end(KP_QR, st_, fl);
     CK(cudaGetLastError());
     for (size_t i = 0; i < q.size(); ++i) {
       if (!pieces[i]) continue;
@@ -662,8 +738,14 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     Pack pk;
     const size_t o = pk.add(ct);
     pk.upload(task_dev, st_);
+    double fl = 0.0;  // full-rank bound of the pivoted QR flops
+    for (const CpqrTask& t : ct) {
+      const double mm = t.rows, nn = std::min(t.rows, t.n);
+      fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
+    }
+    g_prof.begin(st_);
     launch_cpqr(pk.at<CpqrTask>(task_dev, o), int(nq), smem, gws.get(), st_);
-    ++g_launches;
+    g_prof.end(KP_CPQR, st_, fl);
     CK(cudaGetLastError());
   }
   std::vector<int> h_jp(jp_total), h_steps(nq);
@@ -752,8 +834,11 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     Pack pk;
     const size_t o = pk.add(it);
     pk.upload(task_dev, st_);
+    double fl = 0.0;
+    for (const InterpTask& t : it) fl += 4.0 * t.k * t.k * double(t.n - t.k);
+    g_prof.begin(st_);
     launch_interp(pk.at<InterpTask>(task_dev, o), int(it.size()), max_k, st_);
-    ++g_launches;
+    g_prof.end(KP_INTERP, st_, fl);
     CK(cudaGetLastError());
   }
   CK(cudaStreamSynchronize(st_));
@@ -786,8 +871,9 @@ void Problem::rhs_plane(int kind, const double* angles, int m, double amp,
   dout.alloc(4 * size_t(n_) * m);
   CK(cudaMemcpyAsync(da.get(), angles, 8 * size_t(m), cudaMemcpyHostToDevice, st_));
   const int rn = int(acfg_.rhs_nodes * acfg_.refine + 0.5);
+  g_prof.begin(st_);
   launch_rhs_plane(dctx(), n_, kind, da.get(), m, amp, rn, dout.get(), st_);
-  ++g_launches;
+  g_prof.end(KP_RHS, st_, 2.0 * n_ * m * rn);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_host, dout.get(), 32 * size_t(n_) * m, cudaMemcpyDeviceToHost, st_));
   CK(cudaStreamSynchronize(st_));
@@ -795,9 +881,10 @@ void Problem::rhs_plane(int kind, const double* angles, int m, double amp,
 
 // ------------------------------------------------------------ batched LA
 namespace {
-template <class T, class F>
+template <class T, class F, class U>
 void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
-                 void (*launch)(const T*, const int*, int, int, cudaStream_t)) {
+                 void (*launch)(const T*, const int*, int, int, cudaStream_t),
+                 int id, U units_of) {
   if (t.empty()) return;
   std::vector<int> boff(t.size());
   int total = 0;
@@ -810,9 +897,12 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
   const size_t o1 = pk.add(t);
   const size_t o2 = pk.add(boff);
   pk.upload(P.task_dev, P.stream());
+  double units = 0.0;
+  for (const T& x : t) units += units_of(x);
+  g_prof.begin(P.stream());
   launch(pk.at<T>(P.task_dev, o1), pk.at<int>(P.task_dev, o2), int(t.size()),
          total, P.stream());
-  ++g_launches;
+  g_prof.end(id, P.stream(), units);
   CK(cudaGetLastError());
   // task_dev is reused by the next upload: keep the host from racing ahead
   CK(cudaStreamSynchronize(P.stream()));
@@ -821,15 +911,18 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
 
 void run_copies(Problem& P, const std::vector<CopyTask>& t) {
   run_blocked(P, t, [](const CopyTask& c) { return copy_blocks(c.rows, c.cols); },
-              launch_copy);
+              launch_copy, KP_COPY,
+              [](const CopyTask& c) { return 32.0 * c.rows * c.cols; });
 }
 void run_gemms(Problem& P, const std::vector<GemmTask>& t) {
   run_blocked(P, t, [](const GemmTask& g) { return g.k > 0 ? gemm_blocks(g.m, g.n) : 0; },
-              launch_gemm);
+              launch_gemm, KP_GEMM,
+              [](const GemmTask& g) { return 8.0 * g.m * g.n * double(g.k); });
 }
 void run_getrs(Problem& P, const std::vector<LuSolveTask>& t) {
   run_blocked(P, t, [](const LuSolveTask& s) { return s.n > 0 ? getrs_blocks(s.nrhs) : 0; },
-              launch_getrs);
+              launch_getrs, KP_GETRS,
+              [](const LuSolveTask& s) { return 8.0 * s.n * double(s.n) * s.nrhs; });
 }
 std::vector<int> run_getrf(Problem& P, std::vector<LuTask> t) {
   std::vector<int> info(t.size(), 0);
@@ -849,8 +942,11 @@ std::vector<int> run_getrf(Problem& P, std::vector<LuTask> t) {
   Pack pk;
   const size_t o = pk.add(t);
   pk.upload(P.task_dev, P.stream());
+  double fl = 0.0;
+  for (const LuTask& x : t) fl += 8.0 / 3.0 * double(x.n) * x.n * x.n;
+  g_prof.begin(P.stream());
   launch_getrf(pk.at<LuTask>(P.task_dev, o), int(t.size()), smem, P.gws.get(), P.stream());
-  ++g_launches;
+  g_prof.end(KP_GETRF, P.stream(), fl);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(info.data(), dinfo.get(), 4 * t.size(), cudaMemcpyDeviceToHost, P.stream()));
   CK(cudaStreamSynchronize(P.stream()));
@@ -945,6 +1041,10 @@ void Fds::reduced_diagonal(FillPlan& plan, std::vector<CopyTask>& copies,
 
 void Fds::build() {
   const double t_start = now();
+  cudaEvent_t ev0, ev1;
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  CK(cudaEventRecord(ev0, P_.stream()));
   const int n = P_.n();
   const int ncells = (2 << depth_) - 1;
   cells_.assign(ncells, Cell{});
@@ -1164,6 +1264,13 @@ void Fds::build() {
   }
   CK(cudaStreamSynchronize(P_.stream()));
   stats_.top_factor_seconds = now() - t_top;
+  CK(cudaEventRecord(ev1, P_.stream()));
+  CK(cudaEventSynchronize(ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ev0, ev1));
+  stats_.factorize_device_seconds = 1e-3 * ms;
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
 }
 
 void Fds::debug_cell(int cell, int which, double* out) const {
@@ -1228,6 +1335,10 @@ void Fds::solve_device(const double* rhs, int m, double* x,
   auto F = [&](int c) { return ws_f_.get() + 2 * fo[c] * m; };
   auto FT = [&](int c) { return ws_ft_.get() + 2 * ko[c] * m; };
   auto TT = [&](int c) { return ws_t_.get() + 2 * ko[c] * m; };
+  cudaEvent_t ev0, ev1;
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  CK(cudaEventRecord(ev0, P_.stream()));
   const double t0 = now();
   // leaves: f = [rhs[a:a+s]; rhs[N+a:N+a+s]]
   {
@@ -1334,6 +1445,14 @@ void Fds::solve_device(const double* rhs, int m, double* x,
     timing->top_seconds = t2 - t1;
     timing->downward_seconds = t3 - t2;
   }
+  CK(cudaEventRecord(ev1, P_.stream()));
+  CK(cudaEventSynchronize(ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ev0, ev1));
+  last_solve_device_seconds_ = 1e-3 * ms;
+  if (timing) timing->device_seconds = last_solve_device_seconds_;
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
 }
 
 }  // namespace ebem_gpu

@@ -33,6 +33,37 @@ void cuda_check(cudaError_t e, const char* what);
 
 extern std::atomic<long long> g_launches;
 
+// ---------------------------------------------------------------- profiler
+// Optional per-kernel device timing (CUDA events on the launching stream)
+// and algorithmic work units (quadrature point evaluations for the fill
+// kernels, bytes or flops for the rest); enabled by ebem_gpu_prof_enable.
+enum KernelId {
+  KP_PROXY = 0, KP_NEAR_SEP, KP_NEAR_SING, KP_GATHER, KP_QR, KP_CPQR,
+  KP_INTERP, KP_GETRF, KP_GETRS, KP_GEMM, KP_COPY, KP_RHS, KP_COUNT
+};
+const char* kernel_name(int id);
+
+class Profiler {
+ public:
+  bool on = false;
+  void begin(cudaStream_t st);
+  void end(int id, cudaStream_t st, double units);
+  void collect();
+  void reset();
+  double ms[KP_COUNT] = {};
+  long long count[KP_COUNT] = {};
+  double units[KP_COUNT] = {};
+  unsigned long long* near_points = nullptr;  // device counter (on only)
+
+ private:
+  struct Rec { int id; cudaEvent_t a, b; double units; };
+  std::vector<Rec> pending_;
+  std::vector<cudaEvent_t> pool_;
+  cudaEvent_t cur_ = nullptr;
+  cudaEvent_t ev();
+};
+extern Profiler g_prof;
+
 // ----------------------------------------------------------------- buffers
 template <class T>
 class DBuf {
@@ -272,6 +303,7 @@ class Fds {
   DBuf<int> top_ipiv_;
   int top_dim_ = 0;
   ebem_fds_stats stats_{};
+  double last_solve_device_seconds_ = 0.0;
   // solve workspaces (grow-only)
   DBuf<double> ws_f_, ws_ainvf_, ws_ft_, ws_x_, ws_t_;
 };
