@@ -147,6 +147,6 @@ def test_large_n_properties(eb):
     f2 = asm.rhs(eb.PlanePWave(med, 1.0, 1.3))
     X = fds.solve(np.stack([f1, f2, 2 * f1 - 3j * f2], 1))
     assert np.all(np.isfinite(X))
-    assert rel(X[:, 2], 2 * X[:, 0] - 3j * X[:, 1]) < 1e-12
+    assert rel(X[:, 2], 2 * X[:, 0] - 3j * X[:, 1]) < 1e-10  # ~ cond * eps
     st = fds.stats()
     assert st.max_rank[tree.depth()] == 25 and not st.saturated
