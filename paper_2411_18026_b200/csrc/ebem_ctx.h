@@ -3,6 +3,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <vector_types.h>
 
 namespace ebem_gpu {
 
@@ -21,6 +22,22 @@ struct DevMedium {
   double kappa;          // mu / (2 pi (lam + 2 mu))
   double ccon;           // (lam + mu) / (8 pi (lam + 2 mu))
   double alpha_re, alpha_im;
+  // derived constants of the fast kernel path (host-computed once)
+  double inv_kT, inv_kL;
+  double log_half_kT, log_half_kL;  // ln(k/2): ln(k r / 2) = ln r + ln(k/2)
+  double sd1, sd3;                  // static d1 = sd1 / r, d3 = sd3 / r
+  double sn[5];                     // static n1, n2, n4, n5, n7 = sn[i] / r^2
+  double c_n5;                      // lam * aratio * kL^2
+};
+
+// Remainder series of one scalar in parity form:
+//   sum_p (a_p + b_p ln r) r^(par + 2p),  p = 0 .. nt-1
+// (every series carries powers of a single parity: d's odd, n's even).
+constexpr int kParTerms = 26;
+struct ParSeries {
+  int par[10], nt[10];
+  double2 a[10][kParTerms];
+  double2 b[10][kParTerms];
 };
 
 // Element geometry, structure of arrays over the N elements (element e runs
@@ -35,6 +52,7 @@ struct DevCtx {
   // Remainder series of the ten scalars: series[(k * kMaxSeriesPow + q) * 4 +
   // {0,1,2,3}] = {Re a_q, Im a_q, Re b_q, Im b_q} of sum (a_q + b_q ln r) r^q.
   alignas(16) double series[10 * kMaxSeriesPow * 4];
+  ParSeries pser;
   // Gauss-Legendre rules on [0,1]; order n occupies [n(n-1)/2, n(n+1)/2).
   double gx[kGaussSlots];
   double gw[kGaussSlots];

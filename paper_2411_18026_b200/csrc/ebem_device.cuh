@@ -333,4 +333,168 @@ __device__ __forceinline__ void q0_kernel(double qfactor, double r, double zx,
   q[3] = lr - qfactor * (zy * zy);
 }
 
+// ------------------------------------------------------- fast D/N path
+// The fill only ever needs the traction scalars d1, d2, d3 (always the full
+// values) and the hypersingular scalars n1, n2, n4, n5, n7 (full for the
+// proxy blocks, remainders for the exact Galerkin pairs): gpsi / gchi feed
+// only G, which the Burton-Miller operator never uses.  One ln r per point
+// serves the series branch, the Hankel small-argument log terms and q0.
+
+// D/N series (scalars 2..9) staged in shared memory once per CTA.
+struct SerSm {
+  int par[8], nt[8];
+  double2 a[8][kParTerms];
+  double2 b[8][kParTerms];
+};
+
+__device__ __forceinline__ void load_sersm(const DevCtx* __restrict__ ctx, SerSm& s) {
+  const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+  const int nth = blockDim.x * blockDim.y;
+  for (int i = tid; i < 8 * kParTerms; i += nth) {
+    const int k = i / kParTerms, p = i - k * kParTerms;
+    s.a[k][p] = ctx->pser.a[k + 2][p];
+    s.b[k][p] = ctx->pser.b[k + 2][p];
+  }
+  if (tid < 8) {
+    s.par[tid] = ctx->pser.par[tid + 2];
+    s.nt[tid] = ctx->pser.nt[tid + 2];
+  }
+}
+
+struct DN {
+  cplx d[3];  // d1, d2, d3
+  cplx n[5];  // n1, n2, n4, n5, n7
+};
+
+// sum_p (a_p + b_p ln r) u^p * r^par, Horner in u = r^2.
+__device__ __forceinline__ cplx par_series(const SerSm& S, int k, double u,
+                                           double logr, double r) {
+  const int nt = S.nt[k];
+  cplx A = mk(0.0), B = mk(0.0);
+  for (int p = nt - 1; p >= 0; --p) {
+    const double2 a = S.a[k][p], b = S.b[k][p];
+    A = mk(fma(A.re, u, a.x), fma(A.im, u, a.y));
+    B = mk(fma(B.re, u, b.x), fma(B.im, u, b.y));
+  }
+  cplx v = mk(fma(B.re, logr, A.re), fma(B.im, logr, A.im));
+  return S.par[k] ? v * r : v;
+}
+
+// H0, H1 with ln(x/2) supplied by the caller (small-argument branch).
+__device__ __forceinline__ void hankel01_lg(double x, double log_half_x,
+                                            cplx& h0, cplx& h1) {
+  if (x <= 8.0) {
+    const double q = x * 0.125;
+    const double t = q * q;
+    const double j0 = clenshaw01(kJ0Small, t);
+    const double j1 = clenshaw01(kJ1Small, t) * x;
+    const double lg = kTwoOverPi * (log_half_x + kEulerGamma);
+    const double y0 = fma(lg, j0, clenshaw01(kV0Small, t));
+    const double y1 = clenshaw01(kV1Small, t) * x + lg * j1 - kTwoOverPi / x;
+    h0 = mk(j0, y0);
+    h1 = mk(j1, y1);
+    return;
+  }
+  hankel01(x, h0, h1);
+}
+
+// kRem = false: full d and n (proxy blocks, kernel_cross_block);
+// kRem = true: full d, remainder n (PairIntegrator::separated).
+template <bool kRem>
+__device__ __forceinline__ void dn_eval(const DevMedium& m, const SerSm& S,
+                                        double r, double ir, double logr,
+                                        DN& o) {
+  const double ir2 = ir * ir;
+  if (r < m.series_radius) {
+    const double u = r * r;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) o.d[k] = par_series(S, k, u, logr, r);
+    o.d[0].re += m.sd1 * ir;
+    o.d[1].re -= m.sd1 * ir;
+    o.d[2].re += m.sd3 * ir;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      o.n[k] = par_series(S, 3 + k, u, logr, r);
+      if (!kRem) o.n[k].re += m.sn[k] * ir2;
+    }
+    return;
+  }
+  const double kT = m.kT, kL = m.kL, mu = m.mu, ar = m.aratio;
+  const double zT = kT * r, zL = kL * r;
+  cplx h0T, h1T, h0L, h1L;
+  hankel01_lg(zT, logr + m.log_half_kT, h0T, h1T);
+  hankel01_lg(zL, logr + m.log_half_kL, h0L, h1L);
+  auto i4 = [](cplx z) { return mk(-0.25 * z.im, 0.25 * z.re); };
+  const double izT = ir * m.inv_kT, izL = ir * m.inv_kL;
+  const cplx chiL = i4(h0L);
+  const cplx chiT1 = -(kT * i4(h1T));
+  const cplx chiL1 = -(kL * i4(h1L));
+  const cplx chiT2 = -(kT * kT) * i4(h0T - h1T * izT);
+  const cplx chiL2 = -(kL * kL) * i4(h0L - h1L * izL);
+  const cplx chiT3 = -(kT * kT * kT) * i4(-h1T - h0T * izT + (2.0 * izT * izT) * h1T);
+  const cplx chiL3 = -(kL * kL * kL) * i4(-h1L - h0L * izL + (2.0 * izL * izL) * h1L);
+  const cplx chiT4 = -(kT * kT * kT * kT) *
+                     i4(-h0T + (2.0 * izT) * h1T + (3.0 * izT * izT) * h0T -
+                        (6.0 * izT * izT * izT) * h1T);
+  const cplx chiL4 = -(kL * kL * kL * kL) *
+                     i4(-h0L + (2.0 * izL) * h1L + (3.0 * izL * izL) * h0L -
+                        (6.0 * izL * izL * izL) * h1L);
+  const double ikT2 = m.inv_kT * m.inv_kT;
+  const cplx psi1 = (chiT1 - chiL1) * ikT2;
+  const cplx psi2 = (chiT2 - chiL2) * ikT2;
+  const cplx psi3 = (chiT3 - chiL3) * ikT2;
+  const cplx psi4 = (chiT4 - chiL4) * ikT2;
+  const cplx gchi = psi2 - psi1 * ir;
+  const cplx w = gchi * ir;
+  const cplx gam = gchi * ir2;
+  const cplx bet = (psi3 - 3.0 * w) * ir;
+  const cplx alf = psi4 - (6.0 * ir) * psi3 + 15.0 * gam;
+  o.d[0] = ar * chiL1 + 2.0 * w;
+  o.d[1] = chiT1 + 2.0 * w;
+  o.d[2] = 2.0 * (psi3 - 3.0 * w);
+  o.n[0] = (-2.0 * mu * ir) * chiT1 - (4.0 * mu) * gam;
+  o.n[1] = (-mu) * (chiT2 - chiT1 * ir) - (4.0 * mu) * bet;
+  o.n[2] = (-4.0 * mu) * alf;
+  o.n[3] = m.c_n5 * chiL - (4.0 * mu * ar * ir) * chiL1 - (4.0 * mu) * gam;
+  o.n[4] = (-2.0 * mu * ar) * (chiL2 - chiL1 * ir) - (4.0 * mu) * bet;
+  if (kRem) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) o.n[k].re -= m.sn[k] * ir2;
+  }
+}
+
+__device__ __forceinline__ void combine_D(const DN& s, double zx, double zy,
+                                          double nyx, double nyy, CMat2& m) {
+  const double nz = nyx * zx + nyy * zy;
+  const cplx d1 = s.d[0], d2 = s.d[1], d3 = s.d[2];
+  m.a[0] = -(d1 * (nyx * zx) + d2 * (nz + nyx * zx) + d3 * (nz * zx * zx));
+  m.a[1] = -(d1 * (nyy * zx) + d2 * (nyx * zy) + d3 * (nz * zx * zy));
+  m.a[2] = -(d1 * (nyx * zy) + d2 * (nyy * zx) + d3 * (nz * zy * zx));
+  m.a[3] = -(d1 * (nyy * zy) + d2 * (nz + nyy * zy) + d3 * (nz * zy * zy));
+}
+
+__device__ __forceinline__ void combine_N(const DN& s, double zx, double zy,
+                                          double mx, double my, double nx,
+                                          double ny, CMat2& out) {
+  const double mn = mx * nx + my * ny;
+  const double mz = mx * zx + my * zy;
+  const double nz = nx * zx + ny * zy;
+  const double mv[2] = {mx, my}, nv[2] = {nx, ny}, zv[2] = {zx, zy};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double dij = (i == j) ? 1.0 : 0.0;
+      const double c1 = mn * dij + nv[i] * mv[j];
+      const double c2 = mn * zv[i] * zv[j] + mz * nz * dij + mz * nv[i] * zv[j] +
+                        nz * zv[i] * mv[j];
+      const double c4 = mz * nz * zv[i] * zv[j];
+      const double c5 = mv[i] * nv[j];
+      const double c7 = mz * zv[i] * nv[j] + nz * mv[i] * zv[j];
+      out.a[2 * i + j] = s.n[0] * c1 + s.n[1] * c2 + s.n[2] * c4 +
+                         s.n[3] * c5 + s.n[4] * c7;
+    }
+  }
+}
+
 }  // namespace ebem_gpu

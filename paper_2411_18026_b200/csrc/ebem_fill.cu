@@ -89,11 +89,17 @@ __device__ __forceinline__ int bidx(int la, int lb, int i, int j) {
 // --------------------------------------------------------------- separated
 // One thread per element pair.  Pairs that touch (coincident / adjacent) are
 // skipped here and produced by k_near_singular.
-__global__ void __launch_bounds__(128)
+#ifndef EBEM_NEAR_MINB
+#define EBEM_NEAR_MINB 3
+#endif
+__global__ void __launch_bounds__(128, EBEM_NEAR_MINB)
 k_near_separated(const DevCtx* __restrict__ ctx, const NearJob* __restrict__ jobs,
                  const long long* __restrict__ job_pair_off, int n_jobs,
                  const int* __restrict__ elems, long long n_pairs,
                  double* __restrict__ bundles, unsigned long long* points) {
+  __shared__ SerSm S;
+  load_sersm(ctx, S);
+  __syncthreads();
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   const int jb = find_job(job_pair_off, n_jobs, p);
@@ -142,14 +148,17 @@ k_near_separated(const DevCtx* __restrict__ ctx, const NearJob* __restrict__ job
       const double zy = xy - (pby + t * dby);
       const double r = hypot(zx, zy);
       const double ir = 1.0 / r;
+      const double logr = log(r);
       const double zhx = ir * zx, zhy = ir * zy;
-      Scalars fs, rs;
-      scalars_split(ctx, r, fs, rs);
+      DN dn;
+      dn_eval<true>(ctx->med, S, r, ir, logr, dn);
       CMat2 dm, nm;
-      combine_D(fs, zhx, zhy, nyx, nyy, dm);
-      combine_N(rs, zhx, zhy, nxx, nxy, nyx, nyy, nm);
-      double qm[4];
-      q0_kernel(qfac, r, zhx, zhy, qm);
+      combine_D(dn, zhx, zhy, nyx, nyy, dm);
+      combine_N(dn, zhx, zhy, nxx, nxy, nyx, nyy, nm);
+      // integrated-by-parts static hypersingular kernel (q0_kernel)
+      const double lq = qfac * logr;
+      const double qm[4] = {lq - qfac * (zhx * zhx), -qfac * (zhx * zhy),
+                            -qfac * (zhx * zhy), lq - qfac * (zhy * zhy)};
       const double ww = ws * wt;
       const double wgt = ww * hx * hy;
       // K = D + alpha N (the reference adds alpha N at scatter time)
@@ -385,12 +394,18 @@ k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pa
 // of both orientations go through shared memory and are reduced over i.
 constexpr int kProxyThreads = 256;
 
-__global__ void __launch_bounds__(kProxyThreads)
+#ifndef EBEM_PROXY_MINB
+#define EBEM_PROXY_MINB 2
+#endif
+__global__ void __launch_bounds__(kProxyThreads, EBEM_PROXY_MINB)
 k_proxy_pairs(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ jobs,
               const int* __restrict__ job_block_off, int n_jobs,
               const int* __restrict__ elems, double* __restrict__ bundles,
               int kProxyPairs) {
   extern __shared__ double2 sh[];  // [kProxyPairs * ng][2 orient][2][4]
+  __shared__ SerSm S;
+  load_sersm(ctx, S);
+  __syncthreads();
   const int ng = ctx->proxy_n;
   const int m = ctx->m_prime;
   const int jb = find_job(job_block_off, n_jobs, (int)blockIdx.x);
@@ -438,8 +453,8 @@ k_proxy_pairs(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ jobs,
       const double r = hypot(zx, zy);
       const double ir = 1.0 / r;
       const double zhx = ir * zx, zhy = ir * zy;
-      Scalars fs;
-      scalars_full(ctx, r, fs);
+      DN fs;
+      dn_eval<false>(ctx->med, S, r, ir, log(r), fs);
       CMat2 dm, nm;
       // V: test on the polygon (normal pn), trial on the curve (normal mn)
       combine_D(fs, zhx, zhy, mnx, mny, dm);

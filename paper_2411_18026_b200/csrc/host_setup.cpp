@@ -133,6 +133,19 @@ DevMedium make_medium(double lam, double mu, double rho, double omega,
   m.ccon = (lam + mu) / (8.0 * kPiD * (lam + 2.0 * mu));
   m.alpha_re = alpha_re;
   m.alpha_im = alpha_im;
+  m.inv_kT = 1.0 / m.kT;
+  m.inv_kL = 1.0 / m.kL;
+  m.log_half_kT = std::log(0.5 * m.kT);
+  m.log_half_kL = std::log(0.5 * m.kL);
+  const double l2m = lam + 2.0 * mu;
+  m.sd1 = mu / (2.0 * kPiD * l2m);
+  m.sd3 = -8.0 * m.cconst;
+  m.sn[0] = mu * mu / (kPiD * l2m);
+  m.sn[1] = mu * lam / (kPiD * l2m);
+  m.sn[2] = -8.0 * m.qfactor;
+  m.sn[3] = mu * (lam - mu) / (kPiD * l2m);
+  m.sn[4] = 2.0 * mu * mu / (kPiD * l2m);
+  m.c_n5 = lam * m.aratio * m.kL * m.kL;
   return m;
 }
 
@@ -190,6 +203,31 @@ int build_series(const DevMedium& m, double* out, int max_pow) {
     }
   }
   return maxq;
+}
+
+void build_parity_series(const double* dense, int max_pow, ParSeries& ps) {
+  for (int k = 0; k < 10; ++k) {
+    int lo = -1, hi = -1;
+    for (int q = 0; q < max_pow; ++q) {
+      const double* c = dense + (k * max_pow + q) * 4;
+      if (c[0] != 0.0 || c[1] != 0.0 || c[2] != 0.0 || c[3] != 0.0) {
+        if (lo < 0) lo = q;
+        hi = q;
+        if ((q - lo) % 2 != 0)
+          throw std::logic_error("KernelScalars: series of mixed parity");
+      }
+    }
+    ps.par[k] = lo < 0 ? 0 : lo % 2;
+    ps.nt[k] = lo < 0 ? 0 : (hi - ps.par[k]) / 2 + 1;
+    if (ps.nt[k] > kParTerms)
+      throw std::logic_error("KernelScalars: series longer than the device table");
+    for (int p = 0; p < kParTerms; ++p) {
+      const int q = ps.par[k] + 2 * p;
+      const double* c = (p < ps.nt[k] && q < max_pow) ? dense + (k * max_pow + q) * 4 : nullptr;
+      ps.a[k][p] = c ? double2{c[0], c[1]} : double2{0.0, 0.0};
+      ps.b[k][p] = c ? double2{c[2], c[3]} : double2{0.0, 0.0};
+    }
+  }
 }
 
 void gauss_rule(int n, double* x, double* w) {

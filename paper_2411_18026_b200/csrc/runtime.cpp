@@ -194,6 +194,7 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   hctx_.n_nodes = n;
   try {
     hctx_.series_maxq = build_series(med, hctx_.series, kMaxSeriesPow);
+    build_parity_series(hctx_.series, kMaxSeriesPow, hctx_.pser);
   } catch (const std::logic_error& e) {
     throw Error(EBEM_LOGIC_ERROR, e.what());
   }
