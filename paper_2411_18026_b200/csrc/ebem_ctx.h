@@ -40,6 +40,15 @@ struct ParSeries {
   double2 b[10][kParTerms];
 };
 
+// Fill-kernel parameter block (passed by value as a __grid_constant__
+// kernel argument): medium constants + the D/N remainder series (scalars
+// d1 d2 d3 n1 n2 n4 n5 n7) as coefficients of u^p, u = r^2.
+struct FillConst {
+  DevMedium med;
+  double2 a[8][kParTerms];
+  double2 b[8][kParTerms];
+};
+
 // Element geometry, structure of arrays over the N elements (element e runs
 // from node e to node (e+1) mod N): p = start node, d = end - start, t = unit
 // tangent, n = unit normal (+90 deg rotation of t), h = length.

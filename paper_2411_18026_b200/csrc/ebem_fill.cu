@@ -92,14 +92,20 @@ __device__ __forceinline__ int bidx(int la, int lb, int i, int j) {
 #ifndef EBEM_NEAR_MINB
 #define EBEM_NEAR_MINB 3
 #endif
+template <int NT>
 __global__ void __launch_bounds__(128, EBEM_NEAR_MINB)
-k_near_separated(const DevCtx* __restrict__ ctx, const NearJob* __restrict__ jobs,
+k_near_separated(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
+                 const NearJob* __restrict__ jobs,
                  const long long* __restrict__ job_pair_off, int n_jobs,
                  const int* __restrict__ elems, long long n_pairs,
                  double* __restrict__ bundles, unsigned long long* points) {
+#if !EBEM_SERIES_PARAM
   __shared__ SerSm S;
   load_sersm(ctx, S);
   __syncthreads();
+#else
+  const SerSm& S = *reinterpret_cast<const SerSm*>(ctx);  // unused
+#endif
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   const int jb = find_job(job_pair_off, n_jobs, p);
@@ -151,7 +157,7 @@ k_near_separated(const DevCtx* __restrict__ ctx, const NearJob* __restrict__ job
       const double logr = log(r);
       const double zhx = ir * zx, zhy = ir * zy;
       DN dn;
-      dn_eval<true>(ctx->med, S, r, ir, logr, dn);
+      dn_eval2<true, NT>(fc, S, r, ir, logr, dn);
       CMat2 dm, nm;
       combine_D(dn, zhx, zhy, nyx, nyy, dm);
       combine_N(dn, zhx, zhy, nxx, nxy, nyx, nyy, nm);
@@ -397,15 +403,21 @@ constexpr int kProxyThreads = 256;
 #ifndef EBEM_PROXY_MINB
 #define EBEM_PROXY_MINB 2
 #endif
+template <int NT>
 __global__ void __launch_bounds__(kProxyThreads, EBEM_PROXY_MINB)
-k_proxy_pairs(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ jobs,
+k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
+              const ProxyJob* __restrict__ jobs,
               const int* __restrict__ job_block_off, int n_jobs,
               const int* __restrict__ elems, double* __restrict__ bundles,
               int kProxyPairs) {
   extern __shared__ double2 sh[];  // [kProxyPairs * ng][2 orient][2][4]
+#if !EBEM_SERIES_PARAM
   __shared__ SerSm S;
   load_sersm(ctx, S);
   __syncthreads();
+#else
+  const SerSm& S = *reinterpret_cast<const SerSm*>(ctx);  // unused
+#endif
   const int ng = ctx->proxy_n;
   const int m = ctx->m_prime;
   const int jb = find_job(job_block_off, n_jobs, (int)blockIdx.x);
@@ -454,7 +466,7 @@ k_proxy_pairs(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ jobs,
       const double ir = 1.0 / r;
       const double zhx = ir * zx, zhy = ir * zy;
       DN fs;
-      dn_eval<false>(ctx->med, S, r, ir, log(r), fs);
+      dn_eval2<false, NT>(fc, S, r, ir, log(r), fs);
       CMat2 dm, nm;
       // V: test on the polygon (normal pn), trial on the curve (normal mn)
       combine_D(fs, zhx, zhy, mnx, mny, dm);
@@ -560,14 +572,34 @@ k_gather(const GatherJob* __restrict__ jobs, const long long* __restrict__ job_e
 }
 
 // ------------------------------------------------------------ host wrappers
-void launch_near_separated(const DevCtx* ctx, const NearJob* jobs,
-                           const long long* job_pair_off, int n_jobs,
-                           const int* elems, long long n_pairs, double* bundles,
-                           unsigned long long* points, cudaStream_t st) {
+int fill_nt_bucket(int nt) {
+  for (int b : {8, 12, 16, 20, kParTerms})
+    if (nt <= b) return b;
+  return -1;
+}
+
+#define EBEM_NT_DISPATCH(NTV, CALL) \
+  switch (NTV) {                    \
+    case 8: CALL(8); break;         \
+    case 12: CALL(12); break;       \
+    case 16: CALL(16); break;       \
+    case 20: CALL(20); break;       \
+    default: CALL(kParTerms); break; \
+  }
+
+void launch_near_separated(const DevCtx* ctx, const FillConst& fc, int nt,
+                           const NearJob* jobs, const long long* job_pair_off,
+                           int n_jobs, const int* elems, long long n_pairs,
+                           double* bundles, unsigned long long* points,
+                           cudaStream_t st) {
   if (n_pairs <= 0) return;
   const int bs = 128;
-  k_near_separated<<<(unsigned)((n_pairs + bs - 1) / bs), bs, 0, st>>>(
-      ctx, jobs, job_pair_off, n_jobs, elems, n_pairs, bundles, points);
+  const unsigned grid = (unsigned)((n_pairs + bs - 1) / bs);
+#define EBEM_NEAR_CALL(N)                                                   \
+  k_near_separated<N><<<grid, bs, 0, st>>>(ctx, fc, jobs, job_pair_off, n_jobs, \
+                                           elems, n_pairs, bundles, points)
+  EBEM_NT_DISPATCH(fill_nt_bucket(nt), EBEM_NEAR_CALL)
+#undef EBEM_NEAR_CALL
 }
 
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,
@@ -588,21 +620,23 @@ int proxy_blocks_for(int m_prime, int nE, int n_gauss) {
   return (m_prime * nE + p - 1) / p;
 }
 
-void launch_proxy_pairs(const DevCtx* ctx, int n_gauss, const ProxyJob* jobs,
+void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int nt,
+                        int n_gauss, const ProxyJob* jobs,
                         const int* job_block_off, int n_jobs, int n_blocks,
                         const int* elems, double* bundles, cudaStream_t st) {
   if (n_blocks <= 0) return;
   const int p = proxy_pairs_per_block(n_gauss);
   const int threads = p * n_gauss;
   const size_t shmem = size_t(threads) * 16 * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_proxy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kProxyThreads * 16 * (int)sizeof(double2));
-    attr = true;
-  }
-  k_proxy_pairs<<<n_blocks, threads, shmem, st>>>(ctx, jobs, job_block_off,
-                                                  n_jobs, elems, bundles, p);
+#define EBEM_PROXY_CALL(N)                                                      \
+  do {                                                                          \
+    cudaFuncSetAttribute(k_proxy_pairs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         kProxyThreads * 16 * (int)sizeof(double2));            \
+    k_proxy_pairs<N><<<n_blocks, threads, shmem, st>>>(ctx, fc, jobs, job_block_off, \
+                                                       n_jobs, elems, bundles, p); \
+  } while (0)
+  EBEM_NT_DISPATCH(fill_nt_bucket(nt), EBEM_PROXY_CALL)
+#undef EBEM_PROXY_CALL
 }
 
 void launch_gather(const GatherJob* jobs, const long long* job_entry_off,

@@ -9,15 +9,18 @@
 namespace ebem_gpu {
 
 // ---- fill (ebem_fill.cu)
-void launch_near_separated(const DevCtx* ctx, const NearJob* jobs,
-                           const long long* job_pair_off, int n_jobs,
-                           const int* elems, long long n_pairs, double* bundles,
-                           unsigned long long* points, cudaStream_t st);
+int fill_nt_bucket(int nt);
+void launch_near_separated(const DevCtx* ctx, const FillConst& fc, int nt,
+                           const NearJob* jobs, const long long* job_pair_off,
+                           int n_jobs, const int* elems, long long n_pairs,
+                           double* bundles, unsigned long long* points,
+                           cudaStream_t st);
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,
                           const int* pair_elems, int n, double* bundles, int* bad,
                           cudaStream_t st);
 int proxy_blocks_for(int m_prime, int nE, int n_gauss);
-void launch_proxy_pairs(const DevCtx* ctx, int n_gauss, const ProxyJob* jobs,
+void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int nt,
+                        int n_gauss, const ProxyJob* jobs,
                         const int* job_block_off, int n_jobs, int n_blocks,
                         const int* elems, double* bundles, cudaStream_t st);
 void launch_gather(const GatherJob* jobs, const long long* job_entry_off,

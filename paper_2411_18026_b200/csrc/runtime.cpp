@@ -195,6 +195,19 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   try {
     hctx_.series_maxq = build_series(med, hctx_.series, kMaxSeriesPow);
     build_parity_series(hctx_.series, kMaxSeriesPow, hctx_.pser);
+    fc_.med = med;
+    for (int k = 0; k < 8; ++k) {
+      const int par = hctx_.pser.par[k + 2];
+      if (par != (k < 3 ? 1 : 0))
+        throw std::logic_error("KernelScalars: unexpected series parity");
+      fc_nt_ = std::max(fc_nt_, hctx_.pser.nt[k + 2]);
+      for (int p = 0; p < kParTerms; ++p) {
+        fc_.a[k][p] = hctx_.pser.a[k + 2][p];
+        fc_.b[k][p] = hctx_.pser.b[k + 2][p];
+      }
+    }
+    if (fill_nt_bucket(fc_nt_) < 0)
+      throw std::logic_error("KernelScalars: series longer than the device table");
   } catch (const std::logic_error& e) {
     throw Error(EBEM_LOGIC_ERROR, e.what());
   }
@@ -514,14 +527,14 @@ void Problem::execute(FillPlan& plan) {
     for (const ProxyJob& j : plan.proxy_)
       pts += double(pcfg_.m_prime) * j.nE * pcfg_.n_gauss * pcfg_.n_gauss;
     g_prof.begin(st_);
-    launch_proxy_pairs(dctx(), pcfg_.n_gauss, pk.at<ProxyJob>(plan_dev, o_pj),
+    launch_proxy_pairs(dctx(), fc_, fc_nt_, pcfg_.n_gauss, pk.at<ProxyJob>(plan_dev, o_pj),
                        pk.at<int>(plan_dev, o_pb), int(plan.proxy_.size()),
                        plan.proxy_blocks_, el, bundles.get(), st_);
     g_prof.end(KP_PROXY, st_, pts);
   }
   if (plan.near_pairs_ > 0) {
     g_prof.begin(st_);
-    launch_near_separated(dctx(), pk.at<NearJob>(plan_dev, o_nj),
+    launch_near_separated(dctx(), fc_, fc_nt_, pk.at<NearJob>(plan_dev, o_nj),
                           pk.at<long long>(plan_dev, o_nl), int(plan.near_.size()),
                           el, plan.near_pairs_, bundles.get(),
                           g_prof.on ? g_prof.near_points : nullptr, st_);

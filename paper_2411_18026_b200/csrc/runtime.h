@@ -213,6 +213,8 @@ class Problem {
   ebem_assembly_config acfg_;
   ebem_proxy_config pcfg_;
   DevCtx hctx_{};
+  FillConst fc_{};
+  int fc_nt_ = 0;
   DBuf<DevCtx> dctx_;
   DBuf<double> delem_, dxy_;
   cudaStream_t st_ = nullptr;
