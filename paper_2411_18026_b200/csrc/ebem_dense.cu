@@ -30,6 +30,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef EBEM_QR_THREADS
+#define EBEM_QR_THREADS 512
+#endif
+constexpr int kQrThreads = EBEM_QR_THREADS;  // QR / CPQR / LU CTAs
 
 __device__ __forceinline__ double2 zmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -79,7 +83,7 @@ __device__ double block_sum(double v, double* red) {
   __syncthreads();
   double s = 0.0;
   if (threadIdx.x < 32) {
-    s = threadIdx.x < kWarps ? red[threadIdx.x] : 0.0;
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     s = warp_sum(s);
     if (threadIdx.x == 0) red[0] = s;
   }
@@ -138,7 +142,8 @@ __device__ void apply_reflector(double2* A, int m, int ld, int i, int col,
   const double2 ctau = zconj(tau);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const double2* v = A + (size_t)col * ld;
-  for (int j = c0 + w; j < n; j += kWarps) {
+  const int nw = blockDim.x >> 5;
+  for (int j = c0 + w; j < n; j += nw) {
     double2* cj = A + (size_t)j * ld;
     // s = v^H c_j
     double2 s = make_double2(0.0, 0.0);
@@ -158,10 +163,10 @@ __device__ void apply_reflector(double2* A, int m, int ld, int i, int col,
 }  // namespace
 
 // ------------------------------------------------------------ QR reduction
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kQrThreads)
 k_qr_reduce(const QrTask* __restrict__ tasks, double2* __restrict__ gws) {
   extern __shared__ double2 smem[];
-  __shared__ double red[kWarps + 1];
+  __shared__ double red[33];
   const QrTask T = tasks[blockIdx.x];
   const int m = T.rows, n = T.n;
   double2* A = T.in_smem ? smem : gws + T.ws_off;
@@ -183,10 +188,11 @@ k_qr_reduce(const QrTask* __restrict__ tasks, double2* __restrict__ gws) {
 }
 
 // --------------------------------------------------------------------- CPQR
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kQrThreads)
 k_cpqr(const CpqrTask* __restrict__ tasks, double2* __restrict__ gws) {
   extern __shared__ double2 smem[];
-  __shared__ double red[kWarps + 1];
+  __shared__ double red[33];
+  const int nw = blockDim.x >> 5;
   __shared__ double vn1[kMaxCpqrCols], vn2[kMaxCpqrCols];
   __shared__ int jp[kMaxCpqrCols];
   __shared__ int s_pvt;
@@ -199,7 +205,7 @@ k_cpqr(const CpqrTask* __restrict__ tasks, double2* __restrict__ gws) {
   __syncthreads();
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   // initial column norms
-  for (int j = w; j < n; j += kWarps) {
+  for (int j = w; j < n; j += nw) {
     const double2* c = A + (size_t)j * m;
     double s = 0.0;
     for (int r = l; r < m; r += 32) s = fma(c[r].x, c[r].x, fma(c[r].y, c[r].y, s));
@@ -264,7 +270,7 @@ k_cpqr(const CpqrTask* __restrict__ tasks, double2* __restrict__ gws) {
     apply_reflector(A, m, m, i, i, tau, i + 1, n);
     __syncthreads();
     // partial norm downdate (zlaqp2)
-    for (int j = i + 1 + w; j < n; j += kWarps) {
+    for (int j = i + 1 + w; j < n; j += nw) {
       const double v1 = vn1[j];
       if (v1 == 0.0) continue;
       const double2 aij = A[(size_t)j * m + i];
@@ -340,7 +346,7 @@ k_interp(const InterpTask* __restrict__ tasks) {
 }
 
 // ----------------------------------------------------------------------- LU
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kQrThreads)
 k_getrf(const LuTask* __restrict__ tasks, double2* __restrict__ gws) {
   extern __shared__ double2 smem[];
   __shared__ int s_p;
@@ -391,7 +397,7 @@ k_getrf(const LuTask* __restrict__ tasks, double2* __restrict__ gws) {
     }
     __syncthreads();
     // rank-1 update of the trailing block, one warp per column
-    for (int j = k + 1 + w; j < n; j += kWarps) {
+    for (int j = k + 1 + w; j < n; j += (int)(blockDim.x >> 5)) {
       const double2 akj = A[(size_t)j * n + k];
       for (int r = k + 1 + l; r < n; r += 32)
         A[(size_t)j * n + r] = zfms(A[(size_t)j * n + r], A[(size_t)k * n + r], akj);
@@ -569,12 +575,12 @@ void dense_init() {
 void launch_qr_reduce(const QrTask* tasks, int n, size_t smem, double2* gws,
                       cudaStream_t st) {
   if (n <= 0) return;
-  k_qr_reduce<<<n, kThreads, smem, st>>>(tasks, gws);
+  k_qr_reduce<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
 void launch_cpqr(const CpqrTask* tasks, int n, size_t smem, double2* gws,
                  cudaStream_t st) {
   if (n <= 0) return;
-  k_cpqr<<<n, kThreads, smem, st>>>(tasks, gws);
+  k_cpqr<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
 void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st) {
   if (n <= 0) return;
@@ -584,7 +590,7 @@ void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st) {
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st) {
   if (n <= 0) return;
-  k_getrf<<<n, kThreads, smem, st>>>(tasks, gws);
+  k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
 int getrs_blocks(int nrhs) { return (nrhs + kWarps - 1) / kWarps; }
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,

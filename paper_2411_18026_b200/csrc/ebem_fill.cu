@@ -394,6 +394,182 @@ k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pa
   store_bundle(bundles, pairs[t], v);
 }
 
+// ------------------------------------------------------- symmetric near
+// Tier class of every sym pair (0..3 = far, far+2, far+5, far+9 points;
+// 7 = touching pair, handled by k_near_singular), for the bucketing sort.
+__global__ void __launch_bounds__(256)
+k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
+               const long long* __restrict__ job_off, int n_jobs,
+               const int* __restrict__ elems, long long n_pairs,
+               unsigned char* __restrict__ keys, int* __restrict__ vals) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= n_pairs) return;
+  const int jb = find_job(job_off, n_jobs, p);
+  const SymJob J = jobs[jb];
+  const long long local = p - J.local_off;
+  const int a = int(local / J.nE);
+  const int q = int(local - (long long)a * J.nE);
+  const int ea = __ldg(elems + J.a_off + a);
+  const int eb = __ldg(elems + J.e_off + q);
+  const int N = ctx->n_nodes;
+  const int na = ea + 1 == N ? 0 : ea + 1;
+  const int nb = eb + 1 == N ? 0 : eb + 1;
+  unsigned char key = 7;
+  if (!(ea == eb || na == eb || nb == ea)) {
+    const double hx = ef(ctx, EH, ea), hy = ef(ctx, EH, eb);
+    const double rq = element_distance(ctx, ea, eb) / fmax(hx, hy);
+    key = rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3;
+  }
+  keys[p] = key;
+  vals[p] = int(p);
+}
+
+// CTA = P pairs x n threads; thread (pair, i) fixes the test point s_i on the
+// enclosed element and sweeps the n points on the cell element, evaluating
+// the scalars once for both orientations (r is symmetric).
+__global__ void __launch_bounds__(256, 2)
+k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
+           const long long* __restrict__ job_off, int n_jobs,
+           const int* __restrict__ elems, const int* __restrict__ pair_ids,
+           int count, int n, double* __restrict__ bundles) {
+  extern __shared__ double2 sh[];  // [P * n][8 V + 8 U cplx + 2 (Q as re/im pairs)]
+  __shared__ SerSm S;
+  load_sersm(ctx, S);
+  const int P = blockDim.x / n;
+  const int lp = threadIdx.x / n;
+  const int i = threadIdx.x - lp * n;
+  const int idx = blockIdx.x * P + lp;
+  const bool active = lp < P && idx < count;
+  const double* gx = ctx->gx + gauss_offset(n);
+  const double* gw = ctx->gw + gauss_offset(n);
+  __syncthreads();
+  int ea = 0, eb = 0;
+  long long vdst = 0, udst = 0;
+  if (active) {
+    const long long p = __ldg(pair_ids + idx);
+    const int jb = find_job(job_off, n_jobs, p);
+    const SymJob J = jobs[jb];
+    const long long local = p - J.local_off;
+    const int a = int(local / J.nE);
+    const int q = int(local - (long long)a * J.nE);
+    ea = __ldg(elems + J.a_off + a);
+    eb = __ldg(elems + J.e_off + q);
+    vdst = J.v_off + local;
+    udst = J.u_off + (long long)q * J.nA + a;
+    const double pax = ef(ctx, EPX, ea), pay = ef(ctx, EPY, ea);
+    const double dax = ef(ctx, EDX, ea), day = ef(ctx, EDY, ea);
+    const double pbx = ef(ctx, EPX, eb), pby = ef(ctx, EPY, eb);
+    const double dbx = ef(ctx, EDX, eb), dby = ef(ctx, EDY, eb);
+    const double nax = ef(ctx, ENX, ea), nay = ef(ctx, ENY, ea);
+    const double nbx = ef(ctx, ENX, eb), nby = ef(ctx, ENY, eb);
+    const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
+    const double qfac = ctx->med.qfactor;
+    const double s = __ldg(gx + i);
+    const double xx = pax + s * dax, xy = pay + s * day;
+    cplx rv[2][4], ru[2][4];
+    double Q[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) rv[b][e] = ru[b][e] = mk(0.0);
+    for (int j = 0; j < n; ++j) {
+      const double t = __ldg(gx + j);
+      const double wj = __ldg(gw + j);
+      const double zx = xx - (pbx + t * dbx);
+      const double zy = xy - (pby + t * dby);
+      const double r = hypot(zx, zy);
+      const double ir = 1.0 / r;
+      const double logr = log(r);
+      const double zhx = ir * zx, zhy = ir * zy;
+      DN dn;
+      dn_eval<true>(ctx->med, S, r, ir, logr, dn);
+      const double pt[2] = {wj * (1.0 - t), wj * t};
+      CMat2 dm, nm;
+      // V: test on the enclosed element (normal na), trial on the cell element
+      combine_D(dn, zhx, zhy, nbx, nby, dm);
+      combine_N(dn, zhx, zhy, nax, nay, nbx, nby, nm);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const cplx k = dm.a[e] + alpha * nm.a[e];
+        axpy(rv[0][e], pt[0], k);
+        axpy(rv[1][e], pt[1], k);
+      }
+      // U: test on the cell element, trial on the enclosed element
+      combine_D(dn, -zhx, -zhy, nax, nay, dm);
+      combine_N(dn, -zhx, -zhy, nbx, nby, nax, nay, nm);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const cplx k = dm.a[e] + alpha * nm.a[e];
+        axpy(ru[0][e], pt[0], k);
+        axpy(ru[1][e], pt[1], k);
+      }
+      // integrated-by-parts static hypersingular kernel (even in zh)
+      const double lq = qfac * logr;
+      Q[0] = fma(wj, lq - qfac * (zhx * zhx), Q[0]);
+      Q[1] = fma(wj, -qfac * (zhx * zhy), Q[1]);
+      Q[3] = fma(wj, lq - qfac * (zhy * zhy), Q[3]);
+    }
+    Q[2] = Q[1];
+    double2* my = sh + threadIdx.x * 18;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        my[b * 4 + e] = make_double2(rv[b][e].re, rv[b][e].im);
+        my[8 + b * 4 + e] = make_double2(ru[b][e].re, ru[b][e].im);
+      }
+    my[16] = make_double2(Q[0], Q[1]);
+    my[17] = make_double2(Q[2], Q[3]);
+  }
+  __syncthreads();
+  // reduction over i; each pair's first thread handles nothing special:
+  // threads stride over (pair, orientation, 16 outputs)
+  const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
+  for (int o = threadIdx.x; o < P * 2 * kBundle; o += blockDim.x) {
+    const int lp2 = o / (2 * kBundle);
+    const int rem = o - lp2 * 2 * kBundle;
+    const int orient = rem / kBundle;
+    const int k = rem - orient * kBundle;  // bidx(la, lb, i, j)
+    const int idx2 = blockIdx.x * P + lp2;
+    if (idx2 >= count) continue;
+    const int la = k >> 3, lb = (k >> 2) & 1, e = k & 3;
+    double ar = 0.0, ai = 0.0, qs = 0.0;
+    for (int ii = 0; ii < n; ++ii) {
+      const double sv = __ldg(gx + ii);
+      const double wi = __ldg(gw + ii);
+      const double shape = orient == 0 ? (la == 0 ? 1.0 - sv : sv)
+                                       : (lb == 0 ? 1.0 - sv : sv);
+      const int slot = orient == 0 ? (lb * 4 + e) : (8 + la * 4 + e);
+      const double2* row = sh + (lp2 * n + ii) * 18;
+      const double2 v = row[slot];
+      ar = fma(wi * shape, v.x, ar);
+      ai = fma(wi * shape, v.y, ai);
+      const double2 qq = row[16 + (e >> 1)];
+      qs = fma(wi, (e & 1) ? qq.y : qq.x, qs);
+    }
+    // element lengths of this pair (recomputed from the ids)
+    const long long p2 = __ldg(pair_ids + idx2);
+    const int jb2 = find_job(job_off, n_jobs, p2);
+    const SymJob J2 = jobs[jb2];
+    const long long local2 = p2 - J2.local_off;
+    const int a2 = int(local2 / J2.nE);
+    const int q2 = int(local2 - (long long)a2 * J2.nE);
+    const int ea2 = __ldg(elems + J2.a_off + a2);
+    const int eb2 = __ldg(elems + J2.e_off + q2);
+    const double hh = ef(ctx, EH, ea2) * ef(ctx, EH, eb2);
+    const double sg = (la == lb) ? 1.0 : -1.0;  // slope_la * slope_lb
+    const double re = fma(hh, ar, sg * qs * alpha.re);
+    const double im = fma(hh, ai, sg * qs * alpha.im);
+    const long long dst = orient == 0 ? J2.v_off + local2
+                                      : J2.u_off + (long long)q2 * J2.nA + a2;
+    reinterpret_cast<double2*>(bundles)[dst * kBundle + k] = make_double2(re, im);
+  }
+  (void)ea;
+  (void)eb;
+  (void)vdst;
+  (void)udst;
+}
+
 // ------------------------------------------------------------------- proxy
 // CTA = kProxyPairs element pairs x n_g threads; thread (pair, i) fixes the
 // polygon quadrature point s_i and sweeps the curve points t_j.  The row sums
@@ -600,6 +776,33 @@ void launch_near_separated(const DevCtx* ctx, const FillConst& fc, int nt,
                                            elems, n_pairs, bundles, points)
   EBEM_NT_DISPATCH(fill_nt_bucket(nt), EBEM_NEAR_CALL)
 #undef EBEM_NEAR_CALL
+}
+
+void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
+                         const long long* job_off, int n_jobs, const int* elems,
+                         long long n_pairs, unsigned char* keys, int* vals,
+                         cudaStream_t st) {
+  if (n_pairs <= 0) return;
+  k_sym_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, st>>>(
+      ctx, jobs, job_off, n_jobs, elems, n_pairs, keys, vals);
+}
+
+void launch_near_sym(const DevCtx* ctx, const SymJob* jobs,
+                     const long long* job_off, int n_jobs, const int* elems,
+                     const int* pair_ids, int count, int n, double* bundles,
+                     cudaStream_t st) {
+  if (count <= 0) return;
+  const int P = 256 / n;
+  const int threads = P * n;
+  const size_t smem = size_t(threads) * 18 * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_near_sym, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         256 * 18 * (int)sizeof(double2));
+    attr = true;
+  }
+  k_near_sym<<<(count + P - 1) / P, threads, smem, st>>>(
+      ctx, jobs, job_off, n_jobs, elems, pair_ids, count, n, bundles);
 }
 
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,

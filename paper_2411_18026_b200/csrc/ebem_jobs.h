@@ -43,6 +43,17 @@ struct ProxyJob {
   double cx, cy, radius;
 };
 
+// Both near blocks of one cell from one scalar evaluation per point:
+// pairs (a in enclosed elements A, q in cell elements E);
+// V bundle (test A[a], trial E[q]) at v_off + a * nE + q,
+// U bundle (test E[q], trial A[a]) at u_off + q * nA + a.
+struct SymJob {
+  long long v_off, u_off;
+  long long local_off;  // first pair of this job in the wave's sym numbering
+  int a_off, nA;
+  int e_off, nE;
+};
+
 // Scatter of bundles into one output block.
 struct GatherJob {
   long long pair_off;   // bundle index of (row element 0, col element 0)

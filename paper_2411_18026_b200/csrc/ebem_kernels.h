@@ -18,6 +18,21 @@ void launch_near_separated(const DevCtx* ctx, const FillConst& fc, int nt,
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,
                           const int* pair_elems, int n, double* bundles, int* bad,
                           cudaStream_t st);
+void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
+                         const long long* job_off, int n_jobs, const int* elems,
+                         long long n_pairs, unsigned char* keys, int* vals,
+                         cudaStream_t st);
+void launch_near_sym(const DevCtx* ctx, const SymJob* jobs,
+                     const long long* job_off, int n_jobs, const int* elems,
+                     const int* pair_ids, int count, int n, double* bundles,
+                     cudaStream_t st);
+// CUB radix sort of (key, value) by the low 3 key bits; temp grows as needed.
+void sort_pairs_by_class(unsigned char* keys_in, unsigned char* keys_out,
+                         int* vals_in, int* vals_out, long long n, void** temp,
+                         size_t* temp_bytes, cudaStream_t st);
+void launch_class_bounds(const unsigned char* sorted_keys, long long n,
+                         int* bounds /* 9 ints: start of class c, c = 0..8 */,
+                         cudaStream_t st);
 int proxy_blocks_for(int m_prime, int nE, int n_gauss);
 void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int nt,
                         int n_gauss, const ProxyJob* jobs,

@@ -24,11 +24,59 @@ namespace ebem_gpu {
 std::atomic<long long> g_launches{0};
 Profiler g_prof;
 
+namespace {
+double wall_now() {
+  return std::chrono::duration<double>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+std::vector<std::pair<std::string, double>>& phases() {
+  static std::vector<std::pair<std::string, double>> v;
+  return v;
+}
+}  // namespace
+
+int verbose_level() {
+  static const int v = [] {
+    const char* e = std::getenv("EBEM_VERBOSE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+void host_phase_add(const char* name, double seconds) {
+  for (auto& kv : phases())
+    if (kv.first == name) {
+      kv.second += seconds;
+      return;
+    }
+  phases().emplace_back(name, seconds);
+}
+
+void host_phase_dump() {
+  if (!verbose_level()) return;
+  double tot = 0.0;
+  for (auto& kv : phases()) tot += kv.second;
+  std::fprintf(stderr, "[ebem] host phases (total %.3f s):\n", tot);
+  for (auto& kv : phases())
+    std::fprintf(stderr, "[ebem]   %-18s %8.3f s\n", kv.first.c_str(), kv.second);
+  phases().clear();
+}
+
+PhaseTimer::PhaseTimer(const char* name, cudaStream_t st)
+    : name_(name), st_(st), t0_(verbose_level() ? wall_now() : 0.0) {}
+
+PhaseTimer::~PhaseTimer() {
+  if (!verbose_level()) return;
+  if (verbose_level() >= 2 && st_) cudaStreamSynchronize(st_);
+  host_phase_add(name_, wall_now() - t0_);
+}
+
 const char* kernel_name(int id) {
   static const char* names[KP_COUNT] = {
       "k_proxy_pairs", "k_near_separated", "k_near_singular", "k_gather",
       "k_qr_reduce", "k_cpqr", "k_interp", "k_getrf", "k_getrs", "k_gemm",
-      "k_copy", "k_rhs_plane"};
+      "k_copy", "k_rhs_plane", "k_near_sym"};
   return (id >= 0 && id < KP_COUNT) ? names[id] : "?";
 }
 
@@ -88,6 +136,46 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     throw Error(EBEM_CUDA_ERROR, std::string("CUDA error in ") + what + ": " +
                                      cudaGetErrorString(e));
+}
+
+Staging::~Staging() {
+  for (Slot& x : s_) {
+    if (x.ev) cudaEventSynchronize(x.ev);
+    if (x.host) cudaFreeHost(x.host);
+    if (x.dev) cudaFree(x.dev);
+    if (x.ev) cudaEventDestroy(x.ev);
+  }
+}
+
+char* Staging::put(const Pack& pk, cudaStream_t st) {
+  cur_ = (cur_ + 1) % int(s_.size());
+  Slot& x = s_[cur_];
+  if (!x.ev) CK(cudaEventCreateWithFlags(&x.ev, cudaEventDisableTiming));
+  if (x.pending) {
+    CK(cudaEventSynchronize(x.ev));
+    x.pending = false;
+  }
+  const size_t bytes = pk.bytes();
+  if (bytes > x.cap) {
+    const size_t cap = std::max(std::max(bytes + bytes / 2, 2 * x.cap), size_t(32) << 20);
+    if (x.host) CK(cudaFreeHost(x.host));
+    if (x.dev) CK(cudaFree(x.dev));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&x.host), cap));
+    CK(cudaMalloc(reinterpret_cast<void**>(&x.dev), cap));
+    x.cap = cap;
+  }
+  if (bytes) {
+    std::memcpy(x.host, pk.data(), bytes);
+    CK(cudaMemcpyAsync(x.dev, x.host, bytes, cudaMemcpyHostToDevice, st));
+  }
+  return x.dev;
+}
+
+void Staging::fence(cudaStream_t st) {
+  if (cur_ < 0) return;
+  Slot& x = s_[cur_];
+  CK(cudaEventRecord(x.ev, st));
+  x.pending = true;
 }
 
 void Pack::upload(DBuf<char>& dev, cudaStream_t st) {
@@ -262,6 +350,9 @@ Problem::~Problem() {
     cudaStreamSynchronize(st_);
     cudaStreamDestroy(st_);
   }
+  if (sort_temp_) cudaFree(sort_temp_);
+  if (sym_bounds_host_) cudaFreeHost(sym_bounds_host_);
+  if (sym_ev_) cudaEventDestroy(sym_ev_);
 }
 
 ProxyGeom Problem::build_proxy(int begin, int end) const {
@@ -301,6 +392,9 @@ void Problem::check_domain() {
 // ---------------------------------------------------------------- FillPlan
 void FillPlan::clear() {
   bundles_ = near_pairs_ = entries_ = 0;
+  sym_pairs_ = 0;
+  sym_.clear();
+  sym_off_.clear();
   proxy_blocks_ = 0;
   poly_desc_off_ = -1;
   elems_.clear();
@@ -319,6 +413,38 @@ void FillPlan::clear() {
 // elements g-1 and g), ascending and unique (proj/src/assembly.cpp:342-368).
 void FillPlan::elements_of(const Lists& nodes, std::vector<int>& out) const {
   out.clear();
+  const bool s0 = std::is_sorted(nodes[0].begin(), nodes[0].end());
+  const bool s1 = std::is_sorted(nodes[1].begin(), nodes[1].end());
+  if (s0 && s1) {
+    // Linear path for ascending lists (enclosed sets, leaf ranges): node g
+    // contributes g-1, g, already in order; node 0's element N-1 goes last.
+    auto gen = [&](const std::vector<int>& v, std::vector<int>& o) {
+      o.clear();
+      o.reserve(2 * v.size());
+      bool wrap = false;
+      for (int g : v) {
+        if (g == 0) {
+          wrap = true;
+        } else if (o.empty() || o.back() != g - 1) {
+          o.push_back(g - 1);
+        }
+        if (o.empty() || o.back() != g) o.push_back(g);
+      }
+      if (wrap && (o.empty() || o.back() != N_ - 1)) o.push_back(N_ - 1);
+    };
+    thread_local std::vector<int> a, b;
+    gen(nodes[0], a);
+    if (nodes[1] == nodes[0]) {
+      out = a;
+      return;
+    }
+    gen(nodes[1], b);
+    out.resize(a.size() + b.size());
+    out.erase(std::set_union(a.begin(), a.end(), b.begin(), b.end(), out.begin()),
+              out.end());
+    return;
+  }
+  out.reserve(4 * (nodes[0].size() + nodes[1].size()));
   for (int p = 0; p < 2; ++p)
     for (int g : nodes[p]) {
       out.push_back(g);
@@ -334,20 +460,29 @@ void FillPlan::node_descs(const Lists& nodes, const std::vector<int>& elems,
   auto idx = [&](int e) {
     return int(std::lower_bound(elems.begin(), elems.end(), e) - elems.begin());
   };
+  const int last = idx(N_ - 1);
   for (int p = 0; p < 2; ++p) {
-    for (size_t k = 0; k < nodes[p].size(); ++k) {
-      const int g = nodes[p][k];
+    const std::vector<int>& v = nodes[p];
+    const bool sorted = std::is_sorted(v.begin(), v.end());
+    int cur = 0;  // two-pointer position for ascending lists
+    for (size_t k = 0; k < v.size(); ++k) {
+      const int g = v[k];
       NodeDesc d;
       d.dest = dest_off[p] + int(k);
       int la1, la2;
       if (g == 0) {  // elements 0 (shape 0) and N-1 (shape 1)
         d.e1 = idx(0);
-        d.e2 = idx(N_ - 1);
+        d.e2 = last;
         la1 = 0;
         la2 = 1;
-      } else {  // elements g-1 (shape 1) and g (shape 0)
-        d.e1 = idx(g - 1);
-        d.e2 = idx(g);
+      } else {  // elements g-1 (shape 1) and g (shape 0), adjacent in elems
+        if (sorted) {
+          while (elems[cur] < g - 1) ++cur;
+          d.e1 = cur;
+        } else {
+          d.e1 = idx(g - 1);
+        }
+        d.e2 = d.e1 + 1;
         la1 = 1;
         la2 = 0;
       }
@@ -378,17 +513,22 @@ void FillPlan::add_true_block(const Lists& rows, const Lists& cols,
   near_local_.push_back(near_pairs_);
   const long long np = (long long)J.nres * J.nces;
   near_pairs_ += np;
-  // touching pairs (coincident / adjacent) go to the singular kernel
-  for (int ra = 0; ra < J.nres; ++ra) {
-    const int ea = res[ra];
-    const int cand[3] = {ea == 0 ? N_ - 1 : ea - 1, ea, ea + 1 == N_ ? 0 : ea + 1};
+  // touching pairs (coincident / adjacent) go to the singular kernel;
+  // search from the shorter element list into the longer one
+  const bool rows_short = res.size() <= ces.size();
+  const std::vector<int>& sh = rows_short ? res : ces;
+  const std::vector<int>& lg = rows_short ? ces : res;
+  for (int i = 0; i < int(sh.size()); ++i) {
+    const int e = sh[i];
+    const int cand[3] = {e == 0 ? N_ - 1 : e - 1, e, e + 1 == N_ ? 0 : e + 1};
     for (int c : cand) {
-      auto it = std::lower_bound(ces.begin(), ces.end(), c);
-      if (it != ces.end() && *it == c) {
-        const int cb = int(it - ces.begin());
+      auto it = std::lower_bound(lg.begin(), lg.end(), c);
+      if (it != lg.end() && *it == c) {
+        const int j = int(it - lg.begin());
+        const int ra = rows_short ? i : j, cb = rows_short ? j : i;
         sing_pair_.push_back(J.pair_off + (long long)ra * J.nces + cb);
-        sing_elems_.push_back(ea);
-        sing_elems_.push_back(c);
+        sing_elems_.push_back(res[ra]);
+        sing_elems_.push_back(ces[cb]);
       }
     }
   }
@@ -409,6 +549,96 @@ void FillPlan::add_true_block(const Lists& rows, const Lists& cols,
   gather_off_.push_back(entries_);
   entries_ += (long long)nr * nc;
   bundles_ += np;
+}
+
+void FillPlan::add_sym_near(const std::vector<int>& enc, const Lists& rows,
+                            const Lists& cols, double* tv, int ld_v, double* tu,
+                            int ld_u) {
+  if (enc.empty()) return;
+  const Lists encl{enc, enc};
+  std::vector<int> A, E;
+  elements_of(encl, A);
+  Lists both;
+  both[0] = rows[0];
+  both[0].insert(both[0].end(), rows[1].begin(), rows[1].end());
+  both[1] = cols[0];
+  both[1].insert(both[1].end(), cols[1].begin(), cols[1].end());
+  elements_of(both, E);
+  SymJob J;
+  J.nA = int(A.size());
+  J.nE = int(E.size());
+  J.a_off = int(elems_.size());
+  elems_.insert(elems_.end(), A.begin(), A.end());
+  J.e_off = int(elems_.size());
+  elems_.insert(elems_.end(), E.begin(), E.end());
+  const long long np = (long long)J.nA * J.nE;
+  J.v_off = bundles_;
+  J.u_off = bundles_ + np;
+  J.local_off = sym_pairs_;
+  sym_.push_back(J);
+  sym_off_.push_back(sym_pairs_);
+  sym_pairs_ += np;
+  bundles_ += 2 * np;
+  // touching pairs: both orientations through the singular kernel
+  for (int q = 0; q < J.nE; ++q) {
+    const int e = E[q];
+    const int cand[3] = {e == 0 ? N_ - 1 : e - 1, e, e + 1 == N_ ? 0 : e + 1};
+    for (int c : cand) {
+      auto it = std::lower_bound(A.begin(), A.end(), c);
+      if (it != A.end() && *it == c) {
+        const int a = int(it - A.begin());
+        sing_pair_.push_back(J.v_off + (long long)a * J.nE + q);
+        sing_elems_.push_back(A[a]);
+        sing_elems_.push_back(E[q]);
+        sing_pair_.push_back(J.u_off + (long long)q * J.nA + a);
+        sing_elems_.push_back(E[q]);
+        sing_elems_.push_back(A[a]);
+      }
+    }
+  }
+  const int ne = int(enc.size());
+  const int nr = int(rows[0].size() + rows[1].size());
+  const int nc = int(cols[0].size() + cols[1].size());
+  if (nc > 0) {  // T_V rows 2m'.. : true_block(enc x 2, cols)
+    GatherJob G;
+    G.pair_off = J.v_off;
+    G.entry_off = entries_;
+    G.nces = J.nE;
+    G.rdesc_off = int(desc_.size());
+    const int drow[2] = {2 * m_, 2 * m_ + ne};
+    node_descs(encl, A, drow, desc_);
+    G.nrows = 2 * ne;
+    G.cdesc_off = int(desc_.size());
+    const int dcol[2] = {0, int(cols[0].size())};
+    node_descs(cols, E, dcol, desc_);
+    G.ncols = nc;
+    G.trans = 0;
+    G.ld = ld_v;
+    G.dest = tv;
+    gather_.push_back(G);
+    gather_off_.push_back(entries_);
+    entries_ += (long long)G.nrows * G.ncols;
+  }
+  if (nr > 0) {  // T_U rows 2m'.. : conj(true_block(rows, enc x 2))
+    GatherJob G;
+    G.pair_off = J.u_off;
+    G.entry_off = entries_;
+    G.nces = J.nA;
+    G.rdesc_off = int(desc_.size());
+    const int drow[2] = {0, int(rows[0].size())};
+    node_descs(rows, E, drow, desc_);
+    G.nrows = nr;
+    G.cdesc_off = int(desc_.size());
+    const int dcol[2] = {2 * m_, 2 * m_ + ne};
+    node_descs(encl, A, dcol, desc_);
+    G.ncols = 2 * ne;
+    G.trans = 1;
+    G.ld = ld_u;
+    G.dest = tu;
+    gather_.push_back(G);
+    gather_off_.push_back(entries_);
+    entries_ += (long long)G.nrows * G.ncols;
+  }
 }
 
 // Descriptors of the 2 m' polygon hat functions (both components); the
@@ -508,52 +738,109 @@ void FillPlan::add_proxy(double cx, double cy, double radius, const Lists& rows,
 
 void Problem::execute(FillPlan& plan) {
   if (plan.empty()) return;
+  PhaseTimer t_exec("fill_execute", st_);
   Pack pk;
   const size_t o_el = pk.add(plan.elems_);
   const size_t o_nj = pk.add(plan.near_);
   const size_t o_nl = pk.add(plan.near_local_);
   const size_t o_sp = pk.add(plan.sing_pair_);
   const size_t o_se = pk.add(plan.sing_elems_);
+  const size_t o_sj = pk.add(plan.sym_);
+  const size_t o_so = pk.add(plan.sym_off_);
   const size_t o_pj = pk.add(plan.proxy_);
   const size_t o_pb = pk.add(plan.proxy_boff_);
   const size_t o_gj = pk.add(plan.gather_);
   const size_t o_go = pk.add(plan.gather_off_);
   const size_t o_de = pk.add(plan.desc_);
-  pk.upload(plan_dev, st_);
-  bundles.ensure(size_t(plan.bundles_) * kBundle * 2);
-  const int* el = pk.at<int>(plan_dev, o_el);
+  char* base;
+  {
+    PhaseTimer t_up("fill_upload", nullptr);
+    base = staging.put(pk, st_);
+  }
+  {
+    PhaseTimer t_al("fill_bundle_alloc", nullptr);
+    // grow-only, sized for a full wave up front (a realloc synchronises)
+    const size_t need = size_t(plan.bundles_) * kBundle * 2;
+    if (need > bundles.size())
+      bundles.ensure(std::max(need, size_t(kMaxBundlesPerWave) * kBundle * 2 * 5 / 4));
+  }
+  const int* el = Pack::at<int>(base, o_el);
+  // symmetric near pairs: classify by tier and sort (async), read the class
+  // bounds through an event so the host waits only for these small kernels
+  const long long nsym = plan.sym_pairs_;
+  const SymJob* sj = nullptr;
+  const long long* so = nullptr;
+  if (nsym > 0) {
+    sj = Pack::at<SymJob>(base, o_sj);
+    so = Pack::at<long long>(base, o_so);
+    sym_keys_.ensure(2 * size_t(nsym));
+    sym_vals_.ensure(2 * size_t(nsym));
+    if (!sym_bounds_host_) {
+      CK(cudaMallocHost(reinterpret_cast<void**>(&sym_bounds_host_), 16 * sizeof(int)));
+      CK(cudaEventCreateWithFlags(&sym_ev_, cudaEventDisableTiming));
+      sym_bounds_.alloc(16);
+    }
+    unsigned char* kin = sym_keys_.get();
+    unsigned char* kout = kin + nsym;
+    int* vin = sym_vals_.get();
+    int* vout = vin + nsym;
+    launch_sym_classify(dctx(), sj, so, int(plan.sym_.size()), el, nsym, kin, vin, st_);
+    sort_pairs_by_class(kin, kout, vin, vout, nsym, &sort_temp_, &sort_temp_bytes_, st_);
+    launch_class_bounds(kout, nsym, sym_bounds_.get(), st_);
+    CK(cudaMemcpyAsync(sym_bounds_host_, sym_bounds_.get(), 9 * sizeof(int),
+                       cudaMemcpyDeviceToHost, st_));
+    CK(cudaEventRecord(sym_ev_, st_));
+    g_launches += 3;
+  }
   if (!plan.proxy_.empty()) {
     double pts = 0.0;
     for (const ProxyJob& j : plan.proxy_)
       pts += double(pcfg_.m_prime) * j.nE * pcfg_.n_gauss * pcfg_.n_gauss;
     g_prof.begin(st_);
-    launch_proxy_pairs(dctx(), fc_, fc_nt_, pcfg_.n_gauss, pk.at<ProxyJob>(plan_dev, o_pj),
-                       pk.at<int>(plan_dev, o_pb), int(plan.proxy_.size()),
+    launch_proxy_pairs(dctx(), fc_, fc_nt_, pcfg_.n_gauss, Pack::at<ProxyJob>(base, o_pj),
+                       Pack::at<int>(base, o_pb), int(plan.proxy_.size()),
                        plan.proxy_blocks_, el, bundles.get(), st_);
     g_prof.end(KP_PROXY, st_, pts);
   }
   if (plan.near_pairs_ > 0) {
     g_prof.begin(st_);
-    launch_near_separated(dctx(), fc_, fc_nt_, pk.at<NearJob>(plan_dev, o_nj),
-                          pk.at<long long>(plan_dev, o_nl), int(plan.near_.size()),
+    launch_near_separated(dctx(), fc_, fc_nt_, Pack::at<NearJob>(base, o_nj),
+                          Pack::at<long long>(base, o_nl), int(plan.near_.size()),
                           el, plan.near_pairs_, bundles.get(),
                           g_prof.on ? g_prof.near_points : nullptr, st_);
     g_prof.end(KP_NEAR_SEP, st_, 0.0);
   }
+  if (nsym > 0) {
+    CK(cudaEventSynchronize(sym_ev_));
+    int bnd[9];
+    std::memcpy(bnd, sym_bounds_host_, sizeof(bnd));
+    const int add[4] = {0, 2, 5, 9};
+    const int* vout = sym_vals_.get() + nsym;
+    for (int c = 0; c < 4; ++c) {
+      const int cnt = bnd[c + 1] - bnd[c];
+      if (cnt <= 0) continue;
+      const int nq = int((acfg_.far_nodes + add[c]) * acfg_.refine + 0.5);
+      g_prof.begin(st_);
+      launch_near_sym(dctx(), sj, so, int(plan.sym_.size()), el, vout + bnd[c], cnt,
+                      nq, bundles.get(), st_);
+      g_prof.end(KP_NEAR_SYM, st_, double(cnt) * nq * nq);
+    }
+  }
   if (!plan.sing_pair_.empty()) {
     g_prof.begin(st_);
-    launch_near_singular(dctx(), pk.at<long long>(plan_dev, o_sp),
-                         pk.at<int>(plan_dev, o_se), int(plan.sing_pair_.size()),
+    launch_near_singular(dctx(), Pack::at<long long>(base, o_sp),
+                         Pack::at<int>(base, o_se), int(plan.sing_pair_.size()),
                          bundles.get(), bad.get(), st_);
     g_prof.end(KP_NEAR_SING, st_, double(plan.sing_pair_.size()));
   }
   g_prof.begin(st_);
-  launch_gather(pk.at<GatherJob>(plan_dev, o_gj), pk.at<long long>(plan_dev, o_go),
-                int(plan.gather_.size()), pk.at<NodeDesc>(plan_dev, o_de),
+  launch_gather(Pack::at<GatherJob>(base, o_gj), Pack::at<long long>(base, o_go),
+                int(plan.gather_.size()), Pack::at<NodeDesc>(base, o_de),
                 plan.entries_, bundles.get(), st_);
   // bytes: 4 bundle reads (16 B each) + one 16 B store per entry
   g_prof.end(KP_GATHER, st_, 80.0 * double(plan.entries_));
   CK(cudaGetLastError());
+  staging.fence(st_);
   plan.clear();
 }
 
@@ -570,7 +857,10 @@ void Problem::interaction(const std::vector<BasisReq>& req,
   n_out.resize(nc_);
   size_t run = 0;
   for (size_t c = 0; c < nc_; ++c) {
-    geom[c] = build_proxy(req[c].begin, req[c].end);
+    {
+      PhaseTimer t_geom("proxy_geometry", nullptr);
+      geom[c] = build_proxy(req[c].begin, req[c].end);
+    }
     n_out[c] = 2 * m + 2 * int(geom[c].enclosed.size());
     const size_t ncol = (*req[c].cols)[0].size() + (*req[c].cols)[1].size();
     const size_t nrow = (*req[c].rows)[0].size() + (*req[c].rows)[1].size();
@@ -579,7 +869,10 @@ void Problem::interaction(const std::vector<BasisReq>& req,
     tu_off[c] = run;
     run += size_t(n_out[c]) * nrow;
   }
-  tbuf.ensure(2 * run + 2);
+  {
+    PhaseTimer t_alloc("alloc_tbuf", nullptr);
+    tbuf.ensure(2 * run + 2);
+  }
   FillPlan plan(n_, m, pcfg_.n_gauss);
   double* base = tbuf.get();
   for (size_t c = 0; c < nc_; ++c) {
@@ -588,17 +881,11 @@ void Problem::interaction(const std::vector<BasisReq>& req,
     double* tv = base + 2 * tv_off[c];
     double* tu = base + 2 * tu_off[c];
     const int no = n_out[c];
-    plan.add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv, no,
-                   tu, no);
-    if (!geom[c].enclosed.empty()) {
-      const Lists enc{geom[c].enclosed, geom[c].enclosed};
-      const int ne = int(geom[c].enclosed.size());
-      const int drow_v[2] = {2 * m, 2 * m + ne};
-      const int dcol_v[2] = {0, int(cols[0].size())};
-      plan.add_true_block(enc, cols, tv, no, drow_v, dcol_v, 0);
-      const int drow_u[2] = {0, int(rows[0].size())};
-      const int dcol_u[2] = {2 * m, 2 * m + ne};
-      plan.add_true_block(rows, enc, tu, no, drow_u, dcol_u, 1);
+    {
+      PhaseTimer t_plan("fill_plan", nullptr);
+      plan.add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv, no,
+                     tu, no);
+      plan.add_sym_near(geom[c].enclosed, rows, cols, tv, no, tu, no);
     }
     if (plan.bundles() > kMaxBundlesPerWave) execute(plan);
   }
@@ -614,14 +901,13 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
   std::vector<ProxyGeom> geom;
   std::vector<size_t> tv_off, tu_off;
   std::vector<int> n_out;
-  DBuf<double> tbuf;
+  DBuf<double>& tbuf = tbuf_;
   const double t0 = now();
   interaction(req, geom, tv_off, tu_off, n_out, tbuf);
   if (fill_seconds) {
     CK(cudaStreamSynchronize(st_));
     *fill_seconds = now() - t0;
   }
-  check_domain();
 
   // ---- the four ID inputs per cell: column halves of T_V and T_U
   struct QIn {
@@ -644,8 +930,9 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     q[4 * c + 2] = {tu, no, nr0, no};
     q[4 * c + 3] = {tu + 2 * size_t(no) * nr0, no, nr1, no};
   }
+  PhaseTimer* t_qr = new PhaseTimer("id_tsqr", st_);
   // ---- TSQR rounds until each input fits one CTA's shared memory
-  std::vector<DBuf<double>> rounds;
+  size_t round = 0;
   for (;;) {
     std::vector<QrTask> tasks;
     std::vector<size_t> out_off(q.size(), 0);
@@ -661,9 +948,10 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
       out_total += size_t(pieces[i]) * x.n * x.n;
     }
     if (out_total == 0) break;
-    rounds.emplace_back();
-    rounds.back().alloc(2 * out_total);
-    double* ob = rounds.back().get();
+    if (qr_rounds_.size() <= round) qr_rounds_.emplace_back();
+    qr_rounds_[round].ensure(2 * out_total);
+    double* ob = qr_rounds_[round].get();
+    ++round;
     for (size_t i = 0; i < q.size(); ++i) {
       if (!pieces[i]) continue;
       const QIn& x = q[i];
@@ -688,7 +976,7 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     gws.ensure(ws_total + 1);
     Pack pk;
     const size_t o = pk.add(tasks);
-    pk.upload(task_dev, st_);
+    char* tb = staging.put(pk, st_);
     size_t smem = 0;
     for (const QrTask& t : tasks)
       if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
@@ -698,18 +986,20 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
       fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
     }
     g_prof.begin(st_);
-    launch_qr_reduce(pk.at<QrTask>(task_dev, o), int(tasks.size()), smem,
+    launch_qr_reduce(Pack::at<QrTask>(tb, o), int(tasks.size()), smem,
                      gws.get(), st_);
     g_prof.end(KP_QR, st_, fl);
     CK(cudaGetLastError());
+    staging.fence(st_);
     for (size_t i = 0; i < q.size(); ++i) {
       if (!pieces[i]) continue;
       q[i].p = ob + 2 * out_off[i];
       q[i].rows = pieces[i] * q[i].n;
       q[i].ld = q[i].rows;
     }
-    CK(cudaStreamSynchronize(st_));  // task_dev is reused next round
   }
+  delete t_qr;
+  PhaseTimer t_cpqr("id_cpqr+interp", st_);
   // ---- pivoted QR of every input
   const size_t nq = q.size();
   size_t jp_total = 0, r_total = 0, ws_total = 0;
@@ -720,12 +1010,14 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     r_off[i] = r_total;
     r_total += size_t(q[i].n) * q[i].n;
   }
-  DBuf<int> d_jp, d_steps;
-  DBuf<double> d_rd, d_r;
-  d_jp.alloc(jp_total);
-  d_steps.alloc(nq);
-  d_rd.alloc(jp_total);
-  d_r.alloc(2 * r_total);
+  DBuf<int>& d_jp = id_jp_;
+  DBuf<int>& d_steps = id_steps_;
+  DBuf<double>& d_rd = id_rd_;
+  DBuf<double>& d_r = id_r_;
+  d_jp.ensure(jp_total);
+  d_steps.ensure(nq);
+  d_rd.ensure(jp_total);
+  d_r.ensure(2 * r_total);
   std::vector<CpqrTask> ct(nq);
   size_t smem = 0;
   for (size_t i = 0; i < nq; ++i) {
@@ -751,16 +1043,17 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
   {
     Pack pk;
     const size_t o = pk.add(ct);
-    pk.upload(task_dev, st_);
+    char* tb = staging.put(pk, st_);
     double fl = 0.0;  // full-rank bound of the pivoted QR flops
     for (const CpqrTask& t : ct) {
       const double mm = t.rows, nn = std::min(t.rows, t.n);
       fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
     }
     g_prof.begin(st_);
-    launch_cpqr(pk.at<CpqrTask>(task_dev, o), int(nq), smem, gws.get(), st_);
+    launch_cpqr(Pack::at<CpqrTask>(tb, o), int(nq), smem, gws.get(), st_);
     g_prof.end(KP_CPQR, st_, fl);
     CK(cudaGetLastError());
+    staging.fence(st_);
   }
   std::vector<int> h_jp(jp_total), h_steps(nq);
   std::vector<double> h_rd(jp_total);
@@ -768,6 +1061,7 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
   CK(cudaMemcpyAsync(h_steps.data(), d_steps.get(), nq * 4, cudaMemcpyDeviceToHost, st_));
   CK(cudaMemcpyAsync(h_rd.data(), d_rd.get(), jp_total * 8, cudaMemcpyDeviceToHost, st_));
   CK(cudaStreamSynchronize(st_));
+  check_domain();  // the fill's element-length guard, read after the sync
 
   // ---- shared rank (basis_from_interactions, compression.cpp:92-99)
   size_t v_total = 0, u_total = 0;
@@ -847,15 +1141,15 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
   if (!it.empty()) {
     Pack pk;
     const size_t o = pk.add(it);
-    pk.upload(task_dev, st_);
+    char* tb = staging.put(pk, st_);
     double fl = 0.0;
     for (const InterpTask& t : it) fl += 4.0 * t.k * t.k * double(t.n - t.k);
     g_prof.begin(st_);
-    launch_interp(pk.at<InterpTask>(task_dev, o), int(it.size()), max_k, st_);
+    launch_interp(Pack::at<InterpTask>(tb, o), int(it.size()), max_k, st_);
     g_prof.end(KP_INTERP, st_, fl);
     CK(cudaGetLastError());
+    staging.fence(st_);
   }
-  CK(cudaStreamSynchronize(st_));
 }
 
 void Problem::true_block_host(const Lists& rows, const Lists& cols, double* out) {
@@ -910,16 +1204,16 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
   Pack pk;
   const size_t o1 = pk.add(t);
   const size_t o2 = pk.add(boff);
-  pk.upload(P.task_dev, P.stream());
+  char* tb = P.staging.put(pk, P.stream());
   double units = 0.0;
   for (const T& x : t) units += units_of(x);
   g_prof.begin(P.stream());
-  launch(pk.at<T>(P.task_dev, o1), pk.at<int>(P.task_dev, o2), int(t.size()),
-         total, P.stream());
+  launch(Pack::at<T>(tb, o1), Pack::at<int>(tb, o2), int(t.size()), total,
+         P.stream());
   g_prof.end(id, P.stream(), units);
+  P.staging.fence(P.stream());
   CK(cudaGetLastError());
-  // task_dev is reused by the next upload: keep the host from racing ahead
-  CK(cudaStreamSynchronize(P.stream()));
+
 }
 }  // namespace
 
@@ -938,14 +1232,10 @@ void run_getrs(Problem& P, const std::vector<LuSolveTask>& t) {
               launch_getrs, KP_GETRS,
               [](const LuSolveTask& s) { return 8.0 * s.n * double(s.n) * s.nrhs; });
 }
-std::vector<int> run_getrf(Problem& P, std::vector<LuTask> t) {
-  std::vector<int> info(t.size(), 0);
-  if (t.empty()) return info;
-  DBuf<int> dinfo;
-  dinfo.alloc(t.size());
+void run_getrf(Problem& P, std::vector<LuTask> t) {
+  if (t.empty()) return;
   size_t smem = 0, ws = 0;
   for (size_t i = 0; i < t.size(); ++i) {
-    t[i].info = dinfo.get() + i;
     const size_t bytes = size_t(t[i].n) * t[i].n * 16;
     t[i].in_smem = bytes <= size_t(kSmemCap);
     t[i].ws_off = (long long)ws;
@@ -955,16 +1245,14 @@ std::vector<int> run_getrf(Problem& P, std::vector<LuTask> t) {
   P.gws.ensure(ws + 1);
   Pack pk;
   const size_t o = pk.add(t);
-  pk.upload(P.task_dev, P.stream());
+  char* tb = P.staging.put(pk, P.stream());
   double fl = 0.0;
   for (const LuTask& x : t) fl += 8.0 / 3.0 * double(x.n) * x.n * x.n;
   g_prof.begin(P.stream());
-  launch_getrf(pk.at<LuTask>(P.task_dev, o), int(t.size()), smem, P.gws.get(), P.stream());
+  launch_getrf(Pack::at<LuTask>(tb, o), int(t.size()), smem, P.gws.get(), P.stream());
   g_prof.end(KP_GETRF, P.stream(), fl);
+  P.staging.fence(P.stream());
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(info.data(), dinfo.get(), 4 * t.size(), cudaMemcpyDeviceToHost, P.stream()));
-  CK(cudaStreamSynchronize(P.stream()));
-  return info;
 }
 
 namespace {
@@ -1027,6 +1315,13 @@ Fds::Fds(Problem& p, int depth, const ebem_fds_config& cfg)
   build();
 }
 
+int* Fds::lu_info(int n) {
+  info_n_.push_back(n);
+  if (info_n_.size() > info_.size())
+    throw Error(EBEM_LOGIC_ERROR, "FdsSolver: LU info slots exhausted");
+  return info_.get() + (info_n_.size() - 1);
+}
+
 void Fds::reduced_diagonal(FillPlan& plan, std::vector<CopyTask>& copies,
                            int cell, double* dest, int ld, int off) {
   // proj/src/fds.cpp:33-54
@@ -1066,6 +1361,9 @@ void Fds::build() {
   stats_ = ebem_fds_stats{};
   stats_.depth = depth_;
   const int leaf = n >> depth_;
+  info_.alloc(2 * size_t(ncells) + 2);
+  CK(cudaMemsetAsync(info_.get(), 0, 4 * (2 * size_t(ncells) + 2), P_.stream()));
+  info_n_.clear();
   for (int l = 0; l <= depth_; ++l)
     for (int c = first(l); c <= last(l); ++c) {
       cells_[c].begin = (c - first(l)) * (n >> l);
@@ -1091,7 +1389,7 @@ void Fds::build() {
     for (int c = f; c <= L; ++c)
       req[c - f] = BasisReq{&cells_[c].jrow, &cells_[c].jcol, cells_[c].begin, cells_[c].end};
     std::vector<BasisRes> br;
-    DBuf<double> ubuf;
+    DBuf<double>& ubuf = ubuf_;
     const double tb = now();
     P_.bases(req, cfg_.epsilon, br, S.v, ubuf);
     basis_seconds += now() - tb;
@@ -1127,6 +1425,7 @@ void Fds::build() {
       C.v = S.v.get() + 2 * br[i].v_off;
     }
     {
+      PhaseTimer tp("fill_diagonal", P_.stream());
       FillPlan plan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
       std::vector<CopyTask> copies;
       for (int i = 0; i < nlev; ++i) {
@@ -1146,6 +1445,7 @@ void Fds::build() {
     }
     // ---- LU of the diagonal blocks
     {
+      PhaseTimer tp("merge_getrf", P_.stream());
       std::vector<LuTask> lt;
       for (int i = 0; i < nlev; ++i) {
         Cell& C = cells_[f + i];
@@ -1156,12 +1456,12 @@ void Fds::build() {
         t.ld = 2 * C.nloc;
         lt.push_back(t);
       }
-      const std::vector<int> info = run_getrf(P_, lt);
-      for (int i = 0; i < nlev; ++i)
-        if (info[i]) singular_error(info[i], 2 * cells_[f + i].nloc);
+      for (LuTask& t : lt) t.info = lu_info(t.n);
+      run_getrf(P_, lt);
     }
     // ---- A^-1 U with U = blockdiag(u0, u1)
     {
+      PhaseTimer tp("merge_ainv_u", P_.stream());
       std::vector<CopyTask> ct;
       std::vector<LuSolveTask> st;
       for (int i = 0; i < nlev; ++i) {
@@ -1183,10 +1483,11 @@ void Fds::build() {
     }
     // ---- W = [v0 A^-1U_top ; v1 A^-1U_bottom], atilde = W^-1
     {
-      DBuf<double> wbuf;
-      DBuf<int> wpiv;
-      wbuf.alloc(2 * at_total + 2);
-      wpiv.alloc(2 * at_total / 1 + 1);
+      PhaseTimer tp("merge_atilde", P_.stream());
+      DBuf<double>& wbuf = wbuf_;
+      DBuf<int>& wpiv = wpiv_;
+      wbuf.ensure(2 * at_total + 2);
+      wpiv.ensure(at_total + 1);
       std::vector<GemmTask> gt;
       std::vector<LuTask> lt;
       std::vector<CopyTask> ct;
@@ -1214,9 +1515,8 @@ void Fds::build() {
         poff += kk;
       }
       run_gemms(P_, gt);
-      const std::vector<int> info = run_getrf(P_, lt);
-      for (size_t i = 0; i < info.size(); ++i)
-        if (info[i]) singular_error(info[i], lt[i].n);
+      for (LuTask& t : lt) t.info = lu_info(t.n);
+      run_getrf(P_, lt);
       run_copies(P_, ct);
       run_getrs(P_, st);
     }
@@ -1239,6 +1539,7 @@ void Fds::build() {
   stats_.basis_cpu_seconds = basis_seconds;
 
   // ---- dense system over the cells of level ell0 (proj/src/fds.cpp:131-152)
+  PhaseTimer tp_top("top", P_.stream());
   const double t_top = now();
   const int tf = first(cfg_.ell0), tl = last(cfg_.ell0);
   top_off_.assign(tl - tf + 2, 0);
@@ -1272,8 +1573,8 @@ void Fds::build() {
       t.ipiv = top_ipiv_.get();
       t.n = top_dim_;
       t.ld = top_dim_;
-      const std::vector<int> info = run_getrf(P_, {t});
-      if (info[0]) singular_error(info[0], top_dim_);
+      t.info = lu_info(top_dim_);
+      run_getrf(P_, {t});
     }
   }
   CK(cudaStreamSynchronize(P_.stream()));
@@ -1283,6 +1584,13 @@ void Fds::build() {
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ev0, ev1));
   stats_.factorize_device_seconds = 1e-3 * ms;
+  host_phase_dump();
+  // zero pivots, checked once (in factorization order) instead of a sync per LU
+  std::vector<int> info(info_n_.size());
+  if (!info.empty())
+    CK(cudaMemcpy(info.data(), info_.get(), 4 * info.size(), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < info.size(); ++i)
+    if (info[i]) singular_error(info[i], info_n_[i]);
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
 }

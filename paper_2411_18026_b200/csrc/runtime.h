@@ -39,7 +39,7 @@ extern std::atomic<long long> g_launches;
 // kernels, bytes or flops for the rest); enabled by ebem_gpu_prof_enable.
 enum KernelId {
   KP_PROXY = 0, KP_NEAR_SEP, KP_NEAR_SING, KP_GATHER, KP_QR, KP_CPQR,
-  KP_INTERP, KP_GETRF, KP_GETRS, KP_GEMM, KP_COPY, KP_RHS, KP_COUNT
+  KP_INTERP, KP_GETRF, KP_GETRS, KP_GEMM, KP_COPY, KP_RHS, KP_NEAR_SYM, KP_COUNT
 };
 const char* kernel_name(int id);
 
@@ -63,6 +63,23 @@ class Profiler {
   cudaEvent_t ev();
 };
 extern Profiler g_prof;
+
+// Host-side phase timers (EBEM_VERBOSE=1 prints them after a factorization;
+// EBEM_VERBOSE=2 also synchronises the stream at each scope end so device
+// work is attributed to the phase that issued it).
+int verbose_level();
+void host_phase_add(const char* name, double seconds);
+void host_phase_dump();
+class PhaseTimer {
+ public:
+  PhaseTimer(const char* name, cudaStream_t st);
+  ~PhaseTimer();
+
+ private:
+  const char* name_;
+  cudaStream_t st_;
+  double t0_;
+};
 
 // ----------------------------------------------------------------- buffers
 template <class T>
@@ -119,10 +136,38 @@ class Pack {
   T* at(const DBuf<char>& dev, size_t off) const {
     return reinterpret_cast<T*>(dev.get() + off);
   }
+  template <class T>
+  static T* at(char* base, size_t off) {
+    return reinterpret_cast<T*>(base + off);
+  }
   size_t bytes() const { return buf_.size(); }
+  const char* data() const { return buf_.data(); }
 
  private:
   std::vector<char> buf_;
+};
+
+// Ring of pinned host + device staging slots for task/plan uploads: the
+// host copies a pack into a pinned slot and enqueues an async H2D, so it can
+// keep planning while the device works; a slot is reused only after the
+// kernels that read it (fenced by an event) have finished.
+class Staging {
+ public:
+  explicit Staging(int slots = 8) : s_(slots) {}
+  ~Staging();
+  char* put(const Pack& pk, cudaStream_t st);
+  void fence(cudaStream_t st);
+
+ private:
+  struct Slot {
+    char* host = nullptr;
+    char* dev = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+  };
+  std::vector<Slot> s_;
+  int cur_ = -1;
 };
 
 // ------------------------------------------------------------ segment tree
@@ -200,6 +245,18 @@ class Problem {
                  double* out_host);
 
   // scratch shared by the drivers
+  Staging staging;
+  DBuf<double> tbuf_;     // interaction matrices of the current basis batch
+  std::vector<DBuf<double>> qr_rounds_;  // TSQR round outputs (grow-only)
+  DBuf<int> id_jp_, id_steps_;
+  DBuf<double> id_rd_, id_r_;
+  DBuf<unsigned char> sym_keys_;   // 2 x pairs (in, out)
+  DBuf<int> sym_vals_;             // 2 x pairs (in, out)
+  void* sort_temp_ = nullptr;
+  size_t sort_temp_bytes_ = 0;
+  DBuf<int> sym_bounds_;
+  int* sym_bounds_host_ = nullptr;  // pinned
+  cudaEvent_t sym_ev_ = nullptr;
   DBuf<char> plan_dev;
   DBuf<double> bundles;
   DBuf<double2> gws;
@@ -234,6 +291,12 @@ class FillPlan {
   // polygon cols of M_U -> T_U rows [0, 2m') (conj-transposed).
   void add_proxy(double cx, double cy, double radius, const Lists& rows,
                  const Lists& cols, double* tv, int ld_v, double* tu, int ld_u);
+  // Both near blocks of a cell: true_block(enc x 2, cols) into T_V rows
+  // [2m', 2m' + 2|enc|) and true_block(rows, enc x 2)^H into T_U rows, from
+  // one scalar evaluation per point (enc ascending).
+  void add_sym_near(const std::vector<int>& enc, const Lists& rows,
+                    const Lists& cols, double* tv, int ld_v, double* tu,
+                    int ld_u);
   long long bundles() const { return bundles_; }
   bool empty() const { return gather_.empty(); }
   void clear();
@@ -255,6 +318,9 @@ class FillPlan {
   std::vector<long long> near_local_;
   std::vector<long long> sing_pair_;
   std::vector<int> sing_elems_;
+  std::vector<SymJob> sym_;
+  std::vector<long long> sym_off_;
+  long long sym_pairs_ = 0;
   std::vector<ProxyJob> proxy_;
   std::vector<int> proxy_boff_;
   std::vector<GatherJob> gather_;
@@ -306,6 +372,11 @@ class Fds {
   int top_dim_ = 0;
   ebem_fds_stats stats_{};
   double last_solve_device_seconds_ = 0.0;
+  int* lu_info(int n);
+  DBuf<int> info_;            // zero-pivot flags of every LU of the build
+  std::vector<int> info_n_;   // their matrix sizes (for the error message)
+  DBuf<double> ubuf_, wbuf_;  // per-level temporaries (grow-only)
+  DBuf<int> wpiv_;
   // solve workspaces (grow-only)
   DBuf<double> ws_f_, ws_ainvf_, ws_ft_, ws_x_, ws_t_;
 };
@@ -315,7 +386,7 @@ class Fds {
 void run_copies(Problem& P, const std::vector<CopyTask>& t);
 void run_gemms(Problem& P, const std::vector<GemmTask>& t);
 void run_getrs(Problem& P, const std::vector<LuSolveTask>& t);
-// Factors in place; returns per-task info (0 ok).
-std::vector<int> run_getrf(Problem& P, std::vector<LuTask> t);
+// Factors in place; zero-pivot flags land in each task's info pointer.
+void run_getrf(Problem& P, std::vector<LuTask> t);
 
 }  // namespace ebem_gpu
