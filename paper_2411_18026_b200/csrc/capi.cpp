@@ -4,6 +4,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -23,8 +24,14 @@ namespace {
 
 thread_local std::string g_err;
 
+std::recursive_mutex& api_mutex() {
+  static std::recursive_mutex m;
+  return m;
+}
+
 template <class F>
 int guarded(F&& f) {
+  std::lock_guard<std::recursive_mutex> lock(api_mutex());
   try {
     f();
     return EBEM_OK;
@@ -152,6 +159,7 @@ int ebem_gpu_problem_create(const double* nodes_xy, int n_nodes, double lambda,
 
 void ebem_gpu_problem_destroy(ebem_gpu_problem* p) {
   if (!p) return;
+  std::lock_guard<std::recursive_mutex> lock(api_mutex());
   delete p->p;
   delete p;
 }
@@ -293,6 +301,7 @@ int ebem_gpu_fds_create(ebem_gpu_problem* p, int depth,
 
 void ebem_gpu_fds_destroy(ebem_gpu_fds* f) {
   if (!f) return;
+  std::lock_guard<std::recursive_mutex> lock(api_mutex());
   delete f->f;
   delete f;
 }

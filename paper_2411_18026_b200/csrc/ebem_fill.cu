@@ -415,7 +415,7 @@ k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
   const int na = ea + 1 == N ? 0 : ea + 1;
   const int nb = eb + 1 == N ? 0 : eb + 1;
   unsigned char key = 7;
-  if (!(ea == eb || na == eb || nb == ea)) {
+  if (!(ea == eb || na == eb || nb == ea) && !(J.tri && a >= q)) {
     const double hx = ef(ctx, EH, ea), hy = ef(ctx, EH, eb);
     const double rq = element_distance(ctx, ea, eb) / fmax(hx, hy);
     key = rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3;

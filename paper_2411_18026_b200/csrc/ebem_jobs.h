@@ -47,11 +47,14 @@ struct ProxyJob {
 // pairs (a in enclosed elements A, q in cell elements E);
 // V bundle (test A[a], trial E[q]) at v_off + a * nE + q,
 // U bundle (test E[q], trial A[a]) at u_off + q * nA + a.
+// tri = 1 (a diagonal block, A == E, u_off == v_off): only pairs a < q are
+// evaluated; the U bundle of (a, q) is the V bundle of (q, a).
 struct SymJob {
   long long v_off, u_off;
   long long local_off;  // first pair of this job in the wave's sym numbering
   int a_off, nA;
   int e_off, nE;
+  int tri, pad;
 };
 
 // Scatter of bundles into one output block.

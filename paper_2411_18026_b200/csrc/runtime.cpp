@@ -258,10 +258,42 @@ void NodeBoxTree::enclosed(const double* xy, double cx, double cy,
 }
 
 // ---------------------------------------------------------------- Problem
+Scratch& scratch() {
+  // leaked on purpose: CUDA resources must not be released after the
+  // runtime's own teardown at process exit
+  static Scratch* s = [] {
+    auto* x = new Scratch();
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(EBEM_CUDA_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
+    CK(cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking));
+    return x;
+  }();
+  return *s;
+}
+
 Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
                  double omega, double are, double aim,
                  const ebem_assembly_config& a, const ebem_proxy_config& p)
-    : n_(n), acfg_(a), pcfg_(p) {
+    : staging(scratch().staging),
+      tbuf_(scratch().tbuf),
+      qr_rounds_(scratch().qr_rounds),
+      id_jp_(scratch().id_jp),
+      id_steps_(scratch().id_steps),
+      id_rd_(scratch().id_rd),
+      id_r_(scratch().id_r),
+      sym_keys_(scratch().sym_keys),
+      sym_vals_(scratch().sym_vals),
+      sort_temp_(scratch().sort_temp),
+      sort_temp_bytes_(scratch().sort_temp_bytes),
+      sym_bounds_(scratch().sym_bounds),
+      sym_bounds_host_(scratch().sym_bounds_host),
+      sym_ev_(scratch().sym_ev),
+      bundles(scratch().bundles),
+      gws(scratch().gws),
+      n_(n),
+      acfg_(a),
+      pcfg_(p) {
   if (n < 4) throw Error(EBEM_INVALID_ARGUMENT, "Mesh: needs at least 4 nodes");
   if (n < 8) throw Error(EBEM_INVALID_ARGUMENT, "PairIntegrator: mesh too coarse");
   xy_.assign(xy, xy + 2 * size_t(n));
@@ -329,7 +361,7 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw Error(EBEM_CUDA_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
-  CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  st_ = scratch().st;
   delem_.alloc(elem_.size());
   dxy_.alloc(xy_.size());
   CK(cudaMemcpyAsync(delem_.get(), elem_.data(), elem_.size() * 8, cudaMemcpyHostToDevice, st_));
@@ -346,13 +378,7 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
 }
 
 Problem::~Problem() {
-  if (st_) {
-    cudaStreamSynchronize(st_);
-    cudaStreamDestroy(st_);
-  }
-  if (sort_temp_) cudaFree(sort_temp_);
-  if (sym_bounds_host_) cudaFreeHost(sym_bounds_host_);
-  if (sym_ev_) cudaEventDestroy(sym_ev_);
+  if (st_) cudaStreamSynchronize(st_);  // the stream is process-wide
 }
 
 ProxyGeom Problem::build_proxy(int begin, int end) const {
@@ -565,6 +591,8 @@ void FillPlan::add_sym_near(const std::vector<int>& enc, const Lists& rows,
   both[1].insert(both[1].end(), cols[1].begin(), cols[1].end());
   elements_of(both, E);
   SymJob J;
+  J.tri = 0;
+  J.pad = 0;
   J.nA = int(A.size());
   J.nE = int(E.size());
   J.a_off = int(elems_.size());
@@ -639,6 +667,57 @@ void FillPlan::add_sym_near(const std::vector<int>& enc, const Lists& rows,
     gather_off_.push_back(entries_);
     entries_ += (long long)G.nrows * G.ncols;
   }
+}
+
+void FillPlan::add_sym_diag(const std::vector<int>& nodes, double* dest,
+                            int ld) {
+  if (nodes.empty()) return;
+  const Lists L{nodes, nodes};
+  std::vector<int> E;
+  elements_of(L, E);
+  SymJob J;
+  J.tri = 1;
+  J.pad = 0;
+  J.nA = J.nE = int(E.size());
+  J.a_off = J.e_off = int(elems_.size());
+  elems_.insert(elems_.end(), E.begin(), E.end());
+  const long long np = (long long)J.nA * J.nE;
+  J.v_off = J.u_off = bundles_;
+  J.local_off = sym_pairs_;
+  sym_.push_back(J);
+  sym_off_.push_back(sym_pairs_);
+  sym_pairs_ += np;
+  bundles_ += np;
+  // touching pairs (coincident, adjacent): every ordered pair once
+  for (int a = 0; a < J.nA; ++a) {
+    const int e = E[a];
+    const int cand[3] = {e == 0 ? N_ - 1 : e - 1, e, e + 1 == N_ ? 0 : e + 1};
+    for (int c : cand) {
+      auto it = std::lower_bound(E.begin(), E.end(), c);
+      if (it != E.end() && *it == c) {
+        const int q = int(it - E.begin());
+        sing_pair_.push_back(J.v_off + (long long)a * J.nE + q);
+        sing_elems_.push_back(E[a]);
+        sing_elems_.push_back(E[q]);
+      }
+    }
+  }
+  GatherJob G;
+  G.pair_off = J.v_off;
+  G.entry_off = entries_;
+  G.nces = J.nE;
+  G.rdesc_off = int(desc_.size());
+  const int off[2] = {0, int(nodes.size())};
+  node_descs(L, E, off, desc_);
+  G.nrows = 2 * int(nodes.size());
+  G.cdesc_off = G.rdesc_off;
+  G.ncols = G.nrows;
+  G.trans = 0;
+  G.ld = ld;
+  G.dest = dest;
+  gather_.push_back(G);
+  gather_off_.push_back(entries_);
+  entries_ += (long long)G.nrows * G.ncols;
 }
 
 // Descriptors of the 2 m' polygon hat functions (both components); the
@@ -1432,8 +1511,7 @@ void Fds::build() {
         Cell& C = cells_[f + i];
         const int d = 2 * C.nloc;
         if (level == depth_) {
-          const int drow[2] = {0, C.nloc}, dcol[2] = {0, C.nloc};
-          plan.add_true_block(C.jrow, C.jcol, C.lu, d, drow, dcol, 0);
+          plan.add_sym_diag(C.jrow[0], C.lu, d);  // leaf: jrow == jcol, ascending
         } else {
           reduced_diagonal(plan, copies, f + i, C.lu, d, 0);
         }

@@ -209,6 +209,29 @@ struct BasisRes {
 
 class FillPlan;
 
+// Process-wide device scratch and stream shared by every handle: new
+// problems and solvers reuse warm buffers (GBs of bundles, pinned staging)
+// instead of reallocating them.  All C ABI entry points serialise on
+// api_mutex(), so one stream orders every use of the shared buffers.
+struct Scratch {
+  cudaStream_t st = nullptr;
+  Staging staging;
+  DBuf<double> tbuf;
+  std::vector<DBuf<double>> qr_rounds;
+  DBuf<int> id_jp, id_steps;
+  DBuf<double> id_rd, id_r;
+  DBuf<unsigned char> sym_keys;
+  DBuf<int> sym_vals;
+  void* sort_temp = nullptr;
+  size_t sort_temp_bytes = 0;
+  DBuf<int> sym_bounds;
+  int* sym_bounds_host = nullptr;
+  cudaEvent_t sym_ev = nullptr;
+  DBuf<double> bundles;
+  DBuf<double2> gws;
+};
+Scratch& scratch();
+
 class Problem {
  public:
   Problem(const double* xy, int n, double lam, double mu, double rho,
@@ -244,23 +267,23 @@ class Problem {
   void rhs_plane(int kind, const double* angles, int m, double amp,
                  double* out_host);
 
-  // scratch shared by the drivers
-  Staging staging;
-  DBuf<double> tbuf_;     // interaction matrices of the current basis batch
-  std::vector<DBuf<double>> qr_rounds_;  // TSQR round outputs (grow-only)
-  DBuf<int> id_jp_, id_steps_;
-  DBuf<double> id_rd_, id_r_;
-  DBuf<unsigned char> sym_keys_;   // 2 x pairs (in, out)
-  DBuf<int> sym_vals_;             // 2 x pairs (in, out)
-  void* sort_temp_ = nullptr;
-  size_t sort_temp_bytes_ = 0;
-  DBuf<int> sym_bounds_;
-  int* sym_bounds_host_ = nullptr;  // pinned
-  cudaEvent_t sym_ev_ = nullptr;
-  DBuf<char> plan_dev;
-  DBuf<double> bundles;
-  DBuf<double2> gws;
-  DBuf<char> task_dev;
+  // scratch shared by the drivers (process-wide, see Scratch)
+  Staging& staging;
+  DBuf<double>& tbuf_;     // interaction matrices of the current basis batch
+  std::vector<DBuf<double>>& qr_rounds_;  // TSQR round outputs (grow-only)
+  DBuf<int>& id_jp_;
+  DBuf<int>& id_steps_;
+  DBuf<double>& id_rd_;
+  DBuf<double>& id_r_;
+  DBuf<unsigned char>& sym_keys_;   // 2 x pairs (in, out)
+  DBuf<int>& sym_vals_;             // 2 x pairs (in, out)
+  void*& sort_temp_;
+  size_t& sort_temp_bytes_;
+  DBuf<int>& sym_bounds_;
+  int*& sym_bounds_host_;  // pinned
+  cudaEvent_t& sym_ev_;
+  DBuf<double>& bundles;
+  DBuf<double2>& gws;
   DBuf<int> bad;
 
  private:
@@ -297,6 +320,9 @@ class FillPlan {
   void add_sym_near(const std::vector<int>& enc, const Lists& rows,
                     const Lists& cols, double* tv, int ld_v, double* tu,
                     int ld_u);
+  // true_block(J, J) for an ascending node list J (the leaf diagonal) from
+  // the upper triangle of element pairs, both orientations per evaluation.
+  void add_sym_diag(const std::vector<int>& nodes, double* dest, int ld);
   long long bundles() const { return bundles_; }
   bool empty() const { return gather_.empty(); }
   void clear();
