@@ -343,8 +343,12 @@ __device__ __forceinline__ void q0_kernel(double qfactor, double r, double zx,
 // D/N series (scalars 2..9) staged in shared memory once per CTA.
 struct SerSm {
   int par[8], nt[8];
+  int ntmax;
   double2 a[8][kParTerms];
   double2 b[8][kParTerms];
+  // transposed copies for the joint evaluation (8 coefficients per power)
+  double2 at[kParTerms][8];
+  double2 bt[kParTerms][8];
 };
 
 __device__ __forceinline__ void load_sersm(const DevCtx* __restrict__ ctx, SerSm& s) {
@@ -354,10 +358,17 @@ __device__ __forceinline__ void load_sersm(const DevCtx* __restrict__ ctx, SerSm
     const int k = i / kParTerms, p = i - k * kParTerms;
     s.a[k][p] = ctx->pser.a[k + 2][p];
     s.b[k][p] = ctx->pser.b[k + 2][p];
+    s.at[p][k] = ctx->pser.a[k + 2][p];
+    s.bt[p][k] = ctx->pser.b[k + 2][p];
   }
   if (tid < 8) {
     s.par[tid] = ctx->pser.par[tid + 2];
     s.nt[tid] = ctx->pser.nt[tid + 2];
+  }
+  if (tid == 0) {
+    int m = 0;
+    for (int k = 0; k < 8; ++k) m = ctx->pser.nt[k + 2] > m ? ctx->pser.nt[k + 2] : m;
+    s.ntmax = m;
   }
 }
 
@@ -400,6 +411,33 @@ __device__ __forceinline__ void hankel01_lg(double x, double log_half_x,
 
 // kRem = false: full d and n (proxy blocks, kernel_cross_block);
 // kRem = true: full d, remainder n (PairIntegrator::separated).
+// All eight series at once: one loop over powers, 16 independent Horner
+// chains (d-series odd powers, n-series even powers).
+__device__ __forceinline__ void series_joint(const SerSm& S, double u,
+                                             double logr, double r, DN& o) {
+  cplx A[8], B[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) A[k] = B[k] = mk(0.0);
+  for (int p = S.ntmax - 1; p >= 0; --p) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double2 a = S.at[p][k], b = S.bt[p][k];
+      A[k] = mk(fma(A[k].re, u, a.x), fma(A[k].im, u, a.y));
+      B[k] = mk(fma(B[k].re, u, b.x), fma(B[k].im, u, b.y));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    o.d[k] = r * mk(fma(B[k].re, logr, A[k].re), fma(B[k].im, logr, A[k].im));
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+    o.n[k] = mk(fma(B[3 + k].re, logr, A[3 + k].re), fma(B[3 + k].im, logr, A[3 + k].im));
+}
+
+#ifndef EBEM_JOINT_SERIES
+#define EBEM_JOINT_SERIES 1
+#endif
+
 template <bool kRem>
 __device__ __forceinline__ void dn_eval(const DevMedium& m, const SerSm& S,
                                         double r, double ir, double logr,
@@ -407,6 +445,16 @@ __device__ __forceinline__ void dn_eval(const DevMedium& m, const SerSm& S,
   const double ir2 = ir * ir;
   if (r < m.series_radius) {
     const double u = r * r;
+#if EBEM_JOINT_SERIES
+    series_joint(S, u, logr, r, o);
+    o.d[0].re += m.sd1 * ir;
+    o.d[1].re -= m.sd1 * ir;
+    o.d[2].re += m.sd3 * ir;
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+      if (!kRem) o.n[k].re += m.sn[k] * ir2;
+    return;
+#endif
 #pragma unroll
     for (int k = 0; k < 3; ++k) o.d[k] = par_series(S, k, u, logr, r);
     o.d[0].re += m.sd1 * ir;
@@ -587,6 +635,8 @@ __device__ __forceinline__ void dn_eval2(const FillConst& fc, const SerSm& S,
   if (r < m.series_radius) {
 #if EBEM_SERIES_PARAM
     series8<NT>(fc, r * r, logr, r, o);
+#elif EBEM_JOINT_SERIES
+    series_joint(S, r * r, logr, r, o);
 #else
     const double u = r * r;
 #pragma unroll

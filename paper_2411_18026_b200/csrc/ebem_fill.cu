@@ -434,14 +434,19 @@ k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
            int count, int n, double* __restrict__ bundles) {
   extern __shared__ double2 sh[];  // [P * n][8 V + 8 U cplx + 2 (Q as re/im pairs)]
   __shared__ SerSm S;
+  __shared__ double sgx[kMaxGauss], sgw[kMaxGauss];
   load_sersm(ctx, S);
+  if (threadIdx.x < n) {
+    sgx[threadIdx.x] = ctx->gx[gauss_offset(n) + threadIdx.x];
+    sgw[threadIdx.x] = ctx->gw[gauss_offset(n) + threadIdx.x];
+  }
   const int P = blockDim.x / n;
   const int lp = threadIdx.x / n;
   const int i = threadIdx.x - lp * n;
   const int idx = blockIdx.x * P + lp;
   const bool active = lp < P && idx < count;
-  const double* gx = ctx->gx + gauss_offset(n);
-  const double* gw = ctx->gw + gauss_offset(n);
+  const double* gx = sgx;
+  const double* gw = sgw;
   __syncthreads();
   int ea = 0, eb = 0;
   long long vdst = 0, udst = 0;
@@ -464,7 +469,7 @@ k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
     const double nbx = ef(ctx, ENX, eb), nby = ef(ctx, ENY, eb);
     const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
     const double qfac = ctx->med.qfactor;
-    const double s = __ldg(gx + i);
+    const double s = gx[i];
     const double xx = pax + s * dax, xy = pay + s * day;
     cplx rv[2][4], ru[2][4];
     double Q[4] = {0.0, 0.0, 0.0, 0.0};
@@ -473,8 +478,8 @@ k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
 #pragma unroll
       for (int e = 0; e < 4; ++e) rv[b][e] = ru[b][e] = mk(0.0);
     for (int j = 0; j < n; ++j) {
-      const double t = __ldg(gx + j);
-      const double wj = __ldg(gw + j);
+      const double t = gx[j];
+      const double wj = gw[j];
       const double zx = xx - (pbx + t * dbx);
       const double zy = xy - (pby + t * dby);
       const double r = hypot(zx, zy);
@@ -535,8 +540,8 @@ k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
     const int la = k >> 3, lb = (k >> 2) & 1, e = k & 3;
     double ar = 0.0, ai = 0.0, qs = 0.0;
     for (int ii = 0; ii < n; ++ii) {
-      const double sv = __ldg(gx + ii);
-      const double wi = __ldg(gw + ii);
+      const double sv = gx[ii];
+      const double wi = gw[ii];
       const double shape = orient == 0 ? (la == 0 ? 1.0 - sv : sv)
                                        : (lb == 0 ? 1.0 - sv : sv);
       const int slot = orient == 0 ? (lb * 4 + e) : (8 + la * 4 + e);
