@@ -157,6 +157,27 @@ int ebem_gpu_fds_solve(ebem_gpu_fds* f, const double* rhs, int m, double* x,
 int ebem_gpu_fds_solve_device(ebem_gpu_fds* f, const double* rhs_dev, int m,
                               double* x_dev);
 
+/* Any other BlockSource (compression.hpp:66-87), e.g. the reference tests'
+ * MatrixSource / DirectSource: entries and bases come from host callbacks;
+ * the merges (LU, A^-1 U, W, atilde) and every solve run on the device.
+ * Callbacks return 0 on success.  block: out (nr0+nr1) x (nc0+nc1).
+ * basis: k <= min(nr0, nr1, nc0, nc1); skel holds 4*k ids (rs0 rs1 cs0 cs1),
+ * u0 (nr0 x k), u1 (nr1 x k), v0 (k x nc0), v1 (k x nc1), column-major. */
+typedef int (*ebem_block_fn)(void* user, const int* rows0, int nr0,
+                             const int* rows1, int nr1, const int* cols0,
+                             int nc0, const int* cols1, int nc1, double* out);
+typedef int (*ebem_basis_fn)(void* user, const int* rows0, int nr0,
+                             const int* rows1, int nr1, const int* cols0,
+                             int nc0, const int* cols1, int nc1,
+                             int node_begin, int node_end, double epsilon,
+                             int* k, int* saturated, int* skel, double* u0,
+                             double* u1, double* v0, double* v1);
+int ebem_gpu_fds_create_source(int n_nodes, int depth,
+                               const ebem_fds_config* cfg,
+                               ebem_block_fn block, ebem_basis_fn basis,
+                               void* user, ebem_gpu_fds** out,
+                               ebem_fds_stats* stats);
+
 /* FdsSolver::rank_of (proj/include/ebem/fds.hpp:67). */
 int ebem_gpu_fds_rank_of(const ebem_gpu_fds* f, int cell);
 /* Introspection for parity tests: sizes = {nr0, nr1, nc0, nc1, k}; when

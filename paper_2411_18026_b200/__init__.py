@@ -554,15 +554,72 @@ class AssemblerSource(BlockSource):
         return out.view(np.complex128).reshape(-1, 10)
 
 
+_IP = ctypes.POINTER(ctypes.c_int)
+_DP = ctypes.POINTER(ctypes.c_double)
+_BLOCK_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, _IP, ctypes.c_int, _IP,
+                             ctypes.c_int, _IP, ctypes.c_int, _IP, ctypes.c_int, _DP)
+_BASIS_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, _IP, ctypes.c_int, _IP,
+                             ctypes.c_int, _IP, ctypes.c_int, _IP, ctypes.c_int,
+                             ctypes.c_int, ctypes.c_int, ctypes.c_double, _IP, _IP, _IP,
+                             _DP, _DP, _DP, _DP)
+
+
+def _ilist(p, n):
+    return np.ctypeslib.as_array(p, (n,)).copy() if n > 0 else np.zeros(0, np.int32)
+
+
+def _host_callbacks(source: BlockSource, errors: list):
+    """ctypes trampolines exposing a Python BlockSource to the device solver."""
+
+    def block(_, r0, nr0, r1, nr1, c0, nc0, c1, nc1, out):
+        try:
+            rows = (_ilist(r0, nr0), _ilist(r1, nr1))
+            cols = (_ilist(c0, nc0), _ilist(c1, nc1))
+            a = np.asarray(source.block(rows, cols), dtype=np.complex128)
+            nr, nc = nr0 + nr1, nc0 + nc1
+            if a.shape != (nr, nc):
+                raise InvalidArgument(f"BlockSource::block returned {a.shape}, need {(nr, nc)}")
+            if nr and nc:
+                np.ctypeslib.as_array(out, (2 * nr * nc,))[:] = _to_cbuf(a, nr, nc)
+            return 0
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+            return 1 if isinstance(e, ValueError) else 2
+
+    def basis(_, r0, nr0, r1, nr1, c0, nc0, c1, nc1, b, e, eps, k, sat, skel, u0, u1,
+              v0, v1):
+        try:
+            rows = (_ilist(r0, nr0), _ilist(r1, nr1))
+            cols = (_ilist(c0, nc0), _ilist(c1, nc1))
+            cb = source.cell_basis(rows, cols, b, e, eps)
+            kk = int(cb.k)
+            k[0] = kk
+            sat[0] = 1 if cb.saturated else 0
+            if kk:
+                sk = np.concatenate([np.asarray(cb.row_skeleton[0]), np.asarray(cb.row_skeleton[1]),
+                                     np.asarray(cb.col_skeleton[0]), np.asarray(cb.col_skeleton[1])])
+                np.ctypeslib.as_array(skel, (4 * kk,))[:] = sk.astype(np.int32)
+                for ptr, m, (r_, c_) in ((u0, cb.u[0], (nr0, kk)), (u1, cb.u[1], (nr1, kk)),
+                                         (v0, cb.v[0], (kk, nc0)), (v1, cb.v[1], (kk, nc1))):
+                    np.ctypeslib.as_array(ptr, (2 * r_ * c_,))[:] = _to_cbuf(m, r_, c_)
+            return 0
+        except Exception as ex:  # noqa: BLE001
+            errors.append(ex)
+            return 1 if isinstance(ex, ValueError) else 2
+
+    return _BLOCK_FN(block), _BASIS_FN(basis)
+
+
 class FdsSolver:
-    """Hierarchical direct solver, fds.hpp:44-94.  Construction factorizes."""
+    """Hierarchical direct solver, fds.hpp:44-94.  Construction factorizes.
+
+    AssemblerSource runs entirely on the device.  Any other BlockSource (the
+    reference tests' MatrixSource / DirectSource fakes) supplies entries and
+    bases through host callbacks; the merges and solves still run on the
+    device."""
 
     def __init__(self, source: BlockSource, tree: ClusterTree,
                  config: FdsConfig = None):
-        if not isinstance(source, AssemblerSource):
-            raise InvalidArgument(
-                "FdsSolver (B200 path): only AssemblerSource is implemented on "
-                "the device")
         self._source, self._tree = source, tree
         self._config = config or FdsConfig()
         if tree.n_nodes() != source.n_nodes():
@@ -570,8 +627,19 @@ class FdsSolver:
         cfg = _FdsCfg(self._config.epsilon, self._config.ell0)
         st = _FdsStats()
         h = ctypes.c_void_p()
-        _check(lib().ebem_gpu_fds_create(source._h.h, tree.depth(), ctypes.byref(cfg),
-                                         ctypes.byref(h), ctypes.byref(st)))
+        if isinstance(source, AssemblerSource):
+            _check(lib().ebem_gpu_fds_create(source._h.h, tree.depth(), ctypes.byref(cfg),
+                                             ctypes.byref(h), ctypes.byref(st)))
+        else:
+            self._errors = []
+            self._cbs = _host_callbacks(source, self._errors)
+            rc = lib().ebem_gpu_fds_create_source(tree.n_nodes(), tree.depth(),
+                                                  ctypes.byref(cfg), self._cbs[0],
+                                                  self._cbs[1], None, ctypes.byref(h),
+                                                  ctypes.byref(st))
+            if rc != 0 and self._errors:
+                raise self._errors[0]
+            _check(rc)
         self._h = h
         self._stats = FdsStats(
             max_rank=list(st.max_rank)[: tree.depth() + 1], top_dim=st.top_dim,

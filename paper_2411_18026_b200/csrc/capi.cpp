@@ -18,6 +18,8 @@ struct ebem_gpu_problem {
 };
 struct ebem_gpu_fds {
   Fds* f;
+  Problem* own = nullptr;  // source-only problem owned by the solver
+  HostSource hs{};
 };
 
 namespace {
@@ -287,7 +289,7 @@ int ebem_gpu_fds_create(ebem_gpu_problem* p, int depth,
     c.epsilon = 1e-8;
     c.ell0 = 1;
     if (cfg) c = *cfg;
-    auto* h = new ebem_gpu_fds{nullptr};
+    auto* h = new ebem_gpu_fds{};
     try {
       h->f = new Fds(*p->p, depth, c);
     } catch (...) {
@@ -303,7 +305,34 @@ void ebem_gpu_fds_destroy(ebem_gpu_fds* f) {
   if (!f) return;
   std::lock_guard<std::recursive_mutex> lock(api_mutex());
   delete f->f;
+  delete f->own;
   delete f;
+}
+
+int ebem_gpu_fds_create_source(int n_nodes, int depth, const ebem_fds_config* cfg,
+                               ebem_block_fn block, ebem_basis_fn basis,
+                               void* user, ebem_gpu_fds** out,
+                               ebem_fds_stats* stats) {
+  return guarded([&] {
+    if (!block || !basis || !out) throw Error(EBEM_INVALID_ARGUMENT, "null argument");
+    ebem_fds_config c;
+    c.epsilon = 1e-8;
+    c.ell0 = 1;
+    if (cfg) c = *cfg;
+    auto* h = new ebem_gpu_fds{};
+    try {
+      h->hs = HostSource{block, basis, user};
+      h->own = new Problem(n_nodes);
+      h->f = new Fds(*h->own, depth, c, &h->hs);
+    } catch (...) {
+      delete h->f;
+      delete h->own;
+      delete h;
+      throw;
+    }
+    if (stats) *stats = h->f->stats();
+    *out = h;
+  });
 }
 
 int ebem_gpu_fds_solve(ebem_gpu_fds* f, const double* rhs, int m, double* x,

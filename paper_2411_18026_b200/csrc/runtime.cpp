@@ -377,6 +377,33 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   tree_.build(xy_.data(), n);
 }
 
+Problem::Problem(int n)
+    : staging(scratch().staging),
+      tbuf_(scratch().tbuf),
+      qr_rounds_(scratch().qr_rounds),
+      id_jp_(scratch().id_jp),
+      id_steps_(scratch().id_steps),
+      id_rd_(scratch().id_rd),
+      id_r_(scratch().id_r),
+      sym_keys_(scratch().sym_keys),
+      sym_vals_(scratch().sym_vals),
+      sort_temp_(scratch().sort_temp),
+      sort_temp_bytes_(scratch().sort_temp_bytes),
+      sym_bounds_(scratch().sym_bounds),
+      sym_bounds_host_(scratch().sym_bounds_host),
+      sym_ev_(scratch().sym_ev),
+      bundles(scratch().bundles),
+      gws(scratch().gws),
+      n_(n) {
+  if (n <= 0) throw Error(EBEM_INVALID_ARGUMENT, "FdsSolver: node count must be positive");
+  acfg_ = ebem_assembly_config{10, 4, 8, 1.0, size_t(4) << 30};
+  pcfg_ = ebem_proxy_config{1.5, 64, 6};
+  st_ = scratch().st;
+  bad.alloc(1);
+  CK(cudaMemsetAsync(bad.get(), 0, sizeof(int), st_));
+  dense_init();
+}
+
 Problem::~Problem() {
   if (st_) cudaStreamSynchronize(st_);  // the stream is process-wide
 }
@@ -1374,8 +1401,9 @@ void singular_error(int info, int n) {
 }  // namespace
 
 // -------------------------------------------------------------------- Fds
-Fds::Fds(Problem& p, int depth, const ebem_fds_config& cfg)
-    : P_(p), depth_(depth), cfg_(cfg) {
+Fds::Fds(Problem& p, int depth, const ebem_fds_config& cfg,
+         const HostSource* hs)
+    : P_(p), depth_(depth), cfg_(cfg), hs_(hs) {
   const int n = P_.n();
   if (depth < 0) throw Error(EBEM_INVALID_ARGUMENT, "ClusterTree: negative depth");
   if (depth >= EBEM_MAX_LEVELS - 1)
@@ -1470,7 +1498,8 @@ void Fds::build() {
     std::vector<BasisRes> br;
     DBuf<double>& ubuf = ubuf_;
     const double tb = now();
-    P_.bases(req, cfg_.epsilon, br, S.v, ubuf);
+    if (hs_) host_bases(level, br, S.v, ubuf);
+    else P_.bases(req, cfg_.epsilon, br, S.v, ubuf);
     basis_seconds += now() - tb;
     // ---- diagonal blocks (leaf: exact; above: reduced) into the LU arena
     size_t lu_total = 0, piv_total = 0, au_total = 0, at_total = 0;
@@ -1507,7 +1536,19 @@ void Fds::build() {
       PhaseTimer tp("fill_diagonal", P_.stream());
       FillPlan plan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
       std::vector<CopyTask> copies;
-      for (int i = 0; i < nlev; ++i) {
+      for (int i = 0; hs_ && i < nlev; ++i) {  // host source: assemble on host
+        Cell& C = cells_[f + i];
+        const int d = 2 * C.nloc;
+        std::vector<double> h;
+        if (level == depth_) {
+          h = host_block(C.jrow, C.jcol);
+        } else {
+          h.assign(2 * size_t(d) * d, 0.0);
+          host_reduced_diagonal(f + i, h.data(), d);
+        }
+        if (d) CK(cudaMemcpy(C.lu, h.data(), 16 * size_t(d) * d, cudaMemcpyHostToDevice));
+      }
+      for (int i = 0; !hs_ && i < nlev; ++i) {
         Cell& C = cells_[f + i];
         const int d = 2 * C.nloc;
         if (level == depth_) {
@@ -1626,10 +1667,32 @@ void Fds::build() {
   stats_.top_dim = top_dim_;
   top_lu_.alloc(2 * size_t(top_dim_) * top_dim_ + 2);
   top_ipiv_.alloc(top_dim_ + 1);
+  if (hs_ && top_dim_ > 0) {  // host source: the dense top system on the host
+    std::vector<double> h(2 * size_t(top_dim_) * top_dim_, 0.0);
+    for (int i = 0; i <= tl - tf; ++i) {
+      const Cell& ci = cells_[tf + i];
+      for (int j = 0; j <= tl - tf; ++j) {
+        const Cell& cj = cells_[tf + j];
+        const int ri = 2 * ci.nloc, cjn = 2 * cj.nloc;
+        if (!ri || !cjn) continue;
+        std::vector<double> blk;
+        if (i == j) {
+          blk.assign(2 * size_t(ri) * ri, 0.0);
+          host_reduced_diagonal(tf + i, blk.data(), ri);
+        } else {
+          blk = host_block(ci.jrow, cj.jcol);
+        }
+        for (int c = 0; c < cjn; ++c)
+          std::memcpy(h.data() + 2 * (size_t(top_off_[j] + c) * top_dim_ + top_off_[i]),
+                      blk.data() + 2 * size_t(c) * ri, 16 * size_t(ri));
+      }
+    }
+    CK(cudaMemcpy(top_lu_.get(), h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+  }
   {
     FillPlan plan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
     std::vector<CopyTask> copies;
-    for (int i = 0; i <= tl - tf; ++i) {
+    for (int i = 0; !hs_ && i <= tl - tf; ++i) {
       const Cell& ci = cells_[tf + i];
       for (int j = 0; j <= tl - tf; ++j) {
         const Cell& cj = cells_[tf + j];
@@ -1687,6 +1750,91 @@ void Fds::debug_cell(int cell, int which, double* out) const {
     default: throw Error(EBEM_INVALID_ARGUMENT, "debug_cell: bad selector");
   }
   if (src && bytes) CK(cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost));
+}
+
+std::vector<double> Fds::host_block(const Lists& rows, const Lists& cols) {
+  const int nr = int(rows[0].size() + rows[1].size());
+  const int nc = int(cols[0].size() + cols[1].size());
+  std::vector<double> out(2 * size_t(nr) * nc, 0.0);
+  if (!nr || !nc) return out;
+  const int rc = hs_->block(hs_->user, rows[0].data(), int(rows[0].size()),
+                            rows[1].data(), int(rows[1].size()), cols[0].data(),
+                            int(cols[0].size()), cols[1].data(), int(cols[1].size()),
+                            out.data());
+  if (rc) throw Error(rc, "BlockSource::block callback failed");
+  return out;
+}
+
+// FdsSolver::reduced_diagonal (proj/src/fds.cpp:33-54) on the host.
+void Fds::host_reduced_diagonal(int cell, double* out, int ld) {
+  const Cell& c1 = cells_[2 * cell + 1];
+  const Cell& c2 = cells_[2 * cell + 2];
+  const int k1 = c1.k, k2 = c2.k, np = k1 + k2;
+  std::vector<double> a1(2 * size_t(4) * k1 * k1), a2(2 * size_t(4) * k2 * k2);
+  if (k1) CK(cudaMemcpy(a1.data(), c1.atilde, a1.size() * 8, cudaMemcpyDeviceToHost));
+  if (k2) CK(cudaMemcpy(a2.data(), c2.atilde, a2.size() * 8, cudaMemcpyDeviceToHost));
+  const std::vector<double> x12 = host_block(c1.srow, c2.scol);
+  const std::vector<double> x21 = host_block(c2.srow, c1.scol);
+  auto put = [&](int r, int c, const double* src, int sld, int sr, int sc) {
+    out[2 * (size_t(c) * ld + r)] = src[2 * (size_t(sc) * sld + sr)];
+    out[2 * (size_t(c) * ld + r) + 1] = src[2 * (size_t(sc) * sld + sr) + 1];
+  };
+  for (int p = 0; p < 2; ++p)
+    for (int q = 0; q < 2; ++q) {
+      for (int jj = 0; jj < k1; ++jj)
+        for (int ii = 0; ii < k1; ++ii)
+          put(p * np + ii, q * np + jj, a1.data(), 2 * k1, p * k1 + ii, q * k1 + jj);
+      for (int jj = 0; jj < k2; ++jj)
+        for (int ii = 0; ii < k2; ++ii)
+          put(p * np + k1 + ii, q * np + k1 + jj, a2.data(), 2 * k2, p * k2 + ii, q * k2 + jj);
+      for (int jj = 0; jj < k2; ++jj)
+        for (int ii = 0; ii < k1; ++ii)
+          put(p * np + ii, q * np + k1 + jj, x12.data(), 2 * k1, p * k1 + ii, q * k2 + jj);
+      for (int jj = 0; jj < k1; ++jj)
+        for (int ii = 0; ii < k2; ++ii)
+          put(p * np + k1 + ii, q * np + jj, x21.data(), 2 * k2, p * k2 + ii, q * k1 + jj);
+    }
+}
+
+void Fds::host_bases(int level, std::vector<BasisRes>& br, DBuf<double>& vbuf,
+                     DBuf<double>& ubuf) {
+  const int f = first(level), L = last(level), nlev = L - f + 1;
+  br.assign(nlev, BasisRes{});
+  std::vector<double> hv, hu;
+  for (int i = 0; i < nlev; ++i) {
+    Cell& C = cells_[f + i];
+    const int nr0 = int(C.jrow[0].size()), nr1 = int(C.jrow[1].size());
+    const int nc0 = int(C.jcol[0].size()), nc1 = int(C.jcol[1].size());
+    if (!nr0 || !nr1 || !nc0 || !nc1) throw Error(EBEM_INVALID_ARGUMENT, "Cpqr: empty matrix");
+    const int kmax = std::min(std::min(nr0, nr1), std::min(nc0, nc1));
+    std::vector<int> skel(4 * size_t(kmax) + 4);
+    std::vector<double> u0(2 * size_t(nr0) * kmax + 2), u1(2 * size_t(nr1) * kmax + 2);
+    std::vector<double> v0(2 * size_t(nc0) * kmax + 2), v1(2 * size_t(nc1) * kmax + 2);
+    int k = 0, sat = 0;
+    const int rc = hs_->basis(hs_->user, C.jrow[0].data(), nr0, C.jrow[1].data(), nr1,
+                              C.jcol[0].data(), nc0, C.jcol[1].data(), nc1, C.begin,
+                              C.end, cfg_.epsilon, &k, &sat, skel.data(), u0.data(),
+                              u1.data(), v0.data(), v1.data());
+    if (rc) throw Error(rc, "BlockSource::cell_basis callback failed");
+    if (k < 0 || k > kmax) throw Error(EBEM_LOGIC_ERROR, "BlockSource::cell_basis: rank out of range");
+    BasisRes& r = br[i];
+    r.k = k;
+    r.saturated = sat != 0;
+    r.srow[0].assign(skel.begin(), skel.begin() + k);
+    r.srow[1].assign(skel.begin() + k, skel.begin() + 2 * k);
+    r.scol[0].assign(skel.begin() + 2 * k, skel.begin() + 3 * k);
+    r.scol[1].assign(skel.begin() + 3 * k, skel.begin() + 4 * k);
+    r.v_off = hv.size() / 2;
+    hv.insert(hv.end(), v0.begin(), v0.begin() + 2 * size_t(k) * nc0);
+    hv.insert(hv.end(), v1.begin(), v1.begin() + 2 * size_t(k) * nc1);
+    r.u_off = hu.size() / 2;
+    hu.insert(hu.end(), u0.begin(), u0.begin() + 2 * size_t(k) * nr0);
+    hu.insert(hu.end(), u1.begin(), u1.begin() + 2 * size_t(k) * nr1);
+  }
+  vbuf.ensure(hv.size() + 2);
+  ubuf.ensure(hu.size() + 2);
+  if (!hv.empty()) CK(cudaMemcpy(vbuf.get(), hv.data(), hv.size() * 8, cudaMemcpyHostToDevice));
+  if (!hu.empty()) CK(cudaMemcpy(ubuf.get(), hu.data(), hu.size() * 8, cudaMemcpyHostToDevice));
 }
 
 int Fds::rank_of(int cell) const {

@@ -237,6 +237,8 @@ class Problem {
   Problem(const double* xy, int n, double lam, double mu, double rho,
           double omega, double are, double aim, const ebem_assembly_config& a,
           const ebem_proxy_config& p);
+  // Source-only handle (host BlockSource callbacks): no geometry on device.
+  explicit Problem(int n);
   ~Problem();
 
   int n() const { return n_; }
@@ -355,9 +357,16 @@ class FillPlan {
 };
 
 // ----------------------------------------------------------------- solver
+struct HostSource {
+  ebem_block_fn block;
+  ebem_basis_fn basis;
+  void* user;
+};
+
 class Fds {
  public:
-  Fds(Problem& p, int depth, const ebem_fds_config& cfg);
+  Fds(Problem& p, int depth, const ebem_fds_config& cfg,
+      const HostSource* hs = nullptr);
   void solve_device(const double* rhs, int m, double* x, ebem_fds_solve_timing* t);
   const ebem_fds_stats& stats() const { return stats_; }
   int rank_of(int cell) const;
@@ -382,6 +391,12 @@ class Fds {
     DBuf<int> ipiv;
   };
   void build();
+  // host-source path (callbacks): bases, exact blocks, reduced diagonals
+  void host_bases(int level, std::vector<BasisRes>& br, DBuf<double>& vbuf,
+                  DBuf<double>& ubuf);
+  std::vector<double> host_block(const Lists& rows, const Lists& cols);
+  void host_reduced_diagonal(int cell, double* out, int ld);
+  const HostSource* hs_ = nullptr;
   void reduced_diagonal(FillPlan& plan, std::vector<CopyTask>& copies, int cell,
                         double* dest, int ld, int off);
   int first(int l) const { return (1 << l) - 1; }

@@ -51,9 +51,9 @@ def test_cluster_tree_indexing():
         eb.ClusterTree(100, 3)
 
 
-def test_solver_rejects_non_device_sources():
+def test_solver_checks_tree_size():
     class Fake(eb.BlockSource):
         def n_nodes(self):
             return 64
     with pytest.raises(eb.InvalidArgument):
-        eb.FdsSolver(Fake(), eb.ClusterTree(64, 1))
+        eb.FdsSolver(Fake(), eb.ClusterTree(128, 1))
