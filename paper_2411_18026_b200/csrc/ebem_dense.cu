@@ -412,11 +412,13 @@ k_getrf(const LuTask* __restrict__ tasks, double2* __restrict__ gws) {
 }
 
 // ---------------------------------------------------------------- LU solve
-// One warp per right-hand-side column.  grid = (task, column group).
+// One warp per right-hand-side column.  grid = (task, column group).  The
+// LU factors (and the columns) are staged in shared memory when they fit, so
+// the dependent substitution steps hit ~30-cycle shared memory, not L2.
 __global__ void __launch_bounds__(kThreads)
 k_getrs(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off,
-        int n_tasks) {
-  // find task
+        int n_tasks, int cap) {
+  extern __shared__ double2 sm[];
   int lo = 0, hi = n_tasks - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -425,11 +427,28 @@ k_getrs(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off
   }
   const LuSolveTask T = tasks[lo];
   const int n = T.n;
+  const bool stage = (long long)n * n + (long long)kWarps * n <= cap;
   const double2* A = reinterpret_cast<const double2*>(T.lu);
+  size_t lda = T.ld;
+  if (stage) {
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+      const int j = idx / n, i = idx - j * n;
+      sm[idx] = A[(size_t)j * lda + i];
+    }
+    A = sm;
+    lda = n;
+  }
+  __syncthreads();
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int col = (blockIdx.x - block_off[lo]) * kWarps + w;
   if (col >= T.nrhs) return;
-  double2* b = reinterpret_cast<double2*>(T.b) + (size_t)col * T.ldb;
+  double2* bg = reinterpret_cast<double2*>(T.b) + (size_t)col * T.ldb;
+  double2* b = bg;
+  if (stage) {
+    b = sm + (size_t)n * n + (size_t)w * n;
+    for (int r = l; r < n; r += 32) b[r] = bg[r];
+    __syncwarp();
+  }
   // row interchanges in order
   if (l == 0) {
     for (int k = 0; k < n; ++k) {
@@ -445,17 +464,19 @@ k_getrs(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off
   // L y = b (unit lower)
   for (int k = 0; k < n; ++k) {
     const double2 bk = b[k];
-    for (int r = k + 1 + l; r < n; r += 32) b[r] = zfms(b[r], A[(size_t)k * T.ld + r], bk);
+    for (int r = k + 1 + l; r < n; r += 32) b[r] = zfms(b[r], A[(size_t)k * lda + r], bk);
     __syncwarp();
   }
   // U x = y
   for (int k = n - 1; k >= 0; --k) {
-    if (l == 0) b[k] = zdiv(b[k], A[(size_t)k * T.ld + k]);
+    if (l == 0) b[k] = zdiv(b[k], A[(size_t)k * lda + k]);
     __syncwarp();
     const double2 xk = b[k];
-    for (int r = l; r < k; r += 32) b[r] = zfms(b[r], A[(size_t)k * T.ld + r], xk);
+    for (int r = l; r < k; r += 32) b[r] = zfms(b[r], A[(size_t)k * lda + r], xk);
     __syncwarp();
   }
+  if (stage)
+    for (int r = l; r < n; r += 32) bg[r] = b[r];
 }
 
 // --------------------------------------------------------------------- GEMM
@@ -569,6 +590,7 @@ void dense_init() {
   set_smem_attr((const void*)k_qr_reduce);
   set_smem_attr((const void*)k_cpqr);
   set_smem_attr((const void*)k_getrf);
+  set_smem_attr((const void*)k_getrs);
   done = true;
 }
 
@@ -594,9 +616,15 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
 }
 int getrs_blocks(int nrhs) { return (nrhs + kWarps - 1) / kWarps; }
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
-                  int n_blocks, cudaStream_t st) {
+                  int n_blocks, cudaStream_t st, int smem_bytes) {
   if (n_blocks <= 0) return;
-  k_getrs<<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+  k_getrs<<<n_blocks, kThreads, size_t(smem_bytes), st>>>(tasks, block_off, n_tasks,
+                                                          smem_bytes / 16);
+}
+
+int getrs_smem_bytes(int n) {
+  const long long b = ((long long)n * n + (long long)kWarps * n) * 16;
+  return b <= kSmemCap ? int(b) : 0;
 }
 int gemm_blocks(int m, int n) {
   return ((m + kTile - 1) / kTile) * ((n + kTile - 1) / kTile);

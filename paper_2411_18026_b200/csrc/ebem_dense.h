@@ -88,7 +88,9 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st);
 int getrs_blocks(int nrhs);
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
-                  int n_blocks, cudaStream_t st);
+                  int n_blocks, cudaStream_t st, int smem_bytes = 0);
+// Dynamic shared memory that stages an n x n LU (0 when it does not fit).
+int getrs_smem_bytes(int n);
 int gemm_blocks(int m, int n);
 void launch_gemm(const GemmTask* tasks, const int* block_off, int n_tasks,
                  int n_blocks, cudaStream_t st);

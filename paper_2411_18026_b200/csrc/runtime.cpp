@@ -1295,6 +1295,10 @@ void Problem::rhs_plane(int kind, const double* angles, int m, double amp,
 
 // ------------------------------------------------------------ batched LA
 namespace {
+// k_getrs stages the LU in shared memory up to this many bytes per launch
+// (shared by all tasks of the launch; larger tasks read L2).
+int g_getrs_smem = 0;
+
 template <class T, class F, class U>
 void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
                  void (*launch)(const T*, const int*, int, int, cudaStream_t),
@@ -1307,6 +1311,10 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
     total += blocks_of(t[i]);
   }
   if (total == 0) return;
+  if (P.recorder) {
+    P.recorder->add(id, t, boff, total, id == KP_GETRS ? g_getrs_smem : 0);
+    return;
+  }
   Pack pk;
   const size_t o1 = pk.add(t);
   const size_t o2 = pk.add(boff);
@@ -1323,6 +1331,35 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
 }
 }  // namespace
 
+void Recorder::finalize(cudaStream_t st) {
+  if (!pk_.bytes()) return;
+  dev_.alloc(pk_.bytes());
+  CK(cudaMemcpyAsync(dev_.get(), pk_.data(), pk_.bytes(), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+void Recorder::replay(cudaStream_t st, int phase) {
+  char* base = dev_.get();
+  for (int i = marks_[phase]; i < marks_[phase + 1]; ++i) {
+    const Launch& l = launches_[i];
+    const int* boff = Pack::at<int>(base, l.boff_off);
+    switch (l.kind) {
+      case KP_COPY:
+        launch_copy(Pack::at<CopyTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st);
+        break;
+      case KP_GEMM:
+        launch_gemm(Pack::at<GemmTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st);
+        break;
+      case KP_GETRS:
+        launch_getrs(Pack::at<LuSolveTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st,
+                     l.aux);
+        break;
+      default:
+        throw Error(EBEM_LOGIC_ERROR, "Recorder: unexpected kernel kind");
+    }
+  }
+}
+
 void run_copies(Problem& P, const std::vector<CopyTask>& t) {
   run_blocked(P, t, [](const CopyTask& c) { return copy_blocks(c.rows, c.cols); },
               launch_copy, KP_COPY,
@@ -1333,9 +1370,19 @@ void run_gemms(Problem& P, const std::vector<GemmTask>& t) {
               launch_gemm, KP_GEMM,
               [](const GemmTask& g) { return 8.0 * g.m * g.n * double(g.k); });
 }
+namespace {
+void launch_getrs_staged(const LuSolveTask* t, const int* boff, int nt, int nb,
+                         cudaStream_t st) {
+  launch_getrs(t, boff, nt, nb, st, g_getrs_smem);
+}
+}  // namespace
+
 void run_getrs(Problem& P, const std::vector<LuSolveTask>& t) {
+  int smem = 0;
+  for (const LuSolveTask& x : t) smem = std::max(smem, getrs_smem_bytes(x.n));
+  g_getrs_smem = smem;
   run_blocked(P, t, [](const LuSolveTask& s) { return s.n > 0 ? getrs_blocks(s.nrhs) : 0; },
-              launch_getrs, KP_GETRS,
+              launch_getrs_staged, KP_GETRS,
               [](const LuSolveTask& s) { return 8.0 * s.n * double(s.n) * s.nrhs; });
 }
 void run_getrf(Problem& P, std::vector<LuTask> t) {
@@ -1862,8 +1909,10 @@ void Fds::cell_info(int cell, int* sizes, int* skel) const {
   }
 }
 
-void Fds::solve_device(const double* rhs, int m, double* x,
-                       ebem_fds_solve_timing* timing) {
+void Fds::record_solve(int m) {
+  plan_.reset(new SolvePlan());
+  SolvePlan& S = *plan_;
+  S.m = m;
   const int n = P_.n();
   const int ncells = int(cells_.size());
   const int leaf = n >> depth_;
@@ -1880,14 +1929,15 @@ void Fds::solve_device(const double* rhs, int m, double* x,
   ws_ft_.ensure(2 * ktot * m + 2);
   ws_t_.ensure(2 * ktot * m + 2);
   ws_x_.ensure(2 * size_t(top_dim_) * m + 2);
+  S.rhs.alloc(4 * size_t(n) * m);
+  S.x.alloc(4 * size_t(n) * m);
+  const double* rhs = S.rhs.get();
+  double* x = S.x.get();
   auto F = [&](int c) { return ws_f_.get() + 2 * fo[c] * m; };
   auto FT = [&](int c) { return ws_ft_.get() + 2 * ko[c] * m; };
   auto TT = [&](int c) { return ws_t_.get() + 2 * ko[c] * m; };
-  cudaEvent_t ev0, ev1;
-  CK(cudaEventCreate(&ev0));
-  CK(cudaEventCreate(&ev1));
-  CK(cudaEventRecord(ev0, P_.stream()));
-  const double t0 = now();
+  P_.recorder = &S.rec;
+  S.rec.mark();
   // leaves: f = [rhs[a:a+s]; rhs[N+a:N+a+s]]
   {
     std::vector<CopyTask> ct;
@@ -1932,8 +1982,7 @@ void Fds::solve_device(const double* rhs, int m, double* x,
     }
     run_copies(P_, ct);
   }
-  CK(cudaStreamSynchronize(P_.stream()));
-  const double t1 = now();
+  S.rec.mark();
   // top: stack, solve, unstack (x of the top cells lives in their f blocks)
   {
     const int tf = first(cfg_.ell0), tl = last(cfg_.ell0);
@@ -1951,8 +2000,7 @@ void Fds::solve_device(const double* rhs, int m, double* x,
                                  top_dim_, m, top_dim_}});
     run_copies(P_, back);
   }
-  CK(cudaStreamSynchronize(P_.stream()));
-  const double t2 = now();
+  S.rec.mark();
   // downward: x_child = ainvf + ainv_u (atilde y - ftilde)
   for (int level = cfg_.ell0; level < depth_; ++level) {
     std::vector<CopyTask> ct;
@@ -1986,21 +2034,56 @@ void Fds::solve_device(const double* rhs, int m, double* x,
     }
     run_copies(P_, ct);
   }
-  CK(cudaStreamSynchronize(P_.stream()));
-  const double t3 = now();
-  if (timing) {
-    timing->upward_seconds = t1 - t0;
-    timing->top_seconds = t2 - t1;
-    timing->downward_seconds = t3 - t2;
+  S.rec.mark();
+  P_.recorder = nullptr;
+  S.rec.finalize(P_.stream());
+  for (int q = 0; q < 4; ++q) CK(cudaEventCreate(&S.ev[q]));
+  // one graph per phase (upward, top, downward); timing events go between
+  for (int ph = 0; ph < 3; ++ph) {
+    CK(cudaStreamBeginCapture(P_.stream(), cudaStreamCaptureModeThreadLocal));
+    S.rec.replay(P_.stream(), ph);
+    CK(cudaStreamEndCapture(P_.stream(), &S.graph[ph]));
+    CK(cudaGraphInstantiate(&S.exec[ph], S.graph[ph], 0));
   }
-  CK(cudaEventRecord(ev1, P_.stream()));
-  CK(cudaEventSynchronize(ev1));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, ev0, ev1));
-  last_solve_device_seconds_ = 1e-3 * ms;
-  if (timing) timing->device_seconds = last_solve_device_seconds_;
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
+}
+
+Fds::~Fds() {
+  if (plan_) {
+    for (int ph = 0; ph < 3; ++ph) {
+      if (plan_->exec[ph]) cudaGraphExecDestroy(plan_->exec[ph]);
+      if (plan_->graph[ph]) cudaGraphDestroy(plan_->graph[ph]);
+    }
+    for (auto& e : plan_->ev)
+      if (e) cudaEventDestroy(e);
+  }
+}
+
+void Fds::solve_device(const double* rhs, int m, double* x,
+                       ebem_fds_solve_timing* timing) {
+  const int n = P_.n();
+  if (!plan_ || plan_->m != m) record_solve(m);
+  SolvePlan& S = *plan_;
+  const size_t bytes = 32 * size_t(n) * m;
+  CK(cudaMemcpyAsync(S.rhs.get(), rhs, bytes, cudaMemcpyDefault, P_.stream()));
+  for (int ph = 0; ph < 3; ++ph) {
+    CK(cudaEventRecord(S.ev[ph], P_.stream()));
+    CK(cudaGraphLaunch(S.exec[ph], P_.stream()));
+  }
+  CK(cudaEventRecord(S.ev[3], P_.stream()));
+  CK(cudaMemcpyAsync(x, S.x.get(), bytes, cudaMemcpyDefault, P_.stream()));
+  CK(cudaStreamSynchronize(P_.stream()));
+  float a = 0.f, b = 0.f, c = 0.f;
+  CK(cudaEventElapsedTime(&a, S.ev[0], S.ev[1]));
+  CK(cudaEventElapsedTime(&b, S.ev[1], S.ev[2]));
+  CK(cudaEventElapsedTime(&c, S.ev[2], S.ev[3]));
+  last_solve_device_seconds_ = 1e-3 * (a + b + c);
+  g_launches += long(S.rec.n_launches());
+  if (timing) {
+    timing->upward_seconds = 1e-3 * a;
+    timing->top_seconds = 1e-3 * b;
+    timing->downward_seconds = 1e-3 * c;
+    timing->device_seconds = last_solve_device_seconds_;
+  }
 }
 
 }  // namespace ebem_gpu

@@ -209,6 +209,43 @@ struct BasisRes {
 
 class FillPlan;
 
+// Records batched LA launches (copies, GEMMs, LU solves) instead of issuing
+// them: the task arrays of a whole solve are uploaded once and the launch
+// sequence is captured into a CUDA graph that each solve replays.
+class Recorder {
+ public:
+  template <class T>
+  void add(int kind, const std::vector<T>& t, const std::vector<int>& boff,
+           int total, int aux = 0) {
+    Launch l;
+    l.kind = kind;
+    l.task_off = pk_.add(t);
+    l.boff_off = pk_.add(boff);
+    l.n_tasks = int(t.size());
+    l.n_blocks = total;
+    l.aux = aux;
+    launches_.push_back(l);
+  }
+  void mark() { marks_.push_back(int(launches_.size())); }
+  void finalize(cudaStream_t st);
+  // launches between marks a and b (phase a of the recording)
+  void replay(cudaStream_t st, int phase);
+  int n_marks() const { return int(marks_.size()); }
+  size_t n_launches() const { return launches_.size(); }
+
+ private:
+  struct Launch {
+    int kind;
+    size_t task_off, boff_off;
+    int n_tasks, n_blocks;
+    int aux;  // k_getrs: dynamic shared memory bytes
+  };
+  Pack pk_;
+  std::vector<Launch> launches_;
+  std::vector<int> marks_;
+  DBuf<char> dev_;
+};
+
 // Process-wide device scratch and stream shared by every handle: new
 // problems and solvers reuse warm buffers (GBs of bundles, pinned staging)
 // instead of reallocating them.  All C ABI entry points serialise on
@@ -287,6 +324,7 @@ class Problem {
   DBuf<double>& bundles;
   DBuf<double2>& gws;
   DBuf<int> bad;
+  Recorder* recorder = nullptr;  // set while a solve is being recorded
 
  private:
   int n_;
@@ -418,8 +456,21 @@ class Fds {
   std::vector<int> info_n_;   // their matrix sizes (for the error message)
   DBuf<double> ubuf_, wbuf_;  // per-level temporaries (grow-only)
   DBuf<int> wpiv_;
-  // solve workspaces (grow-only)
+  // solve workspaces and the recorded solve (one cached plan, per m)
   DBuf<double> ws_f_, ws_ainvf_, ws_ft_, ws_x_, ws_t_;
+  void record_solve(int m);
+  struct SolvePlan {
+    int m = -1;
+    Recorder rec;
+    DBuf<double> rhs, x;
+    cudaGraph_t graph[3] = {nullptr, nullptr, nullptr};  // up, top, down
+    cudaGraphExec_t exec[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  };
+  std::unique_ptr<SolvePlan> plan_;
+
+ public:
+  ~Fds();
 };
 
 // ------------------------------------------------------------ batched LA
