@@ -377,14 +377,15 @@ int ebem_gpu_fds_debug_cell(const ebem_gpu_fds* f, int cell, int which,
 int ebem_gpu_eval_hankel(const double* x, int n, double* out) {
   return guarded([&] {
     if (n <= 0) return;
+    scratch();  // the device check (no CPU fallback)
     DBuf<double> dx, dout;
     dx.alloc(n);
     dout.alloc(4 * size_t(n));
-    CK(cudaMemcpy(dx.get(), x, 8 * size_t(n), cudaMemcpyHostToDevice));
-    launch_eval_hankel(dx.get(), n, dout.get(), 0);
+    copy_sync(dx.get(), x, 8 * size_t(n));
+    launch_eval_hankel(dx.get(), n, dout.get(), scratch_stream());
     ++g_launches;  // test hook
     CK(cudaGetLastError());
-    CK(cudaMemcpy(out, dout.get(), 32 * size_t(n), cudaMemcpyDeviceToHost));
+    copy_sync(out, dout.get(), 32 * size_t(n));
   });
 }
 

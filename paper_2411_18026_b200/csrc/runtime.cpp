@@ -121,8 +121,8 @@ void Profiler::collect() {
   pending_.clear();
   if (near_points) {
     unsigned long long h = 0;
-    CK(cudaMemcpy(&h, near_points, 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemset(near_points, 0, 8));
+    copy_sync(&h, near_points, 8);
+    CK(cudaMemsetAsync(near_points, 0, 8, scratch_stream()));
     units[KP_NEAR_SEP] += double(h);
   }
 }
@@ -267,9 +267,23 @@ Scratch& scratch() {
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       throw Error(EBEM_CUDA_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
     CK(cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = ~uint64_t(0);
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     return x;
   }();
   return *s;
+}
+
+cudaStream_t scratch_stream() { return scratch().st; }
+
+void copy_sync(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, scratch().st));
+  CK(cudaStreamSynchronize(scratch().st));
 }
 
 Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
@@ -1547,6 +1561,7 @@ void Fds::build() {
     const double tb = now();
     if (hs_) host_bases(level, br, S.v, ubuf);
     else P_.bases(req, cfg_.epsilon, br, S.v, ubuf);
+    PhaseTimer t_after("level_after_bases", nullptr);
     basis_seconds += now() - tb;
     // ---- diagonal blocks (leaf: exact; above: reduced) into the LU arena
     size_t lu_total = 0, piv_total = 0, au_total = 0, at_total = 0;
@@ -1593,7 +1608,7 @@ void Fds::build() {
           h.assign(2 * size_t(d) * d, 0.0);
           host_reduced_diagonal(f + i, h.data(), d);
         }
-        if (d) CK(cudaMemcpy(C.lu, h.data(), 16 * size_t(d) * d, cudaMemcpyHostToDevice));
+        if (d) copy_sync(C.lu, h.data(), 16 * size_t(d) * d);
       }
       for (int i = 0; !hs_ && i < nlev; ++i) {
         Cell& C = cells_[f + i];
@@ -1734,7 +1749,7 @@ void Fds::build() {
                       blk.data() + 2 * size_t(c) * ri, 16 * size_t(ri));
       }
     }
-    CK(cudaMemcpy(top_lu_.get(), h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    copy_sync(top_lu_.get(), h.data(), h.size() * 8);
   }
   {
     FillPlan plan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
@@ -1776,7 +1791,7 @@ void Fds::build() {
   // zero pivots, checked once (in factorization order) instead of a sync per LU
   std::vector<int> info(info_n_.size());
   if (!info.empty())
-    CK(cudaMemcpy(info.data(), info_.get(), 4 * info.size(), cudaMemcpyDeviceToHost));
+    copy_sync(info.data(), info_.get(), 4 * info.size());
   for (size_t i = 0; i < info.size(); ++i)
     if (info[i]) singular_error(info[i], info_n_[i]);
   cudaEventDestroy(ev0);
@@ -1796,7 +1811,7 @@ void Fds::debug_cell(int cell, int which, double* out) const {
     case 4: src = C.atilde; bytes = 16 * kk * kk; break;
     default: throw Error(EBEM_INVALID_ARGUMENT, "debug_cell: bad selector");
   }
-  if (src && bytes) CK(cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost));
+  if (src && bytes) copy_sync(out, src, bytes);
 }
 
 std::vector<double> Fds::host_block(const Lists& rows, const Lists& cols) {
@@ -1818,8 +1833,8 @@ void Fds::host_reduced_diagonal(int cell, double* out, int ld) {
   const Cell& c2 = cells_[2 * cell + 2];
   const int k1 = c1.k, k2 = c2.k, np = k1 + k2;
   std::vector<double> a1(2 * size_t(4) * k1 * k1), a2(2 * size_t(4) * k2 * k2);
-  if (k1) CK(cudaMemcpy(a1.data(), c1.atilde, a1.size() * 8, cudaMemcpyDeviceToHost));
-  if (k2) CK(cudaMemcpy(a2.data(), c2.atilde, a2.size() * 8, cudaMemcpyDeviceToHost));
+  if (k1) copy_sync(a1.data(), c1.atilde, a1.size() * 8);
+  if (k2) copy_sync(a2.data(), c2.atilde, a2.size() * 8);
   const std::vector<double> x12 = host_block(c1.srow, c2.scol);
   const std::vector<double> x21 = host_block(c2.srow, c1.scol);
   auto put = [&](int r, int c, const double* src, int sld, int sr, int sc) {
@@ -1880,8 +1895,8 @@ void Fds::host_bases(int level, std::vector<BasisRes>& br, DBuf<double>& vbuf,
   }
   vbuf.ensure(hv.size() + 2);
   ubuf.ensure(hu.size() + 2);
-  if (!hv.empty()) CK(cudaMemcpy(vbuf.get(), hv.data(), hv.size() * 8, cudaMemcpyHostToDevice));
-  if (!hu.empty()) CK(cudaMemcpy(ubuf.get(), hu.data(), hu.size() * 8, cudaMemcpyHostToDevice));
+  if (!hv.empty()) copy_sync(vbuf.get(), hv.data(), hv.size() * 8);
+  if (!hu.empty()) copy_sync(ubuf.get(), hu.data(), hu.size() * 8);
 }
 
 int Fds::rank_of(int cell) const {

@@ -64,6 +64,8 @@ class Profiler {
 };
 extern Profiler g_prof;
 
+
+
 // Host-side phase timers (EBEM_VERBOSE=1 prints them after a factorization;
 // EBEM_VERBOSE=2 also synchronises the stream at each scope end so device
 // work is attributed to the phase that issued it).
@@ -81,6 +83,11 @@ class PhaseTimer {
   double t0_;
 };
 
+// The process-wide stream every handle uses (created with the scratch pool).
+cudaStream_t scratch_stream();
+// cudaMemcpyAsync on that stream + synchronise.
+void copy_sync(void* dst, const void* src, size_t bytes);
+
 // ----------------------------------------------------------------- buffers
 template <class T>
 class DBuf {
@@ -94,10 +101,14 @@ class DBuf {
     return *this;
   }
   ~DBuf() { release(); }
+  // Stream-ordered allocation from the device's default memory pool (kept
+  // cached: release threshold = max), on the process-wide stream: no
+  // implicit device synchronisation, no re-mapping of freed pages.
   void alloc(size_t n) {
+    PhaseTimer t("cuda_malloc_free", nullptr);
     release();
     if (n == 0) return;
-    CK(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), scratch_stream()));
     n_ = n;
   }
   // grow-only
@@ -106,7 +117,7 @@ class DBuf {
     alloc(n + n / 4);
   }
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_) cudaFreeAsync(p_, scratch_stream());
     p_ = nullptr;
     n_ = 0;
   }
