@@ -83,6 +83,11 @@ void launch_qr_reduce(const QrTask* tasks, int n, size_t smem, double2* gws,
                       cudaStream_t st);
 void launch_cpqr(const CpqrTask* tasks, int n, size_t smem, double2* gws,
                  cudaStream_t st);
+// Team-layout Householder kernels (ebem_qr.cu), same task descriptors.
+void launch_qr_team(const QrTask* tasks, int n, size_t smem, double2* gws,
+                    cudaStream_t st);
+void launch_cpqr_team(const CpqrTask* tasks, int n, size_t smem, double2* gws,
+                      cudaStream_t st);
 void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st);
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st);

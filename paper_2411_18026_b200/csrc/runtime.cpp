@@ -1106,8 +1106,8 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
       fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
     }
     g_prof.begin(st_);
-    launch_qr_reduce(Pack::at<QrTask>(tb, o), int(tasks.size()), smem,
-                     gws.get(), st_);
+    // (the team-layout k_qr_team measured slower on these shapes: 485 vs 404 ms)
+    launch_qr_reduce(Pack::at<QrTask>(tb, o), int(tasks.size()), smem, gws.get(), st_);
     g_prof.end(KP_QR, st_, fl);
     CK(cudaGetLastError());
     staging.fence(st_);
@@ -1170,7 +1170,7 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
       fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
     }
     g_prof.begin(st_);
-    launch_cpqr(Pack::at<CpqrTask>(tb, o), int(nq), smem, gws.get(), st_);
+    launch_cpqr_team(Pack::at<CpqrTask>(tb, o), int(nq), smem, gws.get(), st_);
     g_prof.end(KP_CPQR, st_, fl);
     CK(cudaGetLastError());
     staging.fence(st_);
