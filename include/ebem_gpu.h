@@ -121,6 +121,14 @@ int ebem_gpu_cell_basis(ebem_gpu_problem* p, const int* rows0, int nr0,
                         double epsilon, int* k, int* saturated, int* skel,
                         double* u0, double* u1, double* v0, double* v1);
 
+/* cell_basis for a batch of contiguous cells [begin_i, end_i) with
+ * rows = cols = the cell's nodes, in one batched device pass (the level
+ * path of the factorization; BASELINE config 5 microbenchmark).  Writes the
+ * shared ranks; device_seconds (may be NULL) gets the CUDA-event time. */
+int ebem_gpu_cell_bases(ebem_gpu_problem* p, int count, const int* begins,
+                        const int* ends, double epsilon, int* k_out,
+                        double* device_seconds);
+
 /* The two interaction matrices cell_basis compresses
  * (proj/src/compression.cpp:139-166): mv (n_out x (nc0+nc1)) and
  * mu ((nr0+nr1) x n_out), n_out = 2 m' + 2 |enclosed|.  NULL buffers query

@@ -520,6 +520,17 @@ class AssemblerSource(BlockSource):
             v=(_from_cbuf(bufs[2][: 2 * kk * c0.size], kk, c0.size),
                _from_cbuf(bufs[3][: 2 * kk * c1.size], kk, c1.size)))
 
+    def cell_bases(self, begins, ends, epsilon):
+        """Batched cell_basis over contiguous cells (one device pass);
+        returns (ranks, device seconds)."""
+        b = _ints(begins)
+        e = _ints(ends)
+        k = np.zeros(b.size, dtype=np.int32)
+        t = ctypes.c_double()
+        _check(lib().ebem_gpu_cell_bases(self._h.h, b.size, _p(b), _p(e),
+                                         ctypes.c_double(epsilon), _p(k), ctypes.byref(t)))
+        return k, float(t.value)
+
     def interaction_matrices(self, rows, cols, node_begin, node_end):
         """(M_V, M_U) of cell_basis (compression.cpp:139-166), for tests."""
         L = lib()

@@ -273,6 +273,40 @@ int ebem_gpu_cell_basis(ebem_gpu_problem* p, const int* rows0, int nr0,
   });
 }
 
+int ebem_gpu_cell_bases(ebem_gpu_problem* p, int count, const int* begins,
+                        const int* ends, double epsilon, int* k_out,
+                        double* device_seconds) {
+  return guarded([&] {
+    Problem& P = *p->p;
+    if (count < 0) throw Error(EBEM_INVALID_ARGUMENT, "negative cell count");
+    std::vector<Lists> lists_(count);
+    std::vector<BasisReq> req(count);
+    for (int c = 0; c < count; ++c) {
+      if (begins[c] < 0 || ends[c] > P.n() || begins[c] >= ends[c])
+        throw Error(EBEM_INVALID_ARGUMENT, "build_proxy: bad node range");
+      std::vector<int> r(ends[c] - begins[c]);
+      for (int i = 0; i < int(r.size()); ++i) r[i] = begins[c] + i;
+      lists_[c] = Lists{r, r};
+      req[c] = BasisReq{&lists_[c], &lists_[c], begins[c], ends[c]};
+    }
+    std::vector<BasisRes> res;
+    DBuf<double> vb, ub;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, P.stream()));
+    P.bases(req, epsilon, res, vb, ub);
+    CK(cudaEventRecord(e1, P.stream()));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (device_seconds) *device_seconds = 1e-3 * ms;
+    for (int c = 0; c < count; ++c) k_out[c] = res[c].k;
+  });
+}
+
 int ebem_gpu_rhs_plane(ebem_gpu_problem* p, int kind, const double* angles,
                        int m, double amplitude, double* out) {
   return guarded([&] {
