@@ -500,11 +500,11 @@ k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
         axpy(rv[1][e], pt[1], k);
       }
       // U: test on the cell element, trial on the enclosed element
+      // N_U = N_V^T (combine_N is symmetric under z -> -z, m <-> n, i <-> j)
       combine_D(dn, -zhx, -zhy, nax, nay, dm);
-      combine_N(dn, -zhx, -zhy, nbx, nby, nax, nay, nm);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const cplx k = dm.a[e] + alpha * nm.a[e];
+        const cplx k = dm.a[e] + alpha * nm.a[(e >> 1) | ((e & 1) << 1)];
         axpy(ru[0][e], pt[0], k);
         axpy(ru[1][e], pt[1], k);
       }
@@ -660,11 +660,11 @@ k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst 
         axpy(rv[1][e], pt[1], k);
       }
       // U: test on the curve, trial on the polygon, zh reversed
+      // N_U = N_V^T (combine_N is symmetric under z -> -z, m <-> n, i <-> j)
       combine_D(fs, -zhx, -zhy, pnx, pny, dm);
-      combine_N(fs, -zhx, -zhy, mnx, mny, pnx, pny, nm);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const cplx k = dm.a[e] + alpha * nm.a[e];
+        const cplx k = dm.a[e] + alpha * nm.a[(e >> 1) | ((e & 1) << 1)];
         axpy(ru[0][e], pt[0], k);
         axpy(ru[1][e], pt[1], k);
       }
