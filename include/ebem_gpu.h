@@ -198,6 +198,12 @@ int ebem_gpu_fds_cell(const ebem_gpu_fds* f, int cell, int* sizes, int* skel);
 int ebem_gpu_eval_hankel(const double* x, int n, double* out);
 int ebem_gpu_eval_scalars(ebem_gpu_problem* p, const double* r, int n,
                           int which, double* out);
+/* Parity hook of the ID's TSQR stage (the reduction before Cpqr,
+ * proj/src/lapack.cpp:101-119): reduces the rows x n complex block a
+ * (column-major, ld) to *r_rows x n rows with the same Gram matrix
+ * (an upper-triangular n x n R when n <= 128); r holds rows x n. */
+int ebem_gpu_tall_reduce(const double* a, int rows, int n, int ld, double* r,
+                         int* r_rows);
 
 /* Number of kernel launches issued by the library since load (bench). */
 long long ebem_gpu_launch_count(void);

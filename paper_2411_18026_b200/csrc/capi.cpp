@@ -423,6 +423,30 @@ int ebem_gpu_eval_hankel(const double* x, int n, double* out) {
   });
 }
 
+int ebem_gpu_tall_reduce(const double* a, int rows, int n, int ld, double* r,
+                         int* r_rows) {
+  return guarded([&] {
+    if (rows <= 0 || n <= 0 || ld < rows || !a || !r || !r_rows)
+      throw Error(EBEM_INVALID_ARGUMENT, "tall_reduce: bad arguments");
+    scratch();
+    cudaStream_t st = scratch_stream();
+    DBuf<double> da;
+    da.alloc(2 * size_t(ld) * n);
+    copy_sync(da.get(), a, 16 * size_t(ld) * n);
+    std::vector<TallBlock> q{TallBlock{da.get(), rows, n, ld}};
+    reduce_tall(q, st, true);
+    ++g_launches;  // test hook
+    CK(cudaGetLastError());
+    const TallBlock& x = q[0];
+    std::vector<double> tmp(2 * size_t(x.ld) * n);
+    copy_sync(tmp.data(), x.p, 16 * size_t(x.ld) * n);
+    for (int j = 0; j < n; ++j)
+      std::memcpy(r + 2 * size_t(j) * x.rows, tmp.data() + 2 * size_t(j) * x.ld,
+                  16 * size_t(x.rows));
+    *r_rows = x.rows;
+  });
+}
+
 int ebem_gpu_eval_scalars(ebem_gpu_problem* p, const double* r, int n,
                           int which, double* out) {
   return guarded([&] {

@@ -1012,6 +1012,126 @@ void Problem::interaction(const std::vector<BasisReq>& req,
   execute(plan);
 }
 
+// TSQR rounds until each block is an n x n R or fits one CTA's shared memory
+// (then the column-pivoted pass takes it directly); updates q in place to
+// point at the reduced blocks (scratch().qr_rounds).
+void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
+  Scratch& S = scratch();
+  std::vector<DBuf<double>>& qr_rounds_ = S.qr_rounds;
+  DBuf<double2>& gws = S.gws;
+  Staging& staging = S.staging;
+  // ---- TSQR rounds until each input is an n x n R or fits one CTA's shared
+  // memory.  Inputs with n <= kTsqrMaxCols stream through k_tsqr (row pieces
+  // sized so a round fills the GPU, the pieces' R factors stacked for the next
+  // round); wider ones use the chunked k_qr_reduce tree.
+  static const int n_sm = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  size_t round = 0;
+  for (;;) {
+    std::vector<QrTask> tasks, stream16, stream8;
+    std::vector<size_t> out_off(q.size(), 0);
+    size_t out_total = 0, ws_total = 0;
+    std::vector<int> pieces(q.size(), 0);
+    std::vector<char> streamed(q.size(), 0);
+    double work = 0.0;  // streamed rows x steps x (n + 64) / block rows
+    for (size_t i = 0; i < q.size(); ++i) {
+      const TallBlock& x = q[i];
+      const size_t bytes = size_t(x.rows) * x.n * 16;
+      if ((bytes <= size_t(kSmemCap) && !force) || x.rows <= x.n) continue;
+      if (tsqr_lanes(x.n) != 0) {
+        streamed[i] = 1;
+        work += double(x.rows) * x.n * (x.n + 64) / tsqr_block_rows(x.n);
+      } else if (x.rows > 2 * x.n) {
+        const int chunk = std::max(2 * x.n, int(kSmemCap / (16 * size_t(x.n))));
+        pieces[i] = (x.rows + chunk - 1) / chunk;
+      }
+    }
+    const double per_cta = work / (4.0 * n_sm);
+    for (size_t i = 0; i < q.size(); ++i) {
+      if (!streamed[i]) continue;
+      const TallBlock& x = q[i];
+      const double w = double(x.rows) * x.n * (x.n + 64) / tsqr_block_rows(x.n);
+      const int cap = std::max(1, x.rows / (4 * x.n));
+      pieces[i] = std::min(cap, std::max(1, int(std::ceil(w / per_cta))));
+    }
+    for (size_t i = 0; i < q.size(); ++i) {
+      if (!pieces[i]) continue;
+      out_off[i] = out_total;
+      out_total += size_t(pieces[i]) * q[i].n * q[i].n;
+    }
+    if (out_total == 0) break;
+    if (qr_rounds_.size() <= round) qr_rounds_.emplace_back();
+    qr_rounds_[round].ensure(2 * out_total);
+    double* ob = qr_rounds_[round].get();
+    ++round;
+    size_t smem16 = 0, smem8 = 0;
+    for (size_t i = 0; i < q.size(); ++i) {
+      if (!pieces[i]) continue;
+      const TallBlock& x = q[i];
+      const int chunk = (x.rows + pieces[i] - 1) / pieces[i];
+      const int ld_out = pieces[i] * x.n;
+      for (int pc = 0; pc < pieces[i]; ++pc) {
+        const int r0 = pc * chunk;
+        const int rr = std::min(chunk, x.rows - r0);
+        QrTask t{};
+        t.src = x.p + 2 * size_t(r0);
+        t.dst = ob + 2 * (out_off[i] + size_t(pc) * x.n);
+        t.rows = rr;
+        t.n = x.n;
+        t.ld = x.ld;
+        t.dst_ld = ld_out;
+        if (streamed[i]) {
+          if (tsqr_lanes(x.n) == 16) {
+            stream16.push_back(t);
+            smem16 = std::max(smem16, tsqr_smem_bytes(x.n));
+          } else {
+            stream8.push_back(t);
+            smem8 = std::max(smem8, tsqr_smem_bytes(x.n));
+          }
+          continue;
+        }
+        t.in_smem = size_t(rr) * x.n * 16 <= size_t(kSmemCap);
+        t.ws_off = (long long)ws_total;
+        if (!t.in_smem) ws_total += size_t(rr) * x.n;
+        tasks.push_back(t);
+      }
+    }
+    gws.ensure(ws_total + 1);
+    Pack pk;
+    const size_t o = pk.add(tasks);
+    const size_t o16 = pk.add(stream16);
+    const size_t o8 = pk.add(stream8);
+    char* tb = staging.put(pk, st);
+    size_t smem = 0;
+    for (const QrTask& t : tasks)
+      if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
+    double fl = 0.0;  // complex Householder QR: 8 m n^2 - 8 n^3 / 3
+    for (const auto* v : {&tasks, &stream16, &stream8})
+      for (const QrTask& t : *v) {
+        const double mm = t.rows, nn = std::min(t.rows, t.n);
+        fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
+      }
+    g_prof.begin(st);
+    // (the team-layout k_qr_team measured slower on these shapes: 485 vs 404 ms)
+    launch_qr_reduce(Pack::at<QrTask>(tb, o), int(tasks.size()), smem, gws.get(), st);
+    launch_tsqr(Pack::at<QrTask>(tb, o16), int(stream16.size()), 16, smem16, st);
+    launch_tsqr(Pack::at<QrTask>(tb, o8), int(stream8.size()), 8, smem8, st);
+    g_prof.end(KP_QR, st, fl);
+    CK(cudaGetLastError());
+    staging.fence(st);
+    for (size_t i = 0; i < q.size(); ++i) {
+      if (!pieces[i]) continue;
+      q[i].p = ob + 2 * out_off[i];
+      q[i].rows = pieces[i] * q[i].n;
+      q[i].ld = q[i].rows;
+    }
+  }
+}
+
 void Problem::bases(const std::vector<BasisReq>& req, double eps,
                     std::vector<BasisRes>& res, DBuf<double>& vbuf,
                     DBuf<double>& ubuf, double* fill_seconds) {
@@ -1030,11 +1150,7 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
   }
 
   // ---- the four ID inputs per cell: column halves of T_V and T_U
-  struct QIn {
-    const double* p;
-    int rows, n, ld;
-  };
-  std::vector<QIn> q(4 * ncell);
+  std::vector<TallBlock> q(4 * ncell);
   for (size_t c = 0; c < ncell; ++c) {
     const Lists& rows = *req[c].rows;
     const Lists& cols = *req[c].cols;
@@ -1051,73 +1167,7 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     q[4 * c + 3] = {tu + 2 * size_t(no) * nr0, no, nr1, no};
   }
   PhaseTimer* t_qr = new PhaseTimer("id_tsqr", st_);
-  // ---- TSQR rounds until each input fits one CTA's shared memory
-  size_t round = 0;
-  for (;;) {
-    std::vector<QrTask> tasks;
-    std::vector<size_t> out_off(q.size(), 0);
-    size_t out_total = 0, ws_total = 0;
-    std::vector<int> pieces(q.size(), 0);
-    for (size_t i = 0; i < q.size(); ++i) {
-      const QIn& x = q[i];
-      const size_t bytes = size_t(x.rows) * x.n * 16;
-      if (bytes <= size_t(kSmemCap) || x.rows <= 2 * x.n) continue;
-      const int chunk = std::max(2 * x.n, int(kSmemCap / (16 * size_t(x.n))));
-      pieces[i] = (x.rows + chunk - 1) / chunk;
-      out_off[i] = out_total;
-      out_total += size_t(pieces[i]) * x.n * x.n;
-    }
-    if (out_total == 0) break;
-    if (qr_rounds_.size() <= round) qr_rounds_.emplace_back();
-    qr_rounds_[round].ensure(2 * out_total);
-    double* ob = qr_rounds_[round].get();
-    ++round;
-    for (size_t i = 0; i < q.size(); ++i) {
-      if (!pieces[i]) continue;
-      const QIn& x = q[i];
-      const int chunk = (x.rows + pieces[i] - 1) / pieces[i];
-      const int ld_out = pieces[i] * x.n;
-      for (int pc = 0; pc < pieces[i]; ++pc) {
-        const int r0 = pc * chunk;
-        const int rr = std::min(chunk, x.rows - r0);
-        QrTask t{};
-        t.src = x.p + 2 * size_t(r0);
-        t.dst = ob + 2 * (out_off[i] + size_t(pc) * x.n);
-        t.rows = rr;
-        t.n = x.n;
-        t.ld = x.ld;
-        t.dst_ld = ld_out;
-        t.in_smem = size_t(rr) * x.n * 16 <= size_t(kSmemCap);
-        t.ws_off = (long long)ws_total;
-        if (!t.in_smem) ws_total += size_t(rr) * x.n;
-        tasks.push_back(t);
-      }
-    }
-    gws.ensure(ws_total + 1);
-    Pack pk;
-    const size_t o = pk.add(tasks);
-    char* tb = staging.put(pk, st_);
-    size_t smem = 0;
-    for (const QrTask& t : tasks)
-      if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
-    double fl = 0.0;  // complex Householder QR: 8 m n^2 - 8 n^3 / 3
-    for (const QrTask& t : tasks) {
-      const double mm = t.rows, nn = std::min(t.rows, t.n);
-      fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
-    }
-    g_prof.begin(st_);
-    // (the team-layout k_qr_team measured slower on these shapes: 485 vs 404 ms)
-    launch_qr_reduce(Pack::at<QrTask>(tb, o), int(tasks.size()), smem, gws.get(), st_);
-    g_prof.end(KP_QR, st_, fl);
-    CK(cudaGetLastError());
-    staging.fence(st_);
-    for (size_t i = 0; i < q.size(); ++i) {
-      if (!pieces[i]) continue;
-      q[i].p = ob + 2 * out_off[i];
-      q[i].rows = pieces[i] * q[i].n;
-      q[i].ld = q[i].rows;
-    }
-  }
+  reduce_tall(q, st_);
   delete t_qr;
   PhaseTimer t_cpqr("id_cpqr+interp", st_);
   // ---- pivoted QR of every input

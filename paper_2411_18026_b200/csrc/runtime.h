@@ -280,6 +280,14 @@ struct Scratch {
 };
 Scratch& scratch();
 
+// A tall complex block (column-major, ld) whose R factor the ID needs.
+struct TallBlock {
+  const double* p;
+  int rows, n, ld;
+};
+// force: also reduce blocks that fit shared memory (parity hook).
+void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force = false);
+
 class Problem {
  public:
   Problem(const double* xy, int n, double lam, double mu, double rho,
