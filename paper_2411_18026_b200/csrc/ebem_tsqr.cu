@@ -12,14 +12,20 @@
 //   columns j > i:  s = R_ij + v^H B(:, j),  f = conj(tau) s,
 //                   R_ij -= f,  B(:, j) -= v f
 // (zlarfg / zlarf semantics, the sign convention of k_qr_reduce).
+//
 // Layout: LANES consecutive lanes own one column, lane g holds rows
-// g, g + LANES, ... of the block; the group owning column i + 1 updates it
-// first and immediately generates reflector i + 1 (look-ahead), so every step
-// costs one barrier.  The R factors of several row pieces of one matrix are
-// stacked and reduced again by the same kernel.
+// g, g + LANES, ... of the block.  The step sequence is a chain: reflector
+// t + 1 needs column t + 1 updated by reflector t.  The group owning column
+// t + 1 applies reflector t to its columns first and immediately generates
+// reflector t + 1 (look-ahead).  Reflectors travel through a ring of kSlots
+// shared-memory slots guarded by mbarriers (full: the producing group's lanes
+// arrive; empty: every warp arrives once it has read the slot), so warps are
+// coupled only through the reflectors they consume: the step time is the
+// producer chain, not a CTA-wide barrier plus the slowest warp.  The R
+// factors of several row pieces of one matrix are stacked and reduced again
+// by the same kernel.
 #include <cuda_runtime.h>
-
-#include <cstdio>
+#include <stdint.h>
 
 #include "ebem_dense.h"
 
@@ -28,9 +34,34 @@ namespace ebem_gpu {
 namespace {
 
 constexpr int kTsqrThreads = 1024;
-constexpr int kRpt = 8;  // block rows per lane
+constexpr int kWarpsPerCta = kTsqrThreads / 32;
+constexpr int kRpt = 8;    // block rows per lane
+constexpr int kSlots = 8;  // reflector ring depth
 
 __device__ __forceinline__ int pidx(int i, int j) { return ((j * (j + 1)) >> 1) + i; }
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 template <int LANES>
 __device__ __forceinline__ double group_sum(double v) {
@@ -39,69 +70,84 @@ __device__ __forceinline__ double group_sum(double v) {
   return v;
 }
 
+// Reflector of column i from the owning group's registers (warp-uniform call;
+// only the `mine` lanes write).  Waits for the slot to be free first.
 template <int LANES>
 __device__ __forceinline__ void make_reflector(double2 (&B)[kRpt], bool mine, int i,
-                                               int g, double2* R, double2* vout,
-                                               double2* tau_out) {
-  double p = 0.0;
+                                               int g, double2* R, long long t,
+                                               double2* vring, double2* tring,
+                                               uint64_t* full, uint64_t* empty) {
+  constexpr int kRows = LANES * kRpt;
+  double p[4] = {0.0, 0.0, 0.0, 0.0};
+  double2 alpha = make_double2(0.0, 0.0);
   if (mine) {
+    alpha = R[pidx(i, i)];
 #pragma unroll
-    for (int k = 0; k < kRpt; ++k) p = fma(B[k].x, B[k].x, fma(B[k].y, B[k].y, p));
+    for (int k = 0; k < kRpt; ++k)
+      p[k & 3] = fma(B[k].x, B[k].x, fma(B[k].y, B[k].y, p[k & 3]));
   }
-  const double xnorm2 = group_sum<LANES>(p);
+  const double xnorm2 = group_sum<LANES>((p[0] + p[1]) + (p[2] + p[3]));
   if (!mine) return;
-  const double2 alpha = R[pidx(i, i)];
-#ifdef EBEM_TSQR_DEBUG
-  if (g == 0 && !(isfinite(xnorm2) && isfinite(alpha.x) && isfinite(alpha.y)))
-    printf("tsqr blk %d col %d: xnorm2 %g alpha %g %g\n", blockIdx.x, i, xnorm2, alpha.x, alpha.y);
-#endif
   double2 tau = make_double2(0.0, 0.0);
   if (!(xnorm2 == 0.0 && alpha.y == 0.0)) {
-    const double nrm = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2);
-    const double beta = alpha.x >= 0.0 ? -nrm : nrm;
-    tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
-    // scal = 1 / (alpha - beta), Smith's division: the residues of columns
-    // that are already eliminated shrink geometrically, and |alpha - beta|^2
-    // would underflow long before |alpha - beta| does
-    const double ar = alpha.x - beta, ai = alpha.y;
-    double2 scal;
-    if (fabs(ar) >= fabs(ai)) {
-      const double q = ai / ar, d = ar + ai * q;
-      scal = make_double2(1.0 / d, -q / d);
-    } else {
-      const double q = ar / ai, d = ai + ar * q;
-      scal = make_double2(q / d, -1.0 / d);
-    }
+    // x2 = |alpha|^2 + ||x||^2;  s = 1 / sqrt(x2);  beta = -+ x2 s.
+    // With ar = Re(alpha) - beta (|ar| >= 1/s >= |ai|) scaled to O(1):
+    // 1 / (alpha - beta) = s (ar s - i ai s) / ((ar s)^2 + (ai s)^2).
+    // Two special functions on the chain, no true division with a zero
+    // numerator (that sends it down its slow path), no underflow in the
+    // squares of the geometrically shrinking residues of eliminated columns.
+    const double x2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, xnorm2));
+    const double s = rsqrt(x2);
+    const double nrm = x2 * s;
+    const bool pos = alpha.x >= 0.0;
+    const double beta = pos ? -nrm : nrm;
+    const double ib = pos ? -s : s;
+    tau = make_double2((beta - alpha.x) * ib, -alpha.y * ib);
+    const double arn = fma(alpha.x, s, pos ? 1.0 : -1.0);  // (alpha.x - beta) s
+    const double ain = alpha.y * s;
+    const double id = s / fma(arn, arn, ain * ain);
+    const double2 scal = make_double2(arn * id, -ain * id);
 #pragma unroll
     for (int k = 0; k < kRpt; ++k)
       B[k] = make_double2(scal.x * B[k].x - scal.y * B[k].y,
                           scal.x * B[k].y + scal.y * B[k].x);
     if (g == 0) R[pidx(i, i)] = make_double2(beta, 0.0);
   }
+  const int slot = int(t % kSlots);
+  if (t >= kSlots) mbar_wait(empty + slot, uint32_t(((t / kSlots) + 1) & 1));
+  double2* v = vring + slot * kRows;
 #pragma unroll
-  for (int k = 0; k < kRpt; ++k) vout[g + LANES * k] = B[k];
-  if (g == 0) *tau_out = tau;
+  for (int k = 0; k < kRpt; ++k) v[g + LANES * k] = B[k];
+  if (g == 0) tring[slot] = tau;
+  mbar_arrive(full + slot);
 }
 
 template <int LANES>
 __global__ void __launch_bounds__(kTsqrThreads, 1)
 k_tsqr(const QrTask* __restrict__ tasks) {
   constexpr int kRows = LANES * kRpt;
-  extern __shared__ double2 R[];  // packed upper triangle, then v[2][kRows], tau[2]
+  constexpr int kGroupsPerWarp = 32 / LANES;
+  extern __shared__ double2 R[];  // packed upper triangle | v ring | tau ring
+  __shared__ uint64_t full[kSlots], empty[kSlots];
   const QrTask T = tasks[blockIdx.x];
   const int n = T.n, rows = T.rows, ld = T.ld;
-  double2* vbuf = R + ((n * (n + 1)) >> 1);
-  double2* tbuf = vbuf + 2 * kRows;
+  double2* vring = R + ((n * (n + 1)) >> 1);
+  double2* tring = vring + kSlots * kRows;
   const int g = threadIdx.x % LANES;
   const int j = threadIdx.x / LANES;  // owned column
-  constexpr int kGroupsPerWarp = 32 / LANES;
+  const int lane = threadIdx.x & 31;
   const int wfirst = (threadIdx.x >> 5) * kGroupsPerWarp;  // first column of the warp
   const int wlast = wfirst + kGroupsPerWarp - 1;
-  for (int t = threadIdx.x; t < ((n * (n + 1)) >> 1); t += blockDim.x)
-    R[t] = make_double2(0.0, 0.0);
+  for (int q = threadIdx.x; q < ((n * (n + 1)) >> 1); q += blockDim.x)
+    R[q] = make_double2(0.0, 0.0);
+  if (threadIdx.x < kSlots) {
+    mbar_init(full + threadIdx.x, LANES);
+    mbar_init(empty + threadIdx.x, kWarpsPerCta);
+  }
   const double2* src = reinterpret_cast<const double2*>(T.src) + (size_t)j * ld;
   const bool own = j < n;
   __syncthreads();
+  long long t = 0;  // global reflector index (block-major)
   for (int r0 = 0; r0 < rows; r0 += kRows) {
     double2 B[kRpt];
 #pragma unroll
@@ -113,30 +159,29 @@ k_tsqr(const QrTask* __restrict__ tasks) {
       const int r = r0 + kRows + g * kRpt;
       if (r < rows) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + r));
     }
-    if (wfirst == 0) make_reflector<LANES>(B, j == 0, 0, g, R, vbuf, tbuf);
-    __syncthreads();
-    for (int i = 0; i < n; ++i) {
-      const int cur = i & 1;
+    if (wfirst == 0)
+      make_reflector<LANES>(B, j == 0, 0, g, R, t, vring, tring, full, empty);
+    for (int i = 0; i < n; ++i, ++t) {
+      const int slot = int(t % kSlots);
+      mbar_wait(full + slot, uint32_t((t / kSlots) & 1));
       if (wlast > i && wfirst < n) {  // warp-uniform: some column j > i here
         const bool act = own && j > i;
-        const double2* v = vbuf + cur * kRows;
-        double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
+        const double2* v = vring + slot * kRows;
+        double2 rij = make_double2(0.0, 0.0);
+        if (act) rij = R[pidx(i, j)];
+        double ar[4] = {0.0, 0.0, 0.0, 0.0}, ai[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int k = 0; k < kRpt; k += 2) {
+        for (int k = 0; k < kRpt; ++k) {
           const double2 a = v[g + LANES * k], b = B[k];
-          sr0 = fma(a.x, b.x, fma(a.y, b.y, sr0));
-          si0 = fma(a.x, b.y, fma(-a.y, b.x, si0));
-          const double2 c = v[g + LANES * (k + 1)], d = B[k + 1];
-          sr1 = fma(c.x, d.x, fma(c.y, d.y, sr1));
-          si1 = fma(c.x, d.y, fma(-c.y, d.x, si1));
+          ar[k & 3] = fma(a.x, b.x, fma(a.y, b.y, ar[k & 3]));
+          ai[k & 3] = fma(a.x, b.y, fma(-a.y, b.x, ai[k & 3]));
         }
-        double sr = group_sum<LANES>(sr0 + sr1);
-        double si = group_sum<LANES>(si0 + si1);
+        double sr = group_sum<LANES>((ar[0] + ar[1]) + (ar[2] + ar[3]));
+        double si = group_sum<LANES>((ai[0] + ai[1]) + (ai[2] + ai[3]));
+        const double2 tau = tring[slot];
         if (act) {
-          const double2 rij = R[pidx(i, j)];
           sr += rij.x;
           si += rij.y;
-          const double2 tau = tbuf[cur];
           // f = conj(tau) s
           const double fr = tau.x * sr + tau.y * si;
           const double fi = tau.x * si - tau.y * sr;
@@ -147,19 +192,19 @@ k_tsqr(const QrTask* __restrict__ tasks) {
             B[k].y = fma(-a.x, fi, fma(-a.y, fr, B[k].y));
           }
           if (g == 0) R[pidx(i, j)] = make_double2(rij.x - fr, rij.y - fi);
-#ifdef EBEM_TSQR_DEBUG
-          if (g == 0 && !(isfinite(fr) && isfinite(fi)) && isfinite(rij.x))
-            printf("tsqr r0 %d step %d col %d: s %g %g tau %g %g rij %g %g\n", r0, i, j, sr, si,
-                   tbuf[cur].x, tbuf[cur].y, rij.x, rij.y);
-#endif
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);  // slot read by this warp
         if (i + 1 < n && wfirst <= i + 1 && i + 1 <= wlast)
-          make_reflector<LANES>(B, j == i + 1, i + 1, g, R, vbuf + (cur ^ 1) * kRows,
-                                tbuf + (cur ^ 1));
+          make_reflector<LANES>(B, j == i + 1, i + 1, g, R, t + 1, vring, tring, full,
+                                empty);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);
       }
-      __syncthreads();
     }
   }
+  __syncthreads();
   double2* out = reinterpret_cast<double2*>(T.dst);
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
     const int c = idx / n, r = idx - c * n;
@@ -172,7 +217,8 @@ k_tsqr(const QrTask* __restrict__ tasks) {
 int tsqr_lanes(int n) { return n <= 64 ? 16 : n <= kTsqrMaxCols ? 8 : 0; }
 int tsqr_block_rows(int n) { return tsqr_lanes(n) * kRpt; }
 size_t tsqr_smem_bytes(int n) {
-  return sizeof(double2) * (size_t(n) * (n + 1) / 2 + 2 * size_t(tsqr_block_rows(n)) + 2);
+  return sizeof(double2) *
+         (size_t(n) * (n + 1) / 2 + kSlots * size_t(tsqr_block_rows(n)) + kSlots);
 }
 
 void launch_tsqr(const QrTask* tasks, int n_tasks, int lanes, size_t smem,
@@ -181,7 +227,7 @@ void launch_tsqr(const QrTask* tasks, int n_tasks, int lanes, size_t smem,
   if (lanes == 16) {
     static bool once = [] {
       cudaFuncSetAttribute(k_tsqr<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           227 * 1024);
+                           200 * 1024);
       return true;
     }();
     (void)once;
@@ -189,7 +235,7 @@ void launch_tsqr(const QrTask* tasks, int n_tasks, int lanes, size_t smem,
   } else {
     static bool once = [] {
       cudaFuncSetAttribute(k_tsqr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           227 * 1024);
+                           200 * 1024);
       return true;
     }();
     (void)once;

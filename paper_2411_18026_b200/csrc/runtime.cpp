@@ -1030,6 +1030,10 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v > 0 ? v : 148;
   }();
+  static const int forced_pieces = [] {  // experiments: EBEM_TSQR_PIECES
+    const char* e = std::getenv("EBEM_TSQR_PIECES");
+    return e ? std::atoi(e) : 0;
+  }();
   size_t round = 0;
   for (;;) {
     std::vector<QrTask> tasks, stream16, stream8;
@@ -1057,6 +1061,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
       const double w = double(x.rows) * x.n * (x.n + 64) / tsqr_block_rows(x.n);
       const int cap = std::max(1, x.rows / (4 * x.n));
       pieces[i] = std::min(cap, std::max(1, int(std::ceil(w / per_cta))));
+      if (forced_pieces > 0) pieces[i] = std::min(forced_pieces, std::max(1, x.rows / x.n));
     }
     for (size_t i = 0; i < q.size(); ++i) {
       if (!pieces[i]) continue;
