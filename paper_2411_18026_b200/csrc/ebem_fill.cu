@@ -90,7 +90,7 @@ __device__ __forceinline__ int bidx(int la, int lb, int i, int j) {
 // One thread per element pair.  Pairs that touch (coincident / adjacent) are
 // skipped here and produced by k_near_singular.
 #ifndef EBEM_NEAR_MINB
-#define EBEM_NEAR_MINB 3
+#define EBEM_NEAR_MINB 2
 #endif
 template <int NT>
 __global__ void __launch_bounds__(128, EBEM_NEAR_MINB)
@@ -427,8 +427,16 @@ k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
 // CTA = P pairs x n threads; thread (pair, i) fixes the test point s_i on the
 // enclosed element and sweeps the n points on the cell element, evaluating
 // the scalars once for both orientations (r is symmetric).
-__global__ void __launch_bounds__(256, 2)
-k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
+#ifndef EBEM_SYM_THREADS
+#define EBEM_SYM_THREADS 256
+#endif
+#ifndef EBEM_SYM_MINB
+#define EBEM_SYM_MINB 1
+#endif
+template <int NT>
+__global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
+k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
+           const SymJob* __restrict__ jobs,
            const long long* __restrict__ job_off, int n_jobs,
            const int* __restrict__ elems, const int* __restrict__ pair_ids,
            int count, int n, double* __restrict__ bundles) {
@@ -467,8 +475,8 @@ k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
     const double dbx = ef(ctx, EDX, eb), dby = ef(ctx, EDY, eb);
     const double nax = ef(ctx, ENX, ea), nay = ef(ctx, ENY, ea);
     const double nbx = ef(ctx, ENX, eb), nby = ef(ctx, ENY, eb);
-    const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
-    const double qfac = ctx->med.qfactor;
+    const cplx alpha = mk(fc.med.alpha_re, fc.med.alpha_im);
+    const double qfac = fc.med.qfactor;
     const double s = gx[i];
     const double xx = pax + s * dax, xy = pay + s * day;
     cplx rv[2][4], ru[2][4];
@@ -487,7 +495,7 @@ k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
       const double logr = log(r);
       const double zhx = ir * zx, zhy = ir * zy;
       DN dn;
-      dn_eval<true>(ctx->med, S, r, ir, logr, dn);
+      dn_eval2<true, NT>(fc, S, r, ir, logr, dn);
       const double pt[2] = {wj * (1.0 - t), wj * t};
       CMat2 dm, nm;
       // V: test on the enclosed element (normal na), trial on the cell element
@@ -529,7 +537,7 @@ k_near_sym(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
   __syncthreads();
   // reduction over i; each pair's first thread handles nothing special:
   // threads stride over (pair, orientation, 16 outputs)
-  const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
+  const cplx alpha = mk(fc.med.alpha_re, fc.med.alpha_im);
   for (int o = threadIdx.x; o < P * 2 * kBundle; o += blockDim.x) {
     const int lp2 = o / (2 * kBundle);
     const int rem = o - lp2 * 2 * kBundle;
@@ -792,22 +800,23 @@ void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
       ctx, jobs, job_off, n_jobs, elems, n_pairs, keys, vals);
 }
 
-void launch_near_sym(const DevCtx* ctx, const SymJob* jobs,
-                     const long long* job_off, int n_jobs, const int* elems,
-                     const int* pair_ids, int count, int n, double* bundles,
-                     cudaStream_t st) {
+void launch_near_sym(const DevCtx* ctx, const FillConst& fc, int nt,
+                     const SymJob* jobs, const long long* job_off, int n_jobs,
+                     const int* elems, const int* pair_ids, int count, int n,
+                     double* bundles, cudaStream_t st) {
   if (count <= 0) return;
-  const int P = 256 / n;
+  const int P = EBEM_SYM_THREADS / n;
   const int threads = P * n;
   const size_t smem = size_t(threads) * 18 * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_near_sym, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         256 * 18 * (int)sizeof(double2));
-    attr = true;
-  }
-  k_near_sym<<<(count + P - 1) / P, threads, smem, st>>>(
-      ctx, jobs, job_off, n_jobs, elems, pair_ids, count, n, bundles);
+#define EBEM_SYM_CALL(N)                                                          \
+  do {                                                                            \
+    cudaFuncSetAttribute(k_near_sym<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         EBEM_SYM_THREADS * 18 * (int)sizeof(double2));           \
+    k_near_sym<N><<<(count + P - 1) / P, threads, smem, st>>>(                    \
+        ctx, fc, jobs, job_off, n_jobs, elems, pair_ids, count, n, bundles);       \
+  } while (0)
+  EBEM_NT_DISPATCH(fill_nt_bucket(nt), EBEM_SYM_CALL)
+#undef EBEM_SYM_CALL
 }
 
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,

@@ -22,10 +22,10 @@ void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
                          const long long* job_off, int n_jobs, const int* elems,
                          long long n_pairs, unsigned char* keys, int* vals,
                          cudaStream_t st);
-void launch_near_sym(const DevCtx* ctx, const SymJob* jobs,
-                     const long long* job_off, int n_jobs, const int* elems,
-                     const int* pair_ids, int count, int n, double* bundles,
-                     cudaStream_t st);
+void launch_near_sym(const DevCtx* ctx, const FillConst& fc, int nt,
+                     const SymJob* jobs, const long long* job_off, int n_jobs,
+                     const int* elems, const int* pair_ids, int count, int n,
+                     double* bundles, cudaStream_t st);
 // CUB radix sort of (key, value) by the low 3 key bits; temp grows as needed.
 void sort_pairs_by_class(unsigned char* keys_in, unsigned char* keys_out,
                          int* vals_in, int* vals_out, long long n, void** temp,

@@ -941,7 +941,7 @@ void Problem::execute(FillPlan& plan) {
       if (cnt <= 0) continue;
       const int nq = int((acfg_.far_nodes + add[c]) * acfg_.refine + 0.5);
       g_prof.begin(st_);
-      launch_near_sym(dctx(), sj, so, int(plan.sym_.size()), el, vout + bnd[c], cnt,
+      launch_near_sym(dctx(), fc_, fc_nt_, sj, so, int(plan.sym_.size()), el, vout + bnd[c], cnt,
                       nq, bundles.get(), st_);
       g_prof.end(KP_NEAR_SYM, st_, double(cnt) * nq * nq);
     }

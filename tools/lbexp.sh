@@ -1,7 +1,8 @@
+# Launch-bounds experiments for the fill kernels (development aid; GPU box).
 set -e
 cd paper_2411_18026_b200/csrc
-for v in 2 3; do
-  touch ebem_fill.cu; make -j8 EXTRA="-DEBEM_SYM_MINB=$v" > /dev/null 2>&1
-  echo "== sym minb $v"
-  (cd ../.. && python tools/scale_probe.py 262144 2>&1 | grep -E "N=|near_sym")
+for v in "-DEBEM_PROXY_MINB=1" "-DEBEM_NEAR_MINB=2" "-DEBEM_NEAR_MINB=1" "-DEBEM_PROXY_MINB=1 -DEBEM_NEAR_MINB=2"; do
+  touch ebem_fill.cu; make -j8 EXTRA="$v" > /dev/null 2>&1
+  echo "== $v"
+  (cd ../.. && python tools/repeat_probe.py 262144 2 --prof 2>&1 | tail -1)
 done
