@@ -15,6 +15,10 @@
 #include <limits>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
+#include <exception>
+#include <mutex>
+#include <thread>
 
 #include "ebem_kernels.h"
 #include "host_setup.h"
@@ -109,14 +113,30 @@ void Profiler::end(int id, cudaStream_t st, double u) {
 void Profiler::collect() {
   if (pending_.empty() && !near_points) return;
   CK(cudaDeviceSynchronize());
-  for (const Rec& r : pending_) {
+  for (size_t k = 0; k < pending_.size(); ++k) {
+    const Rec& r = pending_[k];
     float t = 0.f;
     CK(cudaEventElapsedTime(&t, r.a, r.b));
     ms[r.id] += t;
     count[r.id] += 1;
     units[r.id] += r.units;
+    if (k > 0) {  // one stream: the span between two recorded kernels
+      float g = 0.f;
+      CK(cudaEventElapsedTime(&g, pending_[k - 1].b, r.a));
+      gap_ms[r.id] += g;
+    }
+  }
+  for (const Rec& r : pending_) {
     pool_.push_back(r.a);
     pool_.push_back(r.b);
+  }
+  if (verbose_level() >= 1 && !pending_.empty()) {
+    double tot = 0.0;
+    for (int i = 0; i < KP_COUNT; ++i) tot += gap_ms[i];
+    std::fprintf(stderr, "[ebem] device gaps before kernels (total %.1f ms):", tot);
+    for (int i = 0; i < KP_COUNT; ++i)
+      if (gap_ms[i] > 0.05) std::fprintf(stderr, " %s %.1f", kernel_name(i), gap_ms[i]);
+    std::fprintf(stderr, "\n");
   }
   pending_.clear();
   if (near_points) {
@@ -129,7 +149,7 @@ void Profiler::collect() {
 
 void Profiler::reset() {
   collect();
-  for (int i = 0; i < KP_COUNT; ++i) ms[i] = 0.0, count[i] = 0, units[i] = 0.0;
+  for (int i = 0; i < KP_COUNT; ++i) ms[i] = 0.0, count[i] = 0, units[i] = 0.0, gap_ms[i] = 0.0;
 }
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -456,6 +476,100 @@ void Problem::check_domain() {
   }
 }
 
+// ------------------------------------------------------- planning threads
+namespace {
+
+class PlanPool {
+ public:
+  PlanPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    n_ = int(std::min(16u, std::max(1u, hw)));
+    if (const char* e = std::getenv("EBEM_PLAN_THREADS")) n_ = std::max(1, std::atoi(e));
+    for (int i = 1; i < n_; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~PlanPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (std::thread& t : th_) t.join();
+  }
+  int size() const { return n_; }
+  void run(int n, const std::function<void(int)>& f) {
+    if (n <= 0) return;
+    if (n_ == 1 || n == 1) {
+      for (int i = 0; i < n; ++i) f(i);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      f_.store(&f);
+      total_.store(n);
+      next_.store(0);
+      done_.store(0);
+      err_ = nullptr;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(m_);
+    done_cv_.wait(lk, [&] { return done_.load() == total_.load(); });
+    total_.store(0);
+    if (err_) std::rethrow_exception(err_);
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      const int total = total_.load();
+      const int i = next_.fetch_add(1);
+      if (i >= total) break;
+      try {
+        (*f_.load())(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(m_);
+        if (!err_) err_ = std::current_exception();
+      }
+      if (done_.fetch_add(1) + 1 == total) {
+        std::lock_guard<std::mutex> lk(m_);
+        done_cv_.notify_all();
+      }
+    }
+  }
+  void loop() {
+    unsigned long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  int n_ = 1;
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  std::atomic<const std::function<void(int)>*> f_{nullptr};
+  std::atomic<int> total_{0}, next_{0}, done_{0};
+  std::exception_ptr err_;
+  unsigned long gen_ = 0;
+  bool stop_ = false;
+};
+
+PlanPool& plan_pool() {
+  static PlanPool* p = new PlanPool();  // never destroyed: no join at exit
+  return *p;
+}
+
+}  // namespace
+
+void parallel_for(int n, const std::function<void(int)>& f) { plan_pool().run(n, f); }
+int planning_threads() { return plan_pool().size(); }
+
 // ---------------------------------------------------------------- FillPlan
 void FillPlan::clear() {
   bundles_ = near_pairs_ = entries_ = 0;
@@ -474,6 +588,55 @@ void FillPlan::clear() {
   gather_.clear();
   gather_off_.clear();
   desc_.clear();
+}
+
+void FillPlan::append(const FillPlan& o) {
+  const int eb = int(elems_.size());
+  const long long bb = bundles_, nb = near_pairs_, sb = sym_pairs_, entb = entries_;
+  const int db = int(desc_.size()), pb = proxy_blocks_;
+  elems_.insert(elems_.end(), o.elems_.begin(), o.elems_.end());
+  for (NearJob J : o.near_) {
+    J.pair_off += bb;
+    J.res_off += eb;
+    J.ces_off += eb;
+    near_.push_back(J);
+  }
+  for (long long x : o.near_local_) near_local_.push_back(x + nb);
+  for (long long x : o.sing_pair_) sing_pair_.push_back(x + bb);
+  sing_elems_.insert(sing_elems_.end(), o.sing_elems_.begin(), o.sing_elems_.end());
+  for (SymJob J : o.sym_) {
+    J.v_off += bb;
+    J.u_off += bb;
+    J.local_off += sb;
+    J.a_off += eb;
+    J.e_off += eb;
+    sym_.push_back(J);
+  }
+  for (long long x : o.sym_off_) sym_off_.push_back(x + sb);
+  for (ProxyJob J : o.proxy_) {
+    J.v_off += bb;
+    J.u_off += bb;
+    J.e_off += eb;
+    J.block_off += pb;
+    proxy_.push_back(J);
+  }
+  for (int x : o.proxy_boff_) proxy_boff_.push_back(x + pb);
+  for (GatherJob G : o.gather_) {
+    G.pair_off += bb;
+    G.entry_off += entb;
+    G.rdesc_off += db;
+    G.cdesc_off += db;
+    gather_.push_back(G);
+  }
+  for (long long x : o.gather_off_) gather_off_.push_back(x + entb);
+  desc_.insert(desc_.end(), o.desc_.begin(), o.desc_.end());
+  bundles_ += o.bundles_;
+  near_pairs_ += o.near_pairs_;
+  sym_pairs_ += o.sym_pairs_;
+  entries_ += o.entries_;
+  proxy_blocks_ += o.proxy_blocks_;
+  // o's polygon descriptors were copied with its descriptors; this plan's own
+  // (if any) stay where they are
 }
 
 // Elements supporting the hat functions of the listed nodes (node g owns
@@ -976,11 +1139,11 @@ void Problem::interaction(const std::vector<BasisReq>& req,
   tu_off.resize(nc_);
   n_out.resize(nc_);
   size_t run = 0;
+  {
+    PhaseTimer t_geom("proxy_geometry", nullptr);
+    parallel_for(int(nc_), [&](int c) { geom[c] = build_proxy(req[c].begin, req[c].end); });
+  }
   for (size_t c = 0; c < nc_; ++c) {
-    {
-      PhaseTimer t_geom("proxy_geometry", nullptr);
-      geom[c] = build_proxy(req[c].begin, req[c].end);
-    }
     n_out[c] = 2 * m + 2 * int(geom[c].enclosed.size());
     const size_t ncol = (*req[c].cols)[0].size() + (*req[c].cols)[1].size();
     const size_t nrow = (*req[c].rows)[0].size() + (*req[c].rows)[1].size();
@@ -993,19 +1156,34 @@ void Problem::interaction(const std::vector<BasisReq>& req,
     PhaseTimer t_alloc("alloc_tbuf", nullptr);
     tbuf.ensure(2 * run + 2);
   }
-  FillPlan plan(n_, m, pcfg_.n_gauss);
+  // Cells are planned in contiguous chunks on the planning threads and the
+  // chunk plans appended in cell order: the same jobs, offsets and gather
+  // order as a serial pass.
   double* base = tbuf.get();
-  for (size_t c = 0; c < nc_; ++c) {
-    const Lists& rows = *req[c].rows;
-    const Lists& cols = *req[c].cols;
-    double* tv = base + 2 * tv_off[c];
-    double* tu = base + 2 * tu_off[c];
-    const int no = n_out[c];
+  const int nchunk = int(std::min<size_t>(nc_, size_t(4 * planning_threads())));
+  std::vector<FillPlan> parts(nchunk, FillPlan(n_, m, pcfg_.n_gauss));
+  {
+    PhaseTimer t_plan("fill_plan", nullptr);
+    parallel_for(nchunk, [&](int k) {
+      const size_t c0 = nc_ * size_t(k) / nchunk, c1 = nc_ * size_t(k + 1) / nchunk;
+      for (size_t c = c0; c < c1; ++c) {
+        const Lists& rows = *req[c].rows;
+        const Lists& cols = *req[c].cols;
+        double* tv = base + 2 * tv_off[c];
+        double* tu = base + 2 * tu_off[c];
+        const int no = n_out[c];
+        parts[k].add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv,
+                           no, tu, no);
+        parts[k].add_sym_near(geom[c].enclosed, rows, cols, tv, no, tu, no);
+      }
+    });
+  }
+  FillPlan plan(n_, m, pcfg_.n_gauss);
+  for (int k = 0; k < nchunk; ++k) {
     {
-      PhaseTimer t_plan("fill_plan", nullptr);
-      plan.add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv, no,
-                     tu, no);
-      plan.add_sym_near(geom[c].enclosed, rows, cols, tv, no, tu, no);
+      PhaseTimer t_app("fill_plan_append", nullptr);
+      plan.append(parts[k]);
+      parts[k] = FillPlan(n_, m, pcfg_.n_gauss);
     }
     if (plan.bundles() > kMaxBundlesPerWave) execute(plan);
   }
@@ -1665,15 +1843,31 @@ void Fds::build() {
         }
         if (d) copy_sync(C.lu, h.data(), 16 * size_t(d) * d);
       }
-      for (int i = 0; !hs_ && i < nlev; ++i) {
-        Cell& C = cells_[f + i];
-        const int d = 2 * C.nloc;
-        if (level == depth_) {
-          plan.add_sym_diag(C.jrow[0], C.lu, d);  // leaf: jrow == jcol, ascending
-        } else {
-          reduced_diagonal(plan, copies, f + i, C.lu, d, 0);
+      if (!hs_) {
+        // planned in contiguous chunks on the planning threads, appended in
+        // cell order (same jobs and order as a serial pass)
+        const int nchunk = std::min(nlev, 4 * planning_threads());
+        std::vector<FillPlan> parts(nchunk, FillPlan(n, P_.proxy_cfg().m_prime,
+                                                     P_.proxy_cfg().n_gauss));
+        std::vector<std::vector<CopyTask>> pcopies(nchunk);
+        parallel_for(nchunk, [&](int k) {
+          const int i0 = int(size_t(nlev) * k / nchunk), i1 = int(size_t(nlev) * (k + 1) / nchunk);
+          for (int i = i0; i < i1; ++i) {
+            Cell& C = cells_[f + i];
+            const int d = 2 * C.nloc;
+            if (level == depth_) {
+              parts[k].add_sym_diag(C.jrow[0], C.lu, d);  // leaf: jrow == jcol, ascending
+            } else {
+              reduced_diagonal(parts[k], pcopies[k], f + i, C.lu, d, 0);
+            }
+          }
+        });
+        for (int k = 0; k < nchunk; ++k) {
+          plan.append(parts[k]);
+          parts[k] = FillPlan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
+          copies.insert(copies.end(), pcopies[k].begin(), pcopies[k].end());
+          if (plan.bundles() > kMaxBundlesPerWave) P_.execute(plan);
         }
-        if (plan.bundles() > kMaxBundlesPerWave) P_.execute(plan);
       }
       P_.execute(plan);
       run_copies(P_, copies);

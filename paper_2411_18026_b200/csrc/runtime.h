@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstddef>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -53,6 +54,7 @@ class Profiler {
   double ms[KP_COUNT] = {};
   long long count[KP_COUNT] = {};
   double units[KP_COUNT] = {};
+  double gap_ms[KP_COUNT] = {};  // device idle right before each kernel kind
   unsigned long long* near_points = nullptr;  // device counter (on only)
 
  private:
@@ -280,6 +282,11 @@ struct Scratch {
 };
 Scratch& scratch();
 
+// Runs f(i) for i in [0, n) on the process's planning threads (the calling
+// thread takes part).  f must not throw.
+void parallel_for(int n, const std::function<void(int)>& f);
+int planning_threads();
+
 // A tall complex block (column-major, ld) whose R factor the ID needs.
 struct TallBlock {
   const double* p;
@@ -385,6 +392,9 @@ class FillPlan {
   long long bundles() const { return bundles_; }
   bool empty() const { return gather_.empty(); }
   void clear();
+  // Appends another plan (built independently, e.g. on another host thread)
+  // with its element, bundle, pair, descriptor and entry offsets relocated.
+  void append(const FillPlan& o);
 
  private:
   friend class Problem;
