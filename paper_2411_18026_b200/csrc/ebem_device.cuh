@@ -256,6 +256,39 @@ __device__ __forceinline__ void scalars_split(const DevCtx* __restrict__ ctx,
 // Closed form of int_0^1 u^upow rem(scale*u) du per scalar,
 // proj/src/kernel_scalars.cpp:108-121,333-344.  Sets *bad when the element is
 // too long for the frequency (the reference throws std::domain_error).
+// The three weights upow = 1, 2, 3 of integrated_remainder from one pass
+// over the series (same operations per weight as three separate calls).
+__device__ __forceinline__ void integrated_remainder3(
+    const DevCtx* __restrict__ ctx, double scale, Scalars (&o)[3], int* bad) {
+  if (!(ctx->med.kT * scale < 2.5)) atomicExch(bad, 1);
+  const double logc = log(scale);
+  const int maxq = ctx->series_maxq;
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int k = 0; k < 10; ++k) o[j].s[k] = mk(0.0, 0.0);
+  double cp = 1.0;
+  for (int q = 0; q <= maxq; ++q) {
+    double inv[3], inv2[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      inv[j] = 1.0 / double(q + j + 2);
+      inv2[j] = inv[j] * inv[j];
+    }
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      const double4 c = ld_series(ctx, k, q);
+      const double ar = fma(c.z, logc, c.x), ai = fma(c.w, logc, c.y);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const cplx t = mk(ar * inv[j] - c.z * inv2[j], ai * inv[j] - c.w * inv2[j]);
+        axpy(o[j].s[k], cp, t);
+      }
+    }
+    cp *= scale;
+  }
+}
+
 __device__ __forceinline__ void integrated_remainder(
     const DevCtx* __restrict__ ctx, double scale, int upow, Scalars& o,
     int* bad) {

@@ -279,8 +279,11 @@ __device__ void coincident_bundle(const DevCtx* __restrict__ ctx, int e,
         }
 }
 
+// Points p = part, part + nparts, ... of the 2 n corner-rule points (both
+// Duffy triangles); the caller sums the parts.
 __device__ void adjacent_bundle(const DevCtx* __restrict__ ctx, int ea, int eb,
-                                bool end_start, cplx (&v)[kBundle], int* bad) {
+                                bool end_start, cplx (&v)[kBundle], int* bad,
+                                int part = 0, int nparts = 1) {
   const double hx = ef(ctx, EH, ea), hy = ef(ctx, EH, eb);
   double txx, txy, tyx, tyy;
   double bx0[2], bx1[2], by0[2], by1[2];
@@ -313,8 +316,10 @@ __device__ void adjacent_bundle(const DevCtx* __restrict__ ctx, int ea, int eb,
   const int n = ctx->corner_n;
   const double* gx = ctx->gx + gauss_offset(n);
   const double* gw = ctx->gw + gauss_offset(n);
-  for (int tri = 0; tri < 2; ++tri) {
-    for (int wi = 0; wi < n; ++wi) {
+  for (int pt = part; pt < 2 * n; pt += nparts) {
+    const int tri = pt >= n ? 1 : 0;
+    const int wi = pt - tri * n;
+    {
       const double w = gx[wi];
       const double wt = gw[wi];
       double zvx, zvy;
@@ -330,12 +335,14 @@ __device__ void adjacent_bundle(const DevCtx* __restrict__ ctx, int ea, int eb,
       const double zhx = ig * zvx, zhy = ig * zvy;
       const double logg = log(g);
       CMat2 dmat[3], nmat[3];
+      {
+        Scalars s3[3];
+        integrated_remainder3(ctx, g, s3, bad);
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        Scalars s;
-        integrated_remainder(ctx, g, j + 1, s, bad);
-        combine_D(s, zhx, zhy, nyx, nyy, dmat[j]);
-        combine_N(s, zhx, zhy, nxx, nxy, nyx, nyy, nmat[j]);
+        for (int j = 0; j < 3; ++j) {
+          combine_D(s3[j], zhx, zhy, nyx, nyy, dmat[j]);
+          combine_N(s3[j], zhx, zhy, nxx, nxy, nyx, nyy, nmat[j]);
+        }
       }
       CMat2 dstat;
       combine_D(dhat, zhx, zhy, nyx, nyy, dstat);
@@ -376,22 +383,43 @@ __device__ void adjacent_bundle(const DevCtx* __restrict__ ctx, int ea, int eb,
 
 }  // namespace
 
-__global__ void __launch_bounds__(64)
+// One warp per touching pair: the adjacent (Duffy) rule's points are split
+// over the lanes and summed in a fixed butterfly order; a coincident pair
+// (one closed form plus four 1-D series integrals) is done by lane 0.
+__global__ void __launch_bounds__(128)
 k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pairs,
                 const int* __restrict__ pair_elems, int n, double* __restrict__ bundles,
                 int* bad) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= n) return;  // warp-uniform
   const int ea = pair_elems[2 * t], eb = pair_elems[2 * t + 1];
   const int N = ctx->n_nodes;
   cplx v[kBundle];
   if (ea == eb) {
-    coincident_bundle(ctx, ea, v, bad);
-  } else {
-    const bool end_start = (ea + 1 == N ? 0 : ea + 1) == eb;
-    adjacent_bundle(ctx, ea, eb, end_start, v, bad);
+    if (lane == 0) {
+      coincident_bundle(ctx, ea, v, bad);
+      store_bundle(bundles, pairs[t], v);
+    }
+    return;
   }
-  store_bundle(bundles, pairs[t], v);
+  const bool end_start = (ea + 1 == N ? 0 : ea + 1) == eb;
+  adjacent_bundle(ctx, ea, eb, end_start, v, bad, lane, 32);
+#pragma unroll
+  for (int k = 0; k < kBundle; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v[k].re += __shfl_xor_sync(0xffffffffu, v[k].re, o);
+      v[k].im += __shfl_xor_sync(0xffffffffu, v[k].im, o);
+    }
+  if (lane < kBundle) {
+    cplx mine = v[0];
+#pragma unroll
+    for (int k = 1; k < kBundle; ++k)
+      if (lane == k) mine = v[k];
+    reinterpret_cast<double2*>(bundles)[pairs[t] * kBundle + lane] =
+        make_double2(mine.re, mine.im);
+  }
 }
 
 // ------------------------------------------------------- symmetric near
@@ -823,9 +851,9 @@ void launch_near_singular(const DevCtx* ctx, const long long* pairs,
                           const int* pair_elems, int n, double* bundles, int* bad,
                           cudaStream_t st) {
   if (n <= 0) return;
-  const int bs = 64;
-  k_near_singular<<<(n + bs - 1) / bs, bs, 0, st>>>(ctx, pairs, pair_elems, n,
-                                                     bundles, bad);
+  const int bs = 128;  // 4 pairs per CTA, one warp each
+  k_near_singular<<<(unsigned)((n + 3) / 4), bs, 0, st>>>(ctx, pairs, pair_elems, n,
+                                                          bundles, bad);
 }
 
 int proxy_pairs_per_block(int n_gauss) {
