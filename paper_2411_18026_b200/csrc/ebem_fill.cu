@@ -755,18 +755,28 @@ k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst 
 }
 
 // ------------------------------------------------------------------ gather
-__global__ void __launch_bounds__(256)
-k_gather(const GatherJob* __restrict__ jobs, const long long* __restrict__ job_entry_off,
-         int n_jobs, const NodeDesc* __restrict__ desc, long long n_entries,
+__global__ void __launch_bounds__(kGatherTile)
+k_gather(const GatherJob* __restrict__ jobs, const int* __restrict__ job_block_off,
+         int n_jobs, const NodeDesc* __restrict__ desc,
          const double* __restrict__ bundles) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= n_entries) return;
-  const int jb = find_job(job_entry_off, n_jobs, t);
+  __shared__ int s_jb;
+  if (threadIdx.x == 0) s_jb = find_job(job_block_off, n_jobs, int(blockIdx.x));
+  __syncthreads();
+  const int jb = s_jb;
   const GatherJob& J = jobs[jb];
-  const long long local = t - J.entry_off;
-  // column-major sweep: consecutive threads -> consecutive rows
-  const int c = int(local / J.nrows);
-  const int r = int(local - (long long)c * J.nrows);
+  const long long local =
+      (long long)(blockIdx.x - __ldg(job_block_off + jb)) * kGatherTile + threadIdx.x;
+  if (local >= (long long)J.nrows * J.ncols) return;
+  // consecutive threads -> consecutive destination addresses: down a column
+  // for plain blocks, along a row for the conjugate-transposed ones
+  int r, c;
+  if (J.trans) {
+    r = int(local / J.ncols);
+    c = int(local - (long long)r * J.ncols);
+  } else {
+    c = int(local / J.nrows);
+    r = int(local - (long long)c * J.nrows);
+  }
   const NodeDesc rd = desc[J.rdesc_off + r];
   const NodeDesc cd = desc[J.cdesc_off + c];
   const int i = rd.bits >> 2, j = cd.bits >> 2;
@@ -884,13 +894,12 @@ void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int nt,
 #undef EBEM_PROXY_CALL
 }
 
-void launch_gather(const GatherJob* jobs, const long long* job_entry_off,
-                   int n_jobs, const NodeDesc* desc, long long n_entries,
-                   const double* bundles, cudaStream_t st) {
-  if (n_entries <= 0) return;
-  const int bs = 256;
-  k_gather<<<(unsigned)((n_entries + bs - 1) / bs), bs, 0, st>>>(
-      jobs, job_entry_off, n_jobs, desc, n_entries, bundles);
+void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,
+                   int n_blocks, const NodeDesc* desc, const double* bundles,
+                   cudaStream_t st) {
+  if (n_blocks <= 0) return;
+  k_gather<<<(unsigned)n_blocks, kGatherTile, 0, st>>>(jobs, job_block_off, n_jobs,
+                                                       desc, bundles);
 }
 
 }  // namespace ebem_gpu

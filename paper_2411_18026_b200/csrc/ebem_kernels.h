@@ -38,9 +38,10 @@ void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int nt,
                         int n_gauss, const ProxyJob* jobs,
                         const int* job_block_off, int n_jobs, int n_blocks,
                         const int* elems, double* bundles, cudaStream_t st);
-void launch_gather(const GatherJob* jobs, const long long* job_entry_off,
-                   int n_jobs, const NodeDesc* desc, long long n_entries,
-                   const double* bundles, cudaStream_t st);
+constexpr int kGatherTile = 256;  // output entries per gather CTA
+void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,
+                   int n_blocks, const NodeDesc* desc, const double* bundles,
+                   cudaStream_t st);
 
 // ---- incident-field right-hand sides (ebem_rhs.cu)
 void launch_rhs_plane(const DevCtx* ctx, int n_nodes, int kind,

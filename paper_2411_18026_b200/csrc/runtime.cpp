@@ -1033,7 +1033,15 @@ void Problem::execute(FillPlan& plan) {
   const size_t o_pj = pk.add(plan.proxy_);
   const size_t o_pb = pk.add(plan.proxy_boff_);
   const size_t o_gj = pk.add(plan.gather_);
-  const size_t o_go = pk.add(plan.gather_off_);
+  // CTA tiles of kGatherTile entries, each job starting on its own tile
+  std::vector<int> gblk(plan.gather_.size());
+  int n_gblk = 0;
+  for (size_t g = 0; g < plan.gather_.size(); ++g) {
+    gblk[g] = n_gblk;
+    const long long e = (long long)plan.gather_[g].nrows * plan.gather_[g].ncols;
+    n_gblk += int((e + kGatherTile - 1) / kGatherTile);
+  }
+  const size_t o_go = pk.add(gblk);
   const size_t o_de = pk.add(plan.desc_);
   char* base;
   {
@@ -1117,9 +1125,9 @@ void Problem::execute(FillPlan& plan) {
     g_prof.end(KP_NEAR_SING, st_, double(plan.sing_pair_.size()));
   }
   g_prof.begin(st_);
-  launch_gather(Pack::at<GatherJob>(base, o_gj), Pack::at<long long>(base, o_go),
-                int(plan.gather_.size()), Pack::at<NodeDesc>(base, o_de),
-                plan.entries_, bundles.get(), st_);
+  launch_gather(Pack::at<GatherJob>(base, o_gj), Pack::at<int>(base, o_go),
+                int(plan.gather_.size()), n_gblk, Pack::at<NodeDesc>(base, o_de),
+                bundles.get(), st_);
   // bytes: 4 bundle reads (16 B each) + one 16 B store per entry
   g_prof.end(KP_GATHER, st_, 80.0 * double(plan.entries_));
   CK(cudaGetLastError());
