@@ -22,6 +22,8 @@
 //   k_copy       batched block copies (optionally conjugated)
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "ebem_dense.h"
 
 namespace ebem_gpu {
@@ -579,6 +581,147 @@ k_copy(const CopyTask* __restrict__ tasks, const int* __restrict__ block_off,
   }
 }
 
+// ----------------------------------------------------- LU solve, registers
+// One warp per kCpw right-hand sides; lane l holds rows l, l + 32, ... of
+// each (kMaxS slots).  The LU (and 1 / U_kk) is staged in shared memory when
+// it fits and shared by the CTA's 8 warps; every row value travels by
+// shuffle, so the substitutions need no warp barriers and no division.
+constexpr int kCpw = 4;
+
+__device__ __forceinline__ double2 zrcp(double2 a) {
+  // 1 / a by Smith's method with reciprocals only
+  if (fabs(a.x) >= fabs(a.y)) {
+    const double r = a.y * (1.0 / a.x), d = 1.0 / fma(a.y, r, a.x);
+    return make_double2(d, -r * d);
+  }
+  const double r = a.x * (1.0 / a.y), d = 1.0 / fma(a.x, r, a.y);
+  return make_double2(r * d, -d);
+}
+
+template <int kMaxS>
+__device__ __forceinline__ double2 pick(const double2 (&v)[kMaxS], int s) {
+  double2 o = v[0];
+#pragma unroll
+  for (int q = 1; q < kMaxS; ++q)
+    if (q == s) o = v[q];
+  return o;
+}
+template <int kMaxS>
+__device__ __forceinline__ void put(double2 (&v)[kMaxS], int s, double2 x) {
+#pragma unroll
+  for (int q = 0; q < kMaxS; ++q)
+    if (q == s) v[q] = x;
+}
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+template <int kMaxS>
+__global__ void __launch_bounds__(kThreads)
+k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off,
+            int n_tasks, int cap) {
+  extern __shared__ double2 sm[];
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const LuSolveTask T = tasks[lo];
+  const int n = T.n;
+  const bool stage = (long long)n * n + n <= cap;
+  const double2* A = reinterpret_cast<const double2*>(T.lu);
+  size_t lda = T.ld;
+  double2* invd = sm + (stage ? (size_t)n * n : 0);
+  if (stage) {
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+      const int j = idx / n, i = idx - j * n;
+      sm[idx] = A[(size_t)j * lda + i];
+    }
+    A = sm;
+    lda = n;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += blockDim.x) invd[k] = zrcp(A[(size_t)k * lda + k]);
+  __syncthreads();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int col0 = ((blockIdx.x - block_off[lo]) * kWarps + w) * kCpw;
+  if (col0 >= T.nrhs) return;
+  double2 b[kCpw][kMaxS];
+#pragma unroll
+  for (int c = 0; c < kCpw; ++c) {
+    const int col = col0 + c;
+    const double2* bg = reinterpret_cast<const double2*>(T.b) + (size_t)col * T.ldb;
+#pragma unroll
+    for (int s = 0; s < kMaxS; ++s) {
+      const int r = l + 32 * s;
+      b[c][s] = (col < T.nrhs && r < n) ? bg[r] : make_double2(0.0, 0.0);
+    }
+  }
+  // row interchanges in order (warp-uniform pivots)
+  for (int k = 0; k < n; ++k) {
+    const int p = __ldg(T.ipiv + k);
+    if (p == k) continue;
+    const int sk = k >> 5, lk = k & 31, sp = p >> 5, lp = p & 31;
+#pragma unroll
+    for (int c = 0; c < kCpw; ++c) {
+      const double2 vk = shfl2(pick(b[c], sk), lk);
+      const double2 vp = shfl2(pick(b[c], sp), lp);
+      if (l == lk) put(b[c], sk, vp);
+      if (l == lp) put(b[c], sp, vk);
+    }
+  }
+  // L y = b (unit lower)
+  for (int k = 0; k < n - 1; ++k) {
+    const int sk = k >> 5, lk = k & 31;
+    double2 bk[kCpw];
+#pragma unroll
+    for (int c = 0; c < kCpw; ++c) bk[c] = shfl2(pick(b[c], sk), lk);
+    const double2* Ak = A + (size_t)k * lda;
+#pragma unroll
+    for (int s = 0; s < kMaxS; ++s) {
+      const int r = l + 32 * s;
+      if (r > k && r < n) {
+        const double2 a = Ak[r];
+#pragma unroll
+        for (int c = 0; c < kCpw; ++c) b[c][s] = zfms(b[c][s], a, bk[c]);
+      }
+    }
+  }
+  // U x = y
+  for (int k = n - 1; k >= 0; --k) {
+    const int sk = k >> 5, lk = k & 31;
+    const double2 ik = invd[k];
+    double2 xk[kCpw];
+#pragma unroll
+    for (int c = 0; c < kCpw; ++c) {
+      xk[c] = zmul(shfl2(pick(b[c], sk), lk), ik);
+      if (l == lk) put(b[c], sk, xk[c]);
+    }
+    const double2* Ak = A + (size_t)k * lda;
+#pragma unroll
+    for (int s = 0; s < kMaxS; ++s) {
+      const int r = l + 32 * s;
+      if (r < k) {
+        const double2 a = Ak[r];
+#pragma unroll
+        for (int c = 0; c < kCpw; ++c) b[c][s] = zfms(b[c][s], a, xk[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kCpw; ++c) {
+    const int col = col0 + c;
+    if (col >= T.nrhs) break;
+    double2* bg = reinterpret_cast<double2*>(T.b) + (size_t)col * T.ldb;
+#pragma unroll
+    for (int s = 0; s < kMaxS; ++s) {
+      const int r = l + 32 * s;
+      if (r < n) bg[r] = b[c][s];
+    }
+  }
+}
+
 // ----------------------------------------------------------- host wrappers
 static void set_smem_attr(const void* f) {
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
@@ -591,6 +734,9 @@ void dense_init() {
   set_smem_attr((const void*)k_cpqr);
   set_smem_attr((const void*)k_getrf);
   set_smem_attr((const void*)k_getrs);
+  set_smem_attr((const void*)k_getrs_reg<2>);
+  set_smem_attr((const void*)k_getrs_reg<4>);
+  set_smem_attr((const void*)k_getrs_reg<8>);
   done = true;
 }
 
@@ -614,16 +760,31 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
   if (n <= 0) return;
   k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
-int getrs_blocks(int nrhs) { return (nrhs + kWarps - 1) / kWarps; }
+int getrs_blocks(int nrhs, int max_n) {
+  const int per = max_n <= 256 ? kWarps * kCpw : kWarps;
+  return (nrhs + per - 1) / per;
+}
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
-                  int n_blocks, cudaStream_t st, int smem_bytes) {
+                  int n_blocks, cudaStream_t st, int smem_bytes, int max_n) {
   if (n_blocks <= 0) return;
-  k_getrs<<<n_blocks, kThreads, size_t(smem_bytes), st>>>(tasks, block_off, n_tasks,
-                                                          smem_bytes / 16);
+  // LU staged when it fits (smem_bytes covers the largest staged one);
+  // 1 / U_kk always needs n slots
+  const int bytes = std::max(smem_bytes, 16 * std::max(max_n, 1));
+  if (max_n <= 64)
+    k_getrs_reg<2><<<n_blocks, kThreads, size_t(bytes), st>>>(tasks, block_off, n_tasks, smem_bytes / 16);
+  else if (max_n <= 128)
+    k_getrs_reg<4><<<n_blocks, kThreads, size_t(bytes), st>>>(tasks, block_off, n_tasks, smem_bytes / 16);
+  else if (max_n <= 256)
+    k_getrs_reg<8><<<n_blocks, kThreads, size_t(bytes), st>>>(tasks, block_off, n_tasks, smem_bytes / 16);
+  else
+    k_getrs<<<n_blocks, kThreads, size_t(smem_bytes), st>>>(tasks, block_off, n_tasks,
+                                                            smem_bytes / 16);
 }
 
 int getrs_smem_bytes(int n) {
-  const long long b = ((long long)n * n + (long long)kWarps * n) * 16;
+  // staged LU + 1 / U_kk (register kernel); the wide fallback (n > 256)
+  // stages LU + one column per warp
+  const long long b = ((long long)n * n + (n <= 256 ? n : (long long)kWarps * n)) * 16;
   return b <= kSmemCap ? int(b) : 0;
 }
 int gemm_blocks(int m, int n) {

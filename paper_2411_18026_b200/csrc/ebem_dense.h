@@ -99,9 +99,10 @@ void launch_tsqr(const QrTask* tasks, int n_tasks, int lanes, size_t smem,
 void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st);
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st);
-int getrs_blocks(int nrhs);
+// CTAs per task for a batch whose largest LU has order max_n
+int getrs_blocks(int nrhs, int max_n);
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
-                  int n_blocks, cudaStream_t st, int smem_bytes = 0);
+                  int n_blocks, cudaStream_t st, int smem_bytes, int max_n);
 // Dynamic shared memory that stages an n x n LU (0 when it does not fit).
 int getrs_smem_bytes(int n);
 int gemm_blocks(int m, int n);

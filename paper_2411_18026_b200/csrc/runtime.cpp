@@ -1553,6 +1553,7 @@ namespace {
 // k_getrs stages the LU in shared memory up to this many bytes per launch
 // (shared by all tasks of the launch; larger tasks read L2).
 int g_getrs_smem = 0;
+int g_getrs_maxn = 0;
 
 template <class T, class F, class U>
 void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
@@ -1567,7 +1568,8 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
   }
   if (total == 0) return;
   if (P.recorder) {
-    P.recorder->add(id, t, boff, total, id == KP_GETRS ? g_getrs_smem : 0);
+    P.recorder->add(id, t, boff, total, id == KP_GETRS ? g_getrs_smem : 0,
+                    id == KP_GETRS ? g_getrs_maxn : 0);
     return;
   }
   Pack pk;
@@ -1607,7 +1609,7 @@ void Recorder::replay(cudaStream_t st, int phase) {
         break;
       case KP_GETRS:
         launch_getrs(Pack::at<LuSolveTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st,
-                     l.aux);
+                     l.aux, l.aux2);
         break;
       default:
         throw Error(EBEM_LOGIC_ERROR, "Recorder: unexpected kernel kind");
@@ -1628,15 +1630,18 @@ void run_gemms(Problem& P, const std::vector<GemmTask>& t) {
 namespace {
 void launch_getrs_staged(const LuSolveTask* t, const int* boff, int nt, int nb,
                          cudaStream_t st) {
-  launch_getrs(t, boff, nt, nb, st, g_getrs_smem);
+  launch_getrs(t, boff, nt, nb, st, g_getrs_smem, g_getrs_maxn);
 }
 }  // namespace
 
 void run_getrs(Problem& P, const std::vector<LuSolveTask>& t) {
-  int smem = 0;
-  for (const LuSolveTask& x : t) smem = std::max(smem, getrs_smem_bytes(x.n));
+  int smem = 0, maxn = 0;
+  for (const LuSolveTask& x : t) maxn = std::max(maxn, x.n);
+  for (const LuSolveTask& x : t)
+    if (maxn <= 256 || x.n > 0) smem = std::max(smem, getrs_smem_bytes(x.n));
   g_getrs_smem = smem;
-  run_blocked(P, t, [](const LuSolveTask& s) { return s.n > 0 ? getrs_blocks(s.nrhs) : 0; },
+  g_getrs_maxn = maxn;
+  run_blocked(P, t, [maxn](const LuSolveTask& s) { return s.n > 0 ? getrs_blocks(s.nrhs, maxn) : 0; },
               launch_getrs_staged, KP_GETRS,
               [](const LuSolveTask& s) { return 8.0 * s.n * double(s.n) * s.nrhs; });
 }

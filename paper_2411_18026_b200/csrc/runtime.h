@@ -229,9 +229,10 @@ class Recorder {
  public:
   template <class T>
   void add(int kind, const std::vector<T>& t, const std::vector<int>& boff,
-           int total, int aux = 0) {
+           int total, int aux = 0, int aux2 = 0) {
     Launch l;
     l.kind = kind;
+    l.aux2 = aux2;
     l.task_off = pk_.add(t);
     l.boff_off = pk_.add(boff);
     l.n_tasks = int(t.size());
@@ -252,6 +253,7 @@ class Recorder {
     size_t task_off, boff_off;
     int n_tasks, n_blocks;
     int aux;  // k_getrs: dynamic shared memory bytes
+    int aux2;  // k_getrs: largest LU order of the batch
   };
   Pack pk_;
   std::vector<Launch> launches_;
