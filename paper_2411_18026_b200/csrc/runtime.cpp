@@ -1656,13 +1656,25 @@ void run_getrf(Problem& P, std::vector<LuTask> t) {
     else ws += size_t(t[i].n) * t[i].n;
   }
   P.gws.ensure(ws + 1);
+  // shared-memory LUs: one CTA each; larger ones: blocked, in place
+  std::vector<LuTask> small, big;
+  int big_n = 0;
+  for (const LuTask& x : t) {
+    if (x.in_smem) small.push_back(x);
+    else {
+      big.push_back(x);
+      big_n = std::max(big_n, x.n);
+    }
+  }
   Pack pk;
-  const size_t o = pk.add(t);
+  const size_t o = pk.add(small);
+  const size_t ob = pk.add(big);
   char* tb = P.staging.put(pk, P.stream());
   double fl = 0.0;
   for (const LuTask& x : t) fl += 8.0 / 3.0 * double(x.n) * x.n * x.n;
   g_prof.begin(P.stream());
-  launch_getrf(Pack::at<LuTask>(tb, o), int(t.size()), smem, P.gws.get(), P.stream());
+  launch_getrf(Pack::at<LuTask>(tb, o), int(small.size()), smem, P.gws.get(), P.stream());
+  launch_lu_blocked(Pack::at<LuTask>(tb, ob), int(big.size()), big_n, P.stream());
   g_prof.end(KP_GETRF, P.stream(), fl);
   P.staging.fence(P.stream());
   CK(cudaGetLastError());
