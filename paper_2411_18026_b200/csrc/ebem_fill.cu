@@ -458,6 +458,7 @@ k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
 #ifndef EBEM_SYM_THREADS
 #define EBEM_SYM_THREADS 256
 #endif
+constexpr int kSymMaxPairs = EBEM_SYM_THREADS;  // P = threads / n pairs per CTA
 #ifndef EBEM_SYM_MINB
 #define EBEM_SYM_MINB 1
 #endif
@@ -483,20 +484,24 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
   const bool active = lp < P && idx < count;
   const double* gx = sgx;
   const double* gw = sgw;
-  __syncthreads();
-  int ea = 0, eb = 0;
-  long long vdst = 0, udst = 0;
-  if (active) {
+  // one job lookup per pair (not per thread), shared with the reduction
+  __shared__ int s_ea[kSymMaxPairs], s_eb[kSymMaxPairs];
+  __shared__ long long s_vd[kSymMaxPairs], s_ud[kSymMaxPairs];
+  if (active && i == 0) {
     const long long p = __ldg(pair_ids + idx);
     const int jb = find_job(job_off, n_jobs, p);
     const SymJob J = jobs[jb];
     const long long local = p - J.local_off;
     const int a = int(local / J.nE);
     const int q = int(local - (long long)a * J.nE);
-    ea = __ldg(elems + J.a_off + a);
-    eb = __ldg(elems + J.e_off + q);
-    vdst = J.v_off + local;
-    udst = J.u_off + (long long)q * J.nA + a;
+    s_ea[lp] = __ldg(elems + J.a_off + a);
+    s_eb[lp] = __ldg(elems + J.e_off + q);
+    s_vd[lp] = J.v_off + local;
+    s_ud[lp] = J.u_off + (long long)q * J.nA + a;
+  }
+  __syncthreads();
+  if (active) {
+    const int ea = s_ea[lp], eb = s_eb[lp];
     const double pax = ef(ctx, EPX, ea), pay = ef(ctx, EPY, ea);
     const double dax = ef(ctx, EDX, ea), day = ef(ctx, EDY, ea);
     const double pbx = ef(ctx, EPX, eb), pby = ef(ctx, EPY, eb);
@@ -588,27 +593,13 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
       const double2 qq = row[16 + (e >> 1)];
       qs = fma(wi, (e & 1) ? qq.y : qq.x, qs);
     }
-    // element lengths of this pair (recomputed from the ids)
-    const long long p2 = __ldg(pair_ids + idx2);
-    const int jb2 = find_job(job_off, n_jobs, p2);
-    const SymJob J2 = jobs[jb2];
-    const long long local2 = p2 - J2.local_off;
-    const int a2 = int(local2 / J2.nE);
-    const int q2 = int(local2 - (long long)a2 * J2.nE);
-    const int ea2 = __ldg(elems + J2.a_off + a2);
-    const int eb2 = __ldg(elems + J2.e_off + q2);
-    const double hh = ef(ctx, EH, ea2) * ef(ctx, EH, eb2);
+    const double hh = ef(ctx, EH, s_ea[lp2]) * ef(ctx, EH, s_eb[lp2]);
     const double sg = (la == lb) ? 1.0 : -1.0;  // slope_la * slope_lb
     const double re = fma(hh, ar, sg * qs * alpha.re);
     const double im = fma(hh, ai, sg * qs * alpha.im);
-    const long long dst = orient == 0 ? J2.v_off + local2
-                                      : J2.u_off + (long long)q2 * J2.nA + a2;
+    const long long dst = orient == 0 ? s_vd[lp2] : s_ud[lp2];
     reinterpret_cast<double2*>(bundles)[dst * kBundle + k] = make_double2(re, im);
   }
-  (void)ea;
-  (void)eb;
-  (void)vdst;
-  (void)udst;
 }
 
 // ------------------------------------------------------------------- proxy

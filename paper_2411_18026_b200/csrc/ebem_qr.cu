@@ -72,10 +72,19 @@ __device__ __forceinline__ void team_reflector(double2* __restrict__ c, int m,
   if (xn2 == 0.0 && alpha.y == 0.0) {
     beta = alpha.x;
   } else {
-    const double nrm = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xn2);
-    beta = alpha.x >= 0.0 ? -nrm : nrm;
-    tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
-    const double2 scal = zdiv(make_double2(1.0, 0.0), make_double2(alpha.x - beta, alpha.y));
+    // zlarfg with reciprocals only (a true division with a zero numerator,
+    // e.g. alpha.y = 0, takes the slow path); see make_reflector in
+    // ebem_tsqr.cu for the scaled form of 1 / (alpha - beta)
+    const double x2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, xn2));
+    const double s = rsqrt(x2);
+    const bool pos = alpha.x >= 0.0;
+    beta = pos ? -(x2 * s) : x2 * s;
+    const double ib = pos ? -s : s;
+    tau = make_double2((beta - alpha.x) * ib, -alpha.y * ib);
+    const double arn = fma(alpha.x, s, pos ? 1.0 : -1.0);
+    const double ain = alpha.y * s;
+    const double id = s / fma(arn, arn, ain * ain);
+    const double2 scal = make_double2(arn * id, -ain * id);
     for (int r = i + 1 + sub; r < m; r += kTeamLanes) c[r] = zmul(scal, c[r]);
   }
   __syncwarp(team_mask());
@@ -213,31 +222,34 @@ __device__ __forceinline__ void cpqr_team_body(const CpqrTask& T, double2* __res
     }
     __syncthreads();
     const int pvt = s_pvt;
-    if (pvt != i) {
-      double2* a = A + (size_t)pvt * m;
-      double2* b = A + (size_t)i * m;
-      for (int r = threadIdx.x; r < m; r += blockDim.x) {
-        const double2 t = a[r];
-        a[r] = b[r];
-        b[r] = t;
+    // the step's team swaps the pivot column in and builds the reflector
+    if (team == (i % kTeams)) {
+      if (pvt != i) {
+        double2* a = A + (size_t)pvt * m;
+        double2* b = A + (size_t)i * m;
+        for (int r = sub; r < m; r += kTeamLanes) {
+          const double2 t = a[r];
+          a[r] = b[r];
+          b[r] = t;
+        }
+        if (sub == 0) {
+          const int t = jp[pvt];
+          jp[pvt] = jp[i];
+          jp[i] = t;
+          vn1[pvt] = vn1[i];
+          vn2[pvt] = vn2[i];
+        }
+        __syncwarp(team_mask());
       }
-      if (threadIdx.x == 0) {
-        const int t = jp[pvt];
-        jp[pvt] = jp[i];
-        jp[i] = t;
-        vn1[pvt] = vn1[i];
-        vn2[pvt] = vn2[i];
+      team_reflector(A + (size_t)i * m, m, i, sub, &hh);
+      if (sub == 0) {
+        const double r = fabs(hh.beta);
+        T.rdiag[i] = r;
+        if (i == 0) s_r00 = r;
       }
-      __syncthreads();
     }
-    if (team == (i % kTeams)) team_reflector(A + (size_t)i * m, m, i, sub, &hh);
     __syncthreads();
     const double rii = fabs(hh.beta);
-    if (threadIdx.x == 0) {
-      T.rdiag[i] = rii;
-      if (i == 0) s_r00 = rii;
-    }
-    __syncthreads();
     const double r00 = s_r00;
     if (r00 == 0.0 || rii <= T.stop_rel * r00) {
       steps = i;
@@ -254,10 +266,11 @@ __device__ __forceinline__ void cpqr_team_body(const CpqrTask& T, double2* __res
       if (v1 == 0.0) continue;
       __syncwarp(team_mask());
       const double2 aij = cj[i];
-      double temp = hypot(aij.x, aij.y) / v1;
+      const double iv1 = 1.0 / v1;
+      double temp = hypot(aij.x, aij.y) * iv1;
       temp = 1.0 - temp * temp;
       temp = temp > 0.0 ? temp : 0.0;
-      const double ratio = v1 / vn2[j];
+      const double ratio = v1 * (1.0 / vn2[j]);
       const double temp2 = temp * ratio * ratio;
       if (temp2 <= tol3z) {
         double s = 0.0;
