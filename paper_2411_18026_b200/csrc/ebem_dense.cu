@@ -586,7 +586,7 @@ k_copy(const CopyTask* __restrict__ tasks, const int* __restrict__ block_off,
 // each (kMaxS slots).  The LU (and 1 / U_kk) is staged in shared memory when
 // it fits and shared by the CTA's 8 warps; every row value travels by
 // shuffle, so the substitutions need no warp barriers and no division.
-constexpr int kCpw = 4;
+constexpr int kCpw = 4;  // right-hand sides per warp for wide batches (1 for narrow)
 
 __device__ __forceinline__ double2 zrcp(double2 a) {
   // 1 / a by Smith's method with reciprocals only
@@ -616,7 +616,7 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src) {
   return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-template <int kMaxS>
+template <int kMaxS, int CPW>
 __global__ void __launch_bounds__(kThreads)
 k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off,
             int n_tasks, int cap) {
@@ -645,11 +645,11 @@ k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
   for (int k = threadIdx.x; k < n; k += blockDim.x) invd[k] = zrcp(A[(size_t)k * lda + k]);
   __syncthreads();
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int col0 = ((blockIdx.x - block_off[lo]) * kWarps + w) * kCpw;
+  const int col0 = ((blockIdx.x - block_off[lo]) * kWarps + w) * CPW;
   if (col0 >= T.nrhs) return;
-  double2 b[kCpw][kMaxS];
+  double2 b[CPW][kMaxS];
 #pragma unroll
-  for (int c = 0; c < kCpw; ++c) {
+  for (int c = 0; c < CPW; ++c) {
     const int col = col0 + c;
     const double2* bg = reinterpret_cast<const double2*>(T.b) + (size_t)col * T.ldb;
 #pragma unroll
@@ -664,7 +664,7 @@ k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
     if (p == k) continue;
     const int sk = k >> 5, lk = k & 31, sp = p >> 5, lp = p & 31;
 #pragma unroll
-    for (int c = 0; c < kCpw; ++c) {
+    for (int c = 0; c < CPW; ++c) {
       const double2 vk = shfl2(pick(b[c], sk), lk);
       const double2 vp = shfl2(pick(b[c], sp), lp);
       if (l == lk) put(b[c], sk, vp);
@@ -674,9 +674,9 @@ k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
   // L y = b (unit lower)
   for (int k = 0; k < n - 1; ++k) {
     const int sk = k >> 5, lk = k & 31;
-    double2 bk[kCpw];
+    double2 bk[CPW];
 #pragma unroll
-    for (int c = 0; c < kCpw; ++c) bk[c] = shfl2(pick(b[c], sk), lk);
+    for (int c = 0; c < CPW; ++c) bk[c] = shfl2(pick(b[c], sk), lk);
     const double2* Ak = A + (size_t)k * lda;
 #pragma unroll
     for (int s = 0; s < kMaxS; ++s) {
@@ -684,7 +684,7 @@ k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
       if (r > k && r < n) {
         const double2 a = Ak[r];
 #pragma unroll
-        for (int c = 0; c < kCpw; ++c) b[c][s] = zfms(b[c][s], a, bk[c]);
+        for (int c = 0; c < CPW; ++c) b[c][s] = zfms(b[c][s], a, bk[c]);
       }
     }
   }
@@ -692,9 +692,9 @@ k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
   for (int k = n - 1; k >= 0; --k) {
     const int sk = k >> 5, lk = k & 31;
     const double2 ik = invd[k];
-    double2 xk[kCpw];
+    double2 xk[CPW];
 #pragma unroll
-    for (int c = 0; c < kCpw; ++c) {
+    for (int c = 0; c < CPW; ++c) {
       xk[c] = zmul(shfl2(pick(b[c], sk), lk), ik);
       if (l == lk) put(b[c], sk, xk[c]);
     }
@@ -705,12 +705,12 @@ k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
       if (r < k) {
         const double2 a = Ak[r];
 #pragma unroll
-        for (int c = 0; c < kCpw; ++c) b[c][s] = zfms(b[c][s], a, xk[c]);
+        for (int c = 0; c < CPW; ++c) b[c][s] = zfms(b[c][s], a, xk[c]);
       }
     }
   }
 #pragma unroll
-  for (int c = 0; c < kCpw; ++c) {
+  for (int c = 0; c < CPW; ++c) {
     const int col = col0 + c;
     if (col >= T.nrhs) break;
     double2* bg = reinterpret_cast<double2*>(T.b) + (size_t)col * T.ldb;
@@ -734,9 +734,12 @@ void dense_init() {
   set_smem_attr((const void*)k_cpqr);
   set_smem_attr((const void*)k_getrf);
   set_smem_attr((const void*)k_getrs);
-  set_smem_attr((const void*)k_getrs_reg<2>);
-  set_smem_attr((const void*)k_getrs_reg<4>);
-  set_smem_attr((const void*)k_getrs_reg<8>);
+  set_smem_attr((const void*)k_getrs_reg<2, 1>);
+  set_smem_attr((const void*)k_getrs_reg<4, 1>);
+  set_smem_attr((const void*)k_getrs_reg<8, 1>);
+  set_smem_attr((const void*)k_getrs_reg<2, kCpw>);
+  set_smem_attr((const void*)k_getrs_reg<4, kCpw>);
+  set_smem_attr((const void*)k_getrs_reg<8, kCpw>);
   done = true;
 }
 
@@ -760,25 +763,30 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
   if (n <= 0) return;
   k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
-int getrs_blocks(int nrhs, int max_n) {
-  const int per = max_n <= 256 ? kWarps * kCpw : kWarps;
+int getrs_cpw(int max_nrhs) { return max_nrhs <= kWarps ? 1 : kCpw; }
+int getrs_blocks(int nrhs, int max_n, int cpw) {
+  const int per = max_n <= 256 ? kWarps * cpw : kWarps;
   return (nrhs + per - 1) / per;
 }
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
-                  int n_blocks, cudaStream_t st, int smem_bytes, int max_n) {
+                  int n_blocks, cudaStream_t st, int smem_bytes, int max_n, int cpw) {
   if (n_blocks <= 0) return;
   // LU staged when it fits (smem_bytes covers the largest staged one);
   // 1 / U_kk always needs n slots
   const int bytes = std::max(smem_bytes, 16 * std::max(max_n, 1));
-  if (max_n <= 64)
-    k_getrs_reg<2><<<n_blocks, kThreads, size_t(bytes), st>>>(tasks, block_off, n_tasks, smem_bytes / 16);
-  else if (max_n <= 128)
-    k_getrs_reg<4><<<n_blocks, kThreads, size_t(bytes), st>>>(tasks, block_off, n_tasks, smem_bytes / 16);
-  else if (max_n <= 256)
-    k_getrs_reg<8><<<n_blocks, kThreads, size_t(bytes), st>>>(tasks, block_off, n_tasks, smem_bytes / 16);
-  else
-    k_getrs<<<n_blocks, kThreads, size_t(smem_bytes), st>>>(tasks, block_off, n_tasks,
-                                                            smem_bytes / 16);
+  const int cap = smem_bytes / 16;
+#define EBEM_GETRS(S, C) \
+  k_getrs_reg<S, C><<<n_blocks, kThreads, size_t(bytes), st>>>(tasks, block_off, n_tasks, cap)
+  if (max_n <= 64) {
+    if (cpw == 1) EBEM_GETRS(2, 1); else EBEM_GETRS(2, kCpw);
+  } else if (max_n <= 128) {
+    if (cpw == 1) EBEM_GETRS(4, 1); else EBEM_GETRS(4, kCpw);
+  } else if (max_n <= 256) {
+    if (cpw == 1) EBEM_GETRS(8, 1); else EBEM_GETRS(8, kCpw);
+  } else {
+    k_getrs<<<n_blocks, kThreads, size_t(smem_bytes), st>>>(tasks, block_off, n_tasks, cap);
+  }
+#undef EBEM_GETRS
 }
 
 int getrs_smem_bytes(int n) {

@@ -100,11 +100,12 @@ void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st);
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st);
 // CTAs per task for a batch whose largest LU has order max_n
-int getrs_blocks(int nrhs, int max_n);
+int getrs_cpw(int max_nrhs);  // right-hand sides per warp for a batch
+int getrs_blocks(int nrhs, int max_n, int cpw);
 // Blocked LU (ebem_lu.cu) of the tasks with in_smem == 0, in place.
 void launch_lu_blocked(const LuTask* tasks, int n_tasks, int max_n, cudaStream_t st);
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
-                  int n_blocks, cudaStream_t st, int smem_bytes, int max_n);
+                  int n_blocks, cudaStream_t st, int smem_bytes, int max_n, int cpw);
 // Dynamic shared memory that stages an n x n LU (0 when it does not fit).
 int getrs_smem_bytes(int n);
 int gemm_blocks(int m, int n);

@@ -1554,6 +1554,7 @@ namespace {
 // (shared by all tasks of the launch; larger tasks read L2).
 int g_getrs_smem = 0;
 int g_getrs_maxn = 0;
+int g_getrs_cpw = 1;
 
 template <class T, class F, class U>
 void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
@@ -1569,7 +1570,7 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
   if (total == 0) return;
   if (P.recorder) {
     P.recorder->add(id, t, boff, total, id == KP_GETRS ? g_getrs_smem : 0,
-                    id == KP_GETRS ? g_getrs_maxn : 0);
+                    id == KP_GETRS ? (g_getrs_maxn | (g_getrs_cpw << 16)) : 0);
     return;
   }
   Pack pk;
@@ -1609,7 +1610,7 @@ void Recorder::replay(cudaStream_t st, int phase) {
         break;
       case KP_GETRS:
         launch_getrs(Pack::at<LuSolveTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st,
-                     l.aux, l.aux2);
+                     l.aux, l.aux2 & 0xffff, l.aux2 >> 16);
         break;
       default:
         throw Error(EBEM_LOGIC_ERROR, "Recorder: unexpected kernel kind");
@@ -1630,18 +1631,20 @@ void run_gemms(Problem& P, const std::vector<GemmTask>& t) {
 namespace {
 void launch_getrs_staged(const LuSolveTask* t, const int* boff, int nt, int nb,
                          cudaStream_t st) {
-  launch_getrs(t, boff, nt, nb, st, g_getrs_smem, g_getrs_maxn);
+  launch_getrs(t, boff, nt, nb, st, g_getrs_smem, g_getrs_maxn, g_getrs_cpw);
 }
 }  // namespace
 
 void run_getrs(Problem& P, const std::vector<LuSolveTask>& t) {
-  int smem = 0, maxn = 0;
-  for (const LuSolveTask& x : t) maxn = std::max(maxn, x.n);
+  int smem = 0, maxn = 0, maxr = 0;
+  for (const LuSolveTask& x : t) maxn = std::max(maxn, x.n), maxr = std::max(maxr, x.nrhs);
+  const int cpw = getrs_cpw(maxr);
+  g_getrs_cpw = cpw;
   for (const LuSolveTask& x : t)
     if (maxn <= 256 || x.n > 0) smem = std::max(smem, getrs_smem_bytes(x.n));
   g_getrs_smem = smem;
   g_getrs_maxn = maxn;
-  run_blocked(P, t, [maxn](const LuSolveTask& s) { return s.n > 0 ? getrs_blocks(s.nrhs, maxn) : 0; },
+  run_blocked(P, t, [maxn, cpw](const LuSolveTask& s) { return s.n > 0 ? getrs_blocks(s.nrhs, maxn, cpw) : 0; },
               launch_getrs_staged, KP_GETRS,
               [](const LuSolveTask& s) { return 8.0 * s.n * double(s.n) * s.nrhs; });
 }
