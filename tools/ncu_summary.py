@@ -23,7 +23,9 @@ def launches(path, title=""):
         if r["Metric Name"] != "gpu__time_duration.sum":
             continue
         name = re.sub(r"\(.*", "", r["Kernel Name"]).replace("ebem_gpu::", "")
-        name = re.sub(r"<.*>", "", name)
+        name = name.replace("void ", "").replace("<unnamed>::", "")
+        name = name.replace("(anonymous namespace)::", "")
+        name = re.sub(r"<[^<>]*>$", "", name).strip()
         v = float(r["Metric Value"].replace(",", ""))
         scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(r["Metric Unit"], 1e-6)
         tot[name] += v * scale
