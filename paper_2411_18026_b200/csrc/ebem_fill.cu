@@ -11,6 +11,8 @@
 //                     (proj/src/assembly.cpp:373-407, :493-506)
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "ebem_device.cuh"
 #include "ebem_jobs.h"
 #include "ebem_kernels.h"
@@ -423,8 +425,7 @@ k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pa
 }
 
 // ------------------------------------------------------- symmetric near
-// Tier class of every sym pair (0..3 = far, far+2, far+5, far+9 points;
-// 7 = touching pair, handled by k_near_singular), for the bucketing sort.
+// Class of every near pair (kSymClasses, ebem_jobs.h), for the bucketing sort.
 __global__ void __launch_bounds__(256)
 k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
                const long long* __restrict__ job_off, int n_jobs,
@@ -442,11 +443,11 @@ k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
   const int N = ctx->n_nodes;
   const int na = ea + 1 == N ? 0 : ea + 1;
   const int nb = eb + 1 == N ? 0 : eb + 1;
-  unsigned char key = 7;
+  unsigned char key = kSymClasses - 1;  // skip
   if (!(ea == eb || na == eb || nb == ea) && !(J.tri && a >= q)) {
     const double hx = ef(ctx, EH, ea), hy = ef(ctx, EH, eb);
     const double rq = element_distance(ctx, ea, eb) / fmax(hx, hy);
-    key = rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3;
+    key = (rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3) + (J.onesided ? 4 : 0);
   }
   keys[p] = key;
   vals[p] = int(p);
@@ -462,31 +463,39 @@ constexpr int kSymMaxPairs = EBEM_SYM_THREADS;  // P = threads / n pairs per CTA
 #ifndef EBEM_SYM_MINB
 #define EBEM_SYM_MINB 1
 #endif
-template <int NT>
+template <int NT, bool BOTH>
 __global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
 k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
            const SymJob* __restrict__ jobs,
            const long long* __restrict__ job_off, int n_jobs,
-           const int* __restrict__ elems, const int* __restrict__ pair_ids,
-           int count, int n, double* __restrict__ bundles) {
+           const int* __restrict__ elems, const int* __restrict__ sorted_ids,
+           const int* __restrict__ class_bounds, int cls, int n,
+           double* __restrict__ bundles) {
   extern __shared__ double2 sh[];  // [P * n][8 V + 8 U cplx + 2 (Q as re/im pairs)]
   __shared__ SerSm S;
   __shared__ double sgx[kMaxGauss], sgw[kMaxGauss];
+  // this class's pairs, from the device-side bucket bounds (no host sync)
+  const int first = __ldg(class_bounds + cls);
+  const int count = __ldg(class_bounds + cls + 1) - first;
+  const int P = blockDim.x / n;
+  if ((int)blockIdx.x * P >= count) return;  // uniform per CTA
+  const int* __restrict__ pair_ids = sorted_ids + first;
   load_sersm(ctx, S);
   if (threadIdx.x < n) {
     sgx[threadIdx.x] = ctx->gx[gauss_offset(n) + threadIdx.x];
     sgw[threadIdx.x] = ctx->gw[gauss_offset(n) + threadIdx.x];
   }
-  const int P = blockDim.x / n;
   const int lp = threadIdx.x / n;
   const int i = threadIdx.x - lp * n;
-  const int idx = blockIdx.x * P + lp;
-  const bool active = lp < P && idx < count;
   const double* gx = sgx;
   const double* gw = sgw;
   // one job lookup per pair (not per thread), shared with the reduction
   __shared__ int s_ea[kSymMaxPairs], s_eb[kSymMaxPairs];
   __shared__ long long s_vd[kSymMaxPairs], s_ud[kSymMaxPairs];
+  // persistent CTAs stride over the class's pair groups
+  for (int base = blockIdx.x * P; base < count; base += gridDim.x * P) {
+  const int idx = base + lp;
+  const bool active = lp < P && idx < count;
   if (active && i == 0) {
     const long long p = __ldg(pair_ids + idx);
     const int jb = find_job(job_off, n_jobs, p);
@@ -540,14 +549,16 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
         axpy(rv[0][e], pt[0], k);
         axpy(rv[1][e], pt[1], k);
       }
-      // U: test on the cell element, trial on the enclosed element
-      // N_U = N_V^T (combine_N is symmetric under z -> -z, m <-> n, i <-> j)
-      combine_D(dn, -zhx, -zhy, nax, nay, dm);
+      if (BOTH) {
+        // U: test on the cell element, trial on the enclosed element
+        // N_U = N_V^T (combine_N is symmetric under z -> -z, m <-> n, i <-> j)
+        combine_D(dn, -zhx, -zhy, nax, nay, dm);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const cplx k = dm.a[e] + alpha * nm.a[(e >> 1) | ((e & 1) << 1)];
-        axpy(ru[0][e], pt[0], k);
-        axpy(ru[1][e], pt[1], k);
+        for (int e = 0; e < 4; ++e) {
+          const cplx k = dm.a[e] + alpha * nm.a[(e >> 1) | ((e & 1) << 1)];
+          axpy(ru[0][e], pt[0], k);
+          axpy(ru[1][e], pt[1], k);
+        }
       }
       // integrated-by-parts static hypersingular kernel (even in zh)
       const double lq = qfac * logr;
@@ -571,12 +582,13 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
   // reduction over i; each pair's first thread handles nothing special:
   // threads stride over (pair, orientation, 16 outputs)
   const cplx alpha = mk(fc.med.alpha_re, fc.med.alpha_im);
-  for (int o = threadIdx.x; o < P * 2 * kBundle; o += blockDim.x) {
-    const int lp2 = o / (2 * kBundle);
-    const int rem = o - lp2 * 2 * kBundle;
+  constexpr int kOrient = BOTH ? 2 : 1;
+  for (int o = threadIdx.x; o < P * kOrient * kBundle; o += blockDim.x) {
+    const int lp2 = o / (kOrient * kBundle);
+    const int rem = o - lp2 * kOrient * kBundle;
     const int orient = rem / kBundle;
     const int k = rem - orient * kBundle;  // bidx(la, lb, i, j)
-    const int idx2 = blockIdx.x * P + lp2;
+    const int idx2 = base + lp2;
     if (idx2 >= count) continue;
     const int la = k >> 3, lb = (k >> 2) & 1, e = k & 3;
     double ar = 0.0, ai = 0.0, qs = 0.0;
@@ -599,6 +611,8 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
     const double im = fma(hh, ai, sg * qs * alpha.im);
     const long long dst = orient == 0 ? s_vd[lp2] : s_ud[lp2];
     reinterpret_cast<double2*>(bundles)[dst * kBundle + k] = make_double2(re, im);
+  }
+  __syncthreads();  // shared row sums and pair records are reused
   }
 }
 
@@ -831,21 +845,38 @@ void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
 
 void launch_near_sym(const DevCtx* ctx, const FillConst& fc, int nt,
                      const SymJob* jobs, const long long* job_off, int n_jobs,
-                     const int* elems, const int* pair_ids, int count, int n,
-                     double* bundles, cudaStream_t st) {
-  if (count <= 0) return;
+                     const int* elems, const int* sorted_ids, const int* class_bounds,
+                     int cls, long long max_count, int n, bool both, double* bundles,
+                     cudaStream_t st) {
+  if (max_count <= 0) return;
   const int P = EBEM_SYM_THREADS / n;
   const int threads = P * n;
   const size_t smem = size_t(threads) * 18 * sizeof(double2);
-#define EBEM_SYM_CALL(N)                                                          \
-  do {                                                                            \
-    cudaFuncSetAttribute(k_near_sym<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         EBEM_SYM_THREADS * 18 * (int)sizeof(double2));           \
-    k_near_sym<N><<<(count + P - 1) / P, threads, smem, st>>>(                    \
-        ctx, fc, jobs, job_off, n_jobs, elems, pair_ids, count, n, bundles);       \
+  // persistent grid: a few CTAs per SM, never more than the largest count needs
+  static const int n_sm = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  const long long need = (max_count + P - 1) / P;
+  const int grid = int(std::min<long long>(need, 4LL * n_sm));
+#define EBEM_SYM_LAUNCH(N, B)                                                       \
+  do {                                                                              \
+    cudaFuncSetAttribute(k_near_sym<N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         EBEM_SYM_THREADS * 18 * (int)sizeof(double2));             \
+    k_near_sym<N, B><<<grid, threads, smem, st>>>(ctx, fc, jobs, job_off, n_jobs,     \
+                                                  elems, sorted_ids, class_bounds, cls, \
+                                                  n, bundles);                      \
+  } while (0)
+#define EBEM_SYM_CALL(N)                  \
+  do {                                    \
+    if (both) EBEM_SYM_LAUNCH(N, true);   \
+    else EBEM_SYM_LAUNCH(N, false);       \
   } while (0)
   EBEM_NT_DISPATCH(fill_nt_bucket(nt), EBEM_SYM_CALL)
 #undef EBEM_SYM_CALL
+#undef EBEM_SYM_LAUNCH
 }
 
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,

@@ -49,13 +49,19 @@ struct ProxyJob {
 // U bundle (test E[q], trial A[a]) at u_off + q * nA + a.
 // tri = 1 (a diagonal block, A == E, u_off == v_off): only pairs a < q are
 // evaluated; the U bundle of (a, q) is the V bundle of (q, a).
+// onesided = 1 (a plain true_block(rows = A, cols = E)): V bundles only.
 struct SymJob {
   long long v_off, u_off;
   long long local_off;  // first pair of this job in the wave's sym numbering
   int a_off, nA;
   int e_off, nE;
-  int tri, pad;
+  int tri, onesided;
 };
+
+// Near-pair classes of the bucketing sort: tier (0..3 = far, far+2, far+5,
+// far+9 points) + 4 for one-sided jobs; the last class is "skip" (touching
+// pairs, handled by k_near_singular, and the lower triangle of tri jobs).
+constexpr int kSymClasses = 9;
 
 // Scatter of bundles into one output block.
 struct GatherJob {

@@ -106,13 +106,39 @@ void Profiler::end(int id, cudaStream_t st, double u) {
   if (!on || !cur_) return;
   cudaEvent_t b = ev();
   CK(cudaEventRecord(b, st));
-  pending_.push_back(Rec{id, cur_, b, u});
+  pending_.push_back(Rec{id, cur_, b, u, -1});
+  cur_ = nullptr;
+}
+
+void Profiler::end_counted(int id, cudaStream_t st, const int* dev_bounds, double mult) {
+  ++g_launches;
+  if (!on || !cur_) return;
+  cudaEvent_t b = ev();
+  CK(cudaEventRecord(b, st));
+  if (counts_used_ == counts_cap_) {  // pinned pairs, grown by doubling
+    int* nc = nullptr;
+    const int cap = counts_cap_ ? 2 * counts_cap_ : 256;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&nc), sizeof(int) * 2 * cap));
+    if (counts_) {
+      CK(cudaStreamSynchronize(st));
+      std::memcpy(nc, counts_, sizeof(int) * 2 * counts_used_);
+      CK(cudaFreeHost(counts_));
+    }
+    counts_ = nc;
+    counts_cap_ = cap;
+  }
+  const int slot = counts_used_++;
+  CK(cudaMemcpyAsync(counts_ + 2 * slot, dev_bounds, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  pending_.push_back(Rec{id, cur_, b, mult, slot});
   cur_ = nullptr;
 }
 
 void Profiler::collect() {
   if (pending_.empty() && !near_points) return;
   CK(cudaDeviceSynchronize());
+  for (Rec& r : pending_)
+    if (r.slot >= 0) r.units *= double(counts_[2 * r.slot + 1] - counts_[2 * r.slot]);
+  counts_used_ = 0;
   for (size_t k = 0; k < pending_.size(); ++k) {
     const Rec& r = pending_[k];
     float t = 0.f;
@@ -572,6 +598,7 @@ int planning_threads() { return plan_pool().size(); }
 
 // ---------------------------------------------------------------- FillPlan
 void FillPlan::clear() {
+  has_one_sided_ = has_two_sided_ = false;
   bundles_ = near_pairs_ = entries_ = 0;
   sym_pairs_ = 0;
   sym_.clear();
@@ -635,6 +662,8 @@ void FillPlan::append(const FillPlan& o) {
   sym_pairs_ += o.sym_pairs_;
   entries_ += o.entries_;
   proxy_blocks_ += o.proxy_blocks_;
+  has_one_sided_ = has_one_sided_ || o.has_one_sided_;
+  has_two_sided_ = has_two_sided_ || o.has_two_sided_;
   // o's polygon descriptors were copied with its descriptors; this plan's own
   // (if any) stay where they are
 }
@@ -731,18 +760,24 @@ void FillPlan::add_true_block(const Lists& rows, const Lists& cols,
   std::vector<int> res, ces;
   elements_of(rows, res);
   elements_of(cols, ces);
-  NearJob J;
-  J.pair_off = bundles_;
-  J.res_off = int(elems_.size());
-  J.nres = int(res.size());
+  // a one-sided job of the near-field kernel: test = row elements (A),
+  // trial = column elements (E), bundle (a, q) at v_off + a nE + q
+  SymJob J;
+  J.tri = 0;
+  J.onesided = 1;
+  has_one_sided_ = true;
+  J.nA = int(res.size());
+  J.nE = int(ces.size());
+  J.a_off = int(elems_.size());
   elems_.insert(elems_.end(), res.begin(), res.end());
-  J.ces_off = int(elems_.size());
-  J.nces = int(ces.size());
+  J.e_off = int(elems_.size());
   elems_.insert(elems_.end(), ces.begin(), ces.end());
-  near_.push_back(J);
-  near_local_.push_back(near_pairs_);
-  const long long np = (long long)J.nres * J.nces;
-  near_pairs_ += np;
+  const long long np = (long long)J.nA * J.nE;
+  J.v_off = J.u_off = bundles_;
+  J.local_off = sym_pairs_;
+  sym_.push_back(J);
+  sym_off_.push_back(sym_pairs_);
+  sym_pairs_ += np;
   // touching pairs (coincident / adjacent) go to the singular kernel;
   // search from the shorter element list into the longer one
   const bool rows_short = res.size() <= ces.size();
@@ -756,16 +791,16 @@ void FillPlan::add_true_block(const Lists& rows, const Lists& cols,
       if (it != lg.end() && *it == c) {
         const int j = int(it - lg.begin());
         const int ra = rows_short ? i : j, cb = rows_short ? j : i;
-        sing_pair_.push_back(J.pair_off + (long long)ra * J.nces + cb);
+        sing_pair_.push_back(J.v_off + (long long)ra * J.nE + cb);
         sing_elems_.push_back(res[ra]);
         sing_elems_.push_back(ces[cb]);
       }
     }
   }
   GatherJob G;
-  G.pair_off = J.pair_off;
+  G.pair_off = J.v_off;
   G.entry_off = entries_;
-  G.nces = J.nces;
+  G.nces = J.nE;
   G.rdesc_off = int(desc_.size());
   node_descs(rows, res, drow, desc_);
   G.nrows = nr;
@@ -796,7 +831,8 @@ void FillPlan::add_sym_near(const std::vector<int>& enc, const Lists& rows,
   elements_of(both, E);
   SymJob J;
   J.tri = 0;
-  J.pad = 0;
+  J.onesided = 0;
+  has_two_sided_ = true;
   J.nA = int(A.size());
   J.nE = int(E.size());
   J.a_off = int(elems_.size());
@@ -881,7 +917,8 @@ void FillPlan::add_sym_diag(const std::vector<int>& nodes, double* dest,
   elements_of(L, E);
   SymJob J;
   J.tri = 1;
-  J.pad = 0;
+  J.onesided = 0;
+  has_two_sided_ = true;
   J.nA = J.nE = int(E.size());
   J.a_off = J.e_off = int(elems_.size());
   elems_.insert(elems_.end(), E.begin(), E.end());
@@ -1078,9 +1115,6 @@ void Problem::execute(FillPlan& plan) {
     launch_sym_classify(dctx(), sj, so, int(plan.sym_.size()), el, nsym, kin, vin, st_);
     sort_pairs_by_class(kin, kout, vin, vout, nsym, &sort_temp_, &sort_temp_bytes_, st_);
     launch_class_bounds(kout, nsym, sym_bounds_.get(), st_);
-    CK(cudaMemcpyAsync(sym_bounds_host_, sym_bounds_.get(), 9 * sizeof(int),
-                       cudaMemcpyDeviceToHost, st_));
-    CK(cudaEventRecord(sym_ev_, st_));
     g_launches += 3;
   }
   if (!plan.proxy_.empty()) {
@@ -1102,21 +1136,24 @@ void Problem::execute(FillPlan& plan) {
     g_prof.end(KP_NEAR_SEP, st_, 0.0);
   }
   if (nsym > 0) {
-    CK(cudaEventSynchronize(sym_ev_));
-    int bnd[9];
-    std::memcpy(bnd, sym_bounds_host_, sizeof(bnd));
+    // one launch per class, sized by the wave's pair count; each reads its
+    // range from the device-side bounds (no host round trip)
     const int add[4] = {0, 2, 5, 9};
     const int* vout = sym_vals_.get() + nsym;
-    for (int c = 0; c < 4; ++c) {
-      const int cnt = bnd[c + 1] - bnd[c];
-      if (cnt <= 0) continue;
-      const int nq = int((acfg_.far_nodes + add[c]) * acfg_.refine + 0.5);
+    for (int c = 0; c < kSymClasses - 1; ++c) {  // the last class is "skip"
+      const int tier = c & 3;
+      const bool both = c < 4;  // classes 4..7: one-sided true blocks
+      if (both ? !plan.has_two_sided_ : !plan.has_one_sided_) continue;
+      const int nq = int((acfg_.far_nodes + add[tier]) * acfg_.refine + 0.5);
       g_prof.begin(st_);
-      launch_near_sym(dctx(), fc_, fc_nt_, sj, so, int(plan.sym_.size()), el, vout + bnd[c], cnt,
-                      nq, bundles.get(), st_);
-      g_prof.end(KP_NEAR_SYM, st_, double(cnt) * nq * nq);
+      launch_near_sym(dctx(), fc_, fc_nt_, sj, so, int(plan.sym_.size()), el, vout,
+                      sym_bounds_.get(), c, nsym, nq, both, bundles.get(), st_);
+      // points = class count x nq^2, read back at collect time
+      g_prof.end_counted(both ? KP_NEAR_SYM : KP_NEAR_SEP, st_, sym_bounds_.get() + c,
+                         double(nq) * nq);
     }
   }
+
   if (!plan.sing_pair_.empty()) {
     g_prof.begin(st_);
     launch_near_singular(dctx(), Pack::at<long long>(base, o_sp),
@@ -1813,48 +1850,30 @@ void Fds::build() {
     const int f = first(level), L = last(level);
     const int nlev = L - f + 1;
     Store& S = store_[level];
-    // ---- bases of every cell of the level
-    std::vector<BasisReq> req(nlev);
-    for (int c = f; c <= L; ++c)
-      req[c - f] = BasisReq{&cells_[c].jrow, &cells_[c].jcol, cells_[c].begin, cells_[c].end};
-    std::vector<BasisRes> br;
-    DBuf<double>& ubuf = ubuf_;
-    const double tb = now();
-    if (hs_) host_bases(level, br, S.v, ubuf);
-    else P_.bases(req, cfg_.epsilon, br, S.v, ubuf);
-    PhaseTimer t_after("level_after_bases", nullptr);
-    basis_seconds += now() - tb;
-    // ---- diagonal blocks (leaf: exact; above: reduced) into the LU arena
-    size_t lu_total = 0, piv_total = 0, au_total = 0, at_total = 0;
-    std::vector<size_t> lu_off(nlev), piv_off(nlev), au_off(nlev), at_off(nlev);
+    // ---- diagonal blocks (leaf: exact; above: reduced from the children's
+    // skeletons and Atilde) into the LU arena, and their LU.  They depend on
+    // level+1 only, so they are enqueued before this level's bases: the GPU
+    // fills and factors them while the host plans the interaction fill.
+    size_t lu_total = 0, piv_total = 0;
+    std::vector<size_t> lu_off(nlev), piv_off(nlev);
     for (int i = 0; i < nlev; ++i) {
-      Cell& C = cells_[f + i];
-      C.k = br[i].k;
-      C.srow = br[i].srow;
-      C.scol = br[i].scol;
+      const Cell& C = cells_[f + i];
       lu_off[i] = lu_total;
       lu_total += size_t(2 * C.nloc) * (2 * C.nloc);
       piv_off[i] = piv_total;
       piv_total += 2 * C.nloc;
-      au_off[i] = au_total;
-      au_total += size_t(2 * C.nloc) * (2 * C.k);
-      at_off[i] = at_total;
-      at_total += size_t(2 * C.k) * (2 * C.k);
-      stats_.max_rank[level] = std::max(stats_.max_rank[level], C.k);
-      stats_.saturated = stats_.saturated || br[i].saturated;
     }
     S.lu.alloc(2 * lu_total + 2);
     S.ipiv.alloc(piv_total + 1);
-    S.ainv_u.alloc(2 * au_total + 2);
-    S.atilde.alloc(2 * at_total + 2);
     for (int i = 0; i < nlev; ++i) {
       Cell& C = cells_[f + i];
       C.lu = S.lu.get() + 2 * lu_off[i];
       C.ipiv = S.ipiv.get() + piv_off[i];
-      C.ainv_u = S.ainv_u.get() + 2 * au_off[i];
-      C.atilde = S.atilde.get() + 2 * at_off[i];
-      C.v = S.v.get() + 2 * br[i].v_off;
     }
+    // A host BlockSource sees the reference's callback order (cell_basis of
+    // a cell before its diagonal block, fds.cpp:77-89), so for it this
+    // step runs after the bases.
+    auto diagonal_and_lu = [&]() {
     {
       PhaseTimer tp("fill_diagonal", P_.stream());
       FillPlan plan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
@@ -1899,9 +1918,8 @@ void Fds::build() {
       }
       P_.execute(plan);
       run_copies(P_, copies);
-      P_.check_domain();
+      // element-length guard: read at the bases' synchronisation below
     }
-    // ---- LU of the diagonal blocks
     {
       PhaseTimer tp("merge_getrf", P_.stream());
       std::vector<LuTask> lt;
@@ -1916,6 +1934,42 @@ void Fds::build() {
       }
       for (LuTask& t : lt) t.info = lu_info(t.n);
       run_getrf(P_, lt);
+    }
+    };
+    if (!hs_) diagonal_and_lu();
+    // ---- bases of every cell of the level
+    std::vector<BasisReq> req(nlev);
+    for (int c = f; c <= L; ++c)
+      req[c - f] = BasisReq{&cells_[c].jrow, &cells_[c].jcol, cells_[c].begin, cells_[c].end};
+    std::vector<BasisRes> br;
+    DBuf<double>& ubuf = ubuf_;
+    const double tb = now();
+    if (hs_) host_bases(level, br, S.v, ubuf);
+    else P_.bases(req, cfg_.epsilon, br, S.v, ubuf);
+    PhaseTimer t_after("level_after_bases", nullptr);
+    basis_seconds += now() - tb;
+    if (hs_) diagonal_and_lu();
+    size_t au_total = 0, at_total = 0;
+    std::vector<size_t> au_off(nlev), at_off(nlev);
+    for (int i = 0; i < nlev; ++i) {
+      Cell& C = cells_[f + i];
+      C.k = br[i].k;
+      C.srow = br[i].srow;
+      C.scol = br[i].scol;
+      au_off[i] = au_total;
+      au_total += size_t(2 * C.nloc) * (2 * C.k);
+      at_off[i] = at_total;
+      at_total += size_t(2 * C.k) * (2 * C.k);
+      stats_.max_rank[level] = std::max(stats_.max_rank[level], C.k);
+      stats_.saturated = stats_.saturated || br[i].saturated;
+    }
+    S.ainv_u.alloc(2 * au_total + 2);
+    S.atilde.alloc(2 * at_total + 2);
+    for (int i = 0; i < nlev; ++i) {
+      Cell& C = cells_[f + i];
+      C.ainv_u = S.ainv_u.get() + 2 * au_off[i];
+      C.atilde = S.atilde.get() + 2 * at_off[i];
+      C.v = S.v.get() + 2 * br[i].v_off;
     }
     // ---- A^-1 U with U = blockdiag(u0, u1)
     {

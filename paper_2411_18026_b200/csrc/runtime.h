@@ -49,6 +49,8 @@ class Profiler {
   bool on = false;
   void begin(cudaStream_t st);
   void end(int id, cudaStream_t st, double units);
+  // units = mult x (dev_bounds[1] - dev_bounds[0]), read back at collect()
+  void end_counted(int id, cudaStream_t st, const int* dev_bounds, double mult);
   void collect();
   void reset();
   double ms[KP_COUNT] = {};
@@ -58,7 +60,9 @@ class Profiler {
   unsigned long long* near_points = nullptr;  // device counter (on only)
 
  private:
-  struct Rec { int id; cudaEvent_t a, b; double units; };
+  struct Rec { int id; cudaEvent_t a, b; double units; int slot; };
+  int* counts_ = nullptr;  // pinned (first, last) pairs of end_counted
+  int counts_used_ = 0, counts_cap_ = 0;
   std::vector<Rec> pending_;
   std::vector<cudaEvent_t> pool_;
   cudaEvent_t cur_ = nullptr;
@@ -393,6 +397,7 @@ class FillPlan {
   void add_sym_diag(const std::vector<int>& nodes, double* dest, int ld);
   long long bundles() const { return bundles_; }
   bool empty() const { return gather_.empty(); }
+  bool has_one_sided_ = false, has_two_sided_ = false;  // kinds of near jobs
   void clear();
   // Appends another plan (built independently, e.g. on another host thread)
   // with its element, bundle, pair, descriptor and entry offsets relocated.
