@@ -89,10 +89,6 @@ long long ebem_gpu_launch_count(void) { return g_launches.load(); }
 int ebem_gpu_prof_enable(int on) {
   return guarded([&] {
     g_prof.collect();
-    if (on && !g_prof.near_points) {
-      CK(cudaMalloc(reinterpret_cast<void**>(&g_prof.near_points), 8));
-      CK(cudaMemset(g_prof.near_points, 0, 8));
-    }
     g_prof.on = on != 0;
   });
 }

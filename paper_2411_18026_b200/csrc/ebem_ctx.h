@@ -40,13 +40,10 @@ struct ParSeries {
   double2 b[10][kParTerms];
 };
 
-// Fill-kernel parameter block (passed by value as a __grid_constant__
-// kernel argument): medium constants + the D/N remainder series (scalars
-// d1 d2 d3 n1 n2 n4 n5 n7) as coefficients of u^p, u = r^2.
+// Fill-kernel parameter block, passed by value as a __grid_constant__ kernel
+// argument: the medium constants are then constant-bank operands.
 struct FillConst {
   DevMedium med;
-  double2 a[8][kParTerms];
-  double2 b[8][kParTerms];
 };
 
 // Element geometry, structure of arrays over the N elements (element e runs

@@ -373,13 +373,11 @@ __device__ __forceinline__ void q0_kernel(double qfactor, double r, double zx,
 // only G, which the Burton-Miller operator never uses.  One ln r per point
 // serves the series branch, the Hankel small-argument log terms and q0.
 
-// D/N series (scalars 2..9) staged in shared memory once per CTA.
+// D/N series (scalars 2..9) staged in shared memory once per CTA, one row
+// of 8 coefficients per power (d-series carry odd powers, n-series even
+// powers; parity checked on the host).
 struct SerSm {
-  int par[8], nt[8];
   int ntmax;
-  double2 a[8][kParTerms];
-  double2 b[8][kParTerms];
-  // transposed copies for the joint evaluation (8 coefficients per power)
   double2 at[kParTerms][8];
   double2 bt[kParTerms][8];
 };
@@ -389,14 +387,8 @@ __device__ __forceinline__ void load_sersm(const DevCtx* __restrict__ ctx, SerSm
   const int nth = blockDim.x * blockDim.y;
   for (int i = tid; i < 8 * kParTerms; i += nth) {
     const int k = i / kParTerms, p = i - k * kParTerms;
-    s.a[k][p] = ctx->pser.a[k + 2][p];
-    s.b[k][p] = ctx->pser.b[k + 2][p];
     s.at[p][k] = ctx->pser.a[k + 2][p];
     s.bt[p][k] = ctx->pser.b[k + 2][p];
-  }
-  if (tid < 8) {
-    s.par[tid] = ctx->pser.par[tid + 2];
-    s.nt[tid] = ctx->pser.nt[tid + 2];
   }
   if (tid == 0) {
     int m = 0;
@@ -409,20 +401,6 @@ struct DN {
   cplx d[3];  // d1, d2, d3
   cplx n[5];  // n1, n2, n4, n5, n7
 };
-
-// sum_p (a_p + b_p ln r) u^p * r^par, Horner in u = r^2.
-__device__ __forceinline__ cplx par_series(const SerSm& S, int k, double u,
-                                           double logr, double r) {
-  const int nt = S.nt[k];
-  cplx A = mk(0.0), B = mk(0.0);
-  for (int p = nt - 1; p >= 0; --p) {
-    const double2 a = S.a[k][p], b = S.b[k][p];
-    A = mk(fma(A.re, u, a.x), fma(A.im, u, a.y));
-    B = mk(fma(B.re, u, b.x), fma(B.im, u, b.y));
-  }
-  cplx v = mk(fma(B.re, logr, A.re), fma(B.im, logr, A.im));
-  return S.par[k] ? v * r : v;
-}
 
 // H0, H1 with ln(x/2) supplied by the caller (small-argument branch).
 __device__ __forceinline__ void hankel01_lg(double x, double log_half_x,
@@ -442,10 +420,8 @@ __device__ __forceinline__ void hankel01_lg(double x, double log_half_x,
   hankel01(x, h0, h1);
 }
 
-// kRem = false: full d and n (proxy blocks, kernel_cross_block);
-// kRem = true: full d, remainder n (PairIntegrator::separated).
-// All eight series at once: one loop over powers, 16 independent Horner
-// chains (d-series odd powers, n-series even powers).
+// All eight remainder series at once: one loop over powers, 16 independent
+// Horner chains in u = r^2.
 __device__ __forceinline__ void series_joint(const SerSm& S, double u,
                                              double logr, double r, DN& o) {
   cplx A[8], B[8];
@@ -467,44 +443,31 @@ __device__ __forceinline__ void series_joint(const SerSm& S, double u,
     o.n[k] = mk(fma(B[3 + k].re, logr, A[3 + k].re), fma(B[3 + k].im, logr, A[3 + k].im));
 }
 
-#ifndef EBEM_JOINT_SERIES
-#define EBEM_JOINT_SERIES 1
-#endif
-
+// The scalars of one point.  kRem = false: full d and n (proxy blocks,
+// kernel_cross_block); kRem = true: full d, remainder n
+// (PairIntegrator::separated).  The medium constants come from the
+// __grid_constant__ FillConst kernel parameter (constant-bank operands).
 template <bool kRem>
-__device__ __forceinline__ void dn_eval(const DevMedium& m, const SerSm& S,
+__device__ __forceinline__ void dn_eval(const FillConst& fc, const SerSm& S,
                                         double r, double ir, double logr,
                                         DN& o) {
+  const DevMedium& m = fc.med;
   const double ir2 = ir * ir;
   if (r < m.series_radius) {
-    const double u = r * r;
-#if EBEM_JOINT_SERIES
-    series_joint(S, u, logr, r, o);
+    series_joint(S, r * r, logr, r, o);
     o.d[0].re += m.sd1 * ir;
     o.d[1].re -= m.sd1 * ir;
     o.d[2].re += m.sd3 * ir;
+    if (!kRem) {
 #pragma unroll
-    for (int k = 0; k < 5; ++k)
-      if (!kRem) o.n[k].re += m.sn[k] * ir2;
-    return;
-#endif
-#pragma unroll
-    for (int k = 0; k < 3; ++k) o.d[k] = par_series(S, k, u, logr, r);
-    o.d[0].re += m.sd1 * ir;
-    o.d[1].re -= m.sd1 * ir;
-    o.d[2].re += m.sd3 * ir;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      o.n[k] = par_series(S, 3 + k, u, logr, r);
-      if (!kRem) o.n[k].re += m.sn[k] * ir2;
+      for (int k = 0; k < 5; ++k) o.n[k].re += m.sn[k] * ir2;
     }
     return;
   }
   const double kT = m.kT, kL = m.kL, mu = m.mu, ar = m.aratio;
-  const double zT = kT * r, zL = kL * r;
   cplx h0T, h1T, h0L, h1L;
-  hankel01_lg(zT, logr + m.log_half_kT, h0T, h1T);
-  hankel01_lg(zL, logr + m.log_half_kL, h0L, h1L);
+  hankel01_lg(kT * r, logr + m.log_half_kT, h0T, h1T);
+  hankel01_lg(kL * r, logr + m.log_half_kL, h0L, h1L);
   auto i4 = [](cplx z) { return mk(-0.25 * z.im, 0.25 * z.re); };
   const double izT = ir * m.inv_kT, izL = ir * m.inv_kL;
   const cplx chiL = i4(h0L);
@@ -575,161 +538,6 @@ __device__ __forceinline__ void combine_N(const DN& s, double zx, double zy,
       out.a[2 * i + j] = s.n[0] * c1 + s.n[1] * c2 + s.n[2] * c4 +
                          s.n[3] * c5 + s.n[4] * c7;
     }
-  }
-}
-
-// ------------------------------------------------ kernel-parameter tables
-// The medium constants and the eight D/N remainder series travel as a
-// __grid_constant__ kernel parameter: fully unrolled loops then read every
-// coefficient as a constant-bank operand of the DFMA (no loads, no loop).
-// d-series carry odd powers, n-series even powers (checked on the host).
-
-// Joint Horner of the 8 series in u = r^2: 16 independent chains.
-template <int NT>
-__device__ __forceinline__ void series8(const FillConst& fc, double u,
-                                        double logr, double r, DN& o) {
-  cplx A[8], B[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    A[k] = mk(fc.a[k][NT - 1].x, fc.a[k][NT - 1].y);
-    B[k] = mk(fc.b[k][NT - 1].x, fc.b[k][NT - 1].y);
-  }
-#pragma unroll
-  for (int p = NT - 2; p >= 0; --p) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      A[k] = mk(fma(A[k].re, u, fc.a[k][p].x), fma(A[k].im, u, fc.a[k][p].y));
-      B[k] = mk(fma(B[k].re, u, fc.b[k][p].x), fma(B[k].im, u, fc.b[k][p].y));
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    o.d[k] = r * mk(fma(B[k].re, logr, A[k].re), fma(B[k].im, logr, A[k].im));
-#pragma unroll
-  for (int k = 0; k < 5; ++k)
-    o.n[k] = mk(fma(B[3 + k].re, logr, A[3 + k].re), fma(B[3 + k].im, logr, A[3 + k].im));
-}
-
-// Both Hankel pairs (k_T r and k_L r) with interleaved Clenshaw chains when
-// both arguments are in the small range (k_L < k_T, so z_L < z_T always).
-__device__ __forceinline__ void hankel_pair(double zT, double zL, double logr,
-                                            const DevMedium& m, cplx& h0T,
-                                            cplx& h1T, cplx& h0L, cplx& h1L) {
-  if (zT <= 8.0) {
-    const double qT = zT * 0.125, qL = zL * 0.125;
-    const double yT = 2.0 * (qT * qT) - 1.0, yL = 2.0 * (qL * qL) - 1.0;
-    const double y2T = 2.0 * yT, y2L = 2.0 * yL;
-    double b1[8] = {0, 0, 0, 0, 0, 0, 0, 0}, b2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    constexpr int NMAX = 18;
-#pragma unroll
-    for (int j = NMAX - 1; j >= 1; --j) {
-      const double cj[4] = {j < kJ0SmallN ? kJ0Small[j] : 0.0,
-                            j < kJ1SmallN ? kJ1Small[j] : 0.0,
-                            j < kV0SmallN ? kV0Small[j] : 0.0,
-                            j < kV1SmallN ? kV1Small[j] : 0.0};
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const double y2 = c < 4 ? y2T : y2L;
-        const double t = fma(y2, b1[c], cj[c & 3] - b2[c]);
-        b2[c] = b1[c];
-        b1[c] = t;
-      }
-    }
-    double v[8];
-    const double c0[4] = {kJ0Small[0], kJ1Small[0], kV0Small[0], kV1Small[0]};
-#pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = fma(c < 4 ? yT : yL, b1[c], c0[c & 3] - b2[c]);
-    const double lgT = kTwoOverPi * (logr + m.log_half_kT + kEulerGamma);
-    const double lgL = kTwoOverPi * (logr + m.log_half_kL + kEulerGamma);
-    const double j1T = v[1] * zT, j1L = v[5] * zL;
-    h0T = mk(v[0], fma(lgT, v[0], v[2]));
-    h1T = mk(j1T, v[3] * zT + lgT * j1T - kTwoOverPi / zT);
-    h0L = mk(v[4], fma(lgL, v[4], v[6]));
-    h1L = mk(j1L, v[7] * zL + lgL * j1L - kTwoOverPi / zL);
-    return;
-  }
-  hankel01(zT, h0T, h1T);
-  hankel01_lg(zL, logr + m.log_half_kL, h0L, h1L);
-}
-
-#ifndef EBEM_SERIES_PARAM
-#define EBEM_SERIES_PARAM 0
-#endif
-#ifndef EBEM_HANKEL_PAIR
-#define EBEM_HANKEL_PAIR 0
-#endif
-
-template <bool kRem, int NT>
-__device__ __forceinline__ void dn_eval2(const FillConst& fc, const SerSm& S,
-                                         double r, double ir, double logr,
-                                         DN& o) {
-  const DevMedium& m = fc.med;
-  const double ir2 = ir * ir;
-  if (r < m.series_radius) {
-#if EBEM_SERIES_PARAM
-    series8<NT>(fc, r * r, logr, r, o);
-#elif EBEM_JOINT_SERIES
-    series_joint(S, r * r, logr, r, o);
-#else
-    const double u = r * r;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) o.d[k] = par_series(S, k, u, logr, r);
-#pragma unroll
-    for (int k = 0; k < 5; ++k) o.n[k] = par_series(S, 3 + k, u, logr, r);
-#endif
-    o.d[0].re += m.sd1 * ir;
-    o.d[1].re -= m.sd1 * ir;
-    o.d[2].re += m.sd3 * ir;
-    if (!kRem) {
-#pragma unroll
-      for (int k = 0; k < 5; ++k) o.n[k].re += m.sn[k] * ir2;
-    }
-    return;
-  }
-  const double kT = m.kT, kL = m.kL, mu = m.mu, ar = m.aratio;
-  cplx h0T, h1T, h0L, h1L;
-#if EBEM_HANKEL_PAIR
-  hankel_pair(kT * r, kL * r, logr, m, h0T, h1T, h0L, h1L);
-#else
-  hankel01_lg(kT * r, logr + m.log_half_kT, h0T, h1T);
-  hankel01_lg(kL * r, logr + m.log_half_kL, h0L, h1L);
-#endif
-  auto i4 = [](cplx z) { return mk(-0.25 * z.im, 0.25 * z.re); };
-  const double izT = ir * m.inv_kT, izL = ir * m.inv_kL;
-  const cplx chiL = i4(h0L);
-  const cplx chiT1 = -(kT * i4(h1T));
-  const cplx chiL1 = -(kL * i4(h1L));
-  const cplx chiT2 = -(kT * kT) * i4(h0T - h1T * izT);
-  const cplx chiL2 = -(kL * kL) * i4(h0L - h1L * izL);
-  const cplx chiT3 = -(kT * kT * kT) * i4(-h1T - h0T * izT + (2.0 * izT * izT) * h1T);
-  const cplx chiL3 = -(kL * kL * kL) * i4(-h1L - h0L * izL + (2.0 * izL * izL) * h1L);
-  const cplx chiT4 = -(kT * kT * kT * kT) *
-                     i4(-h0T + (2.0 * izT) * h1T + (3.0 * izT * izT) * h0T -
-                        (6.0 * izT * izT * izT) * h1T);
-  const cplx chiL4 = -(kL * kL * kL * kL) *
-                     i4(-h0L + (2.0 * izL) * h1L + (3.0 * izL * izL) * h0L -
-                        (6.0 * izL * izL * izL) * h1L);
-  const double ikT2 = m.inv_kT * m.inv_kT;
-  const cplx psi1 = (chiT1 - chiL1) * ikT2;
-  const cplx psi2 = (chiT2 - chiL2) * ikT2;
-  const cplx psi3 = (chiT3 - chiL3) * ikT2;
-  const cplx psi4 = (chiT4 - chiL4) * ikT2;
-  const cplx gchi = psi2 - psi1 * ir;
-  const cplx w = gchi * ir;
-  const cplx gam = gchi * ir2;
-  const cplx bet = (psi3 - 3.0 * w) * ir;
-  const cplx alf = psi4 - (6.0 * ir) * psi3 + 15.0 * gam;
-  o.d[0] = ar * chiL1 + 2.0 * w;
-  o.d[1] = chiT1 + 2.0 * w;
-  o.d[2] = 2.0 * (psi3 - 3.0 * w);
-  o.n[0] = (-2.0 * mu * ir) * chiT1 - (4.0 * mu) * gam;
-  o.n[1] = (-mu) * (chiT2 - chiT1 * ir) - (4.0 * mu) * bet;
-  o.n[2] = (-4.0 * mu) * alf;
-  o.n[3] = m.c_n5 * chiL - (4.0 * mu * ar * ir) * chiL1 - (4.0 * mu) * gam;
-  o.n[4] = (-2.0 * mu * ar) * (chiL2 - chiL1 * ir) - (4.0 * mu) * bet;
-  if (kRem) {
-#pragma unroll
-    for (int k = 0; k < 5; ++k) o.n[k].re -= m.sn[k] * ir2;
   }
 }
 

@@ -2,9 +2,12 @@
 //   k_proxy_pairs     proxy polygon <-> curve element pairs, n_g x n_g Gauss,
 //                     full kernel, both orientations from one scalar
 //                     evaluation (kernel_cross_block, proj/src/assembly.cpp:424-509)
-//   k_near_separated  exact Galerkin pairs, tiered tensor Gauss with the
+//   k_sym_classify    quadrature-tier class of every near element pair
+//   k_near_sym        separated element pairs, tiered tensor Gauss with the
 //                     static hypersingular part integrated by parts
-//                     (PairIntegrator::separated, proj/src/assembly.cpp:248-286)
+//                     (PairIntegrator::separated, proj/src/assembly.cpp:248-286);
+//                     both near blocks of a cell from one evaluation, or one
+//                     orientation for plain true blocks
 //   k_near_singular   coincident (closed form + integrated series) and
 //                     adjacent (Duffy) pairs (proj/src/assembly.cpp:70-246)
 //   k_gather          ordered scatter of bundles into output blocks
@@ -87,112 +90,6 @@ __device__ __forceinline__ int bidx(int la, int lb, int i, int j) {
 }
 
 }  // namespace
-
-// --------------------------------------------------------------- separated
-// One thread per element pair.  Pairs that touch (coincident / adjacent) are
-// skipped here and produced by k_near_singular.
-#ifndef EBEM_NEAR_MINB
-#define EBEM_NEAR_MINB 2
-#endif
-template <int NT>
-__global__ void __launch_bounds__(128, EBEM_NEAR_MINB)
-k_near_separated(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
-                 const NearJob* __restrict__ jobs,
-                 const long long* __restrict__ job_pair_off, int n_jobs,
-                 const int* __restrict__ elems, long long n_pairs,
-                 double* __restrict__ bundles, unsigned long long* points) {
-#if !EBEM_SERIES_PARAM
-  __shared__ SerSm S;
-  load_sersm(ctx, S);
-  __syncthreads();
-#else
-  const SerSm& S = *reinterpret_cast<const SerSm*>(ctx);  // unused
-#endif
-  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (p >= n_pairs) return;
-  const int jb = find_job(job_pair_off, n_jobs, p);
-  const NearJob J = jobs[jb];
-  const long long local = p - __ldg(job_pair_off + jb);  // within the job
-  const int ra = int(local / J.nces);
-  const int cb = int(local - (long long)ra * J.nces);
-  const int ea = __ldg(elems + J.res_off + ra);
-  const int eb = __ldg(elems + J.ces_off + cb);
-  const int N = ctx->n_nodes;
-  const int na = ea + 1 == N ? 0 : ea + 1;
-  const int nb = eb + 1 == N ? 0 : eb + 1;
-  if (ea == eb || na == eb || nb == ea) return;  // singular pair
-
-  const double hx = ef(ctx, EH, ea), hy = ef(ctx, EH, eb);
-  const int n = tier_nodes(element_distance(ctx, ea, eb) / fmax(hx, hy),
-                           ctx->far_nodes, ctx->refine);
-  if (points) {  // profiling: count point evaluations (warp-aggregated)
-    const unsigned act = __activemask();
-    const unsigned s = __reduce_add_sync(act, unsigned(n * n));
-    if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(points, (unsigned long long)s);
-  }
-  const double* gx = ctx->gx + gauss_offset(n);
-  const double* gw = ctx->gw + gauss_offset(n);
-  const double pax = ef(ctx, EPX, ea), pay = ef(ctx, EPY, ea);
-  const double dax = ef(ctx, EDX, ea), day = ef(ctx, EDY, ea);
-  const double pbx = ef(ctx, EPX, eb), pby = ef(ctx, EPY, eb);
-  const double dbx = ef(ctx, EDX, eb), dby = ef(ctx, EDY, eb);
-  const double nxx = ef(ctx, ENX, ea), nxy = ef(ctx, ENY, ea);
-  const double nyx = ef(ctx, ENX, eb), nyy = ef(ctx, ENY, eb);
-  const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
-  const double qfac = ctx->med.qfactor;
-
-  cplx acc[kBundle];
-#pragma unroll
-  for (int k = 0; k < kBundle; ++k) acc[k] = mk(0.0, 0.0);
-
-  for (int is = 0; is < n; ++is) {
-    const double s = __ldg(gx + is);
-    const double ws = __ldg(gw + is);
-    const double xx = pax + s * dax, xy = pay + s * day;
-    for (int it = 0; it < n; ++it) {
-      const double t = __ldg(gx + it);
-      const double wt = __ldg(gw + it);
-      const double zx = xx - (pbx + t * dbx);
-      const double zy = xy - (pby + t * dby);
-      const double r = hypot(zx, zy);
-      const double ir = 1.0 / r;
-      const double logr = log(r);
-      const double zhx = ir * zx, zhy = ir * zy;
-      DN dn;
-      dn_eval2<true, NT>(fc, S, r, ir, logr, dn);
-      CMat2 dm, nm;
-      combine_D(dn, zhx, zhy, nyx, nyy, dm);
-      combine_N(dn, zhx, zhy, nxx, nxy, nyx, nyy, nm);
-      // integrated-by-parts static hypersingular kernel (q0_kernel)
-      const double lq = qfac * logr;
-      const double qm[4] = {lq - qfac * (zhx * zhx), -qfac * (zhx * zhy),
-                            -qfac * (zhx * zhy), lq - qfac * (zhy * zhy)};
-      const double ww = ws * wt;
-      const double wgt = ww * hx * hy;
-      // K = D + alpha N (the reference adds alpha N at scatter time)
-      cplx km[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) km[e] = dm.a[e] + alpha * nm.a[e];
-      const double ps[2] = {1.0 - s, s};
-      const double pt[2] = {1.0 - t, t};
-#pragma unroll
-      for (int a = 0; a < 2; ++a) {
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const double f = wgt * ps[a] * pt[b];
-          const double g = ww * ((a == b) ? 1.0 : -1.0);  // slope_a * slope_b
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            cplx& o = acc[(a * 2 + b) * 4 + e];
-            axpy(o, f, km[e]);
-            axpy(o, g * qm[e], alpha);
-          }
-        }
-      }
-    }
-  }
-  store_bundle(bundles, J.pair_off + local, acc);
-}
 
 // ---------------------------------------------------------------- singular
 namespace {
@@ -463,7 +360,7 @@ constexpr int kSymMaxPairs = EBEM_SYM_THREADS;  // P = threads / n pairs per CTA
 #ifndef EBEM_SYM_MINB
 #define EBEM_SYM_MINB 1
 #endif
-template <int NT, bool BOTH>
+template <bool BOTH>
 __global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
 k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
            const SymJob* __restrict__ jobs,
@@ -537,7 +434,7 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
       const double logr = log(r);
       const double zhx = ir * zx, zhy = ir * zy;
       DN dn;
-      dn_eval2<true, NT>(fc, S, r, ir, logr, dn);
+      dn_eval<true>(fc, S, r, ir, logr, dn);
       const double pt[2] = {wj * (1.0 - t), wj * t};
       CMat2 dm, nm;
       // V: test on the enclosed element (normal na), trial on the cell element
@@ -625,7 +522,6 @@ constexpr int kProxyThreads = 256;
 #ifndef EBEM_PROXY_MINB
 #define EBEM_PROXY_MINB 2
 #endif
-template <int NT>
 __global__ void __launch_bounds__(kProxyThreads, EBEM_PROXY_MINB)
 k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
               const ProxyJob* __restrict__ jobs,
@@ -633,13 +529,9 @@ k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst 
               const int* __restrict__ elems, double* __restrict__ bundles,
               int kProxyPairs) {
   extern __shared__ double2 sh[];  // [kProxyPairs * ng][2 orient][2][4]
-#if !EBEM_SERIES_PARAM
   __shared__ SerSm S;
   load_sersm(ctx, S);
   __syncthreads();
-#else
-  const SerSm& S = *reinterpret_cast<const SerSm*>(ctx);  // unused
-#endif
   const int ng = ctx->proxy_n;
   const int m = ctx->m_prime;
   const int jb = find_job(job_block_off, n_jobs, (int)blockIdx.x);
@@ -688,7 +580,7 @@ k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst 
       const double ir = 1.0 / r;
       const double zhx = ir * zx, zhy = ir * zy;
       DN fs;
-      dn_eval2<false, NT>(fc, S, r, ir, log(r), fs);
+      dn_eval<false>(fc, S, r, ir, log(r), fs);
       CMat2 dm, nm;
       // V: test on the polygon (normal pn), trial on the curve (normal mn)
       combine_D(fs, zhx, zhy, mnx, mny, dm);
@@ -804,35 +696,7 @@ k_gather(const GatherJob* __restrict__ jobs, const int* __restrict__ job_block_o
 }
 
 // ------------------------------------------------------------ host wrappers
-int fill_nt_bucket(int nt) {
-  for (int b : {8, 12, 16, 20, kParTerms})
-    if (nt <= b) return b;
-  return -1;
-}
 
-#define EBEM_NT_DISPATCH(NTV, CALL) \
-  switch (NTV) {                    \
-    case 8: CALL(8); break;         \
-    case 12: CALL(12); break;       \
-    case 16: CALL(16); break;       \
-    case 20: CALL(20); break;       \
-    default: CALL(kParTerms); break; \
-  }
-
-void launch_near_separated(const DevCtx* ctx, const FillConst& fc, int nt,
-                           const NearJob* jobs, const long long* job_pair_off,
-                           int n_jobs, const int* elems, long long n_pairs,
-                           double* bundles, unsigned long long* points,
-                           cudaStream_t st) {
-  if (n_pairs <= 0) return;
-  const int bs = 128;
-  const unsigned grid = (unsigned)((n_pairs + bs - 1) / bs);
-#define EBEM_NEAR_CALL(N)                                                   \
-  k_near_separated<N><<<grid, bs, 0, st>>>(ctx, fc, jobs, job_pair_off, n_jobs, \
-                                           elems, n_pairs, bundles, points)
-  EBEM_NT_DISPATCH(fill_nt_bucket(nt), EBEM_NEAR_CALL)
-#undef EBEM_NEAR_CALL
-}
 
 void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
                          const long long* job_off, int n_jobs, const int* elems,
@@ -843,7 +707,7 @@ void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
       ctx, jobs, job_off, n_jobs, elems, n_pairs, keys, vals);
 }
 
-void launch_near_sym(const DevCtx* ctx, const FillConst& fc, int nt,
+void launch_near_sym(const DevCtx* ctx, const FillConst& fc,
                      const SymJob* jobs, const long long* job_off, int n_jobs,
                      const int* elems, const int* sorted_ids, const int* class_bounds,
                      int cls, long long max_count, int n, bool both, double* bundles,
@@ -861,21 +725,15 @@ void launch_near_sym(const DevCtx* ctx, const FillConst& fc, int nt,
   }();
   const long long need = (max_count + P - 1) / P;
   const int grid = int(std::min<long long>(need, 4LL * n_sm));
-#define EBEM_SYM_LAUNCH(N, B)                                                       \
+#define EBEM_SYM_LAUNCH(B)                                                          \
   do {                                                                              \
-    cudaFuncSetAttribute(k_near_sym<N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+    cudaFuncSetAttribute(k_near_sym<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          EBEM_SYM_THREADS * 18 * (int)sizeof(double2));             \
-    k_near_sym<N, B><<<grid, threads, smem, st>>>(ctx, fc, jobs, job_off, n_jobs,     \
-                                                  elems, sorted_ids, class_bounds, cls, \
-                                                  n, bundles);                      \
+    k_near_sym<B><<<grid, threads, smem, st>>>(ctx, fc, jobs, job_off, n_jobs, elems, \
+                                               sorted_ids, class_bounds, cls, n, bundles); \
   } while (0)
-#define EBEM_SYM_CALL(N)                  \
-  do {                                    \
-    if (both) EBEM_SYM_LAUNCH(N, true);   \
-    else EBEM_SYM_LAUNCH(N, false);       \
-  } while (0)
-  EBEM_NT_DISPATCH(fill_nt_bucket(nt), EBEM_SYM_CALL)
-#undef EBEM_SYM_CALL
+  if (both) EBEM_SYM_LAUNCH(true);
+  else EBEM_SYM_LAUNCH(false);
 #undef EBEM_SYM_LAUNCH
 }
 
@@ -897,23 +755,22 @@ int proxy_blocks_for(int m_prime, int nE, int n_gauss) {
   return (m_prime * nE + p - 1) / p;
 }
 
-void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int nt,
-                        int n_gauss, const ProxyJob* jobs,
-                        const int* job_block_off, int n_jobs, int n_blocks,
-                        const int* elems, double* bundles, cudaStream_t st) {
+void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
+                        const ProxyJob* jobs, const int* job_block_off, int n_jobs,
+                        int n_blocks, const int* elems, double* bundles,
+                        cudaStream_t st) {
   if (n_blocks <= 0) return;
   const int p = proxy_pairs_per_block(n_gauss);
   const int threads = p * n_gauss;
   const size_t shmem = size_t(threads) * 16 * sizeof(double2);
-#define EBEM_PROXY_CALL(N)                                                      \
-  do {                                                                          \
-    cudaFuncSetAttribute(k_proxy_pairs<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         kProxyThreads * 16 * (int)sizeof(double2));            \
-    k_proxy_pairs<N><<<n_blocks, threads, shmem, st>>>(ctx, fc, jobs, job_block_off, \
-                                                       n_jobs, elems, bundles, p); \
-  } while (0)
-  EBEM_NT_DISPATCH(fill_nt_bucket(nt), EBEM_PROXY_CALL)
-#undef EBEM_PROXY_CALL
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_proxy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kProxyThreads * 16 * (int)sizeof(double2));
+    return true;
+  }();
+  (void)attr;
+  k_proxy_pairs<<<n_blocks, threads, shmem, st>>>(ctx, fc, jobs, job_block_off, n_jobs,
+                                                  elems, bundles, p);
 }
 
 void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,

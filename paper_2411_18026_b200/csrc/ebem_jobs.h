@@ -24,13 +24,6 @@ struct NodeDesc {
   int bits;  // la1 | la2 << 1 | comp << 2
 };
 
-// Element pairs of one true_block evaluation (res x ces, row-major).
-struct NearJob {
-  long long pair_off;
-  int res_off, nres;  // element ids in the level's element pool
-  int ces_off, nces;
-};
-
 // One proxy interaction job per cell: m' polygon elements x nE curve
 // elements, both orientations from the same scalar evaluations.
 // V bundle (polygon test, curve trial) at v_off + pe * nE + q,

@@ -9,12 +9,6 @@
 namespace ebem_gpu {
 
 // ---- fill (ebem_fill.cu)
-int fill_nt_bucket(int nt);
-void launch_near_separated(const DevCtx* ctx, const FillConst& fc, int nt,
-                           const NearJob* jobs, const long long* job_pair_off,
-                           int n_jobs, const int* elems, long long n_pairs,
-                           double* bundles, unsigned long long* points,
-                           cudaStream_t st);
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,
                           const int* pair_elems, int n, double* bundles, int* bad,
                           cudaStream_t st);
@@ -24,7 +18,7 @@ void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
                          cudaStream_t st);
 // One launch per near-pair class cls; the class's range of the sorted pair
 // ids is read from class_bounds on the device (max_count bounds the grid).
-void launch_near_sym(const DevCtx* ctx, const FillConst& fc, int nt,
+void launch_near_sym(const DevCtx* ctx, const FillConst& fc,
                      const SymJob* jobs, const long long* job_off, int n_jobs,
                      const int* elems, const int* sorted_ids, const int* class_bounds,
                      int cls, long long max_count, int n, bool both, double* bundles,
@@ -37,10 +31,10 @@ void launch_class_bounds(const unsigned char* sorted_keys, long long n,
                          int* bounds /* 9 ints: start of class c, c = 0..8 */,
                          cudaStream_t st);
 int proxy_blocks_for(int m_prime, int nE, int n_gauss);
-void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int nt,
-                        int n_gauss, const ProxyJob* jobs,
-                        const int* job_block_off, int n_jobs, int n_blocks,
-                        const int* elems, double* bundles, cudaStream_t st);
+void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
+                        const ProxyJob* jobs, const int* job_block_off, int n_jobs,
+                        int n_blocks, const int* elems, double* bundles,
+                        cudaStream_t st);
 constexpr int kGatherTile = 256;  // output entries per gather CTA
 void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,
                    int n_blocks, const NodeDesc* desc, const double* bundles,

@@ -78,7 +78,7 @@ PhaseTimer::~PhaseTimer() {
 
 const char* kernel_name(int id) {
   static const char* names[KP_COUNT] = {
-      "k_proxy_pairs", "k_near_separated", "k_near_singular", "k_gather",
+      "k_proxy_pairs", "k_near_onesided", "k_near_singular", "k_gather",
       "k_qr_reduce", "k_cpqr", "k_interp", "k_getrf", "k_getrs", "k_gemm",
       "k_copy", "k_rhs_plane", "k_near_sym"};
   return (id >= 0 && id < KP_COUNT) ? names[id] : "?";
@@ -134,7 +134,7 @@ void Profiler::end_counted(int id, cudaStream_t st, const int* dev_bounds, doubl
 }
 
 void Profiler::collect() {
-  if (pending_.empty() && !near_points) return;
+  if (pending_.empty()) return;
   CK(cudaDeviceSynchronize());
   for (Rec& r : pending_)
     if (r.slot >= 0) r.units *= double(counts_[2 * r.slot + 1] - counts_[2 * r.slot]);
@@ -165,12 +165,6 @@ void Profiler::collect() {
     std::fprintf(stderr, "\n");
   }
   pending_.clear();
-  if (near_points) {
-    unsigned long long h = 0;
-    copy_sync(&h, near_points, 8);
-    CK(cudaMemsetAsync(near_points, 0, 8, scratch_stream()));
-    units[KP_NEAR_SEP] += double(h);
-  }
 }
 
 void Profiler::reset() {
@@ -376,18 +370,11 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
     hctx_.series_maxq = build_series(med, hctx_.series, kMaxSeriesPow);
     build_parity_series(hctx_.series, kMaxSeriesPow, hctx_.pser);
     fc_.med = med;
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 8; ++k) {  // series_joint hard-codes d odd, n even
       const int par = hctx_.pser.par[k + 2];
       if (par != (k < 3 ? 1 : 0))
         throw std::logic_error("KernelScalars: unexpected series parity");
-      fc_nt_ = std::max(fc_nt_, hctx_.pser.nt[k + 2]);
-      for (int p = 0; p < kParTerms; ++p) {
-        fc_.a[k][p] = hctx_.pser.a[k + 2][p];
-        fc_.b[k][p] = hctx_.pser.b[k + 2][p];
-      }
     }
-    if (fill_nt_bucket(fc_nt_) < 0)
-      throw std::logic_error("KernelScalars: series longer than the device table");
   } catch (const std::logic_error& e) {
     throw Error(EBEM_LOGIC_ERROR, e.what());
   }
@@ -599,15 +586,13 @@ int planning_threads() { return plan_pool().size(); }
 // ---------------------------------------------------------------- FillPlan
 void FillPlan::clear() {
   has_one_sided_ = has_two_sided_ = false;
-  bundles_ = near_pairs_ = entries_ = 0;
+  bundles_ = entries_ = 0;
   sym_pairs_ = 0;
   sym_.clear();
   sym_off_.clear();
   proxy_blocks_ = 0;
   poly_desc_off_ = -1;
   elems_.clear();
-  near_.clear();
-  near_local_.clear();
   sing_pair_.clear();
   sing_elems_.clear();
   proxy_.clear();
@@ -619,16 +604,9 @@ void FillPlan::clear() {
 
 void FillPlan::append(const FillPlan& o) {
   const int eb = int(elems_.size());
-  const long long bb = bundles_, nb = near_pairs_, sb = sym_pairs_, entb = entries_;
+  const long long bb = bundles_, sb = sym_pairs_, entb = entries_;
   const int db = int(desc_.size()), pb = proxy_blocks_;
   elems_.insert(elems_.end(), o.elems_.begin(), o.elems_.end());
-  for (NearJob J : o.near_) {
-    J.pair_off += bb;
-    J.res_off += eb;
-    J.ces_off += eb;
-    near_.push_back(J);
-  }
-  for (long long x : o.near_local_) near_local_.push_back(x + nb);
   for (long long x : o.sing_pair_) sing_pair_.push_back(x + bb);
   sing_elems_.insert(sing_elems_.end(), o.sing_elems_.begin(), o.sing_elems_.end());
   for (SymJob J : o.sym_) {
@@ -658,7 +636,6 @@ void FillPlan::append(const FillPlan& o) {
   for (long long x : o.gather_off_) gather_off_.push_back(x + entb);
   desc_.insert(desc_.end(), o.desc_.begin(), o.desc_.end());
   bundles_ += o.bundles_;
-  near_pairs_ += o.near_pairs_;
   sym_pairs_ += o.sym_pairs_;
   entries_ += o.entries_;
   proxy_blocks_ += o.proxy_blocks_;
@@ -1061,8 +1038,6 @@ void Problem::execute(FillPlan& plan) {
   PhaseTimer t_exec("fill_execute", st_);
   Pack pk;
   const size_t o_el = pk.add(plan.elems_);
-  const size_t o_nj = pk.add(plan.near_);
-  const size_t o_nl = pk.add(plan.near_local_);
   const size_t o_sp = pk.add(plan.sing_pair_);
   const size_t o_se = pk.add(plan.sing_elems_);
   const size_t o_sj = pk.add(plan.sym_);
@@ -1122,18 +1097,10 @@ void Problem::execute(FillPlan& plan) {
     for (const ProxyJob& j : plan.proxy_)
       pts += double(pcfg_.m_prime) * j.nE * pcfg_.n_gauss * pcfg_.n_gauss;
     g_prof.begin(st_);
-    launch_proxy_pairs(dctx(), fc_, fc_nt_, pcfg_.n_gauss, Pack::at<ProxyJob>(base, o_pj),
+    launch_proxy_pairs(dctx(), fc_, pcfg_.n_gauss, Pack::at<ProxyJob>(base, o_pj),
                        Pack::at<int>(base, o_pb), int(plan.proxy_.size()),
                        plan.proxy_blocks_, el, bundles.get(), st_);
     g_prof.end(KP_PROXY, st_, pts);
-  }
-  if (plan.near_pairs_ > 0) {
-    g_prof.begin(st_);
-    launch_near_separated(dctx(), fc_, fc_nt_, Pack::at<NearJob>(base, o_nj),
-                          Pack::at<long long>(base, o_nl), int(plan.near_.size()),
-                          el, plan.near_pairs_, bundles.get(),
-                          g_prof.on ? g_prof.near_points : nullptr, st_);
-    g_prof.end(KP_NEAR_SEP, st_, 0.0);
   }
   if (nsym > 0) {
     // one launch per class, sized by the wave's pair count; each reads its
@@ -1146,10 +1113,10 @@ void Problem::execute(FillPlan& plan) {
       if (both ? !plan.has_two_sided_ : !plan.has_one_sided_) continue;
       const int nq = int((acfg_.far_nodes + add[tier]) * acfg_.refine + 0.5);
       g_prof.begin(st_);
-      launch_near_sym(dctx(), fc_, fc_nt_, sj, so, int(plan.sym_.size()), el, vout,
+      launch_near_sym(dctx(), fc_, sj, so, int(plan.sym_.size()), el, vout,
                       sym_bounds_.get(), c, nsym, nq, both, bundles.get(), st_);
       // points = class count x nq^2, read back at collect time
-      g_prof.end_counted(both ? KP_NEAR_SYM : KP_NEAR_SEP, st_, sym_bounds_.get() + c,
+      g_prof.end_counted(both ? KP_NEAR_SYM : KP_NEAR_1S, st_, sym_bounds_.get() + c,
                          double(nq) * nq);
     }
   }

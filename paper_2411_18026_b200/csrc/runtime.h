@@ -39,7 +39,7 @@ extern std::atomic<long long> g_launches;
 // and algorithmic work units (quadrature point evaluations for the fill
 // kernels, bytes or flops for the rest); enabled by ebem_gpu_prof_enable.
 enum KernelId {
-  KP_PROXY = 0, KP_NEAR_SEP, KP_NEAR_SING, KP_GATHER, KP_QR, KP_CPQR,
+  KP_PROXY = 0, KP_NEAR_1S, KP_NEAR_SING, KP_GATHER, KP_QR, KP_CPQR,
   KP_INTERP, KP_GETRF, KP_GETRS, KP_GEMM, KP_COPY, KP_RHS, KP_NEAR_SYM, KP_COUNT
 };
 const char* kernel_name(int id);
@@ -57,7 +57,6 @@ class Profiler {
   long long count[KP_COUNT] = {};
   double units[KP_COUNT] = {};
   double gap_ms[KP_COUNT] = {};  // device idle right before each kernel kind
-  unsigned long long* near_points = nullptr;  // device counter (on only)
 
  private:
   struct Rec { int id; cudaEvent_t a, b; double units; int slot; };
@@ -366,7 +365,6 @@ class Problem {
   ebem_proxy_config pcfg_;
   DevCtx hctx_{};
   FillConst fc_{};
-  int fc_nt_ = 0;
   DBuf<DevCtx> dctx_;
   DBuf<double> delem_, dxy_;
   cudaStream_t st_ = nullptr;
@@ -411,13 +409,10 @@ class FillPlan {
   int poly_descs();
   int N_, m_, ng_;
   long long bundles_ = 0;
-  long long near_pairs_ = 0;
   long long entries_ = 0;
   int proxy_blocks_ = 0;
   int poly_desc_off_ = -1;
   std::vector<int> elems_;
-  std::vector<NearJob> near_;
-  std::vector<long long> near_local_;
   std::vector<long long> sing_pair_;
   std::vector<int> sing_elems_;
   std::vector<SymJob> sym_;
