@@ -44,7 +44,7 @@ LEAF = 32
 # Algorithmic FP64 flops per quadrature-point evaluation (DESIGN.md,
 # "Roofline"): FP64 instructions per point counted by ncu on the kernels
 # (DADD + DMUL + 2 DFMA), divided by the point evaluations of the launch.
-FLOPS_PER_POINT = {"k_near_separated": 1309.9, "k_proxy_pairs": 1521.3, "k_near_sym": 1462.5}
+FLOPS_PER_POINT = {"k_near_onesided": 1222.2, "k_proxy_pairs": 1379.3, "k_near_sym": 1305.7}
 
 
 def config_dict():

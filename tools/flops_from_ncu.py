@@ -14,7 +14,10 @@ acc = collections.defaultdict(lambda: collections.Counter())
 for r in rows[h + 1:]:
     if len(r) <= iv:
         continue
-    name = re.sub(r"^void ", "", r[ik]).split("(")[0].split("<")[0].replace("ebem_gpu::", "")
+    full = r[ik]
+    name = re.sub(r"^void ", "", full).split("(")[0].split("<")[0].replace("ebem_gpu::", "")
+    if name == "k_near_sym" and re.search(r"k_near_sym<(\(bool\))?(0|false)>", full):
+        name = "k_near_onesided"  # the one-sided instantiation (profiler name)
     acc[name][r[im]] += float(r[iv].replace(",", ""))
 pts = {}
 for line in open(plain_log):
