@@ -520,7 +520,7 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
 constexpr int kProxyThreads = 256;
 
 #ifndef EBEM_PROXY_MINB
-#define EBEM_PROXY_MINB 2
+#define EBEM_PROXY_MINB 1
 #endif
 __global__ void __launch_bounds__(kProxyThreads, EBEM_PROXY_MINB)
 k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
@@ -746,8 +746,12 @@ void launch_near_singular(const DevCtx* ctx, const long long* pairs,
                                                           bundles, bad);
 }
 
+#ifndef EBEM_PROXY_PAIRS_CAP
+#define EBEM_PROXY_PAIRS_CAP 64
+#endif
 int proxy_pairs_per_block(int n_gauss) {
-  return n_gauss >= kProxyThreads ? 1 : (kProxyThreads / n_gauss < 32 ? kProxyThreads / n_gauss : 32);
+  const int cap = EBEM_PROXY_PAIRS_CAP;
+  return n_gauss >= kProxyThreads ? 1 : (kProxyThreads / n_gauss < cap ? kProxyThreads / n_gauss : cap);
 }
 
 int proxy_blocks_for(int m_prime, int nE, int n_gauss) {
