@@ -89,12 +89,14 @@ void launch_qr_team(const QrTask* tasks, int n, size_t smem, double2* gws,
 void launch_cpqr_team(const CpqrTask* tasks, int n, size_t smem, double2* gws,
                       cudaStream_t st);
 // Streaming TSQR (ebem_tsqr.cu): same QrTask (in_smem / ws_off unused);
-// n <= kTsqrMaxCols, lanes = tsqr_lanes(n), smem = tsqr_smem_bytes(n).
+// n <= kTsqrMaxCols in two variants (tsqr_variant: 0 for n <= 64, 1 above),
+// smem = tsqr_smem_bytes(n) for the largest n of a launch.
 constexpr int kTsqrMaxCols = 128;
-int tsqr_lanes(int n);
+int tsqr_variant(int n);  // -1: not supported (n > kTsqrMaxCols)
 int tsqr_block_rows(int n);
+int tsqr_ctas_per_sm(int n);
 size_t tsqr_smem_bytes(int n);
-void launch_tsqr(const QrTask* tasks, int n_tasks, int lanes, size_t smem,
+void launch_tsqr(const QrTask* tasks, int n_tasks, int variant, size_t smem,
                  cudaStream_t st);
 void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st);
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,

@@ -25,6 +25,8 @@
 // factors of several row pieces of one matrix are stacked and reduced again
 // by the same kernel.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 
 #include "ebem_dense.h"
@@ -33,9 +35,23 @@ namespace ebem_gpu {
 
 namespace {
 
-constexpr int kTsqrThreads = 1024;
-constexpr int kWarpsPerCta = kTsqrThreads / 32;
 constexpr int kRpt = 8;    // block rows per lane
+// (lanes per column, CTA threads) of the two variants: n <= 64 and n <= 128.
+// Smaller CTAs put several independent reflector chains on one SM.
+#ifndef EBEM_TSQR_S_LANES
+#define EBEM_TSQR_S_LANES 4
+#endif
+#ifndef EBEM_TSQR_S_THREADS
+#define EBEM_TSQR_S_THREADS 256
+#endif
+#ifndef EBEM_TSQR_M_LANES
+#define EBEM_TSQR_M_LANES 4
+#endif
+#ifndef EBEM_TSQR_M_THREADS
+#define EBEM_TSQR_M_THREADS 512
+#endif
+static_assert(EBEM_TSQR_S_THREADS / EBEM_TSQR_S_LANES >= 64, "small variant: 64 columns");
+static_assert(EBEM_TSQR_M_THREADS / EBEM_TSQR_M_LANES >= kTsqrMaxCols, "medium variant");
 constexpr int kSlots = 8;  // reflector ring depth
 
 __device__ __forceinline__ int pidx(int i, int j) { return ((j * (j + 1)) >> 1) + i; }
@@ -122,9 +138,10 @@ __device__ __forceinline__ void make_reflector(double2 (&B)[kRpt], bool mine, in
   mbar_arrive(full + slot);
 }
 
-template <int LANES>
-__global__ void __launch_bounds__(kTsqrThreads, 1)
+template <int LANES, int THREADS>
+__global__ void __launch_bounds__(THREADS, (65536 / (THREADS * 64)) > 0 ? 65536 / (THREADS * 64) : 1)
 k_tsqr(const QrTask* __restrict__ tasks) {
+  constexpr int kWarpsPerCta = THREADS / 32;
   constexpr int kRows = LANES * kRpt;
   constexpr int kGroupsPerWarp = 32 / LANES;
   extern __shared__ double2 R[];  // packed upper triangle | v ring | tau ring
@@ -214,33 +231,38 @@ k_tsqr(const QrTask* __restrict__ tasks) {
 
 }  // namespace
 
-int tsqr_lanes(int n) { return n <= 64 ? 16 : n <= kTsqrMaxCols ? 8 : 0; }
-int tsqr_block_rows(int n) { return tsqr_lanes(n) * kRpt; }
+int tsqr_variant(int n) { return n <= 64 ? 0 : n <= kTsqrMaxCols ? 1 : -1; }
+int tsqr_block_rows(int n) {
+  return tsqr_variant(n) == 0 ? EBEM_TSQR_S_LANES * kRpt : EBEM_TSQR_M_LANES * kRpt;
+}
+int tsqr_ctas_per_sm(int n) {
+  const int t = tsqr_variant(n) == 0 ? EBEM_TSQR_S_THREADS : EBEM_TSQR_M_THREADS;
+  const int by_regs = std::max(1, 65536 / (t * 64));
+  const int by_smem = std::max(1, int((227 * 1024) / (tsqr_smem_bytes(n) + 1024)));
+  return std::min(std::min(by_regs, by_smem), 2048 / t);
+}
 size_t tsqr_smem_bytes(int n) {
   return sizeof(double2) *
          (size_t(n) * (n + 1) / 2 + kSlots * size_t(tsqr_block_rows(n)) + kSlots);
 }
 
-void launch_tsqr(const QrTask* tasks, int n_tasks, int lanes, size_t smem,
+template <int L, int T>
+static void launch_variant(const QrTask* tasks, int n_tasks, size_t smem, cudaStream_t st) {
+  static bool once = [] {
+    cudaFuncSetAttribute(k_tsqr<L, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return true;
+  }();
+  (void)once;
+  k_tsqr<L, T><<<n_tasks, T, smem, st>>>(tasks);
+}
+
+void launch_tsqr(const QrTask* tasks, int n_tasks, int variant, size_t smem,
                  cudaStream_t st) {
   if (n_tasks <= 0) return;
-  if (lanes == 16) {
-    static bool once = [] {
-      cudaFuncSetAttribute(k_tsqr<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           200 * 1024);
-      return true;
-    }();
-    (void)once;
-    k_tsqr<16><<<n_tasks, kTsqrThreads, smem, st>>>(tasks);
-  } else {
-    static bool once = [] {
-      cudaFuncSetAttribute(k_tsqr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           200 * 1024);
-      return true;
-    }();
-    (void)once;
-    k_tsqr<8><<<n_tasks, kTsqrThreads, smem, st>>>(tasks);
-  }
+  if (variant == 0)
+    launch_variant<EBEM_TSQR_S_LANES, EBEM_TSQR_S_THREADS>(tasks, n_tasks, smem, st);
+  else
+    launch_variant<EBEM_TSQR_M_LANES, EBEM_TSQR_M_THREADS>(tasks, n_tasks, smem, st);
 }
 
 }  // namespace ebem_gpu

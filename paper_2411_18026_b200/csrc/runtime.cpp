@@ -1236,7 +1236,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
       const TallBlock& x = q[i];
       const size_t bytes = size_t(x.rows) * x.n * 16;
       if ((bytes <= size_t(kSmemCap) && !force) || x.rows <= x.n) continue;
-      if (tsqr_lanes(x.n) != 0) {
+      if (tsqr_variant(x.n) >= 0) {
         streamed[i] = 1;
         work += double(x.rows) * x.n * (x.n + 64) / tsqr_block_rows(x.n);
       } else if (x.rows > 2 * x.n) {
@@ -1244,7 +1244,10 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
         pieces[i] = (x.rows + chunk - 1) / chunk;
       }
     }
-    const double per_cta = work / (4.0 * n_sm);
+    int cps = 1;  // resident CTAs per SM of the streamed inputs' variants
+    for (size_t i = 0; i < q.size(); ++i)
+      if (streamed[i]) cps = std::max(cps, tsqr_ctas_per_sm(q[i].n));
+    const double per_cta = work / (4.0 * n_sm * cps);
     for (size_t i = 0; i < q.size(); ++i) {
       if (!streamed[i]) continue;
       const TallBlock& x = q[i];
@@ -1280,7 +1283,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
         t.ld = x.ld;
         t.dst_ld = ld_out;
         if (streamed[i]) {
-          if (tsqr_lanes(x.n) == 16) {
+          if (tsqr_variant(x.n) == 0) {
             stream16.push_back(t);
             smem16 = std::max(smem16, tsqr_smem_bytes(x.n));
           } else {
@@ -1313,8 +1316,8 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     g_prof.begin(st);
     // (the team-layout k_qr_team measured slower on these shapes: 485 vs 404 ms)
     launch_qr_reduce(Pack::at<QrTask>(tb, o), int(tasks.size()), smem, gws.get(), st);
-    launch_tsqr(Pack::at<QrTask>(tb, o16), int(stream16.size()), 16, smem16, st);
-    launch_tsqr(Pack::at<QrTask>(tb, o8), int(stream8.size()), 8, smem8, st);
+    launch_tsqr(Pack::at<QrTask>(tb, o16), int(stream16.size()), 0, smem16, st);
+    launch_tsqr(Pack::at<QrTask>(tb, o8), int(stream8.size()), 1, smem8, st);
     g_prof.end(KP_QR, st, fl);
     CK(cudaGetLastError());
     staging.fence(st);
