@@ -375,6 +375,25 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
       if (par != (k < 3 ? 1 : 0))
         throw std::logic_error("KernelScalars: unexpected series parity");
     }
+    // The fill evaluates the D/N series only below the series radius: drop
+    // the terms whose size there is below 1e-21 of the series' largest term
+    // (the reference keeps them; they cannot change a double result).
+    const double rmax = med.series_radius, lr = std::fabs(std::log(rmax));
+    for (int k = 2; k < 10; ++k) {
+      ParSeries& ps = hctx_.pser;
+      double big = 0.0;
+      std::vector<double> mag(ps.nt[k]);
+      for (int p = 0; p < ps.nt[k]; ++p) {
+        const double2 a = ps.a[k][p], b = ps.b[k][p];
+        mag[p] = (std::hypot(a.x, a.y) + std::hypot(b.x, b.y) * lr) *
+                 std::pow(rmax, ps.par[k] + 2 * p);
+        big = std::max(big, mag[p]);
+      }
+      int nt = ps.nt[k];
+      while (nt > 1 && mag[nt - 1] <= 1e-21 * big) --nt;
+      for (int p = nt; p < kParTerms; ++p) ps.a[k][p] = ps.b[k][p] = double2{0.0, 0.0};
+      ps.nt[k] = nt;
+    }
   } catch (const std::logic_error& e) {
     throw Error(EBEM_LOGIC_ERROR, e.what());
   }
