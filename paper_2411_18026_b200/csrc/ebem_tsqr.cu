@@ -138,8 +138,11 @@ __device__ __forceinline__ void make_reflector(double2 (&B)[kRpt], bool mine, in
   mbar_arrive(full + slot);
 }
 
+#ifndef EBEM_TSQR_REGS
+#define EBEM_TSQR_REGS 64  // registers per thread the CTA size is sized for
+#endif
 template <int LANES, int THREADS>
-__global__ void __launch_bounds__(THREADS, (65536 / (THREADS * 64)) > 0 ? 65536 / (THREADS * 64) : 1)
+__global__ void __launch_bounds__(THREADS, (65536 / (THREADS * EBEM_TSQR_REGS)) > 0 ? 65536 / (THREADS * EBEM_TSQR_REGS) : 1)
 k_tsqr(const QrTask* __restrict__ tasks) {
   constexpr int kWarpsPerCta = THREADS / 32;
   constexpr int kRows = LANES * kRpt;
@@ -237,7 +240,7 @@ int tsqr_block_rows(int n) {
 }
 int tsqr_ctas_per_sm(int n) {
   const int t = tsqr_variant(n) == 0 ? EBEM_TSQR_S_THREADS : EBEM_TSQR_M_THREADS;
-  const int by_regs = std::max(1, 65536 / (t * 64));
+  const int by_regs = std::max(1, 65536 / (t * EBEM_TSQR_REGS));
   const int by_smem = std::max(1, int((227 * 1024) / (tsqr_smem_bytes(n) + 1024)));
   return std::min(std::min(by_regs, by_smem), 2048 / t);
 }
