@@ -1442,11 +1442,12 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     CK(cudaGetLastError());
     staging.fence(st_);
   }
-  std::vector<int> h_jp(jp_total), h_steps(nq);
-  std::vector<double> h_rd(jp_total);
-  CK(cudaMemcpyAsync(h_jp.data(), d_jp.get(), jp_total * 4, cudaMemcpyDeviceToHost, st_));
-  CK(cudaMemcpyAsync(h_steps.data(), d_steps.get(), nq * 4, cudaMemcpyDeviceToHost, st_));
-  CK(cudaMemcpyAsync(h_rd.data(), d_rd.get(), jp_total * 8, cudaMemcpyDeviceToHost, st_));
+  int* const h_jp = scratch().h_jp.ensure(jp_total);
+  int* const h_steps = scratch().h_steps.ensure(nq);
+  double* const h_rd = scratch().h_rd.ensure(jp_total);
+  CK(cudaMemcpyAsync(h_jp, d_jp.get(), jp_total * 4, cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(h_steps, d_steps.get(), nq * 4, cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(h_rd, d_rd.get(), jp_total * 8, cudaMemcpyDeviceToHost, st_));
   CK(cudaStreamSynchronize(st_));
   check_domain();  // the fill's element-length guard, read after the sync
 
@@ -1456,7 +1457,7 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     int k = 0, cap = std::numeric_limits<int>::max();
     for (int a = 0; a < 4; ++a) {
       const size_t i = 4 * c + a;
-      const double* rd = h_rd.data() + jp_off[i];
+      const double* rd = h_rd + jp_off[i];
       const int steps = h_steps[i];
       const int mn = std::min(q[i].rows, q[i].n);
       // eps_rank(eps): first j with |R_jj| <= eps |R_00| (0 if R_00 == 0)
@@ -1480,7 +1481,7 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     r.saturated = k >= std::min(std::min(cols[0].size(), cols[1].size()),
                                 std::min(rows[0].size(), rows[1].size()));
     for (int a = 0; a < 4; ++a) {
-      const int* jp = h_jp.data() + jp_off[4 * c + a];
+      const int* jp = h_jp + jp_off[4 * c + a];
       const std::vector<int>& src = a == 0 ? cols[0] : a == 1 ? cols[1] : a == 2 ? rows[0] : rows[1];
       std::vector<int>& dst = a == 0 ? r.scol[0] : a == 1 ? r.scol[1] : a == 2 ? r.srow[0] : r.srow[1];
       dst.resize(k);

@@ -134,6 +134,31 @@ class DBuf {
   size_t n_ = 0;
 };
 
+// Grow-only pinned host buffer (device-to-host readbacks at full speed).
+template <class T>
+class PinnedBuf {
+ public:
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() { if (p_) cudaFreeHost(p_); }
+  T* ensure(size_t n) {
+    if (n > n_) {
+      if (p_) cudaFreeHost(p_);
+      p_ = nullptr;
+      n_ = 0;
+      const size_t cap = n + n / 4 + 64;
+      CK(cudaMallocHost(reinterpret_cast<void**>(&p_), cap * sizeof(T)));
+      n_ = cap;
+    }
+    return p_;
+  }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
 // Packs host arrays into one device upload (16-byte aligned segments).
 class Pack {
  public:
@@ -284,6 +309,8 @@ struct Scratch {
   cudaEvent_t sym_ev = nullptr;
   DBuf<double> bundles;
   DBuf<double2> gws;
+  PinnedBuf<int> h_jp, h_steps;  // pivoted-QR readbacks
+  PinnedBuf<double> h_rd;
 };
 Scratch& scratch();
 
