@@ -13,9 +13,9 @@
  * the reference throws in the same situation; ebem_gpu_last_error() returns
  * the message of the last failure on the calling thread.
  *
- * Thread safety: a problem or solver handle is externally synchronised for
- * construction; solves on a finished solver may be issued from several
- * threads (each call serialises on the handle's stream).
+ * Thread safety: every entry point takes one process-wide mutex and runs on
+ * one process-wide CUDA stream (the device scratch is shared by all
+ * handles), so calls from several threads are safe and serialised.
  */
 #ifndef EBEM_GPU_H
 #define EBEM_GPU_H
