@@ -327,7 +327,8 @@ __global__ void __launch_bounds__(256)
 k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
                const long long* __restrict__ job_off, int n_jobs,
                const int* __restrict__ elems, long long n_pairs,
-               unsigned char* __restrict__ keys, int* __restrict__ vals) {
+               unsigned char* __restrict__ keys, int* __restrict__ vals,
+               int* __restrict__ pair_job) {
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   const int jb = find_job(job_off, n_jobs, p);
@@ -348,6 +349,7 @@ k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
   }
   keys[p] = key;
   vals[p] = int(p);
+  pair_job[p] = jb;  // read back by the near-field kernel (no second search)
 }
 
 // CTA = P pairs x n threads; thread (pair, i) fixes the test point s_i on the
@@ -366,8 +368,8 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
            const SymJob* __restrict__ jobs,
            const long long* __restrict__ job_off, int n_jobs,
            const int* __restrict__ elems, const int* __restrict__ sorted_ids,
-           const int* __restrict__ class_bounds, int cls, int n,
-           double* __restrict__ bundles) {
+           const int* __restrict__ pair_job, const int* __restrict__ class_bounds,
+           int cls, int n, double* __restrict__ bundles) {
   extern __shared__ double2 sh[];  // [P * n][8 V + 8 U cplx + 2 (Q as re/im pairs)]
   __shared__ SerSm S;
   __shared__ double sgx[kMaxGauss], sgw[kMaxGauss];
@@ -395,7 +397,7 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
   const bool active = lp < P && idx < count;
   if (active && i == 0) {
     const long long p = __ldg(pair_ids + idx);
-    const int jb = find_job(job_off, n_jobs, p);
+    const int jb = __ldg(pair_job + p);
     const SymJob J = jobs[jb];
     const long long local = p - J.local_off;
     const int a = int(local / J.nE);
@@ -701,17 +703,17 @@ k_gather(const GatherJob* __restrict__ jobs, const int* __restrict__ job_block_o
 void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
                          const long long* job_off, int n_jobs, const int* elems,
                          long long n_pairs, unsigned char* keys, int* vals,
-                         cudaStream_t st) {
+                         int* pair_job, cudaStream_t st) {
   if (n_pairs <= 0) return;
   k_sym_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, st>>>(
-      ctx, jobs, job_off, n_jobs, elems, n_pairs, keys, vals);
+      ctx, jobs, job_off, n_jobs, elems, n_pairs, keys, vals, pair_job);
 }
 
 void launch_near_sym(const DevCtx* ctx, const FillConst& fc,
                      const SymJob* jobs, const long long* job_off, int n_jobs,
-                     const int* elems, const int* sorted_ids, const int* class_bounds,
-                     int cls, long long max_count, int n, bool both, double* bundles,
-                     cudaStream_t st) {
+                     const int* elems, const int* sorted_ids, const int* pair_job,
+                     const int* class_bounds, int cls, long long max_count, int n,
+                     bool both, double* bundles, cudaStream_t st) {
   if (max_count <= 0) return;
   const int P = EBEM_SYM_THREADS / n;
   const int threads = P * n;
@@ -730,7 +732,8 @@ void launch_near_sym(const DevCtx* ctx, const FillConst& fc,
     cudaFuncSetAttribute(k_near_sym<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          EBEM_SYM_THREADS * 18 * (int)sizeof(double2));             \
     k_near_sym<B><<<grid, threads, smem, st>>>(ctx, fc, jobs, job_off, n_jobs, elems, \
-                                               sorted_ids, class_bounds, cls, n, bundles); \
+                                               sorted_ids, pair_job, class_bounds, cls, n, \
+                                               bundles);                            \
   } while (0)
   if (both) EBEM_SYM_LAUNCH(true);
   else EBEM_SYM_LAUNCH(false);

@@ -1096,7 +1096,7 @@ void Problem::execute(FillPlan& plan) {
     sj = Pack::at<SymJob>(base, o_sj);
     so = Pack::at<long long>(base, o_so);
     sym_keys_.ensure(2 * size_t(nsym));
-    sym_vals_.ensure(2 * size_t(nsym));
+    sym_vals_.ensure(3 * size_t(nsym));  // unsorted | sorted ids | job of each pair
     if (!sym_bounds_host_) {
       CK(cudaMallocHost(reinterpret_cast<void**>(&sym_bounds_host_), 16 * sizeof(int)));
       CK(cudaEventCreateWithFlags(&sym_ev_, cudaEventDisableTiming));
@@ -1106,7 +1106,8 @@ void Problem::execute(FillPlan& plan) {
     unsigned char* kout = kin + nsym;
     int* vin = sym_vals_.get();
     int* vout = vin + nsym;
-    launch_sym_classify(dctx(), sj, so, int(plan.sym_.size()), el, nsym, kin, vin, st_);
+    launch_sym_classify(dctx(), sj, so, int(plan.sym_.size()), el, nsym, kin, vin,
+                        vin + 2 * nsym, st_);
     sort_pairs_by_class(kin, kout, vin, vout, nsym, &sort_temp_, &sort_temp_bytes_, st_);
     launch_class_bounds(kout, nsym, sym_bounds_.get(), st_);
     g_launches += 3;
@@ -1133,7 +1134,8 @@ void Problem::execute(FillPlan& plan) {
       const int nq = int((acfg_.far_nodes + add[tier]) * acfg_.refine + 0.5);
       g_prof.begin(st_);
       launch_near_sym(dctx(), fc_, sj, so, int(plan.sym_.size()), el, vout,
-                      sym_bounds_.get(), c, nsym, nq, both, bundles.get(), st_);
+                      sym_vals_.get() + 2 * nsym, sym_bounds_.get(), c, nsym, nq, both,
+                      bundles.get(), st_);
       // points = class count x nq^2, read back at collect time
       g_prof.end_counted(both ? KP_NEAR_SYM : KP_NEAR_1S, st_, sym_bounds_.get() + c,
                          double(nq) * nq);
