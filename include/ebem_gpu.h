@@ -82,6 +82,16 @@ typedef struct ebem_fds_solve_timing {
 
 typedef struct ebem_gpu_problem ebem_gpu_problem;
 typedef struct ebem_gpu_fds ebem_gpu_fds;
+typedef struct ebem_gpu_conv ebem_gpu_conv;
+
+/* ConvStats (proj/include/ebem/dense_solver.hpp:10-19). */
+typedef struct ebem_conv_stats {
+  double assemble_seconds;
+  double factor_seconds;
+  double rcond;      /* 1-norm reciprocal condition estimate (zgecon's zlacn2) */
+  double min_pivot;  /* min |U_ii| */
+  int condition_warning;
+} ebem_conv_stats;
 
 const char* ebem_gpu_last_error(void);
 
@@ -149,6 +159,20 @@ int ebem_gpu_build_proxy(ebem_gpu_problem* p, int node_begin, int node_end,
  * (not in the reference).  out: 2N x m complex, host memory. */
 int ebem_gpu_rhs_plane(ebem_gpu_problem* p, int kind, const double* angles,
                        int m, double amplitude, double* out);
+
+/* BlockAssembler::dense (proj/src/assembly.cpp:311-330): the full 2N x 2N
+ * Galerkin matrix into out (host, column-major complex); length_error
+ * status past AssemblyConfig::max_dense_bytes. */
+int ebem_gpu_dense(ebem_gpu_problem* p, double* out);
+
+/* ConvSolver(mesh, medium, alpha, config) on the problem's geometry: dense
+ * assembly + partial-pivoted LU (proj/src/dense_solver.cpp:9-22).  The
+ * problem must outlive the solver. */
+int ebem_gpu_conv_create(ebem_gpu_problem* p, ebem_gpu_conv** out,
+                         ebem_conv_stats* stats);
+/* ConvSolver::solve (proj/src/dense_solver.cpp:24-29): rhs, x 2N x m, host. */
+int ebem_gpu_conv_solve(ebem_gpu_conv* c, const double* rhs, int m, double* x);
+void ebem_gpu_conv_destroy(ebem_gpu_conv* c);
 
 /* FdsSolver(source, ClusterTree(N, depth), FdsConfig): factorization
  * (proj/src/fds.cpp:18-154).  The problem must outlive the solver. */

@@ -113,6 +113,12 @@ class _SolveTiming(ctypes.Structure):
                 ("device_seconds", ctypes.c_double)]
 
 
+class _ConvStats(ctypes.Structure):
+    _fields_ = [("assemble_seconds", ctypes.c_double), ("factor_seconds", ctypes.c_double),
+                ("rcond", ctypes.c_double), ("min_pivot", ctypes.c_double),
+                ("condition_warning", ctypes.c_int)]
+
+
 def lib():
     """The loaded native library (raises ImportError when it is not built)."""
     global _lib
@@ -363,6 +369,16 @@ class FdsStats:
 
 
 @dataclass
+class ConvStats:
+    """ConvStats, dense_solver.hpp:10-19."""
+    assemble_seconds: float = 0.0
+    factor_seconds: float = 0.0
+    rcond: float = 1.0
+    min_pivot: float = 0.0
+    condition_warning: bool = False
+
+
+@dataclass
 class FdsSolveTiming:
     upward_seconds: float = 0.0
     top_seconds: float = 0.0
@@ -433,6 +449,12 @@ class _Handle:
                                          _p(c0), c0.size, _p(c1), c1.size, _p(out)))
         return _from_cbuf(out[: 2 * nr * nc], nr, nc)
 
+    def dense(self):
+        d = 2 * self.n
+        out = np.zeros(2 * d * d)
+        _check(lib().ebem_gpu_dense(self.h, _p(out)))
+        return _from_cbuf(out, d, d)
+
     def rhs(self, kind, angles, amplitude):
         a = np.ascontiguousarray(np.atleast_1d(angles), dtype=np.float64)
         out = np.zeros(4 * self.n * a.size)
@@ -459,6 +481,10 @@ class BlockAssembler:
 
     def true_block(self, rows, cols) -> np.ndarray:
         return self._h.true_block(rows, cols)
+
+    def dense(self) -> np.ndarray:
+        """The full 2N x 2N Galerkin matrix (assembly.cpp:311-330)."""
+        return self._h.dense()
 
     def rhs(self, wave) -> np.ndarray:
         return self._h.rhs(wave.kind, [wave.angle], wave.amplitude)[:, 0]
@@ -619,6 +645,49 @@ def _host_callbacks(source: BlockSource, errors: list):
             return 1 if isinstance(ex, ValueError) else 2
 
     return _BLOCK_FN(block), _BASIS_FN(basis)
+
+
+class ConvSolver:
+    """Dense reference solver, dense_solver.hpp:21-45: full Galerkin matrix
+    and one partial-pivoted LU on the device."""
+
+    def __init__(self, mesh: Mesh, medium: Medium, alpha: complex,
+                 config: AssemblyConfig = None):
+        self._asm = BlockAssembler(mesh, medium, alpha, config)
+        st = _ConvStats()
+        h = ctypes.c_void_p()
+        _check(lib().ebem_gpu_conv_create(self._asm._h.h, ctypes.byref(h), ctypes.byref(st)))
+        self._c = h
+        self._stats = ConvStats(st.assemble_seconds, st.factor_seconds, st.rcond,
+                                st.min_pivot, bool(st.condition_warning))
+
+    def __del__(self):
+        if getattr(self, "_c", None) and _lib is not None:
+            _lib.ebem_gpu_conv_destroy(self._c)
+            self._c = None
+
+    def assembler(self) -> BlockAssembler:
+        return self._asm
+
+    def stats(self) -> ConvStats:
+        return self._stats
+
+    def size(self) -> int:
+        return 2 * self._asm.n_nodes()
+
+    def solve(self, rhs) -> np.ndarray:
+        b = np.asarray(rhs, dtype=np.complex128)
+        vec = b.ndim == 1
+        b2 = b.reshape(-1, 1) if vec else b
+        if b2.shape[0] != self.size():
+            raise InvalidArgument(f"LuFactor: right-hand side has {b2.shape[0]} rows, "
+                                  f"need {self.size()}")
+        m = b2.shape[1]
+        buf = np.asfortranarray(b2).ravel(order="F").view(np.float64).copy()
+        out = np.zeros_like(buf)
+        _check(lib().ebem_gpu_conv_solve(self._c, _p(buf), m, _p(out)))
+        x = out.view(np.complex128).reshape(m, self.size()).T
+        return x[:, 0].copy() if vec else np.ascontiguousarray(x)
 
 
 class FdsSolver:

@@ -4,6 +4,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -16,6 +17,10 @@ using namespace ebem_gpu;
 struct ebem_gpu_problem {
   Problem* p;
 };
+struct ebem_gpu_conv {
+  Conv* c;
+};
+
 struct ebem_gpu_fds {
   Fds* f;
   Problem* own = nullptr;  // source-only problem owned by the solver
@@ -329,6 +334,47 @@ int ebem_gpu_fds_create(ebem_gpu_problem* p, int depth,
     if (stats) *stats = h->f->stats();
     *out = h;
   });
+}
+
+int ebem_gpu_dense(ebem_gpu_problem* p, double* out) {
+  return guarded([&] {
+    if (!p || !out) throw Error(EBEM_INVALID_ARGUMENT, "dense: null argument");
+    Conv::dense_host(*p->p, out);
+  });
+}
+
+int ebem_gpu_conv_create(ebem_gpu_problem* p, ebem_gpu_conv** out,
+                         ebem_conv_stats* stats) {
+  return guarded([&] {
+    if (!p || !out) throw Error(EBEM_INVALID_ARGUMENT, "ConvSolver: null argument");
+    *out = nullptr;
+    std::unique_ptr<Conv> c(new Conv(*p->p));
+    if (stats) {
+      const ConvStatsC& s = c->stats();
+      stats->assemble_seconds = s.assemble_seconds;
+      stats->factor_seconds = s.factor_seconds;
+      stats->rcond = s.rcond;
+      stats->min_pivot = s.min_pivot;
+      stats->condition_warning = s.condition_warning ? 1 : 0;
+    }
+    *out = new ebem_gpu_conv{c.release()};
+  });
+}
+
+int ebem_gpu_conv_solve(ebem_gpu_conv* c, const double* rhs, int m, double* x) {
+  return guarded([&] {
+    if (!c || (m > 0 && (!rhs || !x)))
+      throw Error(EBEM_INVALID_ARGUMENT, "ConvSolver: null argument");
+    if (m < 0) throw Error(EBEM_INVALID_ARGUMENT, "ConvSolver: negative column count");
+    c->c->solve_host(rhs, m, x);
+  });
+}
+
+void ebem_gpu_conv_destroy(ebem_gpu_conv* c) {
+  if (!c) return;
+  std::lock_guard<std::recursive_mutex> lock(api_mutex());
+  delete c->c;
+  delete c;
 }
 
 void ebem_gpu_fds_destroy(ebem_gpu_fds* f) {

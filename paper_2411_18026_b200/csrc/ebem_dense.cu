@@ -722,6 +722,61 @@ k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
   }
 }
 
+// ------------------------------------------ LU solve, large n (> 256)
+// One CTA per right-hand side, column-oriented substitutions: step k reads
+// one (coalesced) column of L or U and updates the remaining rows in
+// parallel, one barrier per step.  x lives in shared memory when it fits.
+constexpr int kBigThreads = 1024;
+__global__ void __launch_bounds__(kBigThreads)
+k_getrs_big(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off,
+            int n_tasks, int smem_cap) {
+  extern __shared__ double2 sx[];
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const LuSolveTask T = tasks[lo];
+  const int col = blockIdx.x - block_off[lo];
+  if (col >= T.nrhs) return;
+  const int n = T.n;
+  const double2* A = reinterpret_cast<const double2*>(T.lu);
+  const size_t lda = T.ld;
+  double2* bg = reinterpret_cast<double2*>(T.b) + (size_t)col * T.ldb;
+  const bool in_smem = n <= smem_cap;
+  double2* x = in_smem ? sx : bg;
+  if (in_smem)
+    for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = bg[r];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < n; ++k) {
+      const int p = T.ipiv[k];
+      if (p != k) {
+        const double2 t = x[k];
+        x[k] = x[p];
+        x[p] = t;
+      }
+    }
+  __syncthreads();
+  for (int k = 0; k < n - 1; ++k) {  // unit lower
+    const double2 xk = x[k];
+    const double2* Lk = A + (size_t)k * lda;
+    for (int r = k + 1 + threadIdx.x; r < n; r += blockDim.x) x[r] = zfms(x[r], Lk[r], xk);
+    __syncthreads();
+  }
+  for (int k = n - 1; k >= 0; --k) {  // upper
+    const double2* Uk = A + (size_t)k * lda;
+    const double2 xk = zdiv(x[k], Uk[k]);
+    __syncthreads();
+    if (threadIdx.x == 0) x[k] = xk;
+    for (int r = threadIdx.x; r < k; r += blockDim.x) x[r] = zfms(x[r], Uk[r], xk);
+    __syncthreads();
+  }
+  if (in_smem)
+    for (int r = threadIdx.x; r < n; r += blockDim.x) bg[r] = x[r];
+}
+
 // ----------------------------------------------------------- host wrappers
 static void set_smem_attr(const void* f) {
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
@@ -734,6 +789,7 @@ void dense_init() {
   set_smem_attr((const void*)k_cpqr);
   set_smem_attr((const void*)k_getrf);
   set_smem_attr((const void*)k_getrs);
+  set_smem_attr((const void*)k_getrs_big);
   set_smem_attr((const void*)k_getrs_reg<2, 1>);
   set_smem_attr((const void*)k_getrs_reg<4, 1>);
   set_smem_attr((const void*)k_getrs_reg<8, 1>);
@@ -765,7 +821,7 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
 }
 int getrs_cpw(int max_nrhs) { return max_nrhs <= kWarps ? 1 : kCpw; }
 int getrs_blocks(int nrhs, int max_n, int cpw) {
-  const int per = max_n <= 256 ? kWarps * cpw : kWarps;
+  const int per = max_n <= 256 ? kWarps * cpw : 1;  // large n: one CTA per column
   return (nrhs + per - 1) / per;
 }
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
@@ -784,15 +840,17 @@ void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
   } else if (max_n <= 256) {
     if (cpw == 1) EBEM_GETRS(8, 1); else EBEM_GETRS(8, kCpw);
   } else {
-    k_getrs<<<n_blocks, kThreads, size_t(smem_bytes), st>>>(tasks, block_off, n_tasks, cap);
+    const int xcap = kSmemCap / 16;
+    k_getrs_big<<<n_blocks, kBigThreads, size_t(std::min(max_n, xcap)) * 16, st>>>(
+        tasks, block_off, n_tasks, xcap);
   }
 #undef EBEM_GETRS
 }
 
 int getrs_smem_bytes(int n) {
-  // staged LU + 1 / U_kk (register kernel); the wide fallback (n > 256)
-  // stages LU + one column per warp
-  const long long b = ((long long)n * n + (n <= 256 ? n : (long long)kWarps * n)) * 16;
+  // staged LU + 1 / U_kk (register kernel, n <= 256); larger n stage only x
+  if (n > 256) return 0;
+  const long long b = ((long long)n * n + n) * 16;
   return b <= kSmemCap ? int(b) : 0;
 }
 int gemm_blocks(int m, int n) {

@@ -104,6 +104,11 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
 // CTAs per task for a batch whose largest LU has order max_n
 int getrs_cpw(int max_nrhs);  // right-hand sides per warp for a batch
 int getrs_blocks(int nrhs, int max_n, int cpw);
+// Dense-solver helpers (ebem_lu.cu): column sums of |a_ij| (1-norm), and
+// x := A^-H x with A's LU (one right-hand side, one CTA).
+void launch_col_abs_sum(const double* a, int n, int ld, double* out, cudaStream_t st);
+void launch_getrs_conj(const double* lu, int n, int ld, const int* ipiv, double* x,
+                       cudaStream_t st);
 // Blocked LU (ebem_lu.cu) of the tasks with in_smem == 0, in place.
 void launch_lu_blocked(const LuTask* tasks, int n_tasks, int max_n, cudaStream_t st);
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,

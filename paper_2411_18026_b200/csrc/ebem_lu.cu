@@ -240,3 +240,104 @@ void launch_lu_blocked(const LuTask* tasks, int n_tasks, int max_n, cudaStream_t
 }
 
 }  // namespace ebem_gpu
+
+// ----------------------------------------------- dense-solver helpers
+// (ConvSolver, proj/src/dense_solver.cpp:9-29; LuFactor, proj/src/lapack.cpp)
+namespace ebem_gpu {
+namespace {
+
+// sum_i |a_ij| of every column (one warp per column)
+__global__ void __launch_bounds__(256)
+k_col_abs_sum(const double2* __restrict__ a, int n, int ld, double* __restrict__ out) {
+  const int col = blockIdx.x * 8 + (threadIdx.x >> 5), l = threadIdx.x & 31;
+  if (col >= n) return;
+  const double2* c = a + (size_t)col * ld;
+  double s = 0.0;
+  for (int r = l; r < n; r += 32) s += hypot(c[r].x, c[r].y);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (l == 0) out[col] = s;
+}
+
+__device__ double2 zdiv_robust(double2 a, double2 b) {
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double r = b.y / b.x, d = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / d, (a.y - a.x * r) / d);
+  }
+  const double r = b.x / b.y, d = b.y + b.x * r;
+  return make_double2((a.x * r + a.y) / d, (a.y * r - a.x) / d);
+}
+
+__device__ double2 block_sum2(double2 v, double2* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double2 s = make_double2(0.0, 0.0);
+  for (int k = 0; k < int(blockDim.x >> 5); ++k) s = make_double2(s.x + red[k].x, s.y + red[k].y);
+  return s;
+}
+
+// x := A^-H x for A = P L U (LAPACK ipiv): U^H y = x, L^H z = y, x = P z.
+__global__ void __launch_bounds__(1024)
+k_getrs_conj(const double2* __restrict__ lu, int n, int ld, const int* __restrict__ ipiv,
+             double2* __restrict__ x) {
+  __shared__ double2 red[32];
+  for (int i = 0; i < n; ++i) {  // U^H is lower triangular
+    const double2* ui = lu + (size_t)i * ld;
+    double2 p = make_double2(0.0, 0.0);
+    for (int k = threadIdx.x; k < i; k += blockDim.x) {
+      const double2 u = ui[k], y = x[k];  // conj(u) y
+      p.x += u.x * y.x + u.y * y.y;
+      p.y += u.x * y.y - u.y * y.x;
+    }
+    const double2 s = block_sum2(p, red);
+    if (threadIdx.x == 0) {
+      const double2 d = make_double2(ui[i].x, -ui[i].y);
+      x[i] = zdiv_robust(make_double2(x[i].x - s.x, x[i].y - s.y), d);
+    }
+    __syncthreads();
+  }
+  for (int i = n - 1; i >= 0; --i) {  // L^H is unit upper triangular
+    const double2* li = lu + (size_t)i * ld;
+    double2 p = make_double2(0.0, 0.0);
+    for (int k = i + 1 + threadIdx.x; k < n; k += blockDim.x) {
+      const double2 l = li[k], z = x[k];
+      p.x += l.x * z.x + l.y * z.y;
+      p.y += l.x * z.y - l.y * z.x;
+    }
+    const double2 s = block_sum2(p, red);
+    if (threadIdx.x == 0) x[i] = make_double2(x[i].x - s.x, x[i].y - s.y);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int k = n - 1; k >= 0; --k) {
+      const int p = ipiv[k];
+      if (p != k) {
+        const double2 t = x[k];
+        x[k] = x[p];
+        x[p] = t;
+      }
+    }
+}
+
+}  // namespace
+
+void launch_col_abs_sum(const double* a, int n, int ld, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_col_abs_sum<<<(n + 7) / 8, 256, 0, st>>>(reinterpret_cast<const double2*>(a), n, ld, out);
+}
+
+void launch_getrs_conj(const double* lu, int n, int ld, const int* ipiv, double* x,
+                       cudaStream_t st) {
+  if (n <= 0) return;
+  k_getrs_conj<<<1, 1024, 0, st>>>(reinterpret_cast<const double2*>(lu), n, ld, ipiv,
+                                   reinterpret_cast<double2*>(x));
+}
+
+}  // namespace ebem_gpu

@@ -533,6 +533,34 @@ class Fds {
 
 // ------------------------------------------------------------ batched LA
 // Thin host helpers that upload task arrays and launch the dense kernels.
+// Dense reference solver (ConvSolver, proj/src/dense_solver.cpp:9-29).
+struct ConvStatsC {
+  double assemble_seconds = 0.0, factor_seconds = 0.0, rcond = 1.0, min_pivot = 0.0;
+  bool condition_warning = false;
+};
+class Conv {
+ public:
+  explicit Conv(Problem& p);
+  const ConvStatsC& stats() const { return stats_; }
+  int size() const { return d_; }
+  void solve_host(const double* rhs, int m, double* x);
+  // BlockAssembler::dense into a host buffer (2N x 2N, column-major)
+  static void dense_host(Problem& P, double* out);
+
+ private:
+  static void check_size(const Problem& P);
+  static void assemble(Problem& P, double* dest);
+  void apply_inv(double* x);
+  void apply_inv_h(double* x);
+  double rcond();
+  Problem& P_;
+  int d_;
+  DBuf<double> lu_;
+  DBuf<int> ipiv_, info_;
+  double norm1_ = 0.0;
+  ConvStatsC stats_;
+};
+
 void run_copies(Problem& P, const std::vector<CopyTask>& t);
 void run_gemms(Problem& P, const std::vector<GemmTask>& t);
 void run_getrs(Problem& P, const std::vector<LuSolveTask>& t);
