@@ -160,6 +160,17 @@ int ebem_gpu_build_proxy(ebem_gpu_problem* p, int node_begin, int node_end,
 int ebem_gpu_rhs_plane(ebem_gpu_problem* p, int kind, const double* angles,
                        int m, double amplitude, double* out);
 
+/* evaluate_scattered / evaluate_field (proj/src/postprocess.cpp:56-119):
+ * displacement at m points (points_xy: x0 y0 x1 y1 ...) off the boundary from
+ * the nodal solution boundary_u (2N complex), Gauss order n_gauss per element;
+ * wave_kind < 0: scattered part only, 0: + incident plane P wave, 1: + plane
+ * SV wave (angle, amplitude).  out_u: 2 complex per point (u1, u2);
+ * out_intensity: |u1|^2 + |u2|^2 per point (may be null).  invalid_argument
+ * status for a point within one element length of the curve. */
+int ebem_gpu_field(ebem_gpu_problem* p, const double* boundary_u, const double* points_xy,
+                   int m, int n_gauss, int wave_kind, double angle, double amplitude,
+                   double* out_u, double* out_intensity);
+
 /* BlockAssembler::dense (proj/src/assembly.cpp:311-330): the full 2N x 2N
  * Galerkin matrix into out (host, column-major complex); length_error
  * status past AssemblyConfig::max_dense_bytes. */

@@ -36,6 +36,7 @@
 #include "ebem/assembly.hpp"
 #include "ebem/compression.hpp"
 #include "ebem/dense_solver.hpp"
+#include "ebem/postprocess.hpp"
 #include "ebem/fds.hpp"
 #include "ebem/geometry.hpp"
 #include "ebem/hankel.hpp"
@@ -476,6 +477,34 @@ int ref_conv_solve(void* h, const double* rhs, int m, double* x,
     if (rcond) *rcond = conv.stats().rcond;
     const int n = p->mesh.size();
     put(conv.solve(get(rhs, 2 * n, m)), x);
+  });
+}
+
+// evaluate_scattered / evaluate_field (proj/src/postprocess.cpp:56-119);
+// angle < -10: scattered only.  out: (u1, u2) complex per point.
+int ref_evaluate_field(void* h, const double* u, const double* pts, int m, int ng,
+                       double angle, double amplitude, double* out) {
+  return guarded([&] {
+    auto* p = static_cast<Problem*>(h);
+    const int n = p->mesh.size();
+    Eigen::VectorXcd bu(2 * n);
+    std::memcpy(bu.data(), u, sizeof(cd) * 2 * n);
+    std::vector<Vec2> x(m);
+    for (int i = 0; i < m; ++i) x[i] = Vec2{pts[2 * i], pts[2 * i + 1]};
+    if (angle < -10.0) {
+      const std::vector<CVec2> s = evaluate_scattered(p->mesh, p->medium, bu, x, ng);
+      for (int i = 0; i < m; ++i) {
+        std::memcpy(out + 4 * i, &s[i].x, sizeof(cd));
+        std::memcpy(out + 4 * i + 2, &s[i].y, sizeof(cd));
+      }
+    } else {
+      const PlanePWave wave(p->medium, amplitude, angle);
+      const std::vector<FieldSample> s = evaluate_field(p->mesh, p->medium, wave, bu, x, ng);
+      for (int i = 0; i < m; ++i) {
+        std::memcpy(out + 4 * i, &s[i].displacement.x, sizeof(cd));
+        std::memcpy(out + 4 * i + 2, &s[i].displacement.y, sizeof(cd));
+      }
+    }
   });
 }
 

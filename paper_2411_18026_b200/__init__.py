@@ -647,6 +647,55 @@ def _host_callbacks(source: BlockSource, errors: list):
     return _BLOCK_FN(block), _BASIS_FN(basis)
 
 
+@dataclass
+class FieldSample:
+    """FieldSample, postprocess.hpp:13-18."""
+    location: tuple
+    displacement: tuple  # (u1, u2) complex
+    intensity: float
+
+
+def circle_probes(radius: float, count: int, center=(0.0, 0.0)) -> np.ndarray:
+    """Evenly spaced points on a circle (postprocess.cpp:46-54)."""
+    if radius <= 0.0 or count <= 0:
+        raise InvalidArgument("circle_probes: radius and count must be positive")
+    phi = 2.0 * math.pi * np.arange(count) / count
+    return np.stack([center[0] + radius * np.cos(phi), center[1] + radius * np.sin(phi)], 1)
+
+
+def _field(mesh, medium, u, points, n_gauss, kind, angle, amplitude, assembler):
+    u = np.asarray(u, dtype=np.complex128).ravel()
+    if u.size != 2 * mesh.size():
+        raise InvalidArgument("evaluate_scattered: boundary data size")
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 2))
+    m = pts.shape[0]
+    asm = assembler or BlockAssembler(mesh, medium, medium.default_coupling())
+    ub = np.ascontiguousarray(u).view(np.float64)
+    out = np.zeros(4 * max(m, 1))
+    inten = np.zeros(max(m, 1))
+    _check(lib().ebem_gpu_field(asm._h.h, _p(ub), _p(pts.ravel()), m, int(n_gauss), int(kind),
+                                ctypes.c_double(angle), ctypes.c_double(amplitude), _p(out),
+                                _p(inten)))
+    return pts, out[: 4 * m].view(np.complex128).reshape(m, 2), inten[:m]
+
+
+def evaluate_scattered(mesh: Mesh, medium: Medium, boundary_u, points, n_gauss: int = 8,
+                       assembler: "BlockAssembler" = None) -> np.ndarray:
+    """Scattered displacement at points off the boundary (postprocess.cpp:56-97):
+    (m, 2) complex.  Pass an existing assembler to reuse its device geometry."""
+    return _field(mesh, medium, boundary_u, points, n_gauss, -1, 0.0, 0.0, assembler)[1]
+
+
+def evaluate_field(mesh: Mesh, medium: Medium, wave, boundary_u, points, n_gauss: int = 8,
+                   assembler: "BlockAssembler" = None):
+    """Total field (incident plane wave + scattered) with intensities
+    (postprocess.cpp:99-119); PlaneSVWave also accepted."""
+    pts, u, inten = _field(mesh, medium, boundary_u, points, n_gauss, wave.kind,
+                           wave.angle, wave.amplitude, assembler)
+    return [FieldSample((float(p[0]), float(p[1])), (complex(v[0]), complex(v[1])), float(i))
+            for p, v, i in zip(pts, u, inten)]
+
+
 class ConvSolver:
     """Dense reference solver, dense_solver.hpp:21-45: full Galerkin matrix
     and one partial-pivoted LU on the device."""

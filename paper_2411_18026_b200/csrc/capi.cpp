@@ -336,6 +336,18 @@ int ebem_gpu_fds_create(ebem_gpu_problem* p, int depth,
   });
 }
 
+int ebem_gpu_field(ebem_gpu_problem* p, const double* boundary_u, const double* points_xy,
+                   int m, int n_gauss, int wave_kind, double angle, double amplitude,
+                   double* out_u, double* out_intensity) {
+  return guarded([&] {
+    if (!p || (m > 0 && (!boundary_u || !points_xy || !out_u)))
+      throw Error(EBEM_INVALID_ARGUMENT, "evaluate_scattered: null argument");
+    if (wave_kind > 1) throw Error(EBEM_INVALID_ARGUMENT, "evaluate_field: unknown wave kind");
+    p->p->field(boundary_u, points_xy, m, n_gauss, wave_kind, angle, amplitude, out_u,
+                out_intensity);
+  });
+}
+
 int ebem_gpu_dense(ebem_gpu_problem* p, double* out) {
   return guarded([&] {
     if (!p || !out) throw Error(EBEM_INVALID_ARGUMENT, "dense: null argument");

@@ -41,6 +41,13 @@ void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,
                    cudaStream_t st);
 
 // ---- incident-field right-hand sides (ebem_rhs.cu)
+// Post-processing (proj/src/postprocess.cpp): distance of m points to the
+// boundary, and the scattered (+ incident) displacement at m points.
+void launch_boundary_distance(const DevCtx* ctx, const double* pts, int m, double* out,
+                              cudaStream_t st);
+void launch_field(const DevCtx* ctx, const double* bu, const double* pts, int m, int ng,
+                  int kind, double angle, double amp, double* out_u, double* out_int,
+                  cudaStream_t st);
 void launch_rhs_plane(const DevCtx* ctx, int n_nodes, int kind,
                       const double* angles, int m, double amplitude, int rhs_n,
                       double* out, cudaStream_t st);

@@ -96,6 +96,105 @@ __global__ void k_rhs_plane(const DevCtx* __restrict__ ctx, int kind,
   o[N + g] = make_double2(b2.re, b2.im);
 }
 
+// ------------------------------------------------------- field evaluation
+// boundary_distance (proj/src/postprocess.cpp:24-30): one CTA per point
+__global__ void __launch_bounds__(256)
+k_boundary_distance(const DevCtx* __restrict__ ctx, const double* __restrict__ pts,
+                    double* __restrict__ out) {
+  __shared__ double red[8];
+  const int N = ctx->n_nodes;
+  const double x = pts[2 * blockIdx.x], y = pts[2 * blockIdx.x + 1];
+  double best = 1e300;
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    const double ax = efr(ctx, EPX, e), ay = efr(ctx, EPY, e);
+    const double bx = efr(ctx, EDX, e), by = efr(ctx, EDY, e);  // b - a
+    const double len2 = bx * bx + by * by;
+    double t = len2 > 0.0 ? ((x - ax) * bx + (y - ay) * by) / len2 : 0.0;
+    t = fmin(fmax(t, 0.0), 1.0);
+    best = fmin(best, hypot(x - (ax + t * bx), y - (ay + t * by)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) best = fmin(best, red[w]);
+    out[blockIdx.x] = fmin(best, red[0]);
+  }
+}
+
+// evaluate_scattered / evaluate_field (proj/src/postprocess.cpp:56-119):
+// u_s(x) = -sum_e sum_q w_q h_e D(x, y_q, n_e) u(y_q), u linear on each
+// element; one CTA per point, elements strided over the threads.  Optional
+// incident plane wave (kind 0 P, 1 SV; < 0 none) and intensity.
+__global__ void __launch_bounds__(256)
+k_field(const DevCtx* __restrict__ ctx, const double* __restrict__ bu,
+        const double* __restrict__ pts, int ng, int kind, double angle, double amp,
+        double* __restrict__ out_u, double* __restrict__ out_int) {
+  __shared__ cplx red[8][2];
+  const int N = ctx->n_nodes;
+  const double x = pts[2 * blockIdx.x], y = pts[2 * blockIdx.x + 1];
+  const double* gx = ctx->gx + gauss_offset(ng);
+  const double* gw = ctx->gw + gauss_offset(ng);
+  const double2* u = reinterpret_cast<const double2*>(bu);
+  cplx a1 = mk(0.0), a2 = mk(0.0);
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    const int e2 = e + 1 == N ? 0 : e + 1;
+    const double px = efr(ctx, EPX, e), py = efr(ctx, EPY, e);
+    const double dx = efr(ctx, EDX, e), dy = efr(ctx, EDY, e);
+    const double nx = efr(ctx, ENX, e), ny = efr(ctx, ENY, e);
+    const double len = efr(ctx, EH, e);
+    const double2 ua1 = u[e], ua2 = u[N + e], ub1 = u[e2], ub2 = u[N + e2];
+    for (int q = 0; q < ng; ++q) {
+      const double t = gx[q];
+      const double zx = x - (px + t * dx), zy = y - (py + t * dy);
+      const double r = hypot(zx, zy);
+      Scalars s;
+      scalars_full(ctx, r, s);
+      CMat2 d;
+      combine_D(s, zx / r, zy / r, nx, ny, d);
+      const cplx u1 = mk((1.0 - t) * ua1.x + t * ub1.x, (1.0 - t) * ua1.y + t * ub1.y);
+      const cplx u2 = mk((1.0 - t) * ua2.x + t * ub2.x, (1.0 - t) * ua2.y + t * ub2.y);
+      const double w = gw[q] * len;
+      axpy(a1, w, d.a[0] * u1 + d.a[1] * u2);
+      axpy(a2, w, d.a[2] * u1 + d.a[3] * u2);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a1.re += __shfl_xor_sync(0xffffffffu, a1.re, o);
+    a1.im += __shfl_xor_sync(0xffffffffu, a1.im, o);
+    a2.re += __shfl_xor_sync(0xffffffffu, a2.re, o);
+    a2.im += __shfl_xor_sync(0xffffffffu, a2.im, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5][0] = a1;
+    red[threadIdx.x >> 5][1] = a2;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  cplx s1 = mk(0.0), s2 = mk(0.0);
+  for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+    s1 += red[w][0];
+    s2 += red[w][1];
+  }
+  s1 = -s1;
+  s2 = -s2;
+  if (kind >= 0) {
+    double dys, dxs;
+    sincos(angle, &dys, &dxs);
+    cplx ux, uy, tx, ty;
+    wave_at(ctx->med, kind, dxs, dys, amp, x, y, 0.0, 0.0, ux, uy, tx, ty);
+    s1 += ux;
+    s2 += uy;
+  }
+  out_u[4 * blockIdx.x] = s1.re;
+  out_u[4 * blockIdx.x + 1] = s1.im;
+  out_u[4 * blockIdx.x + 2] = s2.re;
+  out_u[4 * blockIdx.x + 3] = s2.im;
+  if (out_int) out_int[blockIdx.x] = s1.re * s1.re + s1.im * s1.im + s2.re * s2.re + s2.im * s2.im;
+}
+
 __global__ void k_eval_hankel(const double* __restrict__ x, int n,
                               double* __restrict__ out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -179,6 +278,19 @@ void launch_rhs_plane(const DevCtx* ctx, int n_nodes, int kind,
   const int bs = 128;
   k_rhs_plane<<<(unsigned)((total + bs - 1) / bs), bs, 0, st>>>(
       ctx, kind, angles, m, amplitude, rhs_n, out);
+}
+
+void launch_boundary_distance(const DevCtx* ctx, const double* pts, int m, double* out,
+                              cudaStream_t st) {
+  if (m <= 0) return;
+  k_boundary_distance<<<m, 256, 0, st>>>(ctx, pts, out);
+}
+
+void launch_field(const DevCtx* ctx, const double* bu, const double* pts, int m, int ng,
+                  int kind, double angle, double amp, double* out_u, double* out_int,
+                  cudaStream_t st) {
+  if (m <= 0) return;
+  k_field<<<m, 256, 0, st>>>(ctx, bu, pts, ng, kind, angle, amp, out_u, out_int);
 }
 
 void launch_eval_hankel(const double* x, int n, double* out, cudaStream_t st) {

@@ -1577,6 +1577,45 @@ void Problem::rhs_plane(int kind, const double* angles, int m, double amp,
   CK(cudaStreamSynchronize(st_));
 }
 
+void Problem::field(const double* boundary_u, const double* pts, int m, int n_gauss,
+                    int kind, double angle, double amp, double* out_u, double* out_int) {
+  if (m <= 0) return;
+  if (n_gauss < 1 || n_gauss > kMaxGauss)
+    throw Error(EBEM_INVALID_ARGUMENT, "gauss_rule: unsupported order " + std::to_string(n_gauss));
+  double h = 0.0;  // Mesh::max_length
+  for (int e = 0; e < n_; ++e) {
+    const int f = e + 1 == n_ ? 0 : e + 1;
+    h = std::max(h, std::hypot(xy_[2 * f] - xy_[2 * e], xy_[2 * f + 1] - xy_[2 * e + 1]));
+  }
+  DBuf<double> dp, dd, du, dout, dint;
+  dp.alloc(2 * size_t(m));
+  dd.alloc(m);
+  CK(cudaMemcpyAsync(dp.get(), pts, 16 * size_t(m), cudaMemcpyHostToDevice, st_));
+  launch_boundary_distance(dctx(), dp.get(), m, dd.get(), st_);
+  std::vector<double> dist(m);
+  CK(cudaMemcpyAsync(dist.data(), dd.get(), 8 * size_t(m), cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+  for (int p = 0; p < m; ++p)
+    if (dist[p] <= h)
+      throw Error(EBEM_INVALID_ARGUMENT,
+                  "evaluate_scattered: point (" + std::to_string(pts[2 * p]) + ", " +
+                      std::to_string(pts[2 * p + 1]) + ") is " + std::to_string(dist[p]) +
+                      " from the boundary; offset it beyond one element length (" +
+                      std::to_string(h) + ")");
+  du.alloc(4 * size_t(n_));
+  dout.alloc(4 * size_t(m));
+  if (out_int) dint.alloc(m);
+  CK(cudaMemcpyAsync(du.get(), boundary_u, 32 * size_t(n_), cudaMemcpyHostToDevice, st_));
+  launch_field(dctx(), du.get(), dp.get(), m, n_gauss, kind, angle, amp, dout.get(),
+               out_int ? dint.get() : nullptr, st_);
+  ++g_launches;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_u, dout.get(), 32 * size_t(m), cudaMemcpyDeviceToHost, st_));
+  if (out_int)
+    CK(cudaMemcpyAsync(out_int, dint.get(), 8 * size_t(m), cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+}
+
 // ------------------------------------------------------------ batched LA
 namespace {
 // k_getrs stages the LU in shared memory up to this many bytes per launch

@@ -363,6 +363,10 @@ class Problem {
   void true_block_host(const Lists& rows, const Lists& cols, double* out);
   void rhs_plane(int kind, const double* angles, int m, double amp,
                  double* out_host);
+  // evaluate_scattered / evaluate_field (proj/src/postprocess.cpp:56-119);
+  // kind < 0: scattered only.  Host buffers.
+  void field(const double* boundary_u, const double* pts, int m, int n_gauss, int kind,
+             double angle, double amp, double* out_u, double* out_int);
 
   // scratch shared by the drivers (process-wide, see Scratch)
   Staging& staging;

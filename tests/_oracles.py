@@ -219,6 +219,18 @@ class RefProblem:
                                                    _D(amplitude), _ptr(out)))
         return cplx_from(out, 2 * self.n, a.size)
 
+    def evaluate_field(self, u, pts, ng=8, angle=None, amplitude=1.0):
+        """evaluate_scattered (angle None) / evaluate_field with a P wave:
+        (m, 2) complex displacements."""
+        ub = to_buf(np.asarray(u, dtype=np.complex128).reshape(-1, 1))
+        p = np.ascontiguousarray(pts, dtype=np.float64).ravel()
+        m = p.size // 2
+        out = np.zeros(4 * m)
+        self.ref._chk(self.ref.lib.ref_evaluate_field(
+            self.h, _ptr(ub), _ptr(p), m, ng, _D(-100.0 if angle is None else angle),
+            _D(amplitude), _ptr(out)))
+        return out.view(np.complex128).reshape(m, 2)
+
     def conv_solve(self, rhs):
         rhs = np.asarray(rhs, dtype=np.complex128).reshape(2 * self.n, -1)
         m = rhs.shape[1]
