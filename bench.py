@@ -44,7 +44,7 @@ LEAF = 32
 # Algorithmic FP64 flops per quadrature-point evaluation (DESIGN.md,
 # "Roofline"): FP64 instructions per point counted by ncu on the kernels
 # (DADD + DMUL + 2 DFMA), divided by the point evaluations of the launch.
-FLOPS_PER_POINT = {"k_near_onesided": 947.0, "k_proxy_pairs": 1071.3, "k_near_sym": 1114.1}
+FLOPS_PER_POINT = {"k_near_onesided": 723.1, "k_proxy_pairs": 837.8, "k_near_sym": 1006.5}
 
 
 def config_dict():

@@ -38,6 +38,9 @@ struct ParSeries {
   int par[10], nt[10];
   double2 a[10][kParTerms];
   double2 b[10][kParTerms];
+  // Per-point truncation of the D/N series (scalars 2..9): a point at
+  // distance r needs 1 + #{t >= 1 : r > rcut[t]} terms (+inf past nt).
+  double rcut[kParTerms];
 };
 
 // Fill-kernel parameter block, passed by value as a __grid_constant__ kernel

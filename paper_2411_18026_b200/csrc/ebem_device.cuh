@@ -380,6 +380,7 @@ struct SerSm {
   int ntmax;
   double2 at[kParTerms][8];
   double2 bt[kParTerms][8];
+  double rcut[kParTerms];
 };
 
 __device__ __forceinline__ void load_sersm(const DevCtx* __restrict__ ctx, SerSm& s) {
@@ -390,6 +391,7 @@ __device__ __forceinline__ void load_sersm(const DevCtx* __restrict__ ctx, SerSm
     s.at[p][k] = ctx->pser.a[k + 2][p];
     s.bt[p][k] = ctx->pser.b[k + 2][p];
   }
+  for (int i = tid; i < kParTerms; i += nth) s.rcut[i] = ctx->pser.rcut[i];
   if (tid == 0) {
     int m = 0;
     for (int k = 0; k < 8; ++k) m = ctx->pser.nt[k + 2] > m ? ctx->pser.nt[k + 2] : m;
@@ -427,7 +429,9 @@ __device__ __forceinline__ void series_joint(const SerSm& S, double u,
   cplx A[8], B[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) A[k] = B[k] = mk(0.0);
-  for (int p = S.ntmax - 1; p >= 0; --p) {
+  int nt = 1;  // the terms this r needs (ParSeries::rcut)
+  for (int t = 1; t < S.ntmax; ++t) nt += r > S.rcut[t];
+  for (int p = nt - 1; p >= 0; --p) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const double2 a = S.at[p][k], b = S.bt[p][k];

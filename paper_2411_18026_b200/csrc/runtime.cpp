@@ -394,6 +394,50 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
       for (int p = nt; p < kParTerms; ++p) ps.a[k][p] = ps.b[k][p] = double2{0.0, 0.0};
       ps.nt[k] = nt;
     }
+    // The same criterion point by point: on a fine geometric grid below the
+    // series radius find how many terms each r needs (the largest count over
+    // scalars 2..9, evaluated at the upper end of each grid interval), and
+    // record the radius past which t + 1 terms are needed.
+    {
+      ParSeries& ps = hctx_.pser;
+      int ntmax = 1;
+      for (int k = 2; k < 10; ++k) ntmax = std::max(ntmax, ps.nt[k]);
+      auto need = [&](double r) {
+        const double lr = std::fabs(std::log(r));
+        int worst = 1;
+        for (int k = 2; k < 10; ++k) {
+          double big = 0.0, mag[kParTerms];
+          for (int p = 0; p < ps.nt[k]; ++p) {
+            const double2 a = ps.a[k][p], b = ps.b[k][p];
+            mag[p] = (std::hypot(a.x, a.y) + std::hypot(b.x, b.y) * lr) *
+                     std::pow(r, ps.par[k] + 2 * p);
+            big = std::max(big, mag[p]);
+          }
+          int nt = ps.nt[k];
+          while (nt > 1 && mag[nt - 1] <= 1e-22 * big) --nt;
+          worst = std::max(worst, nt);
+        }
+        return worst;
+      };
+      for (int t = 0; t < kParTerms; ++t) ps.rcut[t] = t < ntmax ? 0.0 : HUGE_VAL;
+      // walking down from the series radius: rcut[t] = the largest grid r at
+      // and below which every grid point needs <= t terms
+      std::vector<int> needs;
+      std::vector<double> rs;
+      for (double r = rmax; r > rmax * 1e-12; r *= 0.98) {
+        rs.push_back(r);
+        needs.push_back(need(r));
+      }
+      for (int t = 1; t < ntmax; ++t) {
+        int g = int(rs.size());  // first index of the tail with need <= t
+        while (g > 0 && needs[g - 1] <= t) --g;
+        if (g < int(rs.size())) ps.rcut[t] = rs[g];
+        if (g == 0) ps.rcut[t] = HUGE_VAL;
+      }
+      if (getenv("EBEM_VERBOSE") && atoi(getenv("EBEM_VERBOSE")) >= 2)
+        for (int t = 1; t < ntmax; ++t)
+          fprintf(stderr, "series: r > %.3e needs > %d terms\n", ps.rcut[t], t);
+    }
   } catch (const std::logic_error& e) {
     throw Error(EBEM_LOGIC_ERROR, e.what());
   }
