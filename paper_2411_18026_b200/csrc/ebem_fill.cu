@@ -12,6 +12,7 @@
 //                     adjacent (Duffy) pairs (proj/src/assembly.cpp:70-246)
 //   k_gather          ordered scatter of bundles into output blocks
 //                     (proj/src/assembly.cpp:373-407, :493-506)
+#include <stdexcept>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -352,25 +353,68 @@ k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
   pair_job[p] = jb;  // read back by the near-field kernel (no second search)
 }
 
+// One record per sorted near pair (skip class excluded): the element geometry
+// and output slots the near-field kernel needs, laid out so one CTA stages a
+// whole group of pairs with contiguous async copies (no dependent index
+// chain on the compute kernel's critical path).
+__global__ void __launch_bounds__(256)
+k_sym_records(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
+              const int* __restrict__ elems, const int* __restrict__ sorted_ids,
+              const int* __restrict__ pair_job, const int* __restrict__ class_bounds,
+              double* __restrict__ recs) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= __ldg(class_bounds + kSymClasses - 1)) return;  // skip class at the end
+  const int p = __ldg(sorted_ids + idx);
+  const SymJob J = jobs[__ldg(pair_job + p)];
+  const long long local = p - J.local_off;
+  const int a = int(local / J.nE);
+  const int q = int(local - (long long)a * J.nE);
+  const int ea = __ldg(elems + J.a_off + a);
+  const int eb = __ldg(elems + J.e_off + q);
+  double r[kSymRec];
+  const int f[6] = {EPX, EPY, EDX, EDY, ENX, ENY};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    r[SR_A + k] = ef(ctx, f[k], ea);
+    r[SR_B + k] = ef(ctx, f[k], eb);
+  }
+  r[SR_VD] = __longlong_as_double(J.v_off + local);
+  r[SR_UD] = __longlong_as_double(J.u_off + (long long)q * J.nA + a);
+  r[SR_HH] = ef(ctx, EH, ea) * ef(ctx, EH, eb);
+  r[15] = 0.0;
+  double2* o = reinterpret_cast<double2*>(recs + idx * kSymRec);
+#pragma unroll
+  for (int k = 0; k < kSymRec / 2; ++k) o[k] = make_double2(r[2 * k], r[2 * k + 1]);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
+
 // CTA = P pairs x n threads; thread (pair, i) fixes the test point s_i on the
 // enclosed element and sweeps the n points on the cell element, evaluating
-// the scalars once for both orientations (r is symmetric).
+// the scalars once for both orientations (r is symmetric).  The records of
+// the next pair group are copied into shared memory (cp.async) while the
+// current group is evaluated.
 #ifndef EBEM_SYM_THREADS
 #define EBEM_SYM_THREADS 256
 #endif
-constexpr int kSymMaxPairs = EBEM_SYM_THREADS;  // P = threads / n pairs per CTA
 #ifndef EBEM_SYM_MINB
 #define EBEM_SYM_MINB 1
 #endif
 template <bool BOTH>
 __global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
 k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
-           const SymJob* __restrict__ jobs,
-           const long long* __restrict__ job_off, int n_jobs,
-           const int* __restrict__ elems, const int* __restrict__ sorted_ids,
-           const int* __restrict__ pair_job, const int* __restrict__ class_bounds,
+           const double* __restrict__ recs, const int* __restrict__ class_bounds,
            int cls, int n, double* __restrict__ bundles) {
-  extern __shared__ double2 sh[];  // [P * n][8 V + 8 U cplx + 2 (Q as re/im pairs)]
+  // dynamic: [P * n][8 V + 8 U cplx + 2 (Q as re/im pairs)], then the two
+  // record buffers [2][P][kSymRec]
+  extern __shared__ double2 sh[];
   __shared__ SerSm S;
   __shared__ double sgx[kMaxGauss], sgw[kMaxGauss];
   // this class's pairs, from the device-side bucket bounds (no host sync)
@@ -378,7 +422,17 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
   const int count = __ldg(class_bounds + cls + 1) - first;
   const int P = blockDim.x / n;
   if ((int)blockIdx.x * P >= count) return;  // uniform per CTA
-  const int* __restrict__ pair_ids = sorted_ids + first;
+  double* const s_rec = reinterpret_cast<double*>(sh + blockDim.x * 18);  // [2][P][rec]
+  const double* __restrict__ crec = recs + (long long)first * kSymRec;
+  // stage the records of the group starting at pair g (16 B per copy)
+  auto stage = [&](int g, int buf) {
+    const int np = min(P, count - g);
+    const double* src = crec + (long long)g * kSymRec;
+    for (int c = threadIdx.x; c < np * (kSymRec / 2); c += blockDim.x)
+      cp_async16(s_rec + buf * P * kSymRec + 2 * c, src + 2 * c);
+  };
+  stage(blockIdx.x * P, 0);
+  cp_async_commit();
   load_sersm(ctx, S);
   if (threadIdx.x < n) {
     sgx[threadIdx.x] = ctx->gx[gauss_offset(n) + threadIdx.x];
@@ -388,34 +442,25 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
   const int i = threadIdx.x - lp * n;
   const double* gx = sgx;
   const double* gw = sgw;
-  // one job lookup per pair (not per thread), shared with the reduction
-  __shared__ int s_ea[kSymMaxPairs], s_eb[kSymMaxPairs];
-  __shared__ long long s_vd[kSymMaxPairs], s_ud[kSymMaxPairs];
   // persistent CTAs stride over the class's pair groups
-  for (int base = blockIdx.x * P; base < count; base += gridDim.x * P) {
+  int buf = 0;
+  for (int base = blockIdx.x * P; base < count; base += gridDim.x * P, buf ^= 1) {
+  const int nxt = base + gridDim.x * P;
+  if (nxt < count) stage(nxt, buf ^ 1);
+  cp_async_commit();  // (possibly empty group: keeps the wait count uniform)
+  cp_async_wait1();
+  __syncthreads();
+  const double* rec_all = s_rec + buf * P * kSymRec;
   const int idx = base + lp;
   const bool active = lp < P && idx < count;
-  if (active && i == 0) {
-    const long long p = __ldg(pair_ids + idx);
-    const int jb = __ldg(pair_job + p);
-    const SymJob J = jobs[jb];
-    const long long local = p - J.local_off;
-    const int a = int(local / J.nE);
-    const int q = int(local - (long long)a * J.nE);
-    s_ea[lp] = __ldg(elems + J.a_off + a);
-    s_eb[lp] = __ldg(elems + J.e_off + q);
-    s_vd[lp] = J.v_off + local;
-    s_ud[lp] = J.u_off + (long long)q * J.nA + a;
-  }
-  __syncthreads();
   if (active) {
-    const int ea = s_ea[lp], eb = s_eb[lp];
-    const double pax = ef(ctx, EPX, ea), pay = ef(ctx, EPY, ea);
-    const double dax = ef(ctx, EDX, ea), day = ef(ctx, EDY, ea);
-    const double pbx = ef(ctx, EPX, eb), pby = ef(ctx, EPY, eb);
-    const double dbx = ef(ctx, EDX, eb), dby = ef(ctx, EDY, eb);
-    const double nax = ef(ctx, ENX, ea), nay = ef(ctx, ENY, ea);
-    const double nbx = ef(ctx, ENX, eb), nby = ef(ctx, ENY, eb);
+    const double* R = rec_all + lp * kSymRec;
+    const double pax = R[SR_A + 0], pay = R[SR_A + 1];
+    const double dax = R[SR_A + 2], day = R[SR_A + 3];
+    const double nax = R[SR_A + 4], nay = R[SR_A + 5];
+    const double pbx = R[SR_B + 0], pby = R[SR_B + 1];
+    const double dbx = R[SR_B + 2], dby = R[SR_B + 3];
+    const double nbx = R[SR_B + 4], nby = R[SR_B + 5];
     const cplx alpha = mk(fc.med.alpha_re, fc.med.alpha_im);
     const double qfac = fc.med.qfactor;
     const double s = gx[i];
@@ -504,11 +549,12 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
       const double2 qq = row[16 + (e >> 1)];
       qs = fma(wi, (e & 1) ? qq.y : qq.x, qs);
     }
-    const double hh = ef(ctx, EH, s_ea[lp2]) * ef(ctx, EH, s_eb[lp2]);
+    const double* R2 = rec_all + lp2 * kSymRec;
+    const double hh = R2[SR_HH];
     const double sg = (la == lb) ? 1.0 : -1.0;  // slope_la * slope_lb
     const double re = fma(hh, ar, sg * qs * alpha.re);
     const double im = fma(hh, ai, sg * qs * alpha.im);
-    const long long dst = orient == 0 ? s_vd[lp2] : s_ud[lp2];
+    const long long dst = __double_as_longlong(orient == 0 ? R2[SR_VD] : R2[SR_UD]);
     reinterpret_cast<double2*>(bundles)[dst * kBundle + k] = make_double2(re, im);
   }
   __syncthreads();  // shared row sums and pair records are reused
@@ -709,15 +755,23 @@ void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
       ctx, jobs, job_off, n_jobs, elems, n_pairs, keys, vals, pair_job);
 }
 
-void launch_near_sym(const DevCtx* ctx, const FillConst& fc,
-                     const SymJob* jobs, const long long* job_off, int n_jobs,
-                     const int* elems, const int* sorted_ids, const int* pair_job,
-                     const int* class_bounds, int cls, long long max_count, int n,
-                     bool both, double* bundles, cudaStream_t st) {
+void launch_sym_records(const DevCtx* ctx, const SymJob* jobs, const int* elems,
+                        const int* sorted_ids, const int* pair_job,
+                        const int* class_bounds, long long n_pairs, double* recs,
+                        cudaStream_t st) {
+  if (n_pairs <= 0) return;
+  k_sym_records<<<(unsigned)((n_pairs + 255) / 256), 256, 0, st>>>(
+      ctx, jobs, elems, sorted_ids, pair_job, class_bounds, recs);
+}
+
+void launch_near_sym(const DevCtx* ctx, const FillConst& fc, const double* recs, const int* class_bounds,
+                     int cls, long long max_count, int n, bool both, double* bundles,
+                     cudaStream_t st) {
   if (max_count <= 0) return;
   const int P = EBEM_SYM_THREADS / n;
   const int threads = P * n;
-  const size_t smem = size_t(threads) * 18 * sizeof(double2);
+  const size_t smem = size_t(threads) * 18 * sizeof(double2) +
+                      size_t(2 * P) * kSymRec * sizeof(double);
   // persistent grid: a few CTAs per SM, never more than the largest count needs
   static const int n_sm = [] {
     int dev = 0, v = 0;
@@ -730,9 +784,9 @@ void launch_near_sym(const DevCtx* ctx, const FillConst& fc,
 #define EBEM_SYM_LAUNCH(B)                                                          \
   do {                                                                              \
     cudaFuncSetAttribute(k_near_sym<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         EBEM_SYM_THREADS * 18 * (int)sizeof(double2));             \
-    k_near_sym<B><<<grid, threads, smem, st>>>(ctx, fc, jobs, job_off, n_jobs, elems, \
-                                               sorted_ids, pair_job, class_bounds, cls, n, \
+                         EBEM_SYM_THREADS * (18 * (int)sizeof(double2) +        \
+                                             2 * kSymRec * (int)sizeof(double)));  \
+    k_near_sym<B><<<grid, threads, smem, st>>>(ctx, fc, recs, class_bounds, cls, n,  \
                                                bundles);                            \
   } while (0)
   if (both) EBEM_SYM_LAUNCH(true);

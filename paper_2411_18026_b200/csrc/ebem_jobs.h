@@ -56,6 +56,12 @@ struct SymJob {
 // pairs, handled by k_near_singular, and the lower triangle of tri jobs).
 constexpr int kSymClasses = 9;
 
+// Sorted near-pair record, 16 doubles (128 B): geometry of the enclosed
+// element a and the cell element b (px, py, dx, dy, nx, ny each), the two
+// bundle slots (as long long bit patterns), h_a h_b, padding.
+constexpr int kSymRec = 16;
+enum SymRecField { SR_A = 0, SR_B = 6, SR_VD = 12, SR_UD = 13, SR_HH = 14 };
+
 // Scatter of bundles into one output block.
 struct GatherJob {
   long long pair_off;   // bundle index of (row element 0, col element 0)

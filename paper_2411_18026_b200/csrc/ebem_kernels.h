@@ -16,13 +16,17 @@ void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
                          const long long* job_off, int n_jobs, const int* elems,
                          long long n_pairs, unsigned char* keys, int* vals,
                          int* pair_job, cudaStream_t st);
+// Records of the sorted near pairs (kSymRec doubles each: both elements'
+// geometry, the two bundle slots, the Jacobian product), in class order.
+void launch_sym_records(const DevCtx* ctx, const SymJob* jobs, const int* elems,
+                        const int* sorted_ids, const int* pair_job,
+                        const int* class_bounds, long long n_pairs, double* recs,
+                        cudaStream_t st);
 // One launch per near-pair class cls; the class's range of the sorted pair
-// ids is read from class_bounds on the device (max_count bounds the grid).
-void launch_near_sym(const DevCtx* ctx, const FillConst& fc,
-                     const SymJob* jobs, const long long* job_off, int n_jobs,
-                     const int* elems, const int* sorted_ids, const int* pair_job,
-                     const int* class_bounds, int cls, long long max_count, int n,
-                     bool both, double* bundles, cudaStream_t st);
+// records is read from class_bounds on the device (max_count bounds the grid).
+void launch_near_sym(const DevCtx* ctx, const FillConst& fc, const double* recs, const int* class_bounds,
+                     int cls, long long max_count, int n, bool both, double* bundles,
+                     cudaStream_t st);
 // CUB radix sort of (key, value) by the low 3 key bits; temp grows as needed.
 void sort_pairs_by_class(unsigned char* keys_in, unsigned char* keys_out,
                          int* vals_in, int* vals_out, long long n, void** temp,

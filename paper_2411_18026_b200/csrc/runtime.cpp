@@ -338,6 +338,7 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
       id_r_(scratch().id_r),
       sym_keys_(scratch().sym_keys),
       sym_vals_(scratch().sym_vals),
+      sym_recs_(scratch().sym_recs),
       sort_temp_(scratch().sort_temp),
       sort_temp_bytes_(scratch().sort_temp_bytes),
       sym_bounds_(scratch().sym_bounds),
@@ -497,6 +498,7 @@ Problem::Problem(int n)
       id_r_(scratch().id_r),
       sym_keys_(scratch().sym_keys),
       sym_vals_(scratch().sym_vals),
+      sym_recs_(scratch().sym_recs),
       sort_temp_(scratch().sort_temp),
       sort_temp_bytes_(scratch().sort_temp_bytes),
       sym_bounds_(scratch().sym_bounds),
@@ -1154,7 +1156,10 @@ void Problem::execute(FillPlan& plan) {
                         vin + 2 * nsym, st_);
     sort_pairs_by_class(kin, kout, vin, vout, nsym, &sort_temp_, &sort_temp_bytes_, st_);
     launch_class_bounds(kout, nsym, sym_bounds_.get(), st_);
-    g_launches += 3;
+    sym_recs_.ensure(size_t(kSymRec) * nsym);
+    launch_sym_records(dctx(), sj, el, vout, vin + 2 * nsym, sym_bounds_.get(), nsym,
+                       sym_recs_.get(), st_);
+    g_launches += 4;
   }
   if (!plan.proxy_.empty()) {
     double pts = 0.0;
@@ -1170,15 +1175,13 @@ void Problem::execute(FillPlan& plan) {
     // one launch per class, sized by the wave's pair count; each reads its
     // range from the device-side bounds (no host round trip)
     const int add[4] = {0, 2, 5, 9};
-    const int* vout = sym_vals_.get() + nsym;
     for (int c = 0; c < kSymClasses - 1; ++c) {  // the last class is "skip"
       const int tier = c & 3;
       const bool both = c < 4;  // classes 4..7: one-sided true blocks
       if (both ? !plan.has_two_sided_ : !plan.has_one_sided_) continue;
       const int nq = int((acfg_.far_nodes + add[tier]) * acfg_.refine + 0.5);
       g_prof.begin(st_);
-      launch_near_sym(dctx(), fc_, sj, so, int(plan.sym_.size()), el, vout,
-                      sym_vals_.get() + 2 * nsym, sym_bounds_.get(), c, nsym, nq, both,
+      launch_near_sym(dctx(), fc_, sym_recs_.get(), sym_bounds_.get(), c, nsym, nq, both,
                       bundles.get(), st_);
       // points = class count x nq^2, read back at collect time
       g_prof.end_counted(both ? KP_NEAR_SYM : KP_NEAR_1S, st_, sym_bounds_.get() + c,

@@ -302,6 +302,7 @@ struct Scratch {
   DBuf<double> id_rd, id_r;
   DBuf<unsigned char> sym_keys;
   DBuf<int> sym_vals;
+  DBuf<double> sym_recs;  // kSymRec doubles per sorted near pair
   void* sort_temp = nullptr;
   size_t sort_temp_bytes = 0;
   DBuf<int> sym_bounds;
@@ -378,6 +379,7 @@ class Problem {
   DBuf<double>& id_r_;
   DBuf<unsigned char>& sym_keys_;   // 2 x pairs (in, out)
   DBuf<int>& sym_vals_;             // 2 x pairs (in, out)
+  DBuf<double>& sym_recs_;          // sorted pair records (geometry, outputs)
   void*& sort_temp_;
   size_t& sort_temp_bytes_;
   DBuf<int>& sym_bounds_;
