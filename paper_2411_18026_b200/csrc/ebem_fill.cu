@@ -407,19 +407,18 @@ __device__ __forceinline__ void cp_async_wait1() {
 #ifndef EBEM_SYM_MINB
 #define EBEM_SYM_MINB 1
 #endif
-template <bool BOTH>
-__global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
-k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
-           const double* __restrict__ recs, const int* __restrict__ class_bounds,
-           int cls, int n, double* __restrict__ bundles) {
+// PROXY: the proxy blocks (kernel_cross_block, assembly.cpp:424-509) — full
+// n scalars, no static hypersingular part, records with a negative V slot
+// are padding.
+template <bool BOTH, bool PROXY>
+__device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const FillConst& fc,
+                                          const double* __restrict__ recs, int first,
+                                          int count, int n, double* __restrict__ bundles) {
   // dynamic: [P * n][8 V + 8 U cplx + 2 (Q as re/im pairs)], then the two
   // record buffers [2][P][kSymRec]
   extern __shared__ double2 sh[];
   __shared__ SerSm S;
   __shared__ double sgx[kMaxGauss], sgw[kMaxGauss];
-  // this class's pairs, from the device-side bucket bounds (no host sync)
-  const int first = __ldg(class_bounds + cls);
-  const int count = __ldg(class_bounds + cls + 1) - first;
   const int P = blockDim.x / n;
   if ((int)blockIdx.x * P >= count) return;  // uniform per CTA
   double* const s_rec = reinterpret_cast<double*>(sh + blockDim.x * 18);  // [2][P][rec]
@@ -452,9 +451,10 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
   __syncthreads();
   const double* rec_all = s_rec + buf * P * kSymRec;
   const int idx = base + lp;
-  const bool active = lp < P && idx < count;
+  const double* R = rec_all + lp * kSymRec;
+  const bool active = lp < P && idx < count &&
+                      (!PROXY || __double_as_longlong(R[SR_VD]) >= 0);
   if (active) {
-    const double* R = rec_all + lp * kSymRec;
     const double pax = R[SR_A + 0], pay = R[SR_A + 1];
     const double dax = R[SR_A + 2], day = R[SR_A + 3];
     const double nax = R[SR_A + 4], nay = R[SR_A + 5];
@@ -481,7 +481,7 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
       const double logr = log(r);
       const double zhx = ir * zx, zhy = ir * zy;
       DN dn;
-      dn_eval<true>(fc, S, r, ir, logr, dn);
+      dn_eval<!PROXY>(fc, S, r, ir, logr, dn);
       const double pt[2] = {wj * (1.0 - t), wj * t};
       CMat2 dm, nm;
       // V: test on the enclosed element (normal na), trial on the cell element
@@ -504,11 +504,13 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
           axpy(ru[1][e], pt[1], k);
         }
       }
-      // integrated-by-parts static hypersingular kernel (even in zh)
-      const double lq = qfac * logr;
-      Q[0] = fma(wj, lq - qfac * (zhx * zhx), Q[0]);
-      Q[1] = fma(wj, -qfac * (zhx * zhy), Q[1]);
-      Q[3] = fma(wj, lq - qfac * (zhy * zhy), Q[3]);
+      if (!PROXY) {
+        // integrated-by-parts static hypersingular kernel (even in zh)
+        const double lq = qfac * logr;
+        Q[0] = fma(wj, lq - qfac * (zhx * zhx), Q[0]);
+        Q[1] = fma(wj, -qfac * (zhx * zhy), Q[1]);
+        Q[3] = fma(wj, lq - qfac * (zhy * zhy), Q[3]);
+      }
     }
     Q[2] = Q[1];
     double2* my = sh + threadIdx.x * 18;
@@ -519,8 +521,10 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
         my[b * 4 + e] = make_double2(rv[b][e].re, rv[b][e].im);
         my[8 + b * 4 + e] = make_double2(ru[b][e].re, ru[b][e].im);
       }
-    my[16] = make_double2(Q[0], Q[1]);
-    my[17] = make_double2(Q[2], Q[3]);
+    if (!PROXY) {
+      my[16] = make_double2(Q[0], Q[1]);
+      my[17] = make_double2(Q[2], Q[3]);
+    }
   }
   __syncthreads();
   // reduction over i; each pair's first thread handles nothing special:
@@ -534,6 +538,8 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
     const int k = rem - orient * kBundle;  // bidx(la, lb, i, j)
     const int idx2 = base + lp2;
     if (idx2 >= count) continue;
+    const double* R2 = rec_all + lp2 * kSymRec;
+    if (PROXY && __double_as_longlong(R2[SR_VD]) < 0) continue;
     const int la = k >> 3, lb = (k >> 2) & 1, e = k & 3;
     double ar = 0.0, ai = 0.0, qs = 0.0;
     for (int ii = 0; ii < n; ++ii) {
@@ -546,14 +552,15 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
       const double2 v = row[slot];
       ar = fma(wi * shape, v.x, ar);
       ai = fma(wi * shape, v.y, ai);
-      const double2 qq = row[16 + (e >> 1)];
-      qs = fma(wi, (e & 1) ? qq.y : qq.x, qs);
+      if (!PROXY) {
+        const double2 qq = row[16 + (e >> 1)];
+        qs = fma(wi, (e & 1) ? qq.y : qq.x, qs);
+      }
     }
-    const double* R2 = rec_all + lp2 * kSymRec;
     const double hh = R2[SR_HH];
     const double sg = (la == lb) ? 1.0 : -1.0;  // slope_la * slope_lb
-    const double re = fma(hh, ar, sg * qs * alpha.re);
-    const double im = fma(hh, ai, sg * qs * alpha.im);
+    const double re = PROXY ? hh * ar : fma(hh, ar, sg * qs * alpha.re);
+    const double im = PROXY ? hh * ai : fma(hh, ai, sg * qs * alpha.im);
     const long long dst = __double_as_longlong(orient == 0 ? R2[SR_VD] : R2[SR_UD]);
     reinterpret_cast<double2*>(bundles)[dst * kBundle + k] = make_double2(re, im);
   }
@@ -561,39 +568,42 @@ k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
   }
 }
 
+template <bool BOTH>
+__global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
+k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
+           const double* __restrict__ recs, const int* __restrict__ class_bounds,
+           int cls, int n, double* __restrict__ bundles) {
+  // this class's pairs, from the device-side bucket bounds (no host sync)
+  const int first = __ldg(class_bounds + cls);
+  const int count = __ldg(class_bounds + cls + 1) - first;
+  near_body<BOTH, false>(ctx, fc, recs, first, count, n, bundles);
+}
+
 // ------------------------------------------------------------------- proxy
-// CTA = kProxyPairs element pairs x n_g threads; thread (pair, i) fixes the
-// polygon quadrature point s_i and sweeps the curve points t_j.  The row sums
-// of both orientations go through shared memory and are reduced over i.
+// Proxy blocks: one record per (polygon element, curve element) slot of each
+// job's CTA tiles (kProxyTile slots per tile; the tail of a job's last tile
+// is padding, marked by a negative V slot).  The polygon element is the test
+// side of V ("a"), the curve element the trial side ("b").
 constexpr int kProxyThreads = 256;
 
-#ifndef EBEM_PROXY_MINB
-#define EBEM_PROXY_MINB 1
-#endif
-__global__ void __launch_bounds__(kProxyThreads, EBEM_PROXY_MINB)
-k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
-              const ProxyJob* __restrict__ jobs,
-              const int* __restrict__ job_block_off, int n_jobs,
-              const int* __restrict__ elems, double* __restrict__ bundles,
-              int kProxyPairs) {
-  extern __shared__ double2 sh[];  // [kProxyPairs * ng][2 orient][2][4]
-  __shared__ SerSm S;
-  load_sersm(ctx, S);
-  __syncthreads();
-  const int ng = ctx->proxy_n;
-  const int m = ctx->m_prime;
-  const int jb = find_job(job_block_off, n_jobs, (int)blockIdx.x);
+__global__ void __launch_bounds__(256)
+k_proxy_records(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ jobs,
+                const int* __restrict__ job_block_off, int n_jobs,
+                const int* __restrict__ elems, long long n_slots, int tile,
+                double* __restrict__ recs) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= n_slots) return;
+  const int blk = int(t / tile);
+  const int jb = find_job(job_block_off, n_jobs, blk);
   const ProxyJob J = jobs[jb];
-  const int npairs = m * J.nE;
-  const int pair0 = (blockIdx.x - J.block_off) * kProxyPairs;
-  const int lp = threadIdx.x / ng;
-  const int i = threadIdx.x - lp * ng;
-  const int pair = pair0 + lp;
-  const bool active = lp < kProxyPairs && pair < npairs;
-  const double* gx = ctx->gx + gauss_offset(ng);
-  const double* gw = ctx->gw + gauss_offset(ng);
-
-  if (active) {
+  const int m = ctx->m_prime;
+  const int pair = (blk - J.block_off) * tile + int(t - (long long)blk * tile);
+  double r[kSymRec];
+#pragma unroll
+  for (int k = 0; k < kSymRec; ++k) r[k] = 0.0;
+  if (pair >= m * J.nE) {
+    r[SR_VD] = __longlong_as_double(-1LL);
+  } else {
     const int pe = pair / J.nE;
     const int q = pair - pe * J.nE;
     const int eb = __ldg(elems + J.e_off + q);
@@ -606,97 +616,31 @@ k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst 
     const double pdx = p1x - p0x, pdy = p1y - p0y;
     const double hp = hypot(pdx, pdy);
     const double ptx = pdx / hp, pty = pdy / hp;
-    const double pnx = -pty, pny = ptx;
-    const double mpx = ef(ctx, EPX, eb), mpy = ef(ctx, EPY, eb);
-    const double mdx = ef(ctx, EDX, eb), mdy = ef(ctx, EDY, eb);
-    const double mnx = ef(ctx, ENX, eb), mny = ef(ctx, ENY, eb);
-    const cplx alpha = mk(ctx->med.alpha_re, ctx->med.alpha_im);
+    r[SR_A + 0] = p0x;
+    r[SR_A + 1] = p0y;
+    r[SR_A + 2] = pdx;
+    r[SR_A + 3] = pdy;
+    r[SR_A + 4] = -pty;
+    r[SR_A + 5] = ptx;
+    const int f[6] = {EPX, EPY, EDX, EDY, ENX, ENY};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) r[SR_B + k] = ef(ctx, f[k], eb);
+    r[SR_VD] = __longlong_as_double(J.v_off + pair);
+    r[SR_UD] = __longlong_as_double(J.u_off + (long long)q * m + pe);
+    r[SR_HH] = hp * ef(ctx, EH, eb);
+  }
+  double2* o = reinterpret_cast<double2*>(recs + t * kSymRec);
+#pragma unroll
+  for (int k = 0; k < kSymRec / 2; ++k) o[k] = make_double2(r[2 * k], r[2 * k + 1]);
+}
 
-    const double s = __ldg(gx + i);
-    const double xx = p0x + s * pdx, xy = p0y + s * pdy;
-    cplx rv[2][4], ru[2][4];
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) rv[b][e] = ru[b][e] = mk(0.0);
-    for (int j = 0; j < ng; ++j) {
-      const double t = __ldg(gx + j);
-      const double wj = __ldg(gw + j);
-      const double zx = xx - (mpx + t * mdx);
-      const double zy = xy - (mpy + t * mdy);
-      const double r = hypot(zx, zy);
-      const double ir = 1.0 / r;
-      const double zhx = ir * zx, zhy = ir * zy;
-      DN fs;
-      dn_eval<false>(fc, S, r, ir, log(r), fs);
-      CMat2 dm, nm;
-      // V: test on the polygon (normal pn), trial on the curve (normal mn)
-      combine_D(fs, zhx, zhy, mnx, mny, dm);
-      combine_N(fs, zhx, zhy, pnx, pny, mnx, mny, nm);
-      const double pt[2] = {wj * (1.0 - t), wj * t};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const cplx k = dm.a[e] + alpha * nm.a[e];
-        axpy(rv[0][e], pt[0], k);
-        axpy(rv[1][e], pt[1], k);
-      }
-      // U: test on the curve, trial on the polygon, zh reversed
-      // N_U = N_V^T (combine_N is symmetric under z -> -z, m <-> n, i <-> j)
-      combine_D(fs, -zhx, -zhy, pnx, pny, dm);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const cplx k = dm.a[e] + alpha * nm.a[(e >> 1) | ((e & 1) << 1)];
-        axpy(ru[0][e], pt[0], k);
-        axpy(ru[1][e], pt[1], k);
-      }
-    }
-    double2* my = sh + threadIdx.x * 16;
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        my[b * 4 + e] = make_double2(rv[b][e].re, rv[b][e].im);
-        my[8 + b * 4 + e] = make_double2(ru[b][e].re, ru[b][e].im);
-      }
-  }
-  __syncthreads();
-  // Reduction over i: thread handles (pair lp2, orientation, 16 outputs / 2).
-  const int nthreads = blockDim.x;
-  for (int o = threadIdx.x; o < kProxyPairs * 2 * kBundle; o += nthreads) {
-    const int lp2 = o / (2 * kBundle);
-    const int rem = o - lp2 * 2 * kBundle;
-    const int orient = rem / kBundle;
-    const int k = rem - orient * kBundle;  // bidx(la, lb, i, j)
-    const int p2 = pair0 + lp2;
-    if (p2 >= npairs) continue;
-    const int la = k >> 3, lb = (k >> 2) & 1, e = k & 3;
-    const int pe = p2 / J.nE;
-    const int q = p2 - pe * J.nE;
-    const int pn = pe + 1 == m ? 0 : pe + 1;
-    double2 accv = make_double2(0.0, 0.0);
-    for (int ii = 0; ii < ng; ++ii) {
-      const double s = __ldg(gx + ii);
-      const double wi = __ldg(gw + ii);
-      // V: poly test shape la at s_i, curve trial shape lb summed in row sums
-      // U: curve test shape la in the row sums, poly trial shape lb at s_i
-      const double shape = orient == 0 ? (la == 0 ? 1.0 - s : s)
-                                       : (lb == 0 ? 1.0 - s : s);
-      const int slot = orient == 0 ? (lb * 4 + e) : (8 + la * 4 + e);
-      const double2 v = sh[(lp2 * ng + ii) * 16 + slot];
-      accv.x = fma(wi * shape, v.x, accv.x);
-      accv.y = fma(wi * shape, v.y, accv.y);
-    }
-    // element lengths: recompute (cheap) to scale by h_poly * h_curve
-    const int eb = __ldg(elems + J.e_off + q);
-    const double p0x = J.cx + J.radius * ctx->poly_cs[2 * pe];
-    const double p0y = J.cy + J.radius * ctx->poly_cs[2 * pe + 1];
-    const double p1x = J.cx + J.radius * ctx->poly_cs[2 * pn];
-    const double p1y = J.cy + J.radius * ctx->poly_cs[2 * pn + 1];
-    const double hh = hypot(p1x - p0x, p1y - p0y) * ef(ctx, EH, eb);
-    const long long dst = orient == 0 ? J.v_off + p2 : J.u_off + (long long)q * m + pe;
-    reinterpret_cast<double2*>(bundles)[dst * kBundle + k] =
-        make_double2(hh * accv.x, hh * accv.y);
-  }
+// Same evaluation as the near-field kernel (thread (pair, i) fixes the
+// polygon quadrature point s_i and sweeps the curve points t_j), full scalars.
+__global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
+k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
+              const double* __restrict__ recs, int n_slots, int ng,
+              double* __restrict__ bundles) {
+  near_body<true, true>(ctx, fc, recs, 0, n_slots, ng, bundles);
 }
 
 // ------------------------------------------------------------------ gather
@@ -803,12 +747,8 @@ void launch_near_singular(const DevCtx* ctx, const long long* pairs,
                                                           bundles, bad);
 }
 
-#ifndef EBEM_PROXY_PAIRS_CAP
-#define EBEM_PROXY_PAIRS_CAP 64
-#endif
 int proxy_pairs_per_block(int n_gauss) {
-  const int cap = EBEM_PROXY_PAIRS_CAP;
-  return n_gauss >= kProxyThreads ? 1 : (kProxyThreads / n_gauss < cap ? kProxyThreads / n_gauss : cap);
+  return n_gauss >= kProxyThreads ? 1 : kProxyThreads / n_gauss;
 }
 
 int proxy_blocks_for(int m_prime, int nE, int n_gauss) {
@@ -818,20 +758,33 @@ int proxy_blocks_for(int m_prime, int nE, int n_gauss) {
 
 void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
                         const ProxyJob* jobs, const int* job_block_off, int n_jobs,
-                        int n_blocks, const int* elems, double* bundles,
+                        int n_blocks, const int* elems, double* recs, double* bundles,
                         cudaStream_t st) {
   if (n_blocks <= 0) return;
-  const int p = proxy_pairs_per_block(n_gauss);
-  const int threads = p * n_gauss;
-  const size_t shmem = size_t(threads) * 16 * sizeof(double2);
+  const int tile = proxy_pairs_per_block(n_gauss);
+  const long long n_slots = (long long)n_blocks * tile;
+  k_proxy_records<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(
+      ctx, jobs, job_block_off, n_jobs, elems, n_slots, tile, recs);
+  const int P = EBEM_SYM_THREADS / n_gauss;
+  const int threads = P * n_gauss;
+  const size_t smem = size_t(threads) * 18 * sizeof(double2) +
+                      size_t(2 * P) * kSymRec * sizeof(double);
+  static const int n_sm = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
   static bool attr = [] {
     cudaFuncSetAttribute(k_proxy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kProxyThreads * 16 * (int)sizeof(double2));
+                         EBEM_SYM_THREADS * (18 * (int)sizeof(double2) +
+                                             2 * kSymRec * (int)sizeof(double)));
     return true;
   }();
   (void)attr;
-  k_proxy_pairs<<<n_blocks, threads, shmem, st>>>(ctx, fc, jobs, job_block_off, n_jobs,
-                                                  elems, bundles, p);
+  const long long need = (n_slots + P - 1) / P;
+  const int grid = int(std::min<long long>(need, 4LL * n_sm));
+  k_proxy_pairs<<<grid, threads, smem, st>>>(ctx, fc, recs, int(n_slots), n_gauss, bundles);
 }
 
 void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,

@@ -35,9 +35,12 @@ void launch_class_bounds(const unsigned char* sorted_keys, long long n,
                          int* bounds /* 9 ints: start of class c, c = 0..8 */,
                          cudaStream_t st);
 int proxy_blocks_for(int m_prime, int nE, int n_gauss);
+// Proxy blocks: writes the slot records into recs (proxy_blocks x
+// proxy_pairs_per_block(n_gauss) x kSymRec doubles), then evaluates them.
+int proxy_pairs_per_block(int n_gauss);
 void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
                         const ProxyJob* jobs, const int* job_block_off, int n_jobs,
-                        int n_blocks, const int* elems, double* bundles,
+                        int n_blocks, const int* elems, double* recs, double* bundles,
                         cudaStream_t st);
 constexpr int kGatherTile = 256;  // output entries per gather CTA
 void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,

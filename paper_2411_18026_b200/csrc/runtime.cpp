@@ -1136,6 +1136,10 @@ void Problem::execute(FillPlan& plan) {
   // symmetric near pairs: classify by tier and sort (async), read the class
   // bounds through an event so the host waits only for these small kernels
   const long long nsym = plan.sym_pairs_;
+  // pair records: the sorted near pairs, then the proxy slots
+  const long long proxy_slots =
+      (long long)plan.proxy_blocks_ * proxy_pairs_per_block(pcfg_.n_gauss);
+  if (nsym == 0 && proxy_slots > 0) sym_recs_.ensure(size_t(kSymRec) * proxy_slots);
   const SymJob* sj = nullptr;
   const long long* so = nullptr;
   if (nsym > 0) {
@@ -1156,7 +1160,7 @@ void Problem::execute(FillPlan& plan) {
                         vin + 2 * nsym, st_);
     sort_pairs_by_class(kin, kout, vin, vout, nsym, &sort_temp_, &sort_temp_bytes_, st_);
     launch_class_bounds(kout, nsym, sym_bounds_.get(), st_);
-    sym_recs_.ensure(size_t(kSymRec) * nsym);
+    sym_recs_.ensure(size_t(kSymRec) * (nsym + proxy_slots));
     launch_sym_records(dctx(), sj, el, vout, vin + 2 * nsym, sym_bounds_.get(), nsym,
                        sym_recs_.get(), st_);
     g_launches += 4;
@@ -1168,7 +1172,8 @@ void Problem::execute(FillPlan& plan) {
     g_prof.begin(st_);
     launch_proxy_pairs(dctx(), fc_, pcfg_.n_gauss, Pack::at<ProxyJob>(base, o_pj),
                        Pack::at<int>(base, o_pb), int(plan.proxy_.size()),
-                       plan.proxy_blocks_, el, bundles.get(), st_);
+                       plan.proxy_blocks_, el, sym_recs_.get() + size_t(kSymRec) * nsym,
+                       bundles.get(), st_);
     g_prof.end(KP_PROXY, st_, pts);
   }
   if (nsym > 0) {
