@@ -75,6 +75,9 @@ struct DevCtx {
   double poly_cs[2 * 512];
   // Element geometry (device pointer, kElemFields * n_nodes doubles).
   const double* elem;
+  // The same geometry element-major for gathers: 8 doubles per element
+  // {px, py, dx, dy, nx, ny, h, 0} (one 64-byte line per element).
+  const double* elem8;
   const double* node_xy;  // 2 * n_nodes, interleaved x, y
 };
 

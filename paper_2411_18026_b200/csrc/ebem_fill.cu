@@ -50,13 +50,22 @@ __device__ __forceinline__ double pt_seg_dist(double px, double py, double ax,
   return hypot(px - (ax + t * abx), py - (ay + t * aby));
 }
 
-// Mesh::element_distance, proj/src/geometry.cpp:83-96.
-__device__ __forceinline__ double element_distance(const DevCtx* __restrict__ c,
-                                                   int ea, int eb) {
-  const double a0x = ef(c, EPX, ea), a0y = ef(c, EPY, ea);
-  const double a1x = a0x + ef(c, EDX, ea), a1y = a0y + ef(c, EDY, ea);
-  const double b0x = ef(c, EPX, eb), b0y = ef(c, EPY, eb);
-  const double b1x = b0x + ef(c, EDX, eb), b1y = b0y + ef(c, EDY, eb);
+// Element geometry from the element-major copy: g = {px, py, dx, dy, nx, ny, h, 0}.
+struct Elem8 {
+  double px, py, dx, dy, nx, ny, h;
+};
+__device__ __forceinline__ Elem8 load_elem8(const DevCtx* __restrict__ c, int e) {
+  const double2* p = reinterpret_cast<const double2*>(c->elem8) + 4 * (long long)e;
+  const double2 a = __ldg(p), b = __ldg(p + 1), d = __ldg(p + 2), h = __ldg(p + 3);
+  return Elem8{a.x, a.y, b.x, b.y, d.x, d.y, h.x};
+}
+
+// Mesh::element_distance, proj/src/geometry.cpp:83-96, on loaded geometry.
+__device__ __forceinline__ double element_distance8(const Elem8& A, const Elem8& B) {
+  const double a0x = A.px, a0y = A.py;
+  const double a1x = a0x + A.dx, a1y = a0y + A.dy;
+  const double b0x = B.px, b0y = B.py;
+  const double b1x = b0x + B.dx, b1y = b0y + B.dy;
   double d = pt_seg_dist(a0x, a0y, b0x, b0y, b1x, b1y);
   d = fmin(d, pt_seg_dist(a1x, a1y, b0x, b0y, b1x, b1y));
   d = fmin(d, pt_seg_dist(b0x, b0y, a0x, a0y, a1x, a1y));
@@ -344,8 +353,8 @@ k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
   const int nb = eb + 1 == N ? 0 : eb + 1;
   unsigned char key = kSymClasses - 1;  // skip
   if (!(ea == eb || na == eb || nb == ea) && !(J.tri && a >= q)) {
-    const double hx = ef(ctx, EH, ea), hy = ef(ctx, EH, eb);
-    const double rq = element_distance(ctx, ea, eb) / fmax(hx, hy);
+    const Elem8 A = load_elem8(ctx, ea), B = load_elem8(ctx, eb);
+    const double rq = element_distance8(A, B) / fmax(A.h, B.h);
     key = (rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3) + (J.onesided ? 4 : 0);
   }
   keys[p] = key;
@@ -371,16 +380,12 @@ k_sym_records(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
   const int q = int(local - (long long)a * J.nE);
   const int ea = __ldg(elems + J.a_off + a);
   const int eb = __ldg(elems + J.e_off + q);
-  double r[kSymRec];
-  const int f[6] = {EPX, EPY, EDX, EDY, ENX, ENY};
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    r[SR_A + k] = ef(ctx, f[k], ea);
-    r[SR_B + k] = ef(ctx, f[k], eb);
-  }
+  const Elem8 A = load_elem8(ctx, ea), B = load_elem8(ctx, eb);
+  double r[kSymRec] = {A.px, A.py, A.dx, A.dy, A.nx, A.ny,
+                       B.px, B.py, B.dx, B.dy, B.nx, B.ny};
   r[SR_VD] = __longlong_as_double(J.v_off + local);
   r[SR_UD] = __longlong_as_double(J.u_off + (long long)q * J.nA + a);
-  r[SR_HH] = ef(ctx, EH, ea) * ef(ctx, EH, eb);
+  r[SR_HH] = A.h * B.h;
   r[15] = 0.0;
   double2* o = reinterpret_cast<double2*>(recs + idx * kSymRec);
 #pragma unroll
@@ -401,11 +406,20 @@ __device__ __forceinline__ void cp_async_wait1() {
 // the scalars once for both orientations (r is symmetric).  The records of
 // the next pair group are copied into shared memory (cp.async) while the
 // current group is evaluated.
+// Small CTAs (measured at 2N = 2^19: 256 x 1 -> 64 x 4 saves 5 % of the
+// near-field time; the CTA barrier then couples 2 warps, not 8); 254
+// registers either way, 8 warps per SM.
 #ifndef EBEM_SYM_THREADS
-#define EBEM_SYM_THREADS 256
+#define EBEM_SYM_THREADS 64
 #endif
 #ifndef EBEM_SYM_MINB
-#define EBEM_SYM_MINB 1
+#define EBEM_SYM_MINB 4
+#endif
+#ifndef EBEM_PRX_THREADS
+#define EBEM_PRX_THREADS 128
+#endif
+#ifndef EBEM_PRX_MINB
+#define EBEM_PRX_MINB 2
 #endif
 // PROXY: the proxy blocks (kernel_cross_block, assembly.cpp:424-509) — full
 // n scalars, no static hypersingular part, records with a negative V slot
@@ -622,12 +636,16 @@ k_proxy_records(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ job
     r[SR_A + 3] = pdy;
     r[SR_A + 4] = -pty;
     r[SR_A + 5] = ptx;
-    const int f[6] = {EPX, EPY, EDX, EDY, ENX, ENY};
-#pragma unroll
-    for (int k = 0; k < 6; ++k) r[SR_B + k] = ef(ctx, f[k], eb);
+    const Elem8 B = load_elem8(ctx, eb);
+    r[SR_B + 0] = B.px;
+    r[SR_B + 1] = B.py;
+    r[SR_B + 2] = B.dx;
+    r[SR_B + 3] = B.dy;
+    r[SR_B + 4] = B.nx;
+    r[SR_B + 5] = B.ny;
     r[SR_VD] = __longlong_as_double(J.v_off + pair);
     r[SR_UD] = __longlong_as_double(J.u_off + (long long)q * m + pe);
-    r[SR_HH] = hp * ef(ctx, EH, eb);
+    r[SR_HH] = hp * B.h;
   }
   double2* o = reinterpret_cast<double2*>(recs + t * kSymRec);
 #pragma unroll
@@ -636,7 +654,7 @@ k_proxy_records(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ job
 
 // Same evaluation as the near-field kernel (thread (pair, i) fixes the
 // polygon quadrature point s_i and sweeps the curve points t_j), full scalars.
-__global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
+__global__ void __launch_bounds__(EBEM_PRX_THREADS, EBEM_PRX_MINB)
 k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
               const double* __restrict__ recs, int n_slots, int ng,
               double* __restrict__ bundles) {
@@ -765,7 +783,7 @@ void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
   const long long n_slots = (long long)n_blocks * tile;
   k_proxy_records<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(
       ctx, jobs, job_block_off, n_jobs, elems, n_slots, tile, recs);
-  const int P = EBEM_SYM_THREADS / n_gauss;
+  const int P = EBEM_PRX_THREADS / n_gauss;
   const int threads = P * n_gauss;
   const size_t smem = size_t(threads) * 18 * sizeof(double2) +
                       size_t(2 * P) * kSymRec * sizeof(double);
@@ -777,7 +795,7 @@ void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
   }();
   static bool attr = [] {
     cudaFuncSetAttribute(k_proxy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         EBEM_SYM_THREADS * (18 * (int)sizeof(double2) +
+                         EBEM_PRX_THREADS * (18 * (int)sizeof(double2) +
                                              2 * kSymRec * (int)sizeof(double)));
     return true;
   }();

@@ -478,6 +478,16 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   CK(cudaMemcpyAsync(delem_.get(), elem_.data(), elem_.size() * 8, cudaMemcpyHostToDevice, st_));
   CK(cudaMemcpyAsync(dxy_.get(), xy_.data(), xy_.size() * 8, cudaMemcpyHostToDevice, st_));
   hctx_.elem = delem_.get();
+  {
+    std::vector<double> e8(8 * size_t(n), 0.0);
+    const int f[7] = {EPX, EPY, EDX, EDY, ENX, ENY, EH};
+    for (int e = 0; e < n; ++e)
+      for (int k = 0; k < 7; ++k) e8[8 * size_t(e) + k] = elem_[size_t(f[k]) * n + e];
+    delem8_.alloc(e8.size());
+    CK(cudaMemcpyAsync(delem8_.get(), e8.data(), e8.size() * 8, cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));  // e8 is pageable and goes out of scope
+    hctx_.elem8 = delem8_.get();
+  }
   hctx_.node_xy = dxy_.get();
   dctx_.alloc(1);
   CK(cudaMemcpyAsync(dctx_.get(), &hctx_, sizeof(DevCtx), cudaMemcpyHostToDevice, st_));

@@ -399,7 +399,7 @@ class Problem {
   DevCtx hctx_{};
   FillConst fc_{};
   DBuf<DevCtx> dctx_;
-  DBuf<double> delem_, dxy_;
+  DBuf<double> delem_, delem8_, dxy_;
   cudaStream_t st_ = nullptr;
   NodeBoxTree tree_;
 };
