@@ -1330,7 +1330,11 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     int cps = 1;  // resident CTAs per SM of the streamed inputs' variants
     for (size_t i = 0; i < q.size(); ++i)
       if (streamed[i]) cps = std::max(cps, tsqr_ctas_per_sm(q[i].n));
-    const double per_cta = work / (4.0 * n_sm * cps);
+    static const double waves = [] {  // experiments: EBEM_TSQR_WAVES
+      const char* e = std::getenv("EBEM_TSQR_WAVES");
+      return e ? std::atof(e) : 4.0;
+    }();
+    const double per_cta = work / (waves * n_sm * cps);
     for (size_t i = 0; i < q.size(); ++i) {
       if (!streamed[i]) continue;
       const TallBlock& x = q[i];
