@@ -554,6 +554,59 @@ k_gemm(const GemmTask* __restrict__ tasks, const int* __restrict__ block_off,
   }
 }
 
+// ------------------------------------------------------ narrow GEMM (GEMV)
+// C = alpha A B + beta C with at most kNarrow columns in B and C and no
+// transposes: the solve's per-cell products with one or a few right-hand
+// sides, bound by reading A once.  One CTA per 32-row tile: lane = row
+// (coalesced column reads of A), the 8 warps split K and are summed through
+// shared memory in a fixed order (deterministic).
+template <int NR>
+__global__ void __launch_bounds__(kThreads)
+k_gemv(const GemmTask* __restrict__ tasks, const int* __restrict__ block_off, int n_tasks) {
+  __shared__ double2 part[kWarps][NR][32];
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmTask T = tasks[lo];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int r = (blockIdx.x - block_off[lo]) * 32 + l;
+  const double2* A = reinterpret_cast<const double2*>(T.a);
+  const double2* B = reinterpret_cast<const double2*>(T.b);
+  double2 acc[NR];
+#pragma unroll
+  for (int c = 0; c < NR; ++c) acc[c] = make_double2(0.0, 0.0);
+  if (r < T.m) {
+#pragma unroll 4
+    for (int k = w; k < T.k; k += kWarps) {
+      const double2 a = __ldg(A + (size_t)k * T.lda + r);
+#pragma unroll
+      for (int c = 0; c < NR; ++c)
+        if (c < T.n) acc[c] = zfma(acc[c], a, __ldg(B + (size_t)c * T.ldb + k));
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NR; ++c) part[w][c][l] = acc[c];
+  __syncthreads();
+  if (w != 0 || r >= T.m) return;
+  const double2 alpha = make_double2(T.alpha_re, T.alpha_im);
+  const double2 beta = make_double2(T.beta_re, T.beta_im);
+  double2* C = reinterpret_cast<double2*>(T.c);
+#pragma unroll
+  for (int c = 0; c < NR; ++c) {
+    if (c >= T.n) break;
+    double2 s = part[0][c][l];
+#pragma unroll
+    for (int q = 1; q < kWarps; ++q) s = make_double2(s.x + part[q][c][l].x, s.y + part[q][c][l].y);
+    double2* cp = C + (size_t)c * T.ldc + r;
+    double2 v = zmul(alpha, s);
+    if (beta.x != 0.0 || beta.y != 0.0) v = zfma(v, beta, *cp);
+    *cp = v;
+  }
+}
+
 // --------------------------------------------------------------------- copy
 __global__ void __launch_bounds__(kThreads)
 k_copy(const CopyTask* __restrict__ tasks, const int* __restrict__ block_off,
@@ -722,6 +775,96 @@ k_getrs_reg(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
   }
 }
 
+// ------------------------------------------------- LU solve, one warp each
+// For a few right-hand sides every LU entry is read once, so staging the LU in
+// shared memory buys nothing: one warp per (task, right-hand side), the CTA's
+// warps serve different cells, lane l holds rows l, l + 32, ... and the next
+// column of L / U (and the next reciprocal diagonal) is loaded one step ahead
+// of the substitution that needs it.
+template <int kMaxS>
+__global__ void __launch_bounds__(kThreads)
+k_getrs_warp(const LuSolveTask* __restrict__ tasks, const int* __restrict__ warp_off,
+             int n_tasks, int n_warps) {
+  const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int l = threadIdx.x & 31;
+  if (gw >= n_warps) return;  // warp-uniform
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(warp_off + mid) <= gw) lo = mid;
+    else hi = mid - 1;
+  }
+  const LuSolveTask T = tasks[lo];
+  const int n = T.n;
+  const int col = gw - __ldg(warp_off + lo);
+  if (col >= T.nrhs || n <= 0) return;
+  const double2* A = reinterpret_cast<const double2*>(T.lu);
+  const size_t lda = T.ld;
+  double2* bg = reinterpret_cast<double2*>(T.b) + (size_t)col * T.ldb;
+  double2 b[kMaxS];
+#pragma unroll
+  for (int s = 0; s < kMaxS; ++s) {
+    const int r = l + 32 * s;
+    b[s] = r < n ? bg[r] : make_double2(0.0, 0.0);
+  }
+  auto load_col = [&](int k, double2 (&c)[kMaxS]) {
+    const double2* Ak = A + (size_t)k * lda;
+#pragma unroll
+    for (int s = 0; s < kMaxS; ++s) {
+      const int r = l + 32 * s;
+      c[s] = r < n ? __ldg(Ak + r) : make_double2(0.0, 0.0);
+    }
+  };
+  double2 cur[kMaxS], nxt[kMaxS];
+  load_col(0, nxt);
+  for (int k = 0; k < n; ++k) {  // row interchanges in order (warp-uniform)
+    const int p = __ldg(T.ipiv + k);
+    if (p == k) continue;
+    const int sk = k >> 5, lk = k & 31, sp = p >> 5, lp = p & 31;
+    const double2 vk = shfl2(pick(b, sk), lk);
+    const double2 vp = shfl2(pick(b, sp), lp);
+    if (l == lk) put(b, sk, vp);
+    if (l == lp) put(b, sp, vk);
+  }
+  // L y = b (unit lower)
+  for (int k = 0; k < n - 1; ++k) {
+#pragma unroll
+    for (int s = 0; s < kMaxS; ++s) cur[s] = nxt[s];
+    if (k + 1 < n - 1) load_col(k + 1, nxt);
+    const double2 bk = shfl2(pick(b, k >> 5), k & 31);
+#pragma unroll
+    for (int s = 0; s < kMaxS; ++s) {
+      const int r = l + 32 * s;
+      if (r > k && r < n) b[s] = zfms(b[s], cur[s], bk);
+    }
+  }
+  // U x = y
+  load_col(n - 1, nxt);
+  double2 dnext = __ldg(A + (size_t)(n - 1) * lda + (n - 1));
+  for (int k = n - 1; k >= 0; --k) {
+#pragma unroll
+    for (int s = 0; s < kMaxS; ++s) cur[s] = nxt[s];
+    const double2 ik = zrcp(dnext);
+    if (k > 0) {
+      load_col(k - 1, nxt);
+      dnext = __ldg(A + (size_t)(k - 1) * lda + (k - 1));
+    }
+    const int sk = k >> 5, lk = k & 31;
+    const double2 xk = zmul(shfl2(pick(b, sk), lk), ik);
+    if (l == lk) put(b, sk, xk);
+#pragma unroll
+    for (int s = 0; s < kMaxS; ++s) {
+      const int r = l + 32 * s;
+      if (r < k) b[s] = zfms(b[s], cur[s], xk);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < kMaxS; ++s) {
+    const int r = l + 32 * s;
+    if (r < n) bg[r] = b[s];
+  }
+}
+
 // ------------------------------------------ LU solve, large n (> 256)
 // One CTA per right-hand side, column-oriented substitutions: step k reads
 // one (coalesced) column of L or U and updates the remaining rows in
@@ -819,14 +962,25 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
   if (n <= 0) return;
   k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
-int getrs_cpw(int max_nrhs) { return max_nrhs <= kWarps ? 1 : kCpw; }
+int getrs_cpw(int max_nrhs, int max_n) {
+  if (max_nrhs <= kNarrowRhs && max_n <= 256) return 0;  // one warp per column
+  return max_nrhs <= kWarps ? 1 : kCpw;
+}
 int getrs_blocks(int nrhs, int max_n, int cpw) {
+  if (cpw == 0) return nrhs;  // warps
   const int per = max_n <= 256 ? kWarps * cpw : 1;  // large n: one CTA per column
   return (nrhs + per - 1) / per;
 }
 void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
                   int n_blocks, cudaStream_t st, int smem_bytes, int max_n, int cpw) {
   if (n_blocks <= 0) return;
+  if (cpw == 0) {  // n_blocks counts warps
+    const int grid = (n_blocks + kWarps - 1) / kWarps;
+    if (max_n <= 64) k_getrs_warp<2><<<grid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
+    else if (max_n <= 128) k_getrs_warp<4><<<grid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
+    else k_getrs_warp<8><<<grid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
+    return;
+  }
   // LU staged when it fits (smem_bytes covers the largest staged one);
   // 1 / U_kk always needs n slots
   const int bytes = std::max(smem_bytes, 16 * std::max(max_n, 1));
@@ -853,13 +1007,20 @@ int getrs_smem_bytes(int n) {
   const long long b = ((long long)n * n + n) * 16;
   return b <= kSmemCap ? int(b) : 0;
 }
-int gemm_blocks(int m, int n) {
-  return ((m + kTile - 1) / kTile) * ((n + kTile - 1) / kTile);
+int gemm_narrow(const GemmTask& g) {
+  if (g.trans_a || g.trans_b || g.n > kNarrow) return 0;
+  return g.n <= 1 ? 1 : kNarrow;
+}
+int gemm_blocks(const GemmTask& g, int narrow) {
+  if (narrow) return (g.m + 31) / 32;
+  return ((g.m + kTile - 1) / kTile) * ((g.n + kTile - 1) / kTile);
 }
 void launch_gemm(const GemmTask* tasks, const int* block_off, int n_tasks,
-                 int n_blocks, cudaStream_t st) {
+                 int n_blocks, cudaStream_t st, int narrow) {
   if (n_blocks <= 0) return;
-  k_gemm<<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+  if (narrow == 1) k_gemv<1><<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+  else if (narrow) k_gemv<kNarrow><<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+  else k_gemm<<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
 }
 int copy_blocks(int rows, int cols) {
   const long long t = (long long)rows * cols;

@@ -102,7 +102,10 @@ void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st);
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st);
 // CTAs per task for a batch whose largest LU has order max_n
-int getrs_cpw(int max_nrhs);  // right-hand sides per warp for a batch
+// right-hand sides per warp for a batch (0: the unstaged one-warp-per-column
+// kernel for at most kNarrowRhs columns; getrs_blocks then counts warps)
+constexpr int kNarrowRhs = 8;
+int getrs_cpw(int max_nrhs, int max_n);
 int getrs_blocks(int nrhs, int max_n, int cpw);
 // Dense-solver helpers (ebem_lu.cu): column sums of |a_ij| (1-norm), and
 // x := A^-H x with A's LU (one right-hand side, one CTA).
@@ -115,9 +118,14 @@ void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
                   int n_blocks, cudaStream_t st, int smem_bytes, int max_n, int cpw);
 // Dynamic shared memory that stages an n x n LU (0 when it does not fit).
 int getrs_smem_bytes(int n);
-int gemm_blocks(int m, int n);
+// Narrow products (at most kNarrow columns, no transposes) run as a GEMV
+// kernel: gemm_narrow gives its column template (1 or kNarrow; 0 = tiled GEMM);
+// a launch uses one kind for all its tasks (the smallest common one).
+constexpr int kNarrow = 4;
+int gemm_narrow(const GemmTask& g);
+int gemm_blocks(const GemmTask& g, int narrow);
 void launch_gemm(const GemmTask* tasks, const int* block_off, int n_tasks,
-                 int n_blocks, cudaStream_t st);
+                 int n_blocks, cudaStream_t st, int narrow);
 int copy_blocks(int rows, int cols);
 void launch_copy(const CopyTask* tasks, const int* block_off, int n_tasks,
                  int n_blocks, cudaStream_t st);

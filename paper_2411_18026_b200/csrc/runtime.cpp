@@ -1689,6 +1689,7 @@ namespace {
 int g_getrs_smem = 0;
 int g_getrs_maxn = 0;
 int g_getrs_cpw = 1;
+int g_gemm_narrow = 0;  // GEMV template of the current k_gemm launch (0: tiled)
 
 template <class T, class F, class U>
 void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
@@ -1703,7 +1704,8 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
   }
   if (total == 0) return;
   if (P.recorder) {
-    P.recorder->add(id, t, boff, total, id == KP_GETRS ? g_getrs_smem : 0,
+    P.recorder->add(id, t, boff, total,
+                    id == KP_GETRS ? g_getrs_smem : id == KP_GEMM ? g_gemm_narrow : 0,
                     id == KP_GETRS ? (g_getrs_maxn | (g_getrs_cpw << 16)) : 0);
     return;
   }
@@ -1740,7 +1742,8 @@ void Recorder::replay(cudaStream_t st, int phase) {
         launch_copy(Pack::at<CopyTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st);
         break;
       case KP_GEMM:
-        launch_gemm(Pack::at<GemmTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st);
+        launch_gemm(Pack::at<GemmTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st,
+                    l.aux);
         break;
       case KP_GETRS:
         launch_getrs(Pack::at<LuSolveTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st,
@@ -1757,9 +1760,22 @@ void run_copies(Problem& P, const std::vector<CopyTask>& t) {
               launch_copy, KP_COPY,
               [](const CopyTask& c) { return 32.0 * c.rows * c.cols; });
 }
+namespace {
+void launch_gemm_cur(const GemmTask* t, const int* boff, int nt, int nb, cudaStream_t st) {
+  launch_gemm(t, boff, nt, nb, st, g_gemm_narrow);
+}
+}  // namespace
+
 void run_gemms(Problem& P, const std::vector<GemmTask>& t) {
-  run_blocked(P, t, [](const GemmTask& g) { return g.k > 0 ? gemm_blocks(g.m, g.n) : 0; },
-              launch_gemm, KP_GEMM,
+  int narrow = t.empty() ? 0 : 1;  // the smallest kind every task fits
+  for (const GemmTask& g : t) {
+    const int k = gemm_narrow(g);
+    if (k == 0) { narrow = 0; break; }
+    narrow = std::max(narrow, k);
+  }
+  g_gemm_narrow = narrow;
+  run_blocked(P, t, [narrow](const GemmTask& g) { return g.k > 0 ? gemm_blocks(g, narrow) : 0; },
+              launch_gemm_cur, KP_GEMM,
               [](const GemmTask& g) { return 8.0 * g.m * g.n * double(g.k); });
 }
 namespace {
@@ -1772,7 +1788,7 @@ void launch_getrs_staged(const LuSolveTask* t, const int* boff, int nt, int nb,
 void run_getrs(Problem& P, const std::vector<LuSolveTask>& t) {
   int smem = 0, maxn = 0, maxr = 0;
   for (const LuSolveTask& x : t) maxn = std::max(maxn, x.n), maxr = std::max(maxr, x.nrhs);
-  const int cpw = getrs_cpw(maxr);
+  const int cpw = getrs_cpw(maxr, maxn);
   g_getrs_cpw = cpw;
   for (const LuSolveTask& x : t)
     if (maxn <= 256 || x.n > 0) smem = std::max(smem, getrs_smem_bytes(x.n));
