@@ -815,12 +815,23 @@ k_getrs_warp(const LuSolveTask* __restrict__ tasks, const int* __restrict__ warp
       c[s] = r < n ? __ldg(Ak + r) : make_double2(0.0, 0.0);
     }
   };
+  int piv[kMaxS];  // lane l holds ipiv[l + 32 s]
+#pragma unroll
+  for (int s = 0; s < kMaxS; ++s) {
+    const int r = l + 32 * s;
+    piv[s] = r < n ? __ldg(T.ipiv + r) : r;
+  }
   double2 cur[kMaxS], nxt[kMaxS];
   load_col(0, nxt);
   for (int k = 0; k < n; ++k) {  // row interchanges in order (warp-uniform)
-    const int p = __ldg(T.ipiv + k);
+    const int sk = k >> 5, lk = k & 31;
+    int p = piv[0];
+#pragma unroll
+    for (int s = 1; s < kMaxS; ++s)
+      if (s == sk) p = piv[s];
+    p = __shfl_sync(0xffffffffu, p, lk);
     if (p == k) continue;
-    const int sk = k >> 5, lk = k & 31, sp = p >> 5, lp = p & 31;
+    const int sp = p >> 5, lp = p & 31;
     const double2 vk = shfl2(pick(b, sk), lk);
     const double2 vp = shfl2(pick(b, sp), lp);
     if (l == lk) put(b, sk, vp);
@@ -861,6 +872,142 @@ k_getrs_warp(const LuSolveTask* __restrict__ tasks, const int* __restrict__ warp
 #pragma unroll
   for (int s = 0; s < kMaxS; ++s) {
     const int r = l + 32 * s;
+    if (r < n) bg[r] = b[s];
+  }
+}
+
+// ------------------------------------------------ LU solve, one CTA each
+// One CTA (kThreads) per (task, right-hand side) for orders up to
+// kThreads * kS: thread t keeps rows t, t + kThreads, ... in registers and
+// loads its part of the next column of L / U one step ahead; the new x_k goes
+// through a two-slot shared-memory broadcast, one barrier per step.  The row
+// interchanges run in shared memory first (LAPACK order, one thread).
+template <int kS>
+__global__ void __launch_bounds__(kThreads)
+k_getrs_cta(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off,
+            int n_tasks) {
+  // columns of L / U stream PF steps ahead through a per-thread shared-memory
+  // ring filled by cp.async (a CTA barrier would wait for register loads,
+  // not for these); each thread reads back only the entries it copied
+  constexpr int PF = kS >= 8 ? 2 : 16 / kS;
+  extern __shared__ double2 sx[];  // ring [PF][kS][kThreads] | x (n) | ipiv (n ints)
+  __shared__ double2 bc[2];
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const LuSolveTask T = tasks[lo];
+  const int col = blockIdx.x - block_off[lo];
+  if (col >= T.nrhs) return;
+  const int n = T.n;
+  if (n <= 0) return;
+  const int t = threadIdx.x;
+  const double2* A = reinterpret_cast<const double2*>(T.lu);
+  const size_t lda = T.ld;
+  double2* bg = reinterpret_cast<double2*>(T.b) + (size_t)col * T.ldb;
+  double2* ring = sx;
+  double2* xs = sx + PF * kS * kThreads;
+  int* sp = reinterpret_cast<int*>(xs + n);
+  auto slot = [&](int q, int s) -> double2& { return ring[(q * kS + s) * kThreads + t]; };
+  auto fetch = [&](int k, int q) {  // column k -> slot q (own rows), one group
+    if (k >= 0 && k < n) {
+      const double2* Ak = A + (size_t)k * lda;
+#pragma unroll
+      for (int s = 0; s < kS; ++s) {
+        const int r = t + kThreads * s;
+        if (r < n) {
+          const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(&slot(q, s)));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(Ak + r));
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  auto wait_oldest = [] { asm volatile("cp.async.wait_group %0;\n" ::"n"(PF - 1) : "memory"); };
+  for (int r = t; r < n; r += kThreads) {
+    xs[r] = bg[r];
+    sp[r] = __ldg(T.ipiv + r);
+  }
+#pragma unroll
+  for (int q = 0; q < PF; ++q) fetch(q < n - 1 ? q : -1, q);
+  __syncthreads();
+  if (t == 0)
+    for (int k = 0; k < n; ++k) {
+      const int p = sp[k];
+      if (p != k) {
+        const double2 v = xs[k];
+        xs[k] = xs[p];
+        xs[p] = v;
+      }
+    }
+  __syncthreads();
+  double2 b[kS];
+#pragma unroll
+  for (int s = 0; s < kS; ++s) {
+    const int r = t + kThreads * s;
+    b[s] = r < n ? xs[r] : make_double2(0.0, 0.0);
+  }
+  // L y = b: x_0 is b_0; the owner of row k + 1 publishes it after step k
+  if (t == 0) bc[0] = b[0];
+  __syncthreads();
+  for (int k0 = 0; k0 < n - 1; k0 += PF) {
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int k = k0 + q;
+      if (k < n - 1) {  // CTA-uniform
+        wait_oldest();
+        const double2 xk = bc[k & 1];
+#pragma unroll
+        for (int s = 0; s < kS; ++s) {
+          const int r = t + kThreads * s;
+          if (r > k && r < n) b[s] = zfms(b[s], slot(q, s), xk);
+          if (r == k + 1) bc[(k + 1) & 1] = b[s];
+        }
+        fetch(k + PF < n - 1 ? k + PF : -1, q);
+        __syncthreads();
+      }
+    }
+  }
+  // U x = y: column k in slot (n - 1 - k) % PF; the owner of row k - 1
+  // divides by U_{k-1,k-1} (next slot) and publishes x_{k-1}
+#pragma unroll
+  for (int q = 0; q < PF; ++q) fetch(n - 1 - q, q);
+  wait_oldest();
+#pragma unroll
+  for (int s = 0; s < kS; ++s)
+    if (t + kThreads * s == n - 1) {
+      b[s] = zmul(b[s], zrcp(slot(0, s)));
+      bc[(n - 1) & 1] = b[s];
+    }
+  __syncthreads();
+  for (int k0 = n - 1; k0 >= 1; k0 -= PF) {
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int k = k0 - q;
+      if (k >= 1) {  // CTA-uniform
+        // column k (slot q) is complete; column k - 1 (next slot) is the
+        // group after it: wait for both
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(PF - 2 > 0 ? PF - 2 : 0) : "memory");
+        const double2 xk = bc[k & 1];
+#pragma unroll
+        for (int s = 0; s < kS; ++s) {
+          const int r = t + kThreads * s;
+          if (r < k) b[s] = zfms(b[s], slot(q, s), xk);
+          if (r == k - 1) {
+            b[s] = zmul(b[s], zrcp(slot((q + 1) % PF, s)));
+            bc[(k - 1) & 1] = b[s];
+          }
+        }
+        fetch(k - PF, q);
+        __syncthreads();
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < kS; ++s) {
+    const int r = t + kThreads * s;
     if (r < n) bg[r] = b[s];
   }
 }
@@ -963,11 +1110,14 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
   k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
 int getrs_cpw(int max_nrhs, int max_n) {
-  if (max_nrhs <= kNarrowRhs && max_n <= 256) return 0;  // one warp per column
+  if (max_n > 256 && max_n <= kGetrsCtaMaxN) return -1;  // one CTA per column
+  if (max_nrhs <= kNarrowRhs && max_n <= kGetrsWarpMaxN) return 0;  // one warp per column
+  if (max_nrhs <= kNarrowRhs && max_n <= 256) return -1;
   return max_nrhs <= kWarps ? 1 : kCpw;
 }
 int getrs_blocks(int nrhs, int max_n, int cpw) {
   if (cpw == 0) return nrhs;  // warps
+  if (cpw < 0) return nrhs;   // CTAs
   const int per = max_n <= 256 ? kWarps * cpw : 1;  // large n: one CTA per column
   return (nrhs + per - 1) / per;
 }
@@ -977,8 +1127,26 @@ void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
   if (cpw == 0) {  // n_blocks counts warps
     const int grid = (n_blocks + kWarps - 1) / kWarps;
     if (max_n <= 64) k_getrs_warp<2><<<grid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
-    else if (max_n <= 128) k_getrs_warp<4><<<grid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
-    else k_getrs_warp<8><<<grid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
+    else k_getrs_warp<4><<<grid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
+    return;
+  }
+  if (cpw < 0) {  // one CTA per column, orders up to kThreads * 8
+    const int pf = max_n <= kThreads ? 16 : max_n <= 2 * kThreads ? 8 : max_n <= 4 * kThreads ? 4 : 2;
+    const int ks = max_n <= kThreads ? 1 : max_n <= 2 * kThreads ? 2 : max_n <= 4 * kThreads ? 4 : 8;
+    const size_t sm = 16 * size_t(pf) * ks * kThreads + 20 * size_t(std::max(max_n, 2)) + 16;
+    static const bool attr = [] {
+      const int cap = 160 * 1024;
+      cudaFuncSetAttribute(k_getrs_cta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+      cudaFuncSetAttribute(k_getrs_cta<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+      cudaFuncSetAttribute(k_getrs_cta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+      cudaFuncSetAttribute(k_getrs_cta<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+      return true;
+    }();
+    (void)attr;
+    if (max_n <= kThreads) k_getrs_cta<1><<<n_blocks, kThreads, sm, st>>>(tasks, block_off, n_tasks);
+    else if (max_n <= 2 * kThreads) k_getrs_cta<2><<<n_blocks, kThreads, sm, st>>>(tasks, block_off, n_tasks);
+    else if (max_n <= 4 * kThreads) k_getrs_cta<4><<<n_blocks, kThreads, sm, st>>>(tasks, block_off, n_tasks);
+    else k_getrs_cta<8><<<n_blocks, kThreads, sm, st>>>(tasks, block_off, n_tasks);
     return;
   }
   // LU staged when it fits (smem_bytes covers the largest staged one);

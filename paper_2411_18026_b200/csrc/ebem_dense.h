@@ -104,7 +104,11 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
 // CTAs per task for a batch whose largest LU has order max_n
 // right-hand sides per warp for a batch (0: the unstaged one-warp-per-column
 // kernel for at most kNarrowRhs columns; getrs_blocks then counts warps)
+// -1: one CTA per column (orders above kGetrsWarpMaxN for few columns, and
+// 256 < n <= kGetrsCtaMaxN for any count).
 constexpr int kNarrowRhs = 8;
+constexpr int kGetrsWarpMaxN = 128;
+constexpr int kGetrsCtaMaxN = 2048;
 int getrs_cpw(int max_nrhs, int max_n);
 int getrs_blocks(int nrhs, int max_n, int cpw);
 // Dense-solver helpers (ebem_lu.cu): column sums of |a_ij| (1-norm), and

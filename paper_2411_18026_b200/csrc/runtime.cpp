@@ -1706,7 +1706,7 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
   if (P.recorder) {
     P.recorder->add(id, t, boff, total,
                     id == KP_GETRS ? g_getrs_smem : id == KP_GEMM ? g_gemm_narrow : 0,
-                    id == KP_GETRS ? (g_getrs_maxn | (g_getrs_cpw << 16)) : 0);
+                    id == KP_GETRS ? (g_getrs_maxn | ((g_getrs_cpw + 1) << 16)) : 0);
     return;
   }
   Pack pk;
@@ -1747,7 +1747,7 @@ void Recorder::replay(cudaStream_t st, int phase) {
         break;
       case KP_GETRS:
         launch_getrs(Pack::at<LuSolveTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st,
-                     l.aux, l.aux2 & 0xffff, l.aux2 >> 16);
+                     l.aux, l.aux2 & 0xffff, (l.aux2 >> 16) - 1);
         break;
       default:
         throw Error(EBEM_LOGIC_ERROR, "Recorder: unexpected kernel kind");
