@@ -423,15 +423,23 @@ __device__ __forceinline__ void hankel01_lg(double x, double log_half_x,
 }
 
 // All eight remainder series at once: one loop over powers, 16 independent
-// Horner chains in u = r^2.
-__device__ __forceinline__ void series_joint(const SerSm& S, double u,
-                                             double logr, double r, DN& o) {
+// Horner chains in u = r^2, started at the highest of the nt terms used.
+// nt: ParSeries::rcut terms for the largest distance the caller sweeps.
+__device__ __forceinline__ int series_terms(const SerSm& S, double rmax) {
+  int nt = 1;
+  for (int t = 1; t < S.ntmax; ++t) nt += rmax > S.rcut[t];
+  return nt;
+}
+__device__ __forceinline__ void series_joint(const SerSm& S, double u, double logr,
+                                             double r, int nt, DN& o) {
   cplx A[8], B[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) A[k] = B[k] = mk(0.0);
-  int nt = 1;  // the terms this r needs (ParSeries::rcut)
-  for (int t = 1; t < S.ntmax; ++t) nt += r > S.rcut[t];
-  for (int p = nt - 1; p >= 0; --p) {
+  for (int k = 0; k < 8; ++k) {
+    const double2 a = S.at[nt - 1][k], b = S.bt[nt - 1][k];
+    A[k] = mk(a.x, a.y);
+    B[k] = mk(b.x, b.y);
+  }
+  for (int p = nt - 2; p >= 0; --p) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const double2 a = S.at[p][k], b = S.bt[p][k];
@@ -453,12 +461,12 @@ __device__ __forceinline__ void series_joint(const SerSm& S, double u,
 // __grid_constant__ FillConst kernel parameter (constant-bank operands).
 template <bool kRem>
 __device__ __forceinline__ void dn_eval(const FillConst& fc, const SerSm& S,
-                                        double r, double ir, double logr,
+                                        double r, double ir, double logr, int nt,
                                         DN& o) {
   const DevMedium& m = fc.med;
   const double ir2 = ir * ir;
   if (r < m.series_radius) {
-    series_joint(S, r * r, logr, r, o);
+    series_joint(S, r * r, logr, r, nt, o);
     o.d[0].re += m.sd1 * ir;
     o.d[1].re -= m.sd1 * ir;
     o.d[2].re += m.sd3 * ir;

@@ -424,6 +424,10 @@ __device__ __forceinline__ void cp_async_wait1() {
 // PROXY: the proxy blocks (kernel_cross_block, assembly.cpp:424-509) — full
 // n scalars, no static hypersingular part, records with a negative V slot
 // are padding.
+#ifndef EBEM_J_UNROLL
+#define EBEM_J_UNROLL 1
+#endif
+constexpr int kJUnroll = EBEM_J_UNROLL;  // trial-point loop unroll (experiments)
 template <bool BOTH, bool PROXY>
 __device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const FillConst& fc,
                                           const double* __restrict__ recs, int first,
@@ -479,12 +483,25 @@ __device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const 
     const double qfac = fc.med.qfactor;
     const double s = gx[i];
     const double xx = pax + s * dax, xy = pay + s * day;
+    // series terms for the farthest trial point (a segment's farthest point
+    // from x is an endpoint): one count per thread, not per point
+#ifndef EBEM_NT_PER_POINT
+#define EBEM_NT_PER_POINT 0
+#endif
+    const bool per_point = EBEM_NT_PER_POINT && !PROXY;
+    int nt = 0;
+    if (!per_point) {
+      const double rmax =
+          fmax(hypot(xx - pbx, xy - pby), hypot(xx - pbx - dbx, xy - pby - dby));
+      nt = series_terms(S, rmax);
+    }
     cplx rv[2][4], ru[2][4];
     double Q[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int b = 0; b < 2; ++b)
 #pragma unroll
       for (int e = 0; e < 4; ++e) rv[b][e] = ru[b][e] = mk(0.0);
+#pragma unroll (kJUnroll)
     for (int j = 0; j < n; ++j) {
       const double t = gx[j];
       const double wj = gw[j];
@@ -495,7 +512,7 @@ __device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const 
       const double logr = log(r);
       const double zhx = ir * zx, zhy = ir * zy;
       DN dn;
-      dn_eval<!PROXY>(fc, S, r, ir, logr, dn);
+      dn_eval<!PROXY>(fc, S, r, ir, logr, per_point ? series_terms(S, r) : nt, dn);
       const double pt[2] = {wj * (1.0 - t), wj * t};
       CMat2 dm, nm;
       // V: test on the enclosed element (normal na), trial on the cell element

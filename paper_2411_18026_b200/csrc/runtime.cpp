@@ -584,48 +584,61 @@ class PlanPool {
     for (std::thread& t : th_) t.join();
   }
   int size() const { return n_; }
+  // Items are claimed under the mutex and tagged with the generation of the
+  // call: a worker still leaving the previous call can neither take an item
+  // of the next one with a stale count nor miss its completion signal.
   void run(int n, const std::function<void(int)>& f) {
     if (n <= 0) return;
-    if (n_ == 1 || n == 1) {
+    if (n_ == 1 || n == 1 || in_pool_) {  // (a nested call runs serially)
       for (int i = 0; i < n; ++i) f(i);
       return;
     }
+    struct Mark {
+      Mark() { in_pool_ = true; }
+      ~Mark() { in_pool_ = false; }
+    } mark;
+    unsigned long g;
     {
       std::lock_guard<std::mutex> lk(m_);
-      f_.store(&f);
-      total_.store(n);
-      next_.store(0);
-      done_.store(0);
+      f_ = &f;
+      total_ = n;
+      next_ = 0;
+      done_ = 0;
       err_ = nullptr;
-      ++gen_;
+      g = ++gen_;
     }
     cv_.notify_all();
-    work();
+    work(g);
     std::unique_lock<std::mutex> lk(m_);
-    done_cv_.wait(lk, [&] { return done_.load() == total_.load(); });
-    total_.store(0);
+    done_cv_.wait(lk, [&] { return done_ == total_; });
+    f_ = nullptr;
     if (err_) std::rethrow_exception(err_);
   }
 
  private:
-  void work() {
+  void work(unsigned long g) {
     for (;;) {
-      const int total = total_.load();
-      const int i = next_.fetch_add(1);
-      if (i >= total) break;
+      int i;
+      const std::function<void(int)>* f;
+      {
+        std::lock_guard<std::mutex> lk(m_);
+        if (gen_ != g || next_ >= total_) return;
+        i = next_++;
+        f = f_;
+      }
+      std::exception_ptr e;
       try {
-        (*f_.load())(i);
+        (*f)(i);
       } catch (...) {
-        std::lock_guard<std::mutex> lk(m_);
-        if (!err_) err_ = std::current_exception();
+        e = std::current_exception();
       }
-      if (done_.fetch_add(1) + 1 == total) {
-        std::lock_guard<std::mutex> lk(m_);
-        done_cv_.notify_all();
-      }
+      std::lock_guard<std::mutex> lk(m_);
+      if (e && !err_) err_ = e;
+      if (++done_ == total_) done_cv_.notify_all();
     }
   }
   void loop() {
+    in_pool_ = true;
     unsigned long seen = 0;
     for (;;) {
       {
@@ -634,19 +647,21 @@ class PlanPool {
         if (stop_) return;
         seen = gen_;
       }
-      work();
+      work(seen);
     }
   }
   int n_ = 1;
   std::vector<std::thread> th_;
   std::mutex m_;
   std::condition_variable cv_, done_cv_;
-  std::atomic<const std::function<void(int)>*> f_{nullptr};
-  std::atomic<int> total_{0}, next_{0}, done_{0};
+  const std::function<void(int)>* f_ = nullptr;
+  int total_ = 0, next_ = 0, done_ = 0;
   std::exception_ptr err_;
   unsigned long gen_ = 0;
   bool stop_ = false;
+  static thread_local bool in_pool_;
 };
+thread_local bool PlanPool::in_pool_ = false;
 
 PlanPool& plan_pool() {
   static PlanPool* p = new PlanPool();  // never destroyed: no join at exit
@@ -718,6 +733,100 @@ void FillPlan::append(const FillPlan& o) {
   has_two_sided_ = has_two_sided_ || o.has_two_sided_;
   // o's polygon descriptors were copied with its descriptors; this plan's own
   // (if any) stay where they are
+}
+
+void FillPlan::append_many(const std::vector<FillPlan>& parts, int k0, int k1) {
+  const int np = k1 - k0;
+  if (np <= 0) return;
+  bool regular = np > 1;  // one offset per job, two elements per singular pair
+  for (int k = k0; k < k1 && regular; ++k) {
+    const FillPlan& o = parts[k];
+    regular = o.sym_off_.size() == o.sym_.size() && o.proxy_boff_.size() == o.proxy_.size() &&
+              o.gather_off_.size() == o.gather_.size() &&
+              o.sing_elems_.size() == 2 * o.sing_pair_.size();
+  }
+  if (!regular) {
+    for (int k = k0; k < k1; ++k) append(parts[k]);
+    return;
+  }
+  struct Base {
+    size_t elems, sing, sym, proxy, gather, desc;
+    long long bundles, sym_pairs, entries;
+    int proxy_blocks;
+  };
+  std::vector<Base> base(np + 1);
+  base[0] = Base{elems_.size(), sing_pair_.size(), sym_.size(), proxy_.size(), gather_.size(),
+                 desc_.size(), bundles_, sym_pairs_, entries_, proxy_blocks_};
+  for (int i = 0; i < np; ++i) {
+    const FillPlan& o = parts[k0 + i];
+    Base b = base[i];
+    b.elems += o.elems_.size();
+    b.sing += o.sing_pair_.size();
+    b.sym += o.sym_.size();
+    b.proxy += o.proxy_.size();
+    b.gather += o.gather_.size();
+    b.desc += o.desc_.size();
+    b.bundles += o.bundles_;
+    b.sym_pairs += o.sym_pairs_;
+    b.entries += o.entries_;
+    b.proxy_blocks += o.proxy_blocks_;
+    base[i + 1] = b;
+    has_one_sided_ = has_one_sided_ || o.has_one_sided_;
+    has_two_sided_ = has_two_sided_ || o.has_two_sided_;
+  }
+  const Base& e = base[np];
+  elems_.resize(e.elems);
+  sing_pair_.resize(e.sing);
+  sing_elems_.resize(2 * e.sing);
+  sym_.resize(e.sym);
+  sym_off_.resize(e.sym);
+  proxy_.resize(e.proxy);
+  proxy_boff_.resize(e.proxy);
+  gather_.resize(e.gather);
+  gather_off_.resize(e.gather);
+  desc_.resize(e.desc);
+  parallel_for(np, [&](int i) {
+    const FillPlan& o = parts[k0 + i];
+    const Base& b = base[i];
+    const int eb = int(b.elems), db = int(b.desc), pb = b.proxy_blocks;
+    const long long bb = b.bundles, sb = b.sym_pairs, entb = b.entries;
+    std::copy(o.elems_.begin(), o.elems_.end(), elems_.begin() + b.elems);
+    for (size_t q = 0; q < o.sing_pair_.size(); ++q) sing_pair_[b.sing + q] = o.sing_pair_[q] + bb;
+    std::copy(o.sing_elems_.begin(), o.sing_elems_.end(), sing_elems_.begin() + 2 * b.sing);
+    for (size_t q = 0; q < o.sym_.size(); ++q) {
+      SymJob J = o.sym_[q];
+      J.v_off += bb;
+      J.u_off += bb;
+      J.local_off += sb;
+      J.a_off += eb;
+      J.e_off += eb;
+      sym_[b.sym + q] = J;
+      sym_off_[b.sym + q] = o.sym_off_[q] + sb;
+    }
+    for (size_t q = 0; q < o.proxy_.size(); ++q) {
+      ProxyJob J = o.proxy_[q];
+      J.v_off += bb;
+      J.u_off += bb;
+      J.e_off += eb;
+      J.block_off += pb;
+      proxy_[b.proxy + q] = J;
+      proxy_boff_[b.proxy + q] = o.proxy_boff_[q] + pb;
+    }
+    for (size_t q = 0; q < o.gather_.size(); ++q) {
+      GatherJob G = o.gather_[q];
+      G.pair_off += bb;
+      G.entry_off += entb;
+      G.rdesc_off += db;
+      G.cdesc_off += db;
+      gather_[b.gather + q] = G;
+      gather_off_[b.gather + q] = o.gather_off_[q] + entb;
+    }
+    std::copy(o.desc_.begin(), o.desc_.end(), desc_.begin() + b.desc);
+  });
+  bundles_ = e.bundles;
+  sym_pairs_ = e.sym_pairs;
+  entries_ = e.entries;
+  proxy_blocks_ = e.proxy_blocks;
 }
 
 // Elements supporting the hat functions of the listed nodes (node g owns
@@ -1273,16 +1382,24 @@ void Problem::interaction(const std::vector<BasisReq>& req,
       }
     });
   }
+  // waves: consecutive chunks until the bundle count passes the cap (the
+  // chunk that crosses it closes the wave), concatenated in parallel
   FillPlan plan(n_, m, pcfg_.n_gauss);
+  int k0 = 0;
+  long long acc = 0;
   for (int k = 0; k < nchunk; ++k) {
-    {
-      PhaseTimer t_app("fill_plan_append", nullptr);
-      plan.append(parts[k]);
-      parts[k] = FillPlan(n_, m, pcfg_.n_gauss);
+    acc += parts[k].bundles();
+    if (acc > kMaxBundlesPerWave || k == nchunk - 1) {
+      {
+        PhaseTimer t_app("fill_plan_append", nullptr);
+        plan.append_many(parts, k0, k + 1);
+        for (int q = k0; q <= k; ++q) parts[q] = FillPlan(n_, m, pcfg_.n_gauss);
+      }
+      execute(plan);
+      k0 = k + 1;
+      acc = 0;
     }
-    if (plan.bundles() > kMaxBundlesPerWave) execute(plan);
   }
-  execute(plan);
 }
 
 // TSQR rounds until each block is an n x n R or fits one CTA's shared memory

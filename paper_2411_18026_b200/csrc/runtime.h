@@ -433,6 +433,9 @@ class FillPlan {
   // Appends another plan (built independently, e.g. on another host thread)
   // with its element, bundle, pair, descriptor and entry offsets relocated.
   void append(const FillPlan& o);
+  // append(parts[k0]), ..., append(parts[k1 - 1]) with the copies and
+  // relocations of the parts done in parallel on the planning threads.
+  void append_many(const std::vector<FillPlan>& parts, int k0, int k1);
 
  private:
   friend class Problem;
