@@ -289,12 +289,21 @@ def main():
     # roofline of the dominant kernel
     top = max(prof.items(), key=lambda kv: kv[1][0])
     kname, (kms, kcount, kunits) = top
+    # DRAM traffic per launch of the dominant kernel from an ncu capture of
+    # every launch of one factorization at this workload (committed summary)
+    traffic = None
+    tf_path = ROOT / "profiles" / "r1_ncu_traffic_k_near_sym.json"
+    if kname == "k_near_sym" and tf_path.exists():
+        traffic = json.load(open(tf_path))["dram_bytes_per_launch"]
     roof = None
     if kname in FLOPS_PER_POINT and kms > 0:
         ach = FLOPS_PER_POINT[kname] * kunits / (kms * 1e-3) / 1e12
         roof = {"bound": "fp64", "kernel": kname, "achieved": ach, "peak": fp64_peak,
                 "unit": "TFLOP/s", "frac": ach / fp64_peak if fp64_peak else None,
-                "traffic": None,
+                "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + "
+                                "dram__bytes_write.sum over all launches of one factorization, "
+                                "profiles/r1_ncu_traffic_k_near_sym.json); the kernel is FP64-bound",
                 "peak_source": "measured on this box by ebem_gpu_fp64_peak (DFMA chains); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "units": "quadrature points", "units_per_launch": kunits / max(kcount, 1),
