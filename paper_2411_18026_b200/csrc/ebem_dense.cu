@@ -1012,6 +1012,172 @@ k_getrs_cta(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
   }
 }
 
+// ----------------------------------------- LU solve, blocked, many columns
+// kBlkRhs right-hand sides per CTA held in shared memory (rows permuted on
+// load); L then U in 32-row panels: the panel's triangular solve by the
+// warps (lane = row, two columns per warp, shuffles), then the trailing rows
+// by a register-tiled update (thread = 4 columns x Q rows, the LU column
+// reads coalesced across the 64 row lanes).  Orders up to 64 Q.
+constexpr int kBlkRhs = 16;
+constexpr int kBlkPanel = 32;
+template <int Q>
+__global__ void __launch_bounds__(kThreads)
+k_getrs_blk(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off,
+            int n_tasks) {
+  static_assert(kThreads == 256 && kBlkRhs == 16, "layout: 4 column groups x 64 row lanes");
+  extern __shared__ double2 X[];  // [kBlkRhs][n] | perm (n ints)
+  __shared__ double2 Dp[kBlkPanel][kBlkPanel + 1];  // panel diagonal block, [col][row]
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const LuSolveTask T = tasks[lo];
+  const int n = T.n;
+  const int c0 = (blockIdx.x - block_off[lo]) * kBlkRhs;
+  if (n <= 0 || c0 >= T.nrhs) return;
+  const int nc = min(kBlkRhs, T.nrhs - c0);
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  const double2* A = reinterpret_cast<const double2*>(T.lu);
+  const size_t lda = T.ld;
+  double2* Bg = reinterpret_cast<double2*>(T.b) + (size_t)c0 * T.ldb;
+  int* perm = reinterpret_cast<int*>(X + (size_t)kBlkRhs * n);
+  // row r of the permuted system is row perm[r] of b (LAPACK interchanges)
+  for (int r = t; r < n; r += kThreads) perm[r] = r;
+  __syncthreads();
+  if (t == 0)
+    for (int k = 0; k < n; ++k) {
+      const int p = __ldg(T.ipiv + k);
+      if (p != k) {
+        const int v = perm[k];
+        perm[k] = perm[p];
+        perm[p] = v;
+      }
+    }
+  __syncthreads();
+  for (int idx = t; idx < kBlkRhs * n; idx += kThreads) {
+    const int c = idx / n, r = idx - c * n;
+    X[idx] = c < nc ? Bg[(size_t)c * T.ldb + perm[r]] : make_double2(0.0, 0.0);
+  }
+  const int cg = t >> 6, rl = t & 63;  // update layout: columns 4 cg .. 4 cg + 3
+  // ---- L y = b (unit lower)
+  for (int k0 = 0; k0 < n; k0 += kBlkPanel) {
+    const int k1 = min(k0 + kBlkPanel, n), pw = k1 - k0;
+    for (int idx = t; idx < kBlkPanel * kBlkPanel; idx += kThreads) {
+      const int kk = idx >> 5, rr = idx & 31;
+      Dp[kk][rr] = (kk < pw && rr < pw) ? __ldg(A + (size_t)(k0 + kk) * lda + k0 + rr)
+                                        : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      double2* xc = X + (size_t)(2 * w + cc) * n + k0;
+      double2 x = l < pw ? xc[l] : make_double2(0.0, 0.0);
+      for (int kk = 0; kk < pw - 1; ++kk) {
+        const double2 xk = shfl2(x, kk);
+        if (l > kk) x = zfms(x, Dp[kk][l], xk);
+      }
+      if (l < pw) xc[l] = x;
+    }
+    __syncthreads();
+    if (k1 < n) {
+      double2 acc[Q][4];
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[q][j] = make_double2(0.0, 0.0);
+      for (int kk = 0; kk < pw; ++kk) {
+        double2 xv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xv[j] = X[(size_t)(4 * cg + j) * n + k0 + kk];
+        const double2* Ak = A + (size_t)(k0 + kk) * lda;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int r = k1 + rl + 64 * q;
+          if (r < n) {
+            const double2 a = __ldg(Ak + r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[q][j] = zfma(acc[q][j], a, xv[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int r = k1 + rl + 64 * q;
+        if (r < n)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            double2& xr = X[(size_t)(4 * cg + j) * n + r];
+            xr = make_double2(xr.x - acc[q][j].x, xr.y - acc[q][j].y);
+          }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- U x = y, panels from the bottom
+  for (int k1 = n; k1 > 0; k1 -= kBlkPanel) {
+    const int k0 = max(0, k1 - kBlkPanel), pw = k1 - k0;
+    for (int idx = t; idx < kBlkPanel * kBlkPanel; idx += kThreads) {
+      const int kk = idx >> 5, rr = idx & 31;
+      double2 v = (kk < pw && rr < pw) ? __ldg(A + (size_t)(k0 + kk) * lda + k0 + rr)
+                                       : make_double2(0.0, 0.0);
+      if (kk == rr && kk < pw) v = zrcp(v);  // the diagonal as its reciprocal
+      Dp[kk][rr] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      double2* xc = X + (size_t)(2 * w + cc) * n + k0;
+      double2 x = l < pw ? xc[l] : make_double2(0.0, 0.0);
+      for (int kk = pw - 1; kk >= 0; --kk) {
+        if (l == kk) x = zmul(x, Dp[kk][kk]);
+        const double2 xk = shfl2(x, kk);
+        if (l < kk) x = zfms(x, Dp[kk][l], xk);
+      }
+      if (l < pw) xc[l] = x;
+    }
+    __syncthreads();
+    if (k0 > 0) {
+      double2 acc[Q][4];
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[q][j] = make_double2(0.0, 0.0);
+      for (int kk = 0; kk < pw; ++kk) {
+        double2 xv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xv[j] = X[(size_t)(4 * cg + j) * n + k0 + kk];
+        const double2* Ak = A + (size_t)(k0 + kk) * lda;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int r = rl + 64 * q;
+          if (r < k0) {
+            const double2 a = __ldg(Ak + r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[q][j] = zfma(acc[q][j], a, xv[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int r = rl + 64 * q;
+        if (r < k0)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            double2& xr = X[(size_t)(4 * cg + j) * n + r];
+            xr = make_double2(xr.x - acc[q][j].x, xr.y - acc[q][j].y);
+          }
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = t; idx < kBlkRhs * n; idx += kThreads) {
+    const int c = idx / n, r = idx - c * n;
+    if (c < nc) Bg[(size_t)c * T.ldb + r] = X[idx];
+  }
+}
+
 // ------------------------------------------ LU solve, large n (> 256)
 // One CTA per right-hand side, column-oriented substitutions: step k reads
 // one (coalesced) column of L or U and updates the remaining rows in
@@ -1110,6 +1276,7 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
   k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
 int getrs_cpw(int max_nrhs, int max_n) {
+  if (max_nrhs >= kBlkMinRhs && max_n >= kBlkMinN && max_n <= kGetrsBlkMaxN) return -2;
   if (max_n > 256 && max_n <= kGetrsCtaMaxN) return -1;  // one CTA per column
   if (max_nrhs <= kNarrowRhs && max_n <= kGetrsWarpMaxN) return 0;  // one warp per column
   if (max_nrhs <= kNarrowRhs && max_n <= 256) return -1;
@@ -1117,6 +1284,7 @@ int getrs_cpw(int max_nrhs, int max_n) {
 }
 int getrs_blocks(int nrhs, int max_n, int cpw) {
   if (cpw == 0) return nrhs;  // warps
+  if (cpw == -2) return (nrhs + kBlkRhs - 1) / kBlkRhs;
   if (cpw < 0) return nrhs;   // CTAs
   const int per = max_n <= 256 ? kWarps * cpw : 1;  // large n: one CTA per column
   return (nrhs + per - 1) / per;
@@ -1128,6 +1296,18 @@ void launch_getrs(const LuSolveTask* tasks, const int* block_off, int n_tasks,
     const int grid = (n_blocks + kWarps - 1) / kWarps;
     if (max_n <= 64) k_getrs_warp<2><<<grid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
     else k_getrs_warp<4><<<grid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
+    return;
+  }
+  if (cpw == -2) {  // blocked, kBlkRhs columns per CTA
+    const size_t sm = size_t(max_n) * (kBlkRhs * 16 + 4) + 16;
+    static const bool attr = [] {
+      cudaFuncSetAttribute(k_getrs_blk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(k_getrs_blk<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      return true;
+    }();
+    (void)attr;
+    if (max_n <= 256) k_getrs_blk<4><<<n_blocks, kThreads, sm, st>>>(tasks, block_off, n_tasks);
+    else k_getrs_blk<8><<<n_blocks, kThreads, sm, st>>>(tasks, block_off, n_tasks);
     return;
   }
   if (cpw < 0) {  // one CTA per column, orders up to kThreads * 8

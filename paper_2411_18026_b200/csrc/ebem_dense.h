@@ -109,6 +109,13 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
 constexpr int kNarrowRhs = 8;
 constexpr int kGetrsWarpMaxN = 128;
 constexpr int kGetrsCtaMaxN = 2048;
+// -2: blocked panels for many columns (ebem_dense.cu k_getrs_blk)
+#ifndef EBEM_BLK_MIN_N
+#define EBEM_BLK_MIN_N 96
+#endif
+constexpr int kBlkMinRhs = 16;
+constexpr int kBlkMinN = EBEM_BLK_MIN_N;
+constexpr int kGetrsBlkMaxN = 512;
 int getrs_cpw(int max_nrhs, int max_n);
 int getrs_blocks(int nrhs, int max_n, int cpw);
 // Dense-solver helpers (ebem_lu.cu): column sums of |a_ij| (1-norm), and

@@ -1435,7 +1435,16 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     for (size_t i = 0; i < q.size(); ++i) {
       const TallBlock& x = q[i];
       const size_t bytes = size_t(x.rows) * x.n * 16;
-      if ((bytes <= size_t(kSmemCap) && !force) || x.rows <= x.n) continue;
+      // blocks that fit one CTA go straight to the pivoted QR unless they are
+      // tall enough that reducing them first is cheaper (EBEM_TSQR_RATIO:
+      // rows / n above which a block is reduced anyway; 0 = never; measured
+      // at 2N = 2^19: 3 saves ~7 ms over 0)
+      static const double ratio = [] {
+        const char* e = std::getenv("EBEM_TSQR_RATIO");
+        return e ? std::atof(e) : 3.0;
+      }();
+      const bool tall = ratio > 0.0 && x.rows > ratio * x.n && tsqr_variant(x.n) >= 0;
+      if ((bytes <= size_t(kSmemCap) && !force && !tall) || x.rows <= x.n) continue;
       if (tsqr_variant(x.n) >= 0) {
         streamed[i] = 1;
         work += double(x.rows) * x.n * (x.n + 64) / tsqr_block_rows(x.n);
@@ -1823,7 +1832,7 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
   if (P.recorder) {
     P.recorder->add(id, t, boff, total,
                     id == KP_GETRS ? g_getrs_smem : id == KP_GEMM ? g_gemm_narrow : 0,
-                    id == KP_GETRS ? (g_getrs_maxn | ((g_getrs_cpw + 1) << 16)) : 0);
+                    id == KP_GETRS ? (g_getrs_maxn | ((g_getrs_cpw + 2) << 16)) : 0);
     return;
   }
   Pack pk;
@@ -1864,7 +1873,7 @@ void Recorder::replay(cudaStream_t st, int phase) {
         break;
       case KP_GETRS:
         launch_getrs(Pack::at<LuSolveTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st,
-                     l.aux, l.aux2 & 0xffff, (l.aux2 >> 16) - 1);
+                     l.aux, l.aux2 & 0xffff, (l.aux2 >> 16) - 2);
         break;
       default:
         throw Error(EBEM_LOGIC_ERROR, "Recorder: unexpected kernel kind");
