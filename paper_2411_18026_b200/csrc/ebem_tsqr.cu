@@ -274,14 +274,17 @@ k_tsqr(const QrTask* __restrict__ tasks) {
 
 }  // namespace
 
+// variant 2: n <= 32 (the leaf blocks), 128 threads, so more independent
+// reflector chains share an SM
+constexpr int kTinyThreads = 128;
 static int tsqr_slots(int n) { return n <= 64 ? EBEM_TSQR_S_SLOTS : EBEM_TSQR_M_SLOTS; }
-int tsqr_variant(int n) { return n <= 64 ? 0 : n <= kTsqrMaxCols ? 1 : -1; }
+int tsqr_variant(int n) { return n <= 32 ? 2 : n <= 64 ? 0 : n <= kTsqrMaxCols ? 1 : -1; }
 int tsqr_block_rows(int n) {
-  return tsqr_variant(n) == 0 ? EBEM_TSQR_S_LANES * kRpt : EBEM_TSQR_M_LANES * kRpt;
+  return tsqr_variant(n) == 1 ? EBEM_TSQR_M_LANES * kRpt : EBEM_TSQR_S_LANES * kRpt;
 }
 int tsqr_ctas_per_sm(int n) {
-  const bool small = tsqr_variant(n) == 0;
-  const int t = small ? EBEM_TSQR_S_THREADS : EBEM_TSQR_M_THREADS;
+  const bool small = tsqr_variant(n) != 1;
+  const int t = tsqr_variant(n) == 2 ? kTinyThreads : small ? EBEM_TSQR_S_THREADS : EBEM_TSQR_M_THREADS;
   const int by_regs = std::max(1, 65536 / (t * (small ? EBEM_TSQR_REGS : EBEM_TSQR_M_REGS)));
   const int by_smem = std::max(1, int((227 * 1024) / (tsqr_smem_bytes(n) + 1024)));
   return std::min(std::min(by_regs, by_smem), 2048 / t);
@@ -304,7 +307,9 @@ static void launch_variant(const QrTask* tasks, int n_tasks, size_t smem, cudaSt
 void launch_tsqr(const QrTask* tasks, int n_tasks, int variant, size_t smem,
                  cudaStream_t st) {
   if (n_tasks <= 0) return;
-  if (variant == 0)
+  if (variant == 2)
+    launch_variant<EBEM_TSQR_S_LANES, kTinyThreads, EBEM_TSQR_S_SLOTS, EBEM_TSQR_REGS>(tasks, n_tasks, smem, st);
+  else if (variant == 0)
     launch_variant<EBEM_TSQR_S_LANES, EBEM_TSQR_S_THREADS, EBEM_TSQR_S_SLOTS, EBEM_TSQR_REGS>(tasks, n_tasks, smem, st);
   else
     launch_variant<EBEM_TSQR_M_LANES, EBEM_TSQR_M_THREADS, EBEM_TSQR_M_SLOTS, EBEM_TSQR_M_REGS>(tasks, n_tasks, smem, st);

@@ -1426,7 +1426,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
   }();
   size_t round = 0;
   for (;;) {
-    std::vector<QrTask> tasks, stream16, stream8;
+    std::vector<QrTask> tasks, stream16, stream8, stream4;
     std::vector<size_t> out_off(q.size(), 0);
     size_t out_total = 0, ws_total = 0;
     std::vector<int> pieces(q.size(), 0);
@@ -1479,7 +1479,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     qr_rounds_[round].ensure(2 * out_total);
     double* ob = qr_rounds_[round].get();
     ++round;
-    size_t smem16 = 0, smem8 = 0;
+    size_t smem16 = 0, smem8 = 0, smem4 = 0;
     for (size_t i = 0; i < q.size(); ++i) {
       if (!pieces[i]) continue;
       const TallBlock& x = q[i];
@@ -1496,7 +1496,10 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
         t.ld = x.ld;
         t.dst_ld = ld_out;
         if (streamed[i]) {
-          if (tsqr_variant(x.n) == 0) {
+          if (tsqr_variant(x.n) == 2) {
+            stream4.push_back(t);
+            smem4 = std::max(smem4, tsqr_smem_bytes(x.n));
+          } else if (tsqr_variant(x.n) == 0) {
             stream16.push_back(t);
             smem16 = std::max(smem16, tsqr_smem_bytes(x.n));
           } else {
@@ -1516,12 +1519,13 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     const size_t o = pk.add(tasks);
     const size_t o16 = pk.add(stream16);
     const size_t o8 = pk.add(stream8);
+    const size_t o4 = pk.add(stream4);
     char* tb = staging.put(pk, st);
     size_t smem = 0;
     for (const QrTask& t : tasks)
       if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
     double fl = 0.0;  // complex Householder QR: 8 m n^2 - 8 n^3 / 3
-    for (const auto* v : {&tasks, &stream16, &stream8})
+    for (const auto* v : {&tasks, &stream16, &stream8, &stream4})
       for (const QrTask& t : *v) {
         const double mm = t.rows, nn = std::min(t.rows, t.n);
         fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
@@ -1531,6 +1535,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     launch_qr_reduce(Pack::at<QrTask>(tb, o), int(tasks.size()), smem, gws.get(), st);
     launch_tsqr(Pack::at<QrTask>(tb, o16), int(stream16.size()), 0, smem16, st);
     launch_tsqr(Pack::at<QrTask>(tb, o8), int(stream8.size()), 1, smem8, st);
+    launch_tsqr(Pack::at<QrTask>(tb, o4), int(stream4.size()), 2, smem4, st);
     g_prof.end(KP_QR, st, fl);
     CK(cudaGetLastError());
     staging.fence(st);
