@@ -253,6 +253,17 @@ __device__ __forceinline__ void scalars_split(const DevCtx* __restrict__ ctx,
   }
 }
 
+// Highest power of the dense series a remainder at argument <= scale needs:
+// ParSeries::rcut counts the parity-form terms t (powers par + 2t) whose
+// size exceeds 1e-22 of the largest at that radius (scalars 2..9, the ones
+// the Burton-Miller operator uses); the integrated forms only shrink them.
+__device__ __forceinline__ int series_maxq_at(const DevCtx* __restrict__ ctx, double scale) {
+  int nt = 1;
+  for (int t = 1; t < kParTerms; ++t) nt += scale > ctx->pser.rcut[t];
+  const int q = 2 * nt + 1;
+  return q < ctx->series_maxq ? q : ctx->series_maxq;
+}
+
 // Closed form of int_0^1 u^upow rem(scale*u) du per scalar,
 // proj/src/kernel_scalars.cpp:108-121,333-344.  Sets *bad when the element is
 // too long for the frequency (the reference throws std::domain_error).
@@ -262,7 +273,7 @@ __device__ __forceinline__ void integrated_remainder3(
     const DevCtx* __restrict__ ctx, double scale, Scalars (&o)[3], int* bad) {
   if (!(ctx->med.kT * scale < 2.5)) atomicExch(bad, 1);
   const double logc = log(scale);
-  const int maxq = ctx->series_maxq;
+  const int maxq = series_maxq_at(ctx, scale);
 #pragma unroll
   for (int j = 0; j < 3; ++j)
 #pragma unroll

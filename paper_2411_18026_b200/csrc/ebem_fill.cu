@@ -104,9 +104,71 @@ __device__ __forceinline__ int bidx(int la, int lb, int i, int j) {
 // ---------------------------------------------------------------- singular
 namespace {
 
+// The four integrated remainders of a coincident pair (weights u^0 .. u^3,
+// proj/src/kernel_scalars.cpp:333-344), only the scalars the bundle uses,
+// with the series terms split over the warp's lanes (lane l: powers l,
+// l + 32) and summed in a fixed butterfly order.  Call with all 32 lanes.
+struct CoincRem {
+  cplx n0[5], n1[5], n3[5];  // u^0, u^1, u^3: n1 n2 n4 n5 n7
+  cplx d1[2], d2[2];         // u^1, u^2: d1 d2
+};
+__device__ __forceinline__ void coincident_remainders(const DevCtx* __restrict__ ctx,
+                                                      double scale, int lane,
+                                                      CoincRem& o, int* bad) {
+  if (lane == 0 && !(ctx->med.kT * scale < 2.5)) atomicExch(bad, 1);
+  const double logc = log(scale);
+  const int maxq = series_maxq_at(ctx, scale);
+  double acc[38];
+#pragma unroll
+  for (int k = 0; k < 38; ++k) acc[k] = 0.0;
+  for (int q = lane; q <= maxq; q += 32) {
+    // c^q by squaring (deterministic per q)
+    double cq = 1.0, base = scale;
+    for (int e = q; e > 0; e >>= 1) {
+      if (e & 1) cq *= base;
+      base *= base;
+    }
+    auto term = [&](int k, int upow, double* dst) {
+      const double4 c = ld_series(ctx, k, q);
+      const double inv = 1.0 / double(q + upow + 1), inv2 = inv * inv;
+      dst[0] = fma(cq, fma(c.z, logc, c.x) * inv - c.z * inv2, dst[0]);
+      dst[1] = fma(cq, fma(c.w, logc, c.y) * inv - c.w * inv2, dst[1]);
+    };
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      term(5 + k, 0, acc + 2 * k);
+      term(5 + k, 1, acc + 10 + 2 * k);
+      term(5 + k, 3, acc + 20 + 2 * k);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      term(2 + k, 1, acc + 30 + 2 * k);
+      term(2 + k, 2, acc + 34 + 2 * k);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 38; ++k)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    o.n0[k] = mk(acc[2 * k], acc[2 * k + 1]);
+    o.n1[k] = mk(acc[10 + 2 * k], acc[10 + 2 * k + 1]);
+    o.n3[k] = mk(acc[20 + 2 * k], acc[20 + 2 * k + 1]);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    o.d1[k] = mk(acc[30 + 2 * k], acc[30 + 2 * k + 1]);
+    o.d2[k] = mk(acc[34 + 2 * k], acc[34 + 2 * k + 1]);
+  }
+}
+
 __device__ void coincident_bundle(const DevCtx* __restrict__ ctx, int e,
-                                  cplx (&v)[kBundle], int* bad) {
+                                  cplx (&v)[kBundle], int* bad, int lane) {
   const double h = ef(ctx, EH, e);
+  CoincRem rm;
+  coincident_remainders(ctx, h, lane, rm, bad);
+  if (lane != 0) return;
   const double tx = ef(ctx, ETX, e), ty = ef(ctx, ETY, e);
   const double nx = ef(ctx, ENX, e), ny = ef(ctx, ENY, e);
   const double logh = log(h);
@@ -125,11 +187,8 @@ __device__ void coincident_bundle(const DevCtx* __restrict__ ctx, int e,
   D[bidx(1, 0, 0, 1)] += mk(-dcoef);
   D[bidx(1, 0, 1, 0)] += mk(dcoef);
 
-  Scalars f0, f1, f2, f3;
-  integrated_remainder(ctx, h, 1, f1, bad);
-  integrated_remainder(ctx, h, 2, f2, bad);
-  const cplx i1 = f2.s[2] - f1.s[2];
-  const cplx i2 = f2.s[3] - f1.s[3];
+  const cplx i1 = rm.d2[0] - rm.d1[0];
+  const cplx i2 = rm.d2[1] - rm.d1[1];
   const double h2 = h * h;
   const double tv[2] = {tx, ty}, nv[2] = {nx, ny};
 #pragma unroll
@@ -140,7 +199,7 @@ __device__ void coincident_bundle(const DevCtx* __restrict__ ctx, int e,
       D[bidx(0, 1, i, j)] += val;
       D[bidx(1, 0, i, j)] -= val;
     }
-  // hypersingular, static part by parts
+// hypersingular, static part by parts
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -154,14 +213,15 @@ __device__ void coincident_bundle(const DevCtx* __restrict__ ctx, int e,
           Nn[bidx(a, b, i, j)] += mk(sgn * qfac * ((logh - 1.5) * dij - tv[i] * tv[j]));
         }
     }
-  // hypersingular remainder: even reduction weights
-  integrated_remainder(ctx, h, 0, f0, bad);
-  integrated_remainder(ctx, h, 3, f3, bad);
+  // hypersingular remainder: even reduction weights (n scalars only:
+  // combine_N reads s[5..9])
   Scalars sdiag, soff;
 #pragma unroll
-  for (int k = 0; k < 10; ++k) {
-    sdiag.s[k] = f3.s[k] / 3.0 - f1.s[k] + (2.0 * f0.s[k]) / 3.0;
-    soff.s[k] = (f0.s[k] - f3.s[k]) / 3.0;
+  for (int k = 0; k < 10; ++k) sdiag.s[k] = soff.s[k] = mk(0.0);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    sdiag.s[5 + k] = rm.n3[k] / 3.0 - rm.n1[k] + (2.0 * rm.n0[k]) / 3.0;
+    soff.s[5 + k] = (rm.n0[k] - rm.n3[k]) / 3.0;
   }
   CMat2 nd, no;
   combine_N(sdiag, tx, ty, nx, ny, nx, ny, nd);
@@ -306,10 +366,8 @@ k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pa
   const int N = ctx->n_nodes;
   cplx v[kBundle];
   if (ea == eb) {
-    if (lane == 0) {
-      coincident_bundle(ctx, ea, v, bad);
-      store_bundle(bundles, pairs[t], v);
-    }
+    coincident_bundle(ctx, ea, v, bad, lane);  // all lanes: split series sums
+    if (lane == 0) store_bundle(bundles, pairs[t], v);
     return;
   }
   const bool end_start = (ea + 1 == N ? 0 : ea + 1) == eb;
