@@ -87,11 +87,18 @@ __device__ __forceinline__ int tier_nodes(double q, int far, double refine) {
   return int(n * refine + 0.5);
 }
 
+// Bundle storage, component-plane major: entry k = bidx(la, lb, i, j) of
+// slot p lives at ((i, j) plane) * 4 nb + 4 p + (la, lb), so the gather of one
+// component block reads a slot's four shape entries as one 64-byte chunk.
+__device__ __forceinline__ long long bslot(long long p, int k, long long nb) {
+  return (long long)(k & 3) * nb * 4 + p * 4 + (k >> 2);
+}
+
 __device__ __forceinline__ void store_bundle(double* __restrict__ out, long long p,
-                                             const cplx (&v)[kBundle]) {
-  double2* o = reinterpret_cast<double2*>(out) + p * kBundle;
+                                             const cplx (&v)[kBundle], long long nb) {
+  double2* o = reinterpret_cast<double2*>(out);
 #pragma unroll
-  for (int k = 0; k < kBundle; ++k) o[k] = make_double2(v[k].re, v[k].im);
+  for (int k = 0; k < kBundle; ++k) o[bslot(p, k, nb)] = make_double2(v[k].re, v[k].im);
 }
 
 // bundle index: ((la * 2 + lb) * 2 + i) * 2 + j
@@ -358,7 +365,7 @@ __device__ void adjacent_bundle(const DevCtx* __restrict__ ctx, int ea, int eb,
 __global__ void __launch_bounds__(128)
 k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pairs,
                 const int* __restrict__ pair_elems, int n, double* __restrict__ bundles,
-                int* bad) {
+                long long nb, int* bad) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= n) return;  // warp-uniform
@@ -367,7 +374,7 @@ k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pa
   cplx v[kBundle];
   if (ea == eb) {
     coincident_bundle(ctx, ea, v, bad, lane);  // all lanes: split series sums
-    if (lane == 0) store_bundle(bundles, pairs[t], v);
+    if (lane == 0) store_bundle(bundles, pairs[t], v, nb);
     return;
   }
   const bool end_start = (ea + 1 == N ? 0 : ea + 1) == eb;
@@ -384,7 +391,7 @@ k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pa
 #pragma unroll
     for (int k = 1; k < kBundle; ++k)
       if (lane == k) mine = v[k];
-    reinterpret_cast<double2*>(bundles)[pairs[t] * kBundle + lane] =
+    reinterpret_cast<double2*>(bundles)[bslot(pairs[t], lane, nb)] =
         make_double2(mine.re, mine.im);
   }
 }
@@ -489,7 +496,8 @@ constexpr int kJUnroll = EBEM_J_UNROLL;  // trial-point loop unroll (experiments
 template <bool BOTH, bool PROXY>
 __device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const FillConst& fc,
                                           const double* __restrict__ recs, int first,
-                                          int count, int n, double* __restrict__ bundles) {
+                                          int count, int n, double* __restrict__ bundles,
+                                          long long nb) {
   // dynamic: [P * n][8 V + 8 U cplx + 2 (Q as re/im pairs)], then the two
   // record buffers [2][P][kSymRec]
   extern __shared__ double2 sh[];
@@ -624,7 +632,8 @@ __device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const 
     const int lp2 = o / (kOrient * kBundle);
     const int rem = o - lp2 * kOrient * kBundle;
     const int orient = rem / kBundle;
-    const int k = rem - orient * kBundle;  // bidx(la, lb, i, j)
+    const int kk = rem - orient * kBundle;
+    const int k = ((kk & 3) << 2) | (kk >> 2);  // bidx(la, lb, i, j); kk: plane-major
     const int idx2 = base + lp2;
     if (idx2 >= count) continue;
     const double* R2 = rec_all + lp2 * kSymRec;
@@ -651,7 +660,7 @@ __device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const 
     const double re = PROXY ? hh * ar : fma(hh, ar, sg * qs * alpha.re);
     const double im = PROXY ? hh * ai : fma(hh, ai, sg * qs * alpha.im);
     const long long dst = __double_as_longlong(orient == 0 ? R2[SR_VD] : R2[SR_UD]);
-    reinterpret_cast<double2*>(bundles)[dst * kBundle + k] = make_double2(re, im);
+    reinterpret_cast<double2*>(bundles)[bslot(dst, k, nb)] = make_double2(re, im);
   }
   __syncthreads();  // shared row sums and pair records are reused
   }
@@ -661,11 +670,11 @@ template <bool BOTH>
 __global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
 k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
            const double* __restrict__ recs, const int* __restrict__ class_bounds,
-           int cls, int n, double* __restrict__ bundles) {
+           int cls, int n, double* __restrict__ bundles, long long nb) {
   // this class's pairs, from the device-side bucket bounds (no host sync)
   const int first = __ldg(class_bounds + cls);
   const int count = __ldg(class_bounds + cls + 1) - first;
-  near_body<BOTH, false>(ctx, fc, recs, first, count, n, bundles);
+  near_body<BOTH, false>(ctx, fc, recs, first, count, n, bundles, nb);
 }
 
 // ------------------------------------------------------------------- proxy
@@ -732,15 +741,15 @@ k_proxy_records(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ job
 __global__ void __launch_bounds__(EBEM_PRX_THREADS, EBEM_PRX_MINB)
 k_proxy_pairs(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
               const double* __restrict__ recs, int n_slots, int ng,
-              double* __restrict__ bundles) {
-  near_body<true, true>(ctx, fc, recs, 0, n_slots, ng, bundles);
+              double* __restrict__ bundles, long long nb) {
+  near_body<true, true>(ctx, fc, recs, 0, n_slots, ng, bundles, nb);
 }
 
 // ------------------------------------------------------------------ gather
 __global__ void __launch_bounds__(kGatherTile)
 k_gather(const GatherJob* __restrict__ jobs, const int* __restrict__ job_block_off,
          int n_jobs, const NodeDesc* __restrict__ desc,
-         const double* __restrict__ bundles) {
+         const double* __restrict__ bundles, long long nb) {
   __shared__ int s_jb;
   if (threadIdx.x == 0) s_jb = find_job(job_block_off, n_jobs, int(blockIdx.x));
   __syncthreads();
@@ -771,7 +780,7 @@ k_gather(const GatherJob* __restrict__ jobs, const int* __restrict__ job_block_o
 #pragma unroll
     for (int y = 0; y < 2; ++y) {
       const long long pidx = J.pair_off + (long long)ra[x] * J.nces + cb[y];
-      const double2 v = __ldg(B + pidx * kBundle + bidx(la[x], lb[y], i, j));
+      const double2 v = __ldg(B + bslot(pidx, bidx(la[x], lb[y], i, j), nb));
       re += v.x;
       im += v.y;
     }
@@ -803,7 +812,7 @@ void launch_sym_records(const DevCtx* ctx, const SymJob* jobs, const int* elems,
 
 void launch_near_sym(const DevCtx* ctx, const FillConst& fc, const double* recs, const int* class_bounds,
                      int cls, long long max_count, int n, bool both, double* bundles,
-                     cudaStream_t st) {
+                     long long nb, cudaStream_t st) {
   if (max_count <= 0) return;
   const int P = EBEM_SYM_THREADS / n;
   const int threads = P * n;
@@ -824,7 +833,7 @@ void launch_near_sym(const DevCtx* ctx, const FillConst& fc, const double* recs,
                          EBEM_SYM_THREADS * (18 * (int)sizeof(double2) +        \
                                              2 * kSymRec * (int)sizeof(double)));  \
     k_near_sym<B><<<grid, threads, smem, st>>>(ctx, fc, recs, class_bounds, cls, n,  \
-                                               bundles);                            \
+                                               bundles, nb);                        \
   } while (0)
   if (both) EBEM_SYM_LAUNCH(true);
   else EBEM_SYM_LAUNCH(false);
@@ -832,12 +841,12 @@ void launch_near_sym(const DevCtx* ctx, const FillConst& fc, const double* recs,
 }
 
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,
-                          const int* pair_elems, int n, double* bundles, int* bad,
-                          cudaStream_t st) {
+                          const int* pair_elems, int n, double* bundles, long long nb,
+                          int* bad, cudaStream_t st) {
   if (n <= 0) return;
   const int bs = 128;  // 4 pairs per CTA, one warp each
   k_near_singular<<<(unsigned)((n + 3) / 4), bs, 0, st>>>(ctx, pairs, pair_elems, n,
-                                                          bundles, bad);
+                                                          bundles, nb, bad);
 }
 
 int proxy_pairs_per_block(int n_gauss) {
@@ -852,7 +861,7 @@ int proxy_blocks_for(int m_prime, int nE, int n_gauss) {
 void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
                         const ProxyJob* jobs, const int* job_block_off, int n_jobs,
                         int n_blocks, const int* elems, double* recs, double* bundles,
-                        cudaStream_t st) {
+                        long long nb, cudaStream_t st) {
   if (n_blocks <= 0) return;
   const int tile = proxy_pairs_per_block(n_gauss);
   const long long n_slots = (long long)n_blocks * tile;
@@ -877,15 +886,16 @@ void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
   (void)attr;
   const long long need = (n_slots + P - 1) / P;
   const int grid = int(std::min<long long>(need, 4LL * n_sm));
-  k_proxy_pairs<<<grid, threads, smem, st>>>(ctx, fc, recs, int(n_slots), n_gauss, bundles);
+  k_proxy_pairs<<<grid, threads, smem, st>>>(ctx, fc, recs, int(n_slots), n_gauss, bundles,
+                                             nb);
 }
 
 void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,
                    int n_blocks, const NodeDesc* desc, const double* bundles,
-                   cudaStream_t st) {
+                   long long nb, cudaStream_t st) {
   if (n_blocks <= 0) return;
   k_gather<<<(unsigned)n_blocks, kGatherTile, 0, st>>>(jobs, job_block_off, n_jobs,
-                                                       desc, bundles);
+                                                       desc, bundles, nb);
 }
 
 }  // namespace ebem_gpu

@@ -9,9 +9,11 @@
 namespace ebem_gpu {
 
 // ---- fill (ebem_fill.cu)
+// Bundles (element-pair results, kBundle complex each) are stored
+// component-plane major over the wave's nb slots (bslot in ebem_fill.cu).
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,
-                          const int* pair_elems, int n, double* bundles, int* bad,
-                          cudaStream_t st);
+                          const int* pair_elems, int n, double* bundles, long long nb,
+                          int* bad, cudaStream_t st);
 void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
                          const long long* job_off, int n_jobs, const int* elems,
                          long long n_pairs, unsigned char* keys, int* vals,
@@ -26,7 +28,7 @@ void launch_sym_records(const DevCtx* ctx, const SymJob* jobs, const int* elems,
 // records is read from class_bounds on the device (max_count bounds the grid).
 void launch_near_sym(const DevCtx* ctx, const FillConst& fc, const double* recs, const int* class_bounds,
                      int cls, long long max_count, int n, bool both, double* bundles,
-                     cudaStream_t st);
+                     long long nb, cudaStream_t st);
 // CUB radix sort of (key, value) by the low 3 key bits; temp grows as needed.
 void sort_pairs_by_class(unsigned char* keys_in, unsigned char* keys_out,
                          int* vals_in, int* vals_out, long long n, void** temp,
@@ -41,11 +43,11 @@ int proxy_pairs_per_block(int n_gauss);
 void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
                         const ProxyJob* jobs, const int* job_block_off, int n_jobs,
                         int n_blocks, const int* elems, double* recs, double* bundles,
-                        cudaStream_t st);
+                        long long nb, cudaStream_t st);
 constexpr int kGatherTile = 256;  // output entries per gather CTA
 void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,
                    int n_blocks, const NodeDesc* desc, const double* bundles,
-                   cudaStream_t st);
+                   long long nb, cudaStream_t st);
 
 // ---- incident-field right-hand sides (ebem_rhs.cu)
 // Post-processing (proj/src/postprocess.cpp): distance of m points to the

@@ -1292,7 +1292,7 @@ void Problem::execute(FillPlan& plan) {
     launch_proxy_pairs(dctx(), fc_, pcfg_.n_gauss, Pack::at<ProxyJob>(base, o_pj),
                        Pack::at<int>(base, o_pb), int(plan.proxy_.size()),
                        plan.proxy_blocks_, el, sym_recs_.get() + size_t(kSymRec) * nsym,
-                       bundles.get(), st_);
+                       bundles.get(), plan.bundles_, st_);
     g_prof.end(KP_PROXY, st_, pts);
   }
   if (nsym > 0) {
@@ -1306,7 +1306,7 @@ void Problem::execute(FillPlan& plan) {
       const int nq = int((acfg_.far_nodes + add[tier]) * acfg_.refine + 0.5);
       g_prof.begin(st_);
       launch_near_sym(dctx(), fc_, sym_recs_.get(), sym_bounds_.get(), c, nsym, nq, both,
-                      bundles.get(), st_);
+                      bundles.get(), plan.bundles_, st_);
       // points = class count x nq^2, read back at collect time
       g_prof.end_counted(both ? KP_NEAR_SYM : KP_NEAR_1S, st_, sym_bounds_.get() + c,
                          double(nq) * nq);
@@ -1317,13 +1317,13 @@ void Problem::execute(FillPlan& plan) {
     g_prof.begin(st_);
     launch_near_singular(dctx(), Pack::at<long long>(base, o_sp),
                          Pack::at<int>(base, o_se), int(plan.sing_pair_.size()),
-                         bundles.get(), bad.get(), st_);
+                         bundles.get(), plan.bundles_, bad.get(), st_);
     g_prof.end(KP_NEAR_SING, st_, double(plan.sing_pair_.size()));
   }
   g_prof.begin(st_);
   launch_gather(Pack::at<GatherJob>(base, o_gj), Pack::at<int>(base, o_go),
                 int(plan.gather_.size()), n_gblk, Pack::at<NodeDesc>(base, o_de),
-                bundles.get(), st_);
+                bundles.get(), plan.bundles_, st_);
   // bytes: 4 bundle reads (16 B each) + one 16 B store per entry
   g_prof.end(KP_GATHER, st_, 80.0 * double(plan.entries_));
   CK(cudaGetLastError());
