@@ -513,8 +513,13 @@ class AssemblerSource(BlockSource):
     def __init__(self, assembler: BlockAssembler, proxy: ProxyConfig = None):
         self._asm = assembler
         self._proxy = proxy or ProxyConfig()
-        self._h = _Handle(assembler.mesh(), assembler.medium(), assembler.alpha(),
-                          assembler.config(), self._proxy)
+        # the assembler's native problem (geometry, series tables on the device)
+        # already carries the default proxy settings: share it when they match
+        if self._proxy == ProxyConfig():
+            self._h = assembler._h
+        else:
+            self._h = _Handle(assembler.mesh(), assembler.medium(), assembler.alpha(),
+                              assembler.config(), self._proxy)
 
     def n_nodes(self): return self._asm.n_nodes()
     def assembler(self): return self._asm

@@ -403,15 +403,22 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
       ParSeries& ps = hctx_.pser;
       int ntmax = 1;
       for (int k = 2; k < 10; ++k) ntmax = std::max(ntmax, ps.nt[k]);
+      // coefficient magnitudes once, powers of r incrementally
+      double amag[10][kParTerms], bmag[10][kParTerms];
+      for (int k = 2; k < 10; ++k)
+        for (int p = 0; p < ps.nt[k]; ++p) {
+          amag[k][p] = std::hypot(ps.a[k][p].x, ps.a[k][p].y);
+          bmag[k][p] = std::hypot(ps.b[k][p].x, ps.b[k][p].y);
+        }
       auto need = [&](double r) {
         const double lr = std::fabs(std::log(r));
+        const double r2 = r * r;
         int worst = 1;
         for (int k = 2; k < 10; ++k) {
           double big = 0.0, mag[kParTerms];
-          for (int p = 0; p < ps.nt[k]; ++p) {
-            const double2 a = ps.a[k][p], b = ps.b[k][p];
-            mag[p] = (std::hypot(a.x, a.y) + std::hypot(b.x, b.y) * lr) *
-                     std::pow(r, ps.par[k] + 2 * p);
+          double rp = ps.par[k] == 0 ? 1.0 : std::pow(r, ps.par[k]);
+          for (int p = 0; p < ps.nt[k]; ++p, rp *= r2) {
+            mag[p] = (amag[k][p] + bmag[k][p] * lr) * rp;
             big = std::max(big, mag[p]);
           }
           int nt = ps.nt[k];
