@@ -23,20 +23,26 @@ namespace ebem_gpu {
 
 namespace {
 
-constexpr int kTeamThreads = 512;
-constexpr int kTeamLanes = 8;
+#ifndef EBEM_TEAM_THREADS
+#define EBEM_TEAM_THREADS 512
+#endif
+#ifndef EBEM_TEAM_LANES
+#define EBEM_TEAM_LANES 8
+#endif
+constexpr int kTeamThreads = EBEM_TEAM_THREADS;
+constexpr int kTeamLanes = EBEM_TEAM_LANES;
 constexpr int kTeams = kTeamThreads / kTeamLanes;  // 64
 
 // The 8 lanes of this thread's team (teams of one warp may diverge).
 __device__ __forceinline__ unsigned team_mask() {
-  return 0xFFu << ((threadIdx.x & 31) & ~7);
+  constexpr unsigned kLaneBits = (1u << kTeamLanes) - 1u;
+  return kLaneBits << ((threadIdx.x & 31) & ~(kTeamLanes - 1));
 }
 
 __device__ __forceinline__ double team_sum(double v) {
   const unsigned mk = team_mask();
-  v += __shfl_xor_sync(mk, v, 1);
-  v += __shfl_xor_sync(mk, v, 2);
-  v += __shfl_xor_sync(mk, v, 4);
+#pragma unroll
+  for (int o = 1; o < kTeamLanes; o <<= 1) v += __shfl_xor_sync(mk, v, o);
   return v;
 }
 
