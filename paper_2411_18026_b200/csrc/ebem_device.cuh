@@ -69,6 +69,31 @@ __device__ __forceinline__ double clenshaw01(const double (&c)[N], double u) {
   return fma(y, b1, c[0] - b2);
 }
 
+template <int N>
+__device__ __forceinline__ double horner(const double (&c)[N], double u) {
+  double s = c[N - 1];
+#pragma unroll
+  for (int j = N - 2; j >= 0; --j) s = fma(s, u, c[j]);
+  return s;
+}
+
+// Regular parts of J0, J1/x, Y0, Y1 for x <= 8 in t = (x/8)^2: power series
+// (one FMA per term) up to kTaylorX, Chebyshev (Clenshaw) above.
+__device__ __forceinline__ void small_parts(double x, double t, double& j0, double& j1x,
+                                            double& v0, double& v1) {
+  if (x <= kTaylorX) {
+    j0 = horner(kJ0Taylor, t);
+    j1x = horner(kJ1Taylor, t);
+    v0 = horner(kV0Taylor, t);
+    v1 = horner(kV1Taylor, t);
+  } else {
+    j0 = clenshaw01(kJ0Small, t);
+    j1x = clenshaw01(kJ1Small, t);
+    v0 = clenshaw01(kV0Small, t);
+    v1 = clenshaw01(kV1Small, t);
+  }
+}
+
 constexpr double kTwoOverPi = 0.63661977236758134308;
 constexpr double kEulerGamma = 0.57721566490153286061;
 constexpr double kPio4Hi = 0.78539816339744827900;
@@ -82,11 +107,12 @@ __device__ __forceinline__ void hankel01(double x, cplx& h0, cplx& h1) {
   if (x <= 8.0) {
     const double q = x * 0.125;
     const double t = q * q;
-    const double j0 = clenshaw01(kJ0Small, t);
-    const double j1 = clenshaw01(kJ1Small, t) * x;
+    double j0, j1x, v0, v1;
+    small_parts(x, t, j0, j1x, v0, v1);
+    const double j1 = j1x * x;
     const double lg = kTwoOverPi * (log(0.5 * x) + kEulerGamma);
-    const double y0 = fma(lg, j0, clenshaw01(kV0Small, t));
-    const double y1 = clenshaw01(kV1Small, t) * x + lg * j1 - kTwoOverPi / x;
+    const double y0 = fma(lg, j0, v0);
+    const double y1 = v1 * x + lg * j1 - kTwoOverPi / x;
     h0 = mk(j0, y0);
     h1 = mk(j1, y1);
     return;
@@ -421,11 +447,12 @@ __device__ __forceinline__ void hankel01_lg(double x, double log_half_x,
   if (x <= 8.0) {
     const double q = x * 0.125;
     const double t = q * q;
-    const double j0 = clenshaw01(kJ0Small, t);
-    const double j1 = clenshaw01(kJ1Small, t) * x;
+    double j0, j1x, v0, v1;
+    small_parts(x, t, j0, j1x, v0, v1);
+    const double j1 = j1x * x;
     const double lg = kTwoOverPi * (log_half_x + kEulerGamma);
-    const double y0 = fma(lg, j0, clenshaw01(kV0Small, t));
-    const double y1 = clenshaw01(kV1Small, t) * x + lg * j1 - kTwoOverPi / x;
+    const double y0 = fma(lg, j0, v0);
+    const double y1 = v1 * x + lg * j1 - kTwoOverPi / x;
     h0 = mk(j0, y0);
     h1 = mk(j1, y1);
     return;
