@@ -2,7 +2,8 @@
 //   k_proxy_pairs     proxy polygon <-> curve element pairs, n_g x n_g Gauss,
 //                     full kernel, both orientations from one scalar
 //                     evaluation (kernel_cross_block, proj/src/assembly.cpp:424-509)
-//   k_sym_classify    quadrature-tier class of every near element pair
+//   k_sym_count       quadrature-tier class of every near element pair + counts
+//   k_sym_scatter     per-pair records written straight into their class ranges
 //   k_near_sym        separated element pairs, tiered tensor Gauss with the
 //                     static hypersingular part integrated by parts
 //                     (PairIntegrator::separated, proj/src/assembly.cpp:248-286);
@@ -397,48 +398,98 @@ k_near_singular(const DevCtx* __restrict__ ctx, const long long* __restrict__ pa
 }
 
 // ------------------------------------------------------- symmetric near
-// Class of every near pair (kSymClasses, ebem_jobs.h), for the bucketing sort.
-__global__ void __launch_bounds__(256)
-k_sym_classify(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
-               const long long* __restrict__ job_off, int n_jobs,
-               const int* __restrict__ elems, long long n_pairs,
-               unsigned char* __restrict__ keys, int* __restrict__ vals,
-               int* __restrict__ pair_job) {
+// Bucketing of the symmetric near pairs by quadrature class (kSymClasses,
+// ebem_jobs.h) as a two-pass count-and-scatter: pass 1 classifies every pair
+// and counts the classes, pass 2 writes each non-skipped pair's record
+// straight into its class range.  Within a CTA the pairs of one class keep
+// their pair order (warp ballots + a per-warp prefix), so consecutive records
+// still address consecutive bundle slots; one global atomic per class per CTA.
+constexpr int kBucketThreads = 256;
+// counts / cursors live after the bounds in the same small device array
+constexpr int kBoundsCounts = 16, kBoundsCursors = 32, kBoundsInts = 48;
+
+__global__ void __launch_bounds__(kBucketThreads)
+k_sym_count(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
+            const long long* __restrict__ job_off, int n_jobs,
+            const int* __restrict__ elems, long long n_pairs,
+            unsigned char* __restrict__ keys, int* __restrict__ pair_job,
+            int* __restrict__ bounds) {
+  __shared__ int s_cnt[kSymClasses];
+  if (threadIdx.x < kSymClasses) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (p >= n_pairs) return;
-  const int jb = find_job(job_off, n_jobs, p);
-  const SymJob J = jobs[jb];
-  const long long local = p - J.local_off;
-  const int a = int(local / J.nE);
-  const int q = int(local - (long long)a * J.nE);
-  const int ea = __ldg(elems + J.a_off + a);
-  const int eb = __ldg(elems + J.e_off + q);
-  const int N = ctx->n_nodes;
-  const int na = ea + 1 == N ? 0 : ea + 1;
-  const int nb = eb + 1 == N ? 0 : eb + 1;
-  unsigned char key = kSymClasses - 1;  // skip
-  if (!(ea == eb || na == eb || nb == ea) && !(J.tri && a >= q)) {
-    const Elem8 A = load_elem8(ctx, ea), B = load_elem8(ctx, eb);
-    const double rq = element_distance8(A, B) / fmax(A.h, B.h);
-    key = (rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3) + (J.onesided ? 4 : 0);
+  if (p < n_pairs) {
+    const int jb = find_job(job_off, n_jobs, p);
+    const SymJob J = jobs[jb];
+    const long long local = p - J.local_off;
+    const int a = int(local / J.nE);
+    const int q = int(local - (long long)a * J.nE);
+    const int ea = __ldg(elems + J.a_off + a);
+    const int eb = __ldg(elems + J.e_off + q);
+    const int N = ctx->n_nodes;
+    const int na = ea + 1 == N ? 0 : ea + 1;
+    const int nb = eb + 1 == N ? 0 : eb + 1;
+    unsigned char key = kSymClasses - 1;  // skip
+    if (!(ea == eb || na == eb || nb == ea) && !(J.tri && a >= q)) {
+      const Elem8 A = load_elem8(ctx, ea), B = load_elem8(ctx, eb);
+      const double rq = element_distance8(A, B) / fmax(A.h, B.h);
+      key = (rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3) + (J.onesided ? 4 : 0);
+    }
+    keys[p] = key;
+    pair_job[p] = jb;  // read back by the scatter pass (no second search)
+    atomicAdd(&s_cnt[key], 1);
   }
-  keys[p] = key;
-  vals[p] = int(p);
-  pair_job[p] = jb;  // read back by the near-field kernel (no second search)
+  __syncthreads();
+  if (threadIdx.x < kSymClasses && s_cnt[threadIdx.x])
+    atomicAdd(bounds + kBoundsCounts + threadIdx.x, s_cnt[threadIdx.x]);
 }
 
-// One record per sorted near pair (skip class excluded): the element geometry
-// and output slots the near-field kernel needs, laid out so one CTA stages a
-// whole group of pairs with contiguous async copies (no dependent index
-// chain on the compute kernel's critical path).
-__global__ void __launch_bounds__(256)
-k_sym_records(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
-              const int* __restrict__ elems, const int* __restrict__ sorted_ids,
-              const int* __restrict__ pair_job, const int* __restrict__ class_bounds,
-              double* __restrict__ recs) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= __ldg(class_bounds + kSymClasses - 1)) return;  // skip class at the end
-  const int p = __ldg(sorted_ids + idx);
+// One record per non-skipped near pair, at bounds[class] + its rank: the
+// element geometry and output slots the near-field kernel needs, laid out so
+// one CTA stages a whole group of pairs with contiguous async copies (no
+// dependent index chain on the compute kernel's critical path).  CTA 0 also
+// publishes the class bounds (exclusive prefix of the counts, bounds[9] = n).
+__global__ void __launch_bounds__(kBucketThreads)
+k_sym_scatter(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
+              const int* __restrict__ elems, const unsigned char* __restrict__ keys,
+              const int* __restrict__ pair_job, long long n_pairs,
+              int* __restrict__ bounds, double* __restrict__ recs) {
+  constexpr int kWarps = kBucketThreads / 32;
+  __shared__ int s_start[kSymClasses];       // class starts (prefix of counts)
+  __shared__ int s_wcnt[kWarps][kSymClasses];
+  __shared__ int s_base[kSymClasses];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int c = 0; c < kSymClasses; ++c) {
+      s_start[c] = s;
+      if (blockIdx.x == 0) bounds[c] = s;
+      s += bounds[kBoundsCounts + c];
+    }
+    if (blockIdx.x == 0) bounds[kSymClasses] = s;
+  }
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int key = p < n_pairs ? int(__ldg(keys + p)) : kSymClasses - 1;
+  // per-warp ranks of each lane within its class (pair order kept)
+  const unsigned same = __match_any_sync(0xffffffffu, key);
+  const int rank = __popc(same & ((1u << lane) - 1u));
+  if (lane < kSymClasses) s_wcnt[warp][lane] = 0;
+  __syncwarp();
+  if (rank == 0) s_wcnt[warp][key] = __popc(same);
+  __syncthreads();
+  if (threadIdx.x < kSymClasses - 1) {  // the skip class gets no records
+    const int c = threadIdx.x;
+    int tot = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      const int v = s_wcnt[w][c];
+      s_wcnt[w][c] = tot;
+      tot += v;
+    }
+    s_base[c] = tot ? s_start[c] + atomicAdd(bounds + kBoundsCursors + c, tot) : 0;
+  }
+  __syncthreads();
+  if (key == kSymClasses - 1) return;
+  const long long idx = (long long)s_base[key] + s_wcnt[warp][key] + rank;
   const SymJob J = jobs[__ldg(pair_job + p)];
   const long long local = p - J.local_off;
   const int a = int(local / J.nE);
@@ -792,23 +843,21 @@ k_gather(const GatherJob* __restrict__ jobs, const int* __restrict__ job_block_o
 // ------------------------------------------------------------ host wrappers
 
 
-void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
-                         const long long* job_off, int n_jobs, const int* elems,
-                         long long n_pairs, unsigned char* keys, int* vals,
-                         int* pair_job, cudaStream_t st) {
+void launch_sym_bucket(const DevCtx* ctx, const SymJob* jobs, const long long* job_off,
+                       int n_jobs, const int* elems, long long n_pairs,
+                       unsigned char* keys, int* pair_job, int* bounds, double* recs,
+                       cudaStream_t st) {
   if (n_pairs <= 0) return;
-  k_sym_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, st>>>(
-      ctx, jobs, job_off, n_jobs, elems, n_pairs, keys, vals, pair_job);
+  cudaMemsetAsync(bounds + kBoundsCounts, 0,
+                  size_t(kBoundsInts - kBoundsCounts) * sizeof(int), st);
+  const unsigned grid = (unsigned)((n_pairs + kBucketThreads - 1) / kBucketThreads);
+  k_sym_count<<<grid, kBucketThreads, 0, st>>>(ctx, jobs, job_off, n_jobs, elems, n_pairs,
+                                               keys, pair_job, bounds);
+  k_sym_scatter<<<grid, kBucketThreads, 0, st>>>(ctx, jobs, elems, keys, pair_job, n_pairs,
+                                                 bounds, recs);
 }
 
-void launch_sym_records(const DevCtx* ctx, const SymJob* jobs, const int* elems,
-                        const int* sorted_ids, const int* pair_job,
-                        const int* class_bounds, long long n_pairs, double* recs,
-                        cudaStream_t st) {
-  if (n_pairs <= 0) return;
-  k_sym_records<<<(unsigned)((n_pairs + 255) / 256), 256, 0, st>>>(
-      ctx, jobs, elems, sorted_ids, pair_job, class_bounds, recs);
-}
+int sym_bounds_ints() { return kBoundsInts; }
 
 void launch_near_sym(const DevCtx* ctx, const FillConst& fc, const double* recs, const int* class_bounds,
                      int cls, long long max_count, int n, bool both, double* bundles,

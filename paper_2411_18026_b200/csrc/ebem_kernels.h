@@ -14,28 +14,21 @@ namespace ebem_gpu {
 void launch_near_singular(const DevCtx* ctx, const long long* pairs,
                           const int* pair_elems, int n, double* bundles, long long nb,
                           int* bad, cudaStream_t st);
-void launch_sym_classify(const DevCtx* ctx, const SymJob* jobs,
-                         const long long* job_off, int n_jobs, const int* elems,
-                         long long n_pairs, unsigned char* keys, int* vals,
-                         int* pair_job, cudaStream_t st);
-// Records of the sorted near pairs (kSymRec doubles each: both elements'
-// geometry, the two bundle slots, the Jacobian product), in class order.
-void launch_sym_records(const DevCtx* ctx, const SymJob* jobs, const int* elems,
-                        const int* sorted_ids, const int* pair_job,
-                        const int* class_bounds, long long n_pairs, double* recs,
-                        cudaStream_t st);
-// One launch per near-pair class cls; the class's range of the sorted pair
+// Bucketing of the wave's symmetric near pairs by class (count pass, then a
+// scatter pass that writes each non-skipped pair's record, kSymRec doubles:
+// both elements' geometry, the two bundle slots, the Jacobian product, into
+// its class range).  bounds holds sym_bounds_ints() ints: the class starts
+// bounds[0..kSymClasses] (bounds[kSymClasses] = n_pairs), then counters.
+void launch_sym_bucket(const DevCtx* ctx, const SymJob* jobs, const long long* job_off,
+                       int n_jobs, const int* elems, long long n_pairs,
+                       unsigned char* keys, int* pair_job, int* bounds, double* recs,
+                       cudaStream_t st);
+int sym_bounds_ints();
+// One launch per near-pair class cls; the class's range of the bucketed pair
 // records is read from class_bounds on the device (max_count bounds the grid).
 void launch_near_sym(const DevCtx* ctx, const FillConst& fc, const double* recs, const int* class_bounds,
                      int cls, long long max_count, int n, bool both, double* bundles,
                      long long nb, cudaStream_t st);
-// CUB radix sort of (key, value) by the low 3 key bits; temp grows as needed.
-void sort_pairs_by_class(unsigned char* keys_in, unsigned char* keys_out,
-                         int* vals_in, int* vals_out, long long n, void** temp,
-                         size_t* temp_bytes, cudaStream_t st);
-void launch_class_bounds(const unsigned char* sorted_keys, long long n,
-                         int* bounds /* 9 ints: start of class c, c = 0..8 */,
-                         cudaStream_t st);
 int proxy_blocks_for(int m_prime, int nE, int n_gauss);
 // Proxy blocks: writes the slot records into recs (proxy_blocks x
 // proxy_pairs_per_block(n_gauss) x kSymRec doubles), then evaluates them.

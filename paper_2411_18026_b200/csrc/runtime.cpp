@@ -339,8 +339,6 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
       sym_keys_(scratch().sym_keys),
       sym_vals_(scratch().sym_vals),
       sym_recs_(scratch().sym_recs),
-      sort_temp_(scratch().sort_temp),
-      sort_temp_bytes_(scratch().sort_temp_bytes),
       sym_bounds_(scratch().sym_bounds),
       sym_bounds_host_(scratch().sym_bounds_host),
       sym_ev_(scratch().sym_ev),
@@ -516,8 +514,6 @@ Problem::Problem(int n)
       sym_keys_(scratch().sym_keys),
       sym_vals_(scratch().sym_vals),
       sym_recs_(scratch().sym_recs),
-      sort_temp_(scratch().sort_temp),
-      sort_temp_bytes_(scratch().sort_temp_bytes),
       sym_bounds_(scratch().sym_bounds),
       sym_bounds_host_(scratch().sym_bounds_host),
       sym_ev_(scratch().sym_ev),
@@ -1259,10 +1255,10 @@ void Problem::execute(FillPlan& plan) {
       bundles.ensure(std::max(need, size_t(kMaxBundlesPerWave) * kBundle * 2 * 5 / 4));
   }
   const int* el = Pack::at<int>(base, o_el);
-  // symmetric near pairs: classify by tier and sort (async), read the class
+  // symmetric near pairs: bucket by tier (count + scatter, async), read the class
   // bounds through an event so the host waits only for these small kernels
   const long long nsym = plan.sym_pairs_;
-  // pair records: the sorted near pairs, then the proxy slots
+  // pair records: the bucketed near pairs, then the proxy slots
   const long long proxy_slots =
       (long long)plan.proxy_blocks_ * proxy_pairs_per_block(pcfg_.n_gauss);
   if (nsym == 0 && proxy_slots > 0) sym_recs_.ensure(size_t(kSymRec) * proxy_slots);
@@ -1271,25 +1267,17 @@ void Problem::execute(FillPlan& plan) {
   if (nsym > 0) {
     sj = Pack::at<SymJob>(base, o_sj);
     so = Pack::at<long long>(base, o_so);
-    sym_keys_.ensure(2 * size_t(nsym));
-    sym_vals_.ensure(3 * size_t(nsym));  // unsorted | sorted ids | job of each pair
+    sym_keys_.ensure(size_t(nsym));
+    sym_vals_.ensure(size_t(nsym));  // job of each pair
     if (!sym_bounds_host_) {
       CK(cudaMallocHost(reinterpret_cast<void**>(&sym_bounds_host_), 16 * sizeof(int)));
       CK(cudaEventCreateWithFlags(&sym_ev_, cudaEventDisableTiming));
-      sym_bounds_.alloc(16);
+      sym_bounds_.alloc(size_t(sym_bounds_ints()));
     }
-    unsigned char* kin = sym_keys_.get();
-    unsigned char* kout = kin + nsym;
-    int* vin = sym_vals_.get();
-    int* vout = vin + nsym;
-    launch_sym_classify(dctx(), sj, so, int(plan.sym_.size()), el, nsym, kin, vin,
-                        vin + 2 * nsym, st_);
-    sort_pairs_by_class(kin, kout, vin, vout, nsym, &sort_temp_, &sort_temp_bytes_, st_);
-    launch_class_bounds(kout, nsym, sym_bounds_.get(), st_);
     sym_recs_.ensure(size_t(kSymRec) * (nsym + proxy_slots));
-    launch_sym_records(dctx(), sj, el, vout, vin + 2 * nsym, sym_bounds_.get(), nsym,
-                       sym_recs_.get(), st_);
-    g_launches += 4;
+    launch_sym_bucket(dctx(), sj, so, int(plan.sym_.size()), el, nsym, sym_keys_.get(),
+                      sym_vals_.get(), sym_bounds_.get(), sym_recs_.get(), st_);
+    g_launches += 2;
   }
   if (!plan.proxy_.empty()) {
     double pts = 0.0;

@@ -303,8 +303,6 @@ struct Scratch {
   DBuf<unsigned char> sym_keys;
   DBuf<int> sym_vals;
   DBuf<double> sym_recs;  // kSymRec doubles per sorted near pair
-  void* sort_temp = nullptr;
-  size_t sort_temp_bytes = 0;
   DBuf<int> sym_bounds;
   int* sym_bounds_host = nullptr;
   cudaEvent_t sym_ev = nullptr;
@@ -380,8 +378,6 @@ class Problem {
   DBuf<unsigned char>& sym_keys_;   // 2 x pairs (in, out)
   DBuf<int>& sym_vals_;             // 2 x pairs (in, out)
   DBuf<double>& sym_recs_;          // sorted pair records (geometry, outputs)
-  void*& sort_temp_;
-  size_t& sort_temp_bytes_;
   DBuf<int>& sym_bounds_;
   int*& sym_bounds_host_;  // pinned
   cudaEvent_t& sym_ev_;
