@@ -458,6 +458,9 @@ k_sym_scatter(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
   __shared__ int s_start[kSymClasses];       // class starts (prefix of counts)
   __shared__ int s_wcnt[kWarps][kSymClasses];
   __shared__ int s_base[kSymClasses];
+  constexpr int kRecPad = kSymRec / 2 + 1;  // 144-byte rows: conflict-free 16-byte stores
+  __shared__ double2 s_rec[kWarps * 32 * kRecPad];
+  __shared__ long long s_idx[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     int s = 0;
@@ -488,24 +491,39 @@ k_sym_scatter(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
     s_base[c] = tot ? s_start[c] + atomicAdd(bounds + kBoundsCursors + c, tot) : 0;
   }
   __syncthreads();
-  if (key == kSymClasses - 1) return;
-  const long long idx = (long long)s_base[key] + s_wcnt[warp][key] + rank;
-  const SymJob J = jobs[__ldg(pair_job + p)];
-  const long long local = p - J.local_off;
-  const int a = int(local / J.nE);
-  const int q = int(local - (long long)a * J.nE);
-  const int ea = __ldg(elems + J.a_off + a);
-  const int eb = __ldg(elems + J.e_off + q);
-  const Elem8 A = load_elem8(ctx, ea), B = load_elem8(ctx, eb);
-  double r[kSymRec] = {A.px, A.py, A.dx, A.dy, A.nx, A.ny,
-                       B.px, B.py, B.dx, B.dy, B.nx, B.ny};
-  r[SR_VD] = __longlong_as_double(J.v_off + local);
-  r[SR_UD] = __longlong_as_double(J.u_off + (long long)q * J.nA + a);
-  r[SR_HH] = A.h * B.h;
-  r[15] = 0.0;
-  double2* o = reinterpret_cast<double2*>(recs + idx * kSymRec);
+  // records go through shared memory so that each store instruction writes
+  // 512 contiguous bytes (a warp's records of one class are contiguous)
+  double2* const wrec = s_rec + warp * (32 * kRecPad);
+  if (key != kSymClasses - 1) {
+    const long long idx = (long long)s_base[key] + s_wcnt[warp][key] + rank;
+    const SymJob J = jobs[__ldg(pair_job + p)];
+    const long long local = p - J.local_off;
+    const int a = int(local / J.nE);
+    const int q = int(local - (long long)a * J.nE);
+    const int ea = __ldg(elems + J.a_off + a);
+    const int eb = __ldg(elems + J.e_off + q);
+    const Elem8 A = load_elem8(ctx, ea), B = load_elem8(ctx, eb);
+    double r[kSymRec] = {A.px, A.py, A.dx, A.dy, A.nx, A.ny,
+                         B.px, B.py, B.dx, B.dy, B.nx, B.ny};
+    r[SR_VD] = __longlong_as_double(J.v_off + local);
+    r[SR_UD] = __longlong_as_double(J.u_off + (long long)q * J.nA + a);
+    r[SR_HH] = A.h * B.h;
+    r[15] = 0.0;
 #pragma unroll
-  for (int k = 0; k < kSymRec / 2; ++k) o[k] = make_double2(r[2 * k], r[2 * k + 1]);
+    for (int k = 0; k < kSymRec / 2; ++k)
+      wrec[lane * kRecPad + k] = make_double2(r[2 * k], r[2 * k + 1]);
+    s_idx[warp][lane] = idx;
+  } else {
+    s_idx[warp][lane] = -1;
+  }
+  __syncwarp();
+  double2* const o = reinterpret_cast<double2*>(recs);
+#pragma unroll
+  for (int c = lane; c < 32 * (kSymRec / 2); c += 32) {
+    const int rr = c / (kSymRec / 2), piece = c - rr * (kSymRec / 2);
+    const long long idx = s_idx[warp][rr];
+    if (idx >= 0) o[idx * (kSymRec / 2) + piece] = wrec[rr * kRecPad + piece];
+  }
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {

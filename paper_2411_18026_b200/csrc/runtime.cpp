@@ -1899,6 +1899,28 @@ void run_gemms(Problem& P, const std::vector<GemmTask>& t) {
     if (k == 0) { narrow = 0; break; }
     narrow = std::max(narrow, k);
   }
+  if (narrow == 0) {
+    // EBEM_GEMM_LOG: per-launch shape summary of the tiled merge GEMMs
+    static const bool log = std::getenv("EBEM_GEMM_LOG") != nullptr;
+    if (log) {
+      long long tiles = 0;
+      double mnk = 0, mn = 0;
+      int mmax = 0, nmax = 0, kmax = 0, kmin = 1 << 30;
+      for (const GemmTask& g : t) {
+        if (g.k <= 0) continue;
+        tiles += gemm_blocks(g, 0);
+        mnk += double(g.m) * g.n * g.k;
+        mn += double(g.m) * g.n;
+        mmax = std::max(mmax, g.m); nmax = std::max(nmax, g.n);
+        kmax = std::max(kmax, g.k); kmin = std::min(kmin, g.k);
+      }
+      std::fprintf(stderr,
+                   "gemm launch: tasks %zu tiles %lld mean m*n %.0f "
+                   "mean k %.1f k [%d, %d] max m %d max n %d flops %.3g\n",
+                   t.size(), tiles, mn / t.size(), mnk / mn, kmin, kmax, mmax, nmax,
+                   8 * mnk);
+    }
+  }
   g_gemm_narrow = narrow;
   run_blocked(P, t, [narrow](const GemmTask& g) { return g.k > 0 ? gemm_blocks(g, narrow) : 0; },
               launch_gemm_cur, KP_GEMM,
