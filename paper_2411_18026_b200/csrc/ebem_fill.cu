@@ -432,8 +432,20 @@ k_sym_count(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
     unsigned char key = kSymClasses - 1;  // skip
     if (!(ea == eb || na == eb || nb == ea) && !(J.tri && a >= q)) {
       const Elem8 A = load_elem8(ctx, ea), B = load_elem8(ctx, eb);
-      const double rq = element_distance8(A, B) / fmax(A.h, B.h);
-      key = (rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3) + (J.onesided ? 4 : 0);
+      // most pairs are far (tier 0): the midpoint distance minus the two
+      // half-lengths bounds the segment distance from below, so a pair whose
+      // bound clears 8 h_max (with a 1e-9 relative margin for rounding) is
+      // tier 0 without the four point-segment distances
+      const double hmax = fmax(A.h, B.h);
+      const double cx = (A.px + 0.5 * A.dx) - (B.px + 0.5 * B.dx);
+      const double cy = (A.py + 0.5 * A.dy) - (B.py + 0.5 * B.dy);
+      const double thr = 8.0 * hmax * (1.0 + 1e-9) + 0.5 * (A.h + B.h) * (1.0 + 1e-9);
+      int tier = 0;
+      if (fma(cx, cx, cy * cy) < thr * thr) {
+        const double rq = element_distance8(A, B) / hmax;
+        tier = rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3;
+      }
+      key = tier + (J.onesided ? 4 : 0);
     }
     keys[p] = key;
     pair_job[p] = jb;  // read back by the scatter pass (no second search)
