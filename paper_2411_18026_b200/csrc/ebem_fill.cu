@@ -770,8 +770,13 @@ k_proxy_records(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ job
                 const int* __restrict__ job_block_off, int n_jobs,
                 const int* __restrict__ elems, long long n_slots, int tile,
                 double* __restrict__ recs) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= n_slots) return;
+  constexpr int kRecPad = kSymRec / 2 + 1;  // 144-byte rows, as in k_sym_scatter
+  __shared__ double2 s_rec[8 * 32 * kRecPad];
+  const long long t0 = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31);
+  const long long t = t0 + (threadIdx.x & 31);
+  const int lane = threadIdx.x & 31;
+  double2* const wrec = s_rec + (threadIdx.x >> 5) * (32 * kRecPad);
+  if (t < n_slots) {
   const int blk = int(t / tile);
   const int jb = find_job(job_block_off, n_jobs, blk);
   const ProxyJob J = jobs[jb];
@@ -812,9 +817,20 @@ k_proxy_records(const DevCtx* __restrict__ ctx, const ProxyJob* __restrict__ job
     r[SR_UD] = __longlong_as_double(J.u_off + (long long)q * m + pe);
     r[SR_HH] = hp * B.h;
   }
-  double2* o = reinterpret_cast<double2*>(recs + t * kSymRec);
 #pragma unroll
-  for (int k = 0; k < kSymRec / 2; ++k) o[k] = make_double2(r[2 * k], r[2 * k + 1]);
+  for (int k = 0; k < kSymRec / 2; ++k)
+    wrec[lane * kRecPad + k] = make_double2(r[2 * k], r[2 * k + 1]);
+  }
+  __syncwarp();
+  // the warp's records are consecutive: 512-byte store runs
+  if (t0 >= n_slots) return;
+  const int live = n_slots - t0 < 32 ? int(n_slots - t0) : 32;
+  double2* const o = reinterpret_cast<double2*>(recs + t0 * kSymRec);
+#pragma unroll
+  for (int c = lane; c < 32 * (kSymRec / 2); c += 32) {
+    const int rr = c / (kSymRec / 2);
+    if (rr < live) o[c] = wrec[rr * kRecPad + c - rr * (kSymRec / 2)];
+  }
 }
 
 // Same evaluation as the near-field kernel (thread (pair, i) fixes the
