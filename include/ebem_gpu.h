@@ -134,10 +134,14 @@ int ebem_gpu_cell_basis(ebem_gpu_problem* p, const int* rows0, int nr0,
 /* cell_basis for a batch of contiguous cells [begin_i, end_i) with
  * rows = cols = the cell's nodes, in one batched device pass (the level
  * path of the factorization; BASELINE config 5 microbenchmark).  Writes the
- * shared ranks; device_seconds (may be NULL) gets the CUDA-event time. */
+ * shared ranks; skel_out (may be NULL; capacity 4 * sum(end_i - begin_i))
+ * gets, cell after cell, the row skeletons of both components then the
+ * column skeletons, k_i entries each, in pivot order (CellBasis::
+ * row_skeleton / col_skeleton, compression.hpp:35-44); device_seconds (may
+ * be NULL) gets the CUDA-event time. */
 int ebem_gpu_cell_bases(ebem_gpu_problem* p, int count, const int* begins,
                         const int* ends, double epsilon, int* k_out,
-                        double* device_seconds);
+                        int* skel_out, double* device_seconds);
 
 /* The two interaction matrices cell_basis compresses
  * (proj/src/compression.cpp:139-166): mv (n_out x (nc0+nc1)) and
@@ -233,6 +237,17 @@ int ebem_gpu_fds_cell(const ebem_gpu_fds* f, int cell, int* sizes, int* skel);
 int ebem_gpu_eval_hankel(const double* x, int n, double* out);
 int ebem_gpu_eval_scalars(ebem_gpu_problem* p, const double* r, int n,
                           int which, double* out);
+/* Host-only table hooks (no device needed; CPU tests): the remainder
+ * expansion of the ten kernel scalars for a medium, out[10][max_pow][4] =
+ * (Re a_q, Im a_q, Re b_q, Im b_q) of sum_q (a_q + b_q ln r) r^q
+ * (KernelScalars::remainder below the series radius,
+ * proj/src/kernel_scalars.cpp:123-212, 381-409), *max_q the largest power;
+ * and the n-point Gauss-Legendre rule on [0, 1] (gauss_rule,
+ * proj/src/quadrature.cpp:16-56). */
+int ebem_gpu_series_table(double lambda, double mu, double rho, double omega,
+                          double* out, int max_pow, int* max_q);
+int ebem_gpu_gauss_rule(int n, double* x, double* w);
+
 /* Parity hook of the ID's TSQR stage (the reduction before Cpqr,
  * proj/src/lapack.cpp:101-119): reduces the rows x n complex block a
  * (column-major, ld) to *r_rows x n rows with the same Gram matrix

@@ -627,16 +627,25 @@ def build_proxy(curve: Curve, begin, end, radius_factor=1.5, m_prime=64):
 
 
 # ------------------------------------------------------------------- CPQR
-def cpqr(a):
+def cpqr(a, gaps=None):
     """Column-pivoted Householder QR with LAPACK zlaqp2 pivoting (zgeqp3 as
-    called by Cpqr, proj/src/lapack.cpp:101-119).  Returns (R, jpvt)."""
+    called by Cpqr, proj/src/lapack.cpp:101-119).  Returns (R, jpvt).
+    With a list `gaps`, appends per step the gap between the largest and
+    second-largest partial column norm among the candidates, divided by the
+    largest initial column norm |R_00| (1.0 when a single candidate is left):
+    the matrix entries carry rounding of order eps |R_00|, so a gap near that
+    level means the pivot is a tie that rounding decides."""
     A = np.array(a, dtype=complex, order="F")
     m, n = A.shape
     jp = np.arange(n)
     vn1 = np.linalg.norm(A, axis=0)
     vn2 = vn1.copy()
     tol3z = math.sqrt(2.0 ** -53)
+    r00 = float(vn1.max()) if n else 0.0
     for i in range(min(m, n)):
+        if gaps is not None:
+            c = np.sort(vn1[i:])[::-1]
+            gaps.append(1.0 if c.size < 2 or r00 == 0 else float((c[0] - c[1]) / r00))
         pvt = i + int(np.argmax(vn1[i:]))
         if pvt != i:
             A[:, [i, pvt]] = A[:, [pvt, i]]

@@ -551,16 +551,25 @@ class AssemblerSource(BlockSource):
             v=(_from_cbuf(bufs[2][: 2 * kk * c0.size], kk, c0.size),
                _from_cbuf(bufs[3][: 2 * kk * c1.size], kk, c1.size)))
 
-    def cell_bases(self, begins, ends, epsilon):
+    def cell_bases(self, begins, ends, epsilon, skeletons=False):
         """Batched cell_basis over contiguous cells (one device pass);
-        returns (ranks, device seconds)."""
+        returns (ranks, device seconds) or, with skeletons=True,
+        (ranks, device seconds, [(row0, row1, col0, col1) per cell])."""
         b = _ints(begins)
         e = _ints(ends)
         k = np.zeros(b.size, dtype=np.int32)
         t = ctypes.c_double()
+        sk = np.zeros(max(4 * int((e - b).sum()), 1), np.int32) if skeletons else None
         _check(lib().ebem_gpu_cell_bases(self._h.h, b.size, _p(b), _p(e),
-                                         ctypes.c_double(epsilon), _p(k), ctypes.byref(t)))
-        return k, float(t.value)
+                                         ctypes.c_double(epsilon), _p(k), _p(sk),
+                                         ctypes.byref(t)))
+        if not skeletons:
+            return k, float(t.value)
+        out, o = [], 0
+        for kk in k.tolist():
+            out.append(tuple(sk[o + q * kk: o + (q + 1) * kk].copy() for q in range(4)))
+            o += 4 * kk
+        return k, float(t.value), out
 
     def interaction_matrices(self, rows, cols, node_begin, node_end):
         """(M_V, M_U) of cell_basis (compression.cpp:139-166), for tests."""
@@ -841,15 +850,19 @@ def prof_enable(on: bool = True) -> None:
 
 
 def prof_read(reset: bool = False) -> dict:
-    """{kernel: (milliseconds, launches, work units)} since the last reset."""
+    """{kernel: (milliseconds, launches, work units, algorithmic HBM bytes)}
+    since the last reset."""
     L = lib()
     L.ebem_gpu_prof_name.restype = ctypes.c_char_p
     n = L.ebem_gpu_prof_kernels()
     ms = np.zeros(n)
     cnt = np.zeros(n, dtype=np.int64)
     units = np.zeros(n)
+    byts = np.zeros(n)
+    _check(L.ebem_gpu_prof_bytes(_p(byts), n))
     _check(L.ebem_gpu_prof_read(1 if reset else 0, _p(ms), _p(cnt), _p(units), n))
-    return {L.ebem_gpu_prof_name(i).decode(): (float(ms[i]), int(cnt[i]), float(units[i]))
+    return {L.ebem_gpu_prof_name(i).decode(): (float(ms[i]), int(cnt[i]), float(units[i]),
+                                                float(byts[i]))
             for i in range(n)}
 
 

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "ebem_kernels.h"
+#include "medium_setup.h"
 #include "runtime.h"
 
 using namespace ebem_gpu;
@@ -276,7 +277,7 @@ int ebem_gpu_cell_basis(ebem_gpu_problem* p, const int* rows0, int nr0,
 
 int ebem_gpu_cell_bases(ebem_gpu_problem* p, int count, const int* begins,
                         const int* ends, double epsilon, int* k_out,
-                        double* device_seconds) {
+                        int* skel_out, double* device_seconds) {
   return guarded([&] {
     Problem& P = *p->p;
     if (count < 0) throw Error(EBEM_INVALID_ARGUMENT, "negative cell count");
@@ -304,7 +305,31 @@ int ebem_gpu_cell_bases(ebem_gpu_problem* p, int count, const int* begins,
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (device_seconds) *device_seconds = 1e-3 * ms;
-    for (int c = 0; c < count; ++c) k_out[c] = res[c].k;
+    size_t o = 0;
+    for (int c = 0; c < count; ++c) {
+      k_out[c] = res[c].k;
+      if (!skel_out) continue;
+      for (const auto* l : {&res[c].srow[0], &res[c].srow[1], &res[c].scol[0],
+                            &res[c].scol[1]})
+        for (int v : *l) skel_out[o++] = v;
+    }
+  });
+}
+
+int ebem_gpu_series_table(double lambda, double mu, double rho, double omega,
+                          double* out, int max_pow, int* max_q) {
+  return guarded([&] {
+    if (max_pow < 1) throw Error(EBEM_INVALID_ARGUMENT, "table too short");
+    const DevMedium m = make_medium(lambda, mu, rho, omega, 0.0, 0.0);
+    const int q = build_series(m, out, max_pow);
+    if (max_q) *max_q = q;
+  });
+}
+
+int ebem_gpu_gauss_rule(int n, double* x, double* w) {
+  return guarded([&] {
+    if (n < 1 || n > 64) throw Error(EBEM_INVALID_ARGUMENT, "gauss_rule: order out of range");
+    gauss_rule(n, x, w);
   });
 }
 

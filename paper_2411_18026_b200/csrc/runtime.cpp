@@ -21,7 +21,7 @@
 #include <thread>
 
 #include "ebem_kernels.h"
-#include "host_setup.h"
+#include "medium_setup.h"
 
 namespace ebem_gpu {
 
@@ -101,12 +101,12 @@ void Profiler::begin(cudaStream_t st) {
   CK(cudaEventRecord(cur_, st));
 }
 
-void Profiler::end(int id, cudaStream_t st, double u) {
+void Profiler::end(int id, cudaStream_t st, double u, double by) {
   ++g_launches;
   if (!on || !cur_) return;
   cudaEvent_t b = ev();
   CK(cudaEventRecord(b, st));
-  pending_.push_back(Rec{id, cur_, b, u, -1});
+  pending_.push_back(Rec{id, cur_, b, u, -1, by});
   cur_ = nullptr;
 }
 
@@ -129,7 +129,7 @@ void Profiler::end_counted(int id, cudaStream_t st, const int* dev_bounds, doubl
   }
   const int slot = counts_used_++;
   CK(cudaMemcpyAsync(counts_ + 2 * slot, dev_bounds, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  pending_.push_back(Rec{id, cur_, b, mult, slot});
+  pending_.push_back(Rec{id, cur_, b, mult, slot, 0.0});
   cur_ = nullptr;
 }
 
@@ -146,6 +146,7 @@ void Profiler::collect() {
     ms[r.id] += t;
     count[r.id] += 1;
     units[r.id] += r.units;
+    bytes[r.id] += r.bytes;
     if (k > 0) {  // one stream: the span between two recorded kernels
       float g = 0.f;
       CK(cudaEventElapsedTime(&g, pending_[k - 1].b, r.a));
@@ -169,7 +170,8 @@ void Profiler::collect() {
 
 void Profiler::reset() {
   collect();
-  for (int i = 0; i < KP_COUNT; ++i) ms[i] = 0.0, count[i] = 0, units[i] = 0.0, gap_ms[i] = 0.0;
+  for (int i = 0; i < KP_COUNT; ++i)
+    ms[i] = 0.0, count[i] = 0, units[i] = 0.0, bytes[i] = 0.0, gap_ms[i] = 0.0;
 }
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -1520,10 +1522,12 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     for (const QrTask& t : tasks)
       if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
     double fl = 0.0;  // complex Householder QR: 8 m n^2 - 8 n^3 / 3
+    double by = 0.0;  // the block read once, its reduced rows written once
     for (const auto* v : {&tasks, &stream16, &stream8, &stream4})
       for (const QrTask& t : *v) {
         const double mm = t.rows, nn = std::min(t.rows, t.n);
         fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
+        by += 16.0 * (mm + nn) * t.n;
       }
     g_prof.begin(st);
     // (the team-layout k_qr_team measured slower on these shapes: 485 vs 404 ms)
@@ -1531,7 +1535,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     launch_tsqr(Pack::at<QrTask>(tb, o16), int(stream16.size()), 0, smem16, st);
     launch_tsqr(Pack::at<QrTask>(tb, o8), int(stream8.size()), 1, smem8, st);
     launch_tsqr(Pack::at<QrTask>(tb, o4), int(stream4.size()), 2, smem4, st);
-    g_prof.end(KP_QR, st, fl);
+    g_prof.end(KP_QR, st, fl, by);
     CK(cudaGetLastError());
     staging.fence(st);
     for (size_t i = 0; i < q.size(); ++i) {
@@ -1626,13 +1630,15 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     const size_t o = pk.add(ct);
     char* tb = staging.put(pk, st_);
     double fl = 0.0;  // full-rank bound of the pivoted QR flops
+    double by = 0.0;  // the (reduced) block read once, R written once
     for (const CpqrTask& t : ct) {
       const double mm = t.rows, nn = std::min(t.rows, t.n);
       fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
+      by += 16.0 * (mm + nn) * t.n;
     }
     g_prof.begin(st_);
     launch_cpqr_team(Pack::at<CpqrTask>(tb, o), int(nq), smem, gws.get(), st_);
-    g_prof.end(KP_CPQR, st_, fl);
+    g_prof.end(KP_CPQR, st_, fl, by);
     CK(cudaGetLastError());
     staging.fence(st_);
   }
@@ -1817,6 +1823,17 @@ int g_getrs_maxn = 0;
 int g_getrs_cpw = 1;
 int g_gemm_narrow = 0;  // GEMV template of the current k_gemm launch (0: tiled)
 
+// Algorithmic HBM bytes of one batched-LA task: operands read once, the
+// result written once (complex double = 16 B).
+double task_bytes(const CopyTask& c) { return 32.0 * c.rows * c.cols; }
+double task_bytes(const GemmTask& g) {
+  const bool acc = g.beta_re != 0.0 || g.beta_im != 0.0;
+  return 16.0 * (double(g.m) * g.k + double(g.k) * g.n + (acc ? 2.0 : 1.0) * g.m * g.n);
+}
+double task_bytes(const LuSolveTask& s) {
+  return 16.0 * (double(s.n) * s.n + 2.0 * double(s.n) * s.nrhs);
+}
+
 template <class T, class F, class U>
 void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
                  void (*launch)(const T*, const int*, int, int, cudaStream_t),
@@ -1839,12 +1856,12 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
   const size_t o1 = pk.add(t);
   const size_t o2 = pk.add(boff);
   char* tb = P.staging.put(pk, P.stream());
-  double units = 0.0;
-  for (const T& x : t) units += units_of(x);
+  double units = 0.0, bytes = 0.0;
+  for (const T& x : t) units += units_of(x), bytes += task_bytes(x);
   g_prof.begin(P.stream());
   launch(Pack::at<T>(tb, o1), Pack::at<int>(tb, o2), int(t.size()), total,
          P.stream());
-  g_prof.end(id, P.stream(), units);
+  g_prof.end(id, P.stream(), units, bytes);
   P.staging.fence(P.stream());
   CK(cudaGetLastError());
 

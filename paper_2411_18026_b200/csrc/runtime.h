@@ -48,7 +48,9 @@ class Profiler {
  public:
   bool on = false;
   void begin(cudaStream_t st);
-  void end(int id, cudaStream_t st, double units);
+  // bytes: algorithmic HBM bytes of the launch (operands read once, results
+  // written once), for the HBM roofline of the ID / solve kernels
+  void end(int id, cudaStream_t st, double units, double bytes = 0.0);
   // units = mult x (dev_bounds[1] - dev_bounds[0]), read back at collect()
   void end_counted(int id, cudaStream_t st, const int* dev_bounds, double mult);
   void collect();
@@ -56,10 +58,11 @@ class Profiler {
   double ms[KP_COUNT] = {};
   long long count[KP_COUNT] = {};
   double units[KP_COUNT] = {};
+  double bytes[KP_COUNT] = {};
   double gap_ms[KP_COUNT] = {};  // device idle right before each kernel kind
 
  private:
-  struct Rec { int id; cudaEvent_t a, b; double units; int slot; };
+  struct Rec { int id; cudaEvent_t a, b; double units; int slot; double bytes; };
   int* counts_ = nullptr;  // pinned (first, last) pairs of end_counted
   int counts_used_ = 0, counts_cap_ = 0;
   std::vector<Rec> pending_;

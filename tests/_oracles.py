@@ -3,8 +3,8 @@
 * ``RefLib``   : oracle/_ref/libebem_ref.so, the reference library compiled in
                  place from /root/reference/proj/src (see oracle/Makefile and
                  oracle/ref_capi.cpp for the file:line of every entry point).
-* ``OracleLib``: oracle/_ref/libebem_oracle.so, the from-scratch CPU
-                 restatement (oracle/restate/ebem_oracle.cpp).
+(The from-scratch CPU restatement is the numpy module oracle/ebem_oracle.py,
+imported directly.)
 
 Only tests/, bench.py's CPU legs and __graft_entry__.smoke() import this.
 """
@@ -18,7 +18,6 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parents[1]
 REF_SO = ROOT / "oracle" / "_ref" / "libebem_ref.so"
-ORACLE_SO = ROOT / "oracle" / "_ref" / "libebem_oracle.so"
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int

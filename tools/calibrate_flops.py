@@ -19,6 +19,6 @@ med = eb.Medium.from_lame(1.0, 1.0, 1.0, 1.0)
 mesh = eb.Mesh.star(N, eb.StarShape(1.0, 0.0, 3))
 src = eb.AssemblerSource(eb.BlockAssembler(mesh, med, med.default_coupling()))
 fds = eb.FdsSolver(src, eb.ClusterTree(N, eb.ClusterTree.depth_for(N, 32)), eb.FdsConfig(1e-10, 1))
-for k, (ms, c, u) in eb.prof_read().items():
+for k, (ms, c, u, _b) in eb.prof_read().items():
     if c:
         print(f"POINTS {k} {u:.0f} launches {c}")

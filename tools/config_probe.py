@@ -49,6 +49,6 @@ print(f"config {which}: N={n} factorize {tf:.3f}s (device {st.factorize_device_s
       f"per-RHS {(tm2.device_seconds - t1) / max(len(angles) - 1, 1) * 1e3:.3f} ms, "
       f"first-RHS {st.factorize_device_seconds + t1:.3f}s", flush=True)
 print("batch vs single", np.linalg.norm(X[:, 0] - x1) / np.linalg.norm(x1))
-for k, (ms, c, u) in sorted(eb.prof_read(reset=True).items(), key=lambda kv: -kv[1][0]):
+for k, (ms, c, u, _b) in sorted(eb.prof_read(reset=True).items(), key=lambda kv: -kv[1][0]):
     if c:
         print(f"   {k:18s} {ms:9.2f} ms  {c:5d} launches")

@@ -28,6 +28,6 @@ for N in ns:
     print(f"N={N} factorize {tf:.3f}s ({2*N/tf:.3e} unknowns/s) basis {st.basis_cpu_seconds:.3f}s "
           f"top {st.top_factor_seconds:.3f}s solve {ts*1e3:.2f} ms ranks {st.max_rank} top_dim {st.top_dim}",
           flush=True)
-    for k, (ms, c, u) in sorted(eb.prof_read(reset=True).items(), key=lambda kv: -kv[1][0]):
+    for k, (ms, c, u, _b) in sorted(eb.prof_read(reset=True).items(), key=lambda kv: -kv[1][0]):
         if c:
             print(f"   {k:18s} {ms:9.2f} ms  {c:5d} launches  units {u:.3e}  rate {u/ms*1e3 if ms else 0:.3e}/s")
