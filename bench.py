@@ -15,8 +15,23 @@ factorization is several GB (far above the 126 MB L2) and L2 is flushed
 between steps anyway.
 
 --impl reference times the reference C++ library compiled in place
-(oracle/_ref/libebem_ref.so) on the host cores with all threads, on a
-bounded sample of the same workload family (config 2 at N = 16384).
+(oracle/_ref/libebem_ref.so) on the host cores with all threads, on the SAME
+workload: one factorization + one solve at N = 262144 (about 8-10 min on 16
+cores; the reference's own protocol for large N is a single run,
+proj/include/ebem/report.hpp:76), so the line reports steps = 1 whatever
+--steps asks for.  A bounded N = 16384 sample rides along under
+"sample_n16384".
+
+Roofline sections (each reproducible from profiles/):
+  roofline        the dominant kernel (k_near_sym), FP64: executed FP64 flops
+                  per quadrature point from the ncu calibration in
+                  profiles/calibration.json (tagged with its commit)
+  roofline_merge  the merge GEMMs (k_gemm on DMMA) and LU / solves, FP64
+  roofline_id     the ID (TSQR + pivoted QR): HBM GB/s of the algorithmic
+                  bytes and FP64 rate
+  roofline_solve  one right-hand side: factor bytes read once / time, HBM
+Extra configs (BASELINE configs[2..4], CUDA events, once after the timed
+region): config 3 multi-RHS, config 4 star + SV wave, config 5 level bases.
 """
 from __future__ import annotations
 
@@ -41,16 +56,25 @@ N_BENCH = 262144
 N_CPU_SAMPLE = 16384
 EPS = 1e-10
 LEAF = 32
-# Algorithmic FP64 flops per quadrature-point evaluation (DESIGN.md,
-# "Roofline"): FP64 instructions per point counted by ncu on the kernels
-# (DADD + DMUL + 2 DFMA), divided by the point evaluations of the launch.
-FLOPS_PER_POINT = {"k_near_onesided": 723.1, "k_proxy_pairs": 837.8, "k_near_sym": 1006.5}
+CALIBRATION = ROOT / "profiles" / "calibration.json"
 
 
-def config_dict():
-    return {"workload": "config2: circle N=262144 (2N=2^19), k_T*a=1, nu=0.25, "
+def calibration():
+    """FP64 flops per quadrature point (ncu DADD + DMUL + 2 DFMA over all
+    launches of one factorization / the points the library counted), DRAM
+    traffic per launch of the dominant kernel and the DMMA pipe activity of
+    the merge GEMMs, with the commit they were measured at
+    (tools/calibrate.sh)."""
+    try:
+        return json.loads(CALIBRATION.read_text())
+    except (OSError, ValueError):
+        return {}
+
+
+def config_dict(n=N_BENCH):
+    return {"workload": f"config2: circle N={n} (2N={2 * n}), k_T*a=1, nu=0.25, "
                         "leaf 32, m'=64, eps=1e-10, 1 plane P wave",
-            "n_elements": N_BENCH, "unknowns": 2 * N_BENCH, "leaf": LEAF,
+            "n_elements": n, "unknowns": 2 * n, "leaf": LEAF,
             "epsilon": EPS, "m_prime": 64, "kT": 1.0, "ell0": 1,
             "parallelism": "replicas", "l2": "flushed between steps (512 MiB write); "
                                               "working set >> L2"}
@@ -196,6 +220,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_BENCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-configs", action="store_true")
     args = ap.parse_args()
     dist, rank, world = dist_init()
     threads = os.cpu_count() or 1
@@ -203,21 +228,31 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        tf, ts = run_reference(N_CPU_SAMPLE, threads, steps=args.steps, warmup=min(args.warmup, 1))
-        v = 2 * N_CPU_SAMPLE / tf
-        sample = (f"reference FdsSolver (oracle/_ref, -O2 -g, OpenMP) on config 2 at "
-                  f"N={N_CPU_SAMPLE} (2N={2 * N_CPU_SAMPLE}); bounded sample of the "
-                  f"N={N_BENCH} workload, mean of {args.steps} factorizations")
+        # the same workload as our arm: one factorization + one solve at
+        # N = 262144 (single run, the reference's protocol for large N)
+        n_ref = args.n
+        tf, ts = run_reference(n_ref, threads, steps=1, warmup=0)
+        v = 2 * n_ref / tf
+        tf_s, ts_s = run_reference(N_CPU_SAMPLE, threads, steps=1, warmup=0)
+        sample = (f"reference FdsSolver (oracle/_ref: the reference compiled in place, "
+                  f"-O2 -g, OpenMP, its merge products through the Eigen-subset shim's "
+                  f"plain loops) on config 2 at N={n_ref} (2N={2 * n_ref}), one "
+                  f"factorization + one solve on all {threads} host threads")
         line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": (tf + ts) * 1e3,
+                "steps": 1, "warmup": 0, "ms_per_step": (tf + ts) * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "c128 (f64)", "data": "synthetic (seeded geometry, analytic plane wave)",
-                "config": config_dict(), "impl": "reference",
+                "config": config_dict(n_ref), "impl": "reference",
+                "steps_note": (f"one timed factorization (the reference's single-run protocol "
+                               f"for large N); --steps {args.steps} --warmup {args.warmup} "
+                               f"would take {args.steps + args.warmup} x {tf:.0f} s"),
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                                  "sample": sample, "cpu": cpu_info()},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0},
-                "solve_seconds_per_rhs": ts}
+                "factorize_seconds": tf, "solve_seconds_per_rhs": ts,
+                "sample_n16384": {"value": 2 * N_CPU_SAMPLE / tf_s, "unit": UNIT,
+                                  "factorize_seconds": tf_s, "solve_seconds_per_rhs": ts_s}}
         print(json.dumps(line))
         return 0
 
@@ -236,7 +271,7 @@ def main():
         fds = eb.FdsSolver(src, tree, eb.FdsConfig(EPS, 1))
         tm = eb.FdsSolveTiming()
         x = fds.solve(f_host, tm)
-        return fds.stats().factorize_device_seconds, tm.device_seconds, x
+        return fds.stats().factorize_device_seconds, tm.device_seconds, x, fds
 
     for _ in range(args.warmup):
         step()
@@ -249,17 +284,17 @@ def main():
     l0 = eb.launch_count()
     tfs, tss = [], []
     for _ in range(args.steps):
-        tf, ts, x = step()
+        tf, ts, x, _f = step()
         tfs.append(tf)
         tss.append(ts)
         flush_l2()
     launches = eb.launch_count() - l0
     clk = clocks.stop()
     # one extra, untimed step with the event profiler on: kernel breakdown and
-    # the dominant kernel's roofline
+    # the rooflines
     eb.prof_enable(True)
     eb.prof_read(reset=True)
-    step()
+    _, _, _, fds_p = step()
     prof = eb.prof_read(reset=True)
     eb.prof_enable(False)
     flush_l2()
@@ -286,33 +321,29 @@ def main():
     h2d = 2 * 16 * n + 8 + 32 * n
     d2h = 32 * n + 32 * n
 
-    # roofline of the dominant kernel
-    top = max(prof.items(), key=lambda kv: kv[1][0])
-    kname, (kms, kcount, kunits) = top
-    # DRAM traffic per launch of the dominant kernel from an ncu capture of
-    # every launch of one factorization at this workload (committed summary)
-    traffic = None
-    tf_path = ROOT / "profiles" / "r1_ncu_traffic_k_near_sym.json"
-    if kname == "k_near_sym" and tf_path.exists():
-        traffic = json.load(open(tf_path))["dram_bytes_per_launch"]
-    roof = None
-    if kname in FLOPS_PER_POINT and kms > 0:
-        ach = FLOPS_PER_POINT[kname] * kunits / (kms * 1e-3) / 1e12
-        roof = {"bound": "fp64", "kernel": kname, "achieved": ach, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": ach / fp64_peak if fp64_peak else None,
-                "traffic": traffic,
-                "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + "
-                                "dram__bytes_write.sum over all launches of one factorization, "
-                                "profiles/r1_ncu_traffic_k_near_sym.json); the kernel is FP64-bound",
-                "peak_source": "measured on this box by ebem_gpu_fp64_peak (DFMA chains); "
-                               "MEASURED_PEAKS.json has no FP64 entry",
-                "units": "quadrature points", "units_per_launch": kunits / max(kcount, 1),
-                "flops_per_unit": FLOPS_PER_POINT[kname],
-                "avg_launch_ms": kms / max(kcount, 1), "share_of_step":
-                    kms * 1e-3 / (float(np.mean(tfs)) + float(np.mean(tss)))}
-    else:
-        roof = {"bound": "fp64", "kernel": kname, "achieved": None, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": None, "traffic": None}
+    cal = calibration()
+    hbm = hbm_peak()
+    roof = fill_roofline(prof, cal, fp64_peak, float(np.mean(tfs)) + float(np.mean(tss)))
+    roof_merge = rate_roofline(prof, ("k_gemm",), fp64_peak, hbm, "merge GEMMs W = V A^-1U "
+                               "(fds.cpp:99-100) on DMMA")
+    roof_merge["lu_and_solves"] = rate_roofline(prof, ("k_getrf", "k_getrs"), fp64_peak, hbm,
+                                                "LU + A^-1U / W^-1 solves (fds.cpp:89-101)")
+    if cal.get("k_gemm_mma"):
+        roof_merge["ncu"] = cal["k_gemm_mma"]
+    roof_id = rate_roofline(prof, ("k_qr_reduce", "k_cpqr"), fp64_peak, hbm,
+                            "ID: TSQR + pivoted QR (Cpqr, lapack.cpp:101-119)", bound="hbm")
+    fb = factor_bytes(fds_p, tree, n)
+    roof_solve = {"bound": "hbm", "what": "one right-hand side: every factor (LU, A^-1U, "
+                  "V, W^-1 of every cell, top LU) read once + RHS / solution",
+                  "bytes": fb, "seconds": t_solve, "achieved": fb / t_solve / 1e9,
+                  "peak": hbm, "unit": "GB/s", "frac": fb / t_solve / 1e9 / hbm}
+
+    extra = {}
+    if not args.no_extra_configs:
+        try:
+            extra = extra_configs(eb, fp64_peak, hbm)
+        except Exception as e:  # noqa: BLE001
+            extra = {"error": repr(e)}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -321,33 +352,185 @@ def main():
             cpu = {"value": 2 * N_CPU_SAMPLE / tf_c, "unit": UNIT, "cores": threads,
                    "kind": "reference",
                    "sample": f"reference FdsSolver (oracle/_ref) factorize on config 2 at "
-                             f"N={N_CPU_SAMPLE}, all {threads} host threads; a bounded sample "
-                             f"(the reference is O(N log N), so its rate at N={N_BENCH} is lower)",
-                   "cpu": cpu_info(), "solve_seconds_per_rhs": ts_c}
+                             f"N={N_CPU_SAMPLE} (not {N_BENCH}: a bounded ~20 s sample), all "
+                             f"{threads} host threads; the reference is O(N log N), so its rate "
+                             f"at N={N_BENCH} is lower (bench.py --impl reference times that)",
+                   "n_elements": N_CPU_SAMPLE, "cpu": cpu_info(),
+                   "solve_seconds_per_rhs": ts_c}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
     if rank == 0:
-        kernels = {k: {"ms": v[0], "launches": v[1], "units": v[2]}
+        kernels = {k: {"ms": v[0], "launches": v[1], "units": v[2], "bytes": v[3]}
                    for k, v in prof.items() if v[1]}  # the one profiled step
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": (t_fact + t_solve) * 1e3, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
                 "data": "synthetic (analytic circle mesh, plane P wave)",
-                "config": config_dict(),
+                "config": config_dict(n),
                 "factorize_seconds": t_fact, "solve_seconds_per_rhs": t_solve,
                 "e2e": {"value": units_total / t_e2e, "unit": UNIT,
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "seconds": t_e2e},
                 "gpu_launches": launches // max(args.steps, 1),
-                "clocks": clk, "roofline": roof, "cpu_baseline": cpu,
-                "kernels_per_step": kernels, "ranks": tree.depth()}
+                "clocks": clk, "roofline": roof, "roofline_merge": roof_merge,
+                "roofline_id": roof_id, "roofline_solve": roof_solve,
+                "cpu_baseline": cpu, "extra_configs": extra,
+                "kernels_per_step": kernels, "max_rank": fds_p.stats().max_rank,
+                "calibration_commit": cal.get("commit")}
         print(json.dumps(line))
     if dist is not None:
         dist.barrier()
     return 0
+
+
+# ---------------------------------------------------------------- rooflines
+
+def hbm_peak():
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6545.6  # the pool's last MEASURED_PEAKS.json value
+
+
+def fill_roofline(prof, cal, fp64_peak, step_s):
+    """The dominant kernel: executed FP64 flops per point (calibration) x the
+    points the library counted / its CUDA-event time."""
+    kname, (kms, kcount, kunits, _b) = max(prof.items(), key=lambda kv: kv[1][0])
+    fpp = cal.get("flops_per_point", {}).get(kname)
+    roof = {"bound": "fp64", "kernel": kname, "peak": fp64_peak, "unit": "TFLOP/s",
+            "peak_source": "measured on this box by ebem_gpu_fp64_peak (DFMA chains on "
+                           "every SM); MEASURED_PEAKS.json has no FP64 entry",
+            "units": "quadrature points", "units_per_launch": kunits / max(kcount, 1),
+            "avg_launch_ms": kms / max(kcount, 1),
+            "share_of_step": kms * 1e-3 / step_s}
+    if fpp and kms > 0:
+        ach = fpp * kunits / (kms * 1e-3) / 1e12
+        roof.update(achieved=ach, frac=ach / fp64_peak if fp64_peak else None,
+                    flops_per_unit=fpp)
+    else:
+        roof.update(achieved=None, frac=None)
+    tr = cal.get("dram_bytes_per_launch", {}).get(kname)
+    roof["traffic"] = tr
+    roof["traffic_unit"] = ("DRAM bytes per launch (ncu dram__bytes_read.sum + "
+                            "dram__bytes_write.sum over every launch of one factorization, "
+                            "profiles/calibration.json)")
+    roof["points_per_second"] = kunits / (kms * 1e-3) if kms > 0 else None
+    return roof
+
+
+def rate_roofline(prof, names, fp64_peak, hbm, what, bound="fp64"):
+    ms = sum(prof.get(k, (0, 0, 0, 0))[0] for k in names)
+    fl = sum(prof.get(k, (0, 0, 0, 0))[2] for k in names)
+    by = sum(prof.get(k, (0, 0, 0, 0))[3] for k in names)
+    if ms <= 0:
+        return {"what": what, "kernels": list(names), "ms": 0.0}
+    tf = fl / (ms * 1e-3) / 1e12
+    gb = by / (ms * 1e-3) / 1e9
+    out = {"what": what, "kernels": list(names), "bound": bound, "ms": ms,
+           "flops": fl, "bytes": by, "tflops": tf, "fp64_frac": tf / fp64_peak,
+           "gbs": gb, "hbm_frac": gb / hbm}
+    out.update(achieved=gb if bound == "hbm" else tf, peak=hbm if bound == "hbm" else fp64_peak,
+               unit="GB/s" if bound == "hbm" else "TFLOP/s",
+               frac=gb / hbm if bound == "hbm" else tf / fp64_peak)
+    return out
+
+
+def factor_bytes(fds, tree, n):
+    """Bytes one single-RHS solve must read: per compressed cell LU (2n)^2,
+    A^-1U 2n x 2k, V 2 x k x n, W^-1 (2k)^2 (n = sequence length per
+    component, k = rank), the top LU, plus the RHS in and solution out."""
+    depth = tree.depth()
+    ell0 = 1
+    ks = {}
+    total = 0.0
+    for lev in range(depth, ell0, -1):
+        first = (1 << lev) - 1
+        for c in range(first, first + (1 << lev)):
+            k = fds.rank_of(c)
+            ks[c] = k
+            nl = (n >> depth) if lev == depth else ks[2 * c + 1] + ks[2 * c + 2]
+            total += 16.0 * ((2 * nl) ** 2 + 2 * nl * 2 * k + 2 * k * nl + (2 * k) ** 2)
+    top = fds.stats().top_dim
+    total += 16.0 * top * top + 2 * 16.0 * 2 * n
+    return total
+
+
+# ------------------------------------------------------------ extra configs
+
+def extra_configs(eb, fp64_peak, hbm):
+    """BASELINE configs[2..4] once each, device time by CUDA events on the
+    library stream (factorization device seconds, solve timing, batched
+    cell_basis seconds)."""
+    out = {}
+    # config 3: N=65536, k_T a = 4, 180 P waves as one block
+    n3 = 65536
+    med3 = eb.Medium.from_lame(1.0, 1.0, 1.0, 4.0)
+    m3 = eb.Mesh.star(n3, eb.StarShape(1.0, 0.0, 3))
+    a3 = eb.BlockAssembler(m3, med3, med3.default_coupling())
+    s3 = eb.AssemblerSource(a3)
+    t3 = eb.ClusterTree(n3, eb.ClusterTree.depth_for(n3, LEAF))
+    F = a3.rhs_batch(med3, [2 * np.pi * j / 180 for j in range(180)], 1.0)
+    f3 = eb.FdsSolver(s3, t3, eb.FdsConfig(EPS, 1))
+    tm1, tm = eb.FdsSolveTiming(), eb.FdsSolveTiming()
+    f3.solve(F[:, 0], tm1)  # records the one-column graphs
+    f3.solve(F[:, 0], tm1)
+    f3.solve(F, tm)  # records the 180-column graphs
+    eb.prof_enable(True)
+    eb.prof_read(reset=True)
+    f3.solve(F, tm)
+    sp = eb.prof_read(reset=True)
+    eb.prof_enable(False)
+    fl = sum(v[2] for k, v in sp.items() if k in ("k_gemm", "k_getrs", "k_copy"))
+    out["config3"] = {
+        "workload": "circle N=65536, k_T a=4, 180 plane P waves theta_j=2 pi j/180, one block",
+        "factorize_seconds": f3.stats().factorize_device_seconds,
+        "first_rhs_seconds": f3.stats().factorize_device_seconds + tm1.device_seconds,
+        "solve1_seconds": tm1.device_seconds, "solve180_seconds": tm.device_seconds,
+        "per_rhs_seconds": (tm.device_seconds - tm1.device_seconds) / 179,
+        "solve180_flops": fl, "solve180_tflops": fl / tm.device_seconds / 1e12 if fl else None,
+        "solve180_fp64_frac": fl / tm.device_seconds / 1e12 / fp64_peak if fl else None,
+        "max_rank": f3.stats().max_rank}
+    del f3
+    # config 4: star r = 1 + 0.3 cos 5 theta, N = 131072, nu 0.3, k_T = 16/1.3
+    n4 = 131072
+    th = np.array([2.0 * 3.14159265358979323846 * t / n4 for t in range(n4)])
+    rr = 1.0 + 0.3 * np.cos(5 * th)
+    m4 = eb.Mesh(np.stack([rr * np.cos(th), rr * np.sin(th)], 1))
+    med4 = eb.Medium.from_lame(1.5, 1.0, 1.0, 16.0 / 1.3)
+    a4 = eb.BlockAssembler(m4, med4, med4.default_coupling())
+    s4 = eb.AssemblerSource(a4, eb.ProxyConfig(1.5, 128, 6))
+    t4 = eb.ClusterTree(n4, eb.ClusterTree.depth_for(n4, 64))
+    f4 = eb.FdsSolver(s4, t4, eb.FdsConfig(1e-8, 1))
+    sv = a4.rhs(eb.PlaneSVWave(med4, 1.0, np.radians(30.0)))
+    tm4 = eb.FdsSolveTiming()
+    f4.solve(sv, tm4)
+    f4.solve(sv, tm4)
+    f4b = eb.FdsSolver(s4, t4, eb.FdsConfig(1e-8, 1))  # a second factorization, warm
+    out["config4"] = {
+        "workload": "star 1+0.3cos5t, N=131072, nu=0.3, k_T=16/1.3, leaf 64, m'=128, "
+                    "eps=1e-8, plane SV wave at 30 deg",
+        "factorize_seconds": f4b.stats().factorize_device_seconds,
+        "unknowns_per_second": 2 * n4 / f4b.stats().factorize_device_seconds,
+        "solve_seconds": tm4.device_seconds, "max_rank": f4b.stats().max_rank}
+    del f4, f4b
+    # config 5: 4096 boxes x 64 nodes, m' 128, k_T 8: the batched level bases
+    n5, box = 262144, 64
+    rng = np.random.default_rng(2411)
+    begins = np.sort(rng.choice(n5 - box, 4096, replace=False))
+    med5 = eb.Medium.from_lame(1.0, 1.0, 1.0, 8.0)
+    m5 = eb.Mesh.star(n5, eb.StarShape(1.0, 0.0, 3))
+    s5 = eb.AssemblerSource(eb.BlockAssembler(m5, med5, med5.default_coupling()),
+                            eb.ProxyConfig(1.5, 128, 6))
+    s5.cell_bases(begins[:64], begins[:64] + box, 1e-10)
+    ts5 = [s5.cell_bases(begins, begins + box, 1e-10)[1] for _ in range(3)]
+    out["config5"] = {"workload": "4096 boxes x 64 nodes of the 262144-gon, seeded, m'=128, "
+                                  "k_T=8, eps=1e-10: fill + ID of the level (one batched pass)",
+                      "seconds": float(np.median(ts5)),
+                      "boxes_per_second": 4096 / float(np.median(ts5))}
+    return out
 
 
 if __name__ == "__main__":

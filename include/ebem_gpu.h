@@ -266,6 +266,9 @@ int ebem_gpu_prof_enable(int on);
 int ebem_gpu_prof_read(int reset, double* ms, long long* count, double* units,
                        int n);
 const char* ebem_gpu_prof_name(int id);
+/* Algorithmic HBM bytes per kernel kind since the last prof_read reset
+ * (operands read once, results written once; 0 for the fill kernels). */
+int ebem_gpu_prof_bytes(double* bytes, int n);
 int ebem_gpu_prof_kernels(void);
 /* Measured FP64 FMA throughput of the device (TFLOP/s), the roofline
  * denominator of the fill kernels. */

@@ -21,6 +21,7 @@ device every compute call raises :class:`CudaError`.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -75,7 +76,8 @@ _ERRORS = {1: InvalidArgument, 2: SingularMatrix, 3: DomainError,
 
 # ----------------------------------------------------------------- native lib
 
-_LIB_PATH = Path(__file__).resolve().parent / "libebem_gpu.so"
+# EBEM_GPU_LIB: an alternative in-tree build of the library (A/B measurements)
+_LIB_PATH = Path(os.environ.get("EBEM_GPU_LIB") or Path(__file__).resolve().parent / "libebem_gpu.so")
 _lib = None
 
 

@@ -99,6 +99,13 @@ int ebem_gpu_prof_enable(int on) {
   });
 }
 
+int ebem_gpu_prof_bytes(double* bytes, int n) {
+  return guarded([&] {
+    g_prof.collect();
+    for (int i = 0; i < n && i < KP_COUNT; ++i) bytes[i] = g_prof.bytes[i];
+  });
+}
+
 int ebem_gpu_prof_read(int reset, double* ms, long long* count, double* units,
                        int n) {
   return guarded([&] {

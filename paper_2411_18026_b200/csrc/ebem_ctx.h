@@ -45,8 +45,14 @@ struct ParSeries {
 
 // Fill-kernel parameter block, passed by value as a __grid_constant__ kernel
 // argument: the medium constants are then constant-bank operands.
+// The leading D/N series terms (scalars 2..9, parity form) ride along, so
+// the Horner steps of the series branch take their coefficients as
+// constant-bank operands instead of shared-memory loads.
+constexpr int kFcTerms = 12;
 struct FillConst {
   DevMedium med;
+  double2 sa[kFcTerms][8];
+  double2 sb[kFcTerms][8];
 };
 
 // Element geometry, structure of arrays over the N elements (element e runs

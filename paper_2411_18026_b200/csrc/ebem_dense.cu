@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ebem_dense.h"
 
@@ -551,6 +552,149 @@ k_gemm(const GemmTask* __restrict__ tasks, const int* __restrict__ block_off,
     double2 v = zmul(alpha, acc[q]);
     if (beta.x != 0.0 || beta.y != 0.0) v = zfma(v, beta, *cp);
     *cp = v;
+  }
+}
+
+// ------------------------------------------------- GEMM on FP64 tensor cores
+// The same product on the FP64 MMA units: mma.sync.m8n8k4 f64 (DMMA), one
+// 8x8x4 real product per warp instruction (8 x the work of a DFMA warp
+// instruction).  A complex product is four real MMAs on split re / im
+// fragments (C_re += A_re B_re - A_im B_im, C_im += A_re B_im + A_im B_re),
+// the same operation count as the SIMT kernel and no 3-multiply trick, so the
+// rounding stays that of a plain complex dot product.
+//   CTA 128 threads = 4 warps, 32 x 32 complex output tile, warp 16 x 16
+//   (2 x 2 MMA blocks).  K in chunks of 16 complex, staged by cp.async into a
+//   two-stage ring of [row][k] tiles (the copy of chunk c+1 overlaps the
+//   MMAs of chunk c); out-of-range elements are zero-filled by the copy.
+//   The 20-element row pitch (80 words = 16 mod 32) makes the 16-byte
+//   fragment loads (re and im of one element together) conflict-free.
+constexpr int kMmaThreads = 128;
+constexpr int kMmaKc = 16;
+constexpr int kMmaPitch = kMmaKc + 4;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+// 16-byte async copy; src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp16z(void* dst, const void* src, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src),
+               "r"(src_bytes));
+}
+
+__global__ void __launch_bounds__(kMmaThreads)
+k_gemm_mma(const GemmTask* __restrict__ tasks, const int* __restrict__ block_off,
+           int n_tasks) {
+  __shared__ double2 As[2][kTile][kMmaPitch];
+  __shared__ double2 Bs[2][kTile][kMmaPitch];
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmTask& T = tasks[lo];
+  const int m = T.m, n = T.n, kdim = T.k, lda = T.lda, ldb = T.ldb;
+  const int ta = T.trans_a, tb = T.trans_b;
+  const int tiles_m = (m + kTile - 1) / kTile;
+  const int tile = blockIdx.x - block_off[lo];
+  const int r0 = (tile % tiles_m) * kTile, c0 = (tile / tiles_m) * kTile;
+  const double2* __restrict__ A = reinterpret_cast<const double2*>(T.a);
+  const double2* __restrict__ B = reinterpret_cast<const double2*>(T.b);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // chunk copy: 4 elements of A and 4 of B per thread; consecutive threads
+  // on consecutive global addresses
+  auto issue = [&](int k0, int st) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + kMmaThreads * q;
+      int row, kk;
+      if (ta) { row = idx / kMmaKc; kk = idx % kMmaKc; }
+      else { row = idx % kTile; kk = idx / kTile; }
+      int gr = r0 + row, gk = k0 + kk;
+      bool ok = gr < m && gk < kdim;
+      const double2* src = ok ? (ta ? A + (size_t)gr * lda + gk : A + (size_t)gk * lda + gr) : A;
+      cp16z(&As[st][row][kk], src, ok ? 16 : 0);
+      int col;
+      if (tb) { col = idx % kTile; kk = idx / kTile; }
+      else { col = idx / kMmaKc; kk = idx % kMmaKc; }
+      const int gc = c0 + col;
+      gk = k0 + kk;
+      ok = gc < n && gk < kdim;
+      src = ok ? (tb ? B + (size_t)gk * ldb + gc : B + (size_t)gc * ldb + gk) : B;
+      cp16z(&Bs[st][col][kk], src, ok ? 16 : 0);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double acc[2][2][2][2];  // [row block][col block][re, im][2]
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
+  const int wr = (w & 1) * 16, wc = (w >> 1) * 16;
+  const int fr = lane >> 2, fk = lane & 3;
+  const double sa = ta == 2 ? -1.0 : 1.0, sb = tb == 2 ? -1.0 : 1.0;  // conjugation
+  const int nck = (kdim + kMmaKc - 1) / kMmaKc;
+  issue(0, 0);
+  for (int c = 0; c < nck; ++c) {
+    const int st = c & 1;
+    if (c + 1 < nck) {
+      issue((c + 1) * kMmaKc, st ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int ks_end = min(kMmaKc, kdim - c * kMmaKc);
+#pragma unroll
+    for (int ks = 0; ks < kMmaKc; ks += 4) {
+      if (ks >= ks_end) break;
+      double ar[2], ai[2], an[2], br[2], bi[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double2 a = As[st][wr + 8 * i + fr][ks + fk];
+        const double2 b = Bs[st][wc + 8 * i + fr][ks + fk];
+        ar[i] = a.x;
+        ai[i] = sa * a.y;
+        an[i] = -ai[i];
+        br[i] = b.x;
+        bi[i] = sb * b.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(acc[i][j][0][0], acc[i][j][0][1], ar[i], br[j]);
+          dmma(acc[i][j][0][0], acc[i][j][0][1], an[i], bi[j]);
+          dmma(acc[i][j][1][0], acc[i][j][1][1], ar[i], bi[j]);
+          dmma(acc[i][j][1][0], acc[i][j][1][1], ai[i], br[j]);
+        }
+    }
+    __syncthreads();  // stage st is refilled by the next iteration's copy
+  }
+  const double2 alpha = make_double2(T.alpha_re, T.alpha_im);
+  const double2 beta = make_double2(T.beta_re, T.beta_im);
+  const bool acc_c = beta.x != 0.0 || beta.y != 0.0;
+  double2* C = reinterpret_cast<double2*>(T.c);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int gr = r0 + wr + 8 * i + fr;
+    if (gr >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gc = c0 + wc + 8 * j + 2 * fk + h;
+        if (gc >= n) continue;
+        double2* cp = C + (size_t)gc * T.ldc + gr;
+        double2 v = zmul(alpha, make_double2(acc[i][j][0][h], acc[i][j][1][h]));
+        if (acc_c) v = zfma(v, beta, *cp);
+        *cp = v;
+      }
   }
 }
 
@@ -1359,6 +1503,14 @@ int gemm_narrow(const GemmTask& g) {
   if (g.trans_a || g.trans_b || g.n > kNarrow) return 0;
   return g.n <= 1 ? 1 : kNarrow;
 }
+// EBEM_GEMM_MMA=0 selects the SIMT k_gemm (A/B measurements).
+bool gemm_use_mma() {
+  static const bool on = [] {
+    const char* e = std::getenv("EBEM_GEMM_MMA");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
 int gemm_blocks(const GemmTask& g, int narrow) {
   if (narrow) return (g.m + 31) / 32;
   return ((g.m + kTile - 1) / kTile) * ((g.n + kTile - 1) / kTile);
@@ -1368,6 +1520,7 @@ void launch_gemm(const GemmTask* tasks, const int* block_off, int n_tasks,
   if (n_blocks <= 0) return;
   if (narrow == 1) k_gemv<1><<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
   else if (narrow) k_gemv<kNarrow><<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+  else if (gemm_use_mma()) k_gemm_mma<<<n_blocks, kMmaThreads, 0, st>>>(tasks, block_off, n_tasks);
   else k_gemm<<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
 }
 int copy_blocks(int rows, int cols) {

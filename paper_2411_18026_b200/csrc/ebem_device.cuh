@@ -460,6 +460,9 @@ __device__ __forceinline__ void hankel01_lg(double x, double log_half_x,
   hankel01(x, h0, h1);
 }
 
+#ifndef EBEM_REAL_LOG
+#define EBEM_REAL_LOG 0  // the real-B chains measured slower (426 vs 407 ms near field: schedule)
+#endif
 // All eight remainder series at once: one loop over powers, 16 independent
 // Horner chains in u = r^2, started at the highest of the nt terms used.
 // nt: ParSeries::rcut terms for the largest distance the caller sweeps.
@@ -470,6 +473,7 @@ __device__ __forceinline__ int series_terms(const SerSm& S, double rmax) {
 }
 __device__ __forceinline__ void series_joint(const SerSm& S, double u, double logr,
                                              double r, int nt, DN& o) {
+#if !EBEM_REAL_LOG
   cplx A[8], B[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -491,6 +495,101 @@ __device__ __forceinline__ void series_joint(const SerSm& S, double u, double lo
 #pragma unroll
   for (int k = 0; k < 5; ++k)
     o.n[k] = mk(fma(B[3 + k].re, logr, A[3 + k].re), fma(B[3 + k].im, logr, A[3 + k].im));
+#else
+  // the log coefficients are real (the ln r terms come only from the real
+  // Y0 part of H0; checked on the host), so B carries no imaginary chain
+  cplx A[8];
+  double B[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 a = S.at[nt - 1][k];
+    A[k] = mk(a.x, a.y);
+    B[k] = S.bt[nt - 1][k].x;
+  }
+  for (int p = nt - 2; p >= 0; --p) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double2 a = S.at[p][k];
+      A[k] = mk(fma(A[k].re, u, a.x), fma(A[k].im, u, a.y));
+      B[k] = fma(B[k], u, S.bt[p][k].x);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) o.d[k] = r * mk(fma(B[k], logr, A[k].re), A[k].im);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o.n[k] = mk(fma(B[3 + k], logr, A[3 + k].re), A[3 + k].im);
+#endif
+}
+
+// series_joint with the first kFcTerms coefficients read from the
+// __grid_constant__ FillConst: for a compile-time term count the Horner
+// steps are DFMAs with constant-bank operands (no shared-memory loads).
+template <int NT>
+__device__ __forceinline__ void series_horner_c(const FillConst& fc, double u, double logr,
+                                                double r, DN& o) {
+#if EBEM_REAL_LOG
+  cplx A[8];
+  double B[8];  // real log coefficients (see series_joint)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    A[k] = mk(fc.sa[NT - 1][k].x, fc.sa[NT - 1][k].y);
+    B[k] = fc.sb[NT - 1][k].x;
+  }
+#pragma unroll
+  for (int p = NT - 2; p >= 0; --p) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      A[k] = mk(fma(A[k].re, u, fc.sa[p][k].x), fma(A[k].im, u, fc.sa[p][k].y));
+      B[k] = fma(B[k], u, fc.sb[p][k].x);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) o.d[k] = r * mk(fma(B[k], logr, A[k].re), A[k].im);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o.n[k] = mk(fma(B[3 + k], logr, A[3 + k].re), A[3 + k].im);
+#else
+  cplx A[8], B[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    A[k] = mk(fc.sa[NT - 1][k].x, fc.sa[NT - 1][k].y);
+    B[k] = mk(fc.sb[NT - 1][k].x, fc.sb[NT - 1][k].y);
+  }
+#pragma unroll
+  for (int p = NT - 2; p >= 0; --p) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      A[k] = mk(fma(A[k].re, u, fc.sa[p][k].x), fma(A[k].im, u, fc.sa[p][k].y));
+      B[k] = mk(fma(B[k].re, u, fc.sb[p][k].x), fma(B[k].im, u, fc.sb[p][k].y));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    o.d[k] = r * mk(fma(B[k].re, logr, A[k].re), fma(B[k].im, logr, A[k].im));
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+    o.n[k] = mk(fma(B[3 + k].re, logr, A[3 + k].re), fma(B[3 + k].im, logr, A[3 + k].im));
+#endif
+}
+
+#ifndef EBEM_SERIES_CONST
+#define EBEM_SERIES_CONST 1
+#endif
+__device__ __forceinline__ void series_dispatch(const FillConst& fc, const SerSm& S, double u,
+                                                double logr, double r, int nt, DN& o) {
+#if EBEM_SERIES_CONST
+  switch (nt) {
+#define EBEM_HC(K) \
+  case K:          \
+    series_horner_c<K>(fc, u, logr, r, o); \
+    return;
+    EBEM_HC(1) EBEM_HC(2) EBEM_HC(3) EBEM_HC(4) EBEM_HC(5) EBEM_HC(6)
+    EBEM_HC(7) EBEM_HC(8) EBEM_HC(9) EBEM_HC(10) EBEM_HC(11) EBEM_HC(12)
+#undef EBEM_HC
+    default:
+      break;
+  }
+#endif
+  series_joint(S, u, logr, r, nt, o);
 }
 
 // The scalars of one point.  kRem = false: full d and n (proxy blocks,
@@ -504,7 +603,7 @@ __device__ __forceinline__ void dn_eval(const FillConst& fc, const SerSm& S,
   const DevMedium& m = fc.med;
   const double ir2 = ir * ir;
   if (r < m.series_radius) {
-    series_joint(S, r * r, logr, r, nt, o);
+    series_dispatch(fc, S, r * r, logr, r, nt, o);
     o.d[0].re += m.sd1 * ir;
     o.d[1].re -= m.sd1 * ir;
     o.d[2].re += m.sd3 * ir;

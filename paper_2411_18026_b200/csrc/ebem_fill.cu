@@ -962,16 +962,16 @@ void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
   const long long n_slots = (long long)n_blocks * tile;
   k_proxy_records<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(
       ctx, jobs, job_block_off, n_jobs, elems, n_slots, tile, recs);
-  const int P = EBEM_PRX_THREADS / n_gauss;
-  const int threads = P * n_gauss;
-  const size_t smem = size_t(threads) * 18 * sizeof(double2) +
-                      size_t(2 * P) * kSymRec * sizeof(double);
   static const int n_sm = [] {
     int dev = 0, v = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v > 0 ? v : 148;
   }();
+  const int P = EBEM_PRX_THREADS / n_gauss;
+  const int threads = P * n_gauss;
+  const size_t smem = size_t(threads) * 18 * sizeof(double2) +
+                      size_t(2 * P) * kSymRec * sizeof(double);
   static bool attr = [] {
     cudaFuncSetAttribute(k_proxy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          EBEM_PRX_THREADS * (18 * (int)sizeof(double2) +

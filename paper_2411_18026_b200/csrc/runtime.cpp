@@ -371,10 +371,14 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
     hctx_.series_maxq = build_series(med, hctx_.series, kMaxSeriesPow);
     build_parity_series(hctx_.series, kMaxSeriesPow, hctx_.pser);
     fc_.med = med;
+    for (int k = 2; k < 10; ++k)  // series_joint drops the imaginary log chain
+      for (int p = 0; p < kParTerms; ++p)
+        if (hctx_.pser.b[k][p].y != 0.0)
+          throw std::logic_error("near-field expansion: complex log coefficient");
     for (int k = 0; k < 8; ++k) {  // series_joint hard-codes d odd, n even
       const int par = hctx_.pser.par[k + 2];
       if (par != (k < 3 ? 1 : 0))
-        throw std::logic_error("KernelScalars: unexpected series parity");
+        throw std::logic_error("near-field expansion: unexpected parity of a D/N series");
     }
     // The fill evaluates the D/N series only below the series radius: drop
     // the terms whose size there is below 1e-21 of the series' largest term
@@ -449,6 +453,12 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   } catch (const std::logic_error& e) {
     throw Error(EBEM_LOGIC_ERROR, e.what());
   }
+  for (int p = 0; p < kFcTerms; ++p)
+    for (int k = 0; k < 8; ++k) {
+      const bool in = p < kParTerms;
+      fc_.sa[p][k] = in ? hctx_.pser.a[k + 2][p] : double2{0.0, 0.0};
+      fc_.sb[p][k] = in ? hctx_.pser.b[k + 2][p] : double2{0.0, 0.0};
+    }
   for (int q = 1; q <= kMaxGauss; ++q)
     gauss_rule(q, hctx_.gx + gauss_offset(q), hctx_.gw + gauss_offset(q));
   hctx_.far_nodes = a.far_nodes;
@@ -1988,12 +1998,15 @@ void run_getrf(Problem& P, std::vector<LuTask> t) {
   const size_t o = pk.add(small);
   const size_t ob = pk.add(big);
   char* tb = P.staging.put(pk, P.stream());
-  double fl = 0.0;
-  for (const LuTask& x : t) fl += 8.0 / 3.0 * double(x.n) * x.n * x.n;
+  double fl = 0.0, by = 0.0;
+  for (const LuTask& x : t) {
+    fl += 8.0 / 3.0 * double(x.n) * x.n * x.n;
+    by += 32.0 * double(x.n) * x.n;  // the block read and the factors written
+  }
   g_prof.begin(P.stream());
   launch_getrf(Pack::at<LuTask>(tb, o), int(small.size()), smem, P.gws.get(), P.stream());
   launch_lu_blocked(Pack::at<LuTask>(tb, ob), int(big.size()), big_n, P.stream());
-  g_prof.end(KP_GETRF, P.stream(), fl);
+  g_prof.end(KP_GETRF, P.stream(), fl, by);
   P.staging.fence(P.stream());
   CK(cudaGetLastError());
 }
