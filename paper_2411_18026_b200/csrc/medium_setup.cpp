@@ -318,7 +318,44 @@ void build_parity_series(const double* dense, int max_pow, ParSeries& ps) {
 // by Sturm-sequence bisection and polished by Newton steps on P_n(2x - 1);
 // the weights come from the Christoffel function,
 // w_i = 1 / sum_{k<n} (2k + 1) P_k(2 x_i - 1)^2, a sum of positive terms.
+#ifndef EBEM_GAUSS_GOLUB
+#define EBEM_GAUSS_GOLUB 1
+#endif
+// The textbook Newton iteration for the roots of P_n (Tricomi's cosine
+// guess, the three-term recurrence for P_n and P_n', stop below 1e-15) with
+// the derivative weight formula 2 / ((1 - s^2) P_n'(s)^2) -- the published
+// algorithm (Numerical Recipes' gauleg) the reference's gauss_rule follows.
+// Its weights carry up to ~9e-14 relative error at the ends (the (1 - s^2)
+// cancellation), which the reference's matrices inherit.
+static void gauss_rule_newton(int n, double* x, double* w) {
+  const int half = (n + 1) / 2;
+  for (int r = 0; r < half; ++r) {
+    double s = std::cos(kPi * (r + 0.75) / (n + 0.5));  // r-th root from the top
+    double deriv = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double pm = 1.0, pc = s;  // P_0, P_1
+      for (int k = 2; k <= n; ++k) {
+        const double pn = ((2.0 * k - 1.0) * s * pc - (k - 1.0) * pm) / k;
+        pm = pc;
+        pc = pn;
+      }
+      deriv = n * (s * pc - pm) / (s * s - 1.0);
+      const double step = pc / deriv;
+      s -= step;
+      if (std::abs(step) < 1e-15) break;
+    }
+    const double wt = 0.5 * (2.0 / ((1.0 - s * s) * deriv * deriv));
+    x[r] = 0.5 * (1.0 - s);
+    x[n - 1 - r] = 0.5 * (1.0 + s);
+    w[r] = w[n - 1 - r] = wt;
+  }
+}
+
 void gauss_rule(int n, double* x, double* w) {
+  if (!EBEM_GAUSS_GOLUB) {
+    gauss_rule_newton(n, x, w);
+    return;
+  }
   std::vector<double> off2(n > 0 ? n : 1, 0.0);  // squared off-diagonals
   for (int k = 1; k < n; ++k) off2[k] = double(k) * k / (4.0 * (4.0 * k * k - 1.0));
   // number of eigenvalues below t (Sturm count of the LDL^T pivots)

@@ -49,10 +49,12 @@ def check_solution(meta, fx, x):
     cols = fx.get("x_sample_cols", np.arange(x.shape[1]))
     assert rel(x[::s][:, cols], fx["x_sample"]) < TOL
     np.testing.assert_allclose(np.linalg.norm(x, axis=0), fx["x_norm"], rtol=TOL)
+    # g^H (x - x_ref) for complex Gaussian g (E|g_i|^2 = 2) estimates
+    # sqrt(2) ||x - x_ref|| over ALL 2N entries
     P = probes(2 * meta["n"], meta["n_probes"], meta["probe_seed"])
     got = P.conj().T @ x
-    scale = np.linalg.norm(P, axis=0)[:, None] * fx["x_norm"][None, :]
-    assert np.max(np.abs(got - fx["x_probe"]) / scale) < TOL
+    est = np.abs(got - fx["x_probe"]) / (np.sqrt(2.0) * fx["x_norm"][None, :])
+    assert np.median(est) < TOL
 
 
 # north_star: "skeleton index sets identical except where pivot norms tie to
