@@ -342,8 +342,6 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
       sym_vals_(scratch().sym_vals),
       sym_recs_(scratch().sym_recs),
       sym_bounds_(scratch().sym_bounds),
-      sym_bounds_host_(scratch().sym_bounds_host),
-      sym_ev_(scratch().sym_ev),
       bundles(scratch().bundles),
       gws(scratch().gws),
       n_(n),
@@ -527,8 +525,6 @@ Problem::Problem(int n)
       sym_vals_(scratch().sym_vals),
       sym_recs_(scratch().sym_recs),
       sym_bounds_(scratch().sym_bounds),
-      sym_bounds_host_(scratch().sym_bounds_host),
-      sym_ev_(scratch().sym_ev),
       bundles(scratch().bundles),
       gws(scratch().gws),
       n_(n) {
@@ -1267,8 +1263,8 @@ void Problem::execute(FillPlan& plan) {
       bundles.ensure(std::max(need, size_t(kMaxBundlesPerWave) * kBundle * 2 * 5 / 4));
   }
   const int* el = Pack::at<int>(base, o_el);
-  // symmetric near pairs: bucket by tier (count + scatter, async), read the class
-  // bounds through an event so the host waits only for these small kernels
+  // symmetric near pairs: bucket by tier (count + scatter, async); the class
+  // bounds stay on the device, the near-field launches read them there
   const long long nsym = plan.sym_pairs_;
   // pair records: the bucketed near pairs, then the proxy slots
   const long long proxy_slots =
@@ -1281,11 +1277,7 @@ void Problem::execute(FillPlan& plan) {
     so = Pack::at<long long>(base, o_so);
     sym_keys_.ensure(size_t(nsym));
     sym_vals_.ensure(size_t(nsym));  // job of each pair
-    if (!sym_bounds_host_) {
-      CK(cudaMallocHost(reinterpret_cast<void**>(&sym_bounds_host_), 16 * sizeof(int)));
-      CK(cudaEventCreateWithFlags(&sym_ev_, cudaEventDisableTiming));
-      sym_bounds_.alloc(size_t(sym_bounds_ints()));
-    }
+    if (!sym_bounds_.get()) sym_bounds_.alloc(size_t(sym_bounds_ints()));
     sym_recs_.ensure(size_t(kSymRec) * (nsym + proxy_slots));
     launch_sym_bucket(dctx(), sj, so, int(plan.sym_.size()), el, nsym, sym_keys_.get(),
                       sym_vals_.get(), sym_bounds_.get(), sym_recs_.get(), st_);
@@ -2684,16 +2676,7 @@ void Fds::record_solve(int m) {
   }
 }
 
-Fds::~Fds() {
-  if (plan_) {
-    for (int ph = 0; ph < 3; ++ph) {
-      if (plan_->exec[ph]) cudaGraphExecDestroy(plan_->exec[ph]);
-      if (plan_->graph[ph]) cudaGraphDestroy(plan_->graph[ph]);
-    }
-    for (auto& e : plan_->ev)
-      if (e) cudaEventDestroy(e);
-  }
-}
+Fds::~Fds() = default;  // SolvePlan releases its graphs
 
 void Fds::solve_device(const double* rhs, int m, double* x,
                        ebem_fds_solve_timing* timing) {

@@ -307,8 +307,6 @@ struct Scratch {
   DBuf<int> sym_vals;
   DBuf<double> sym_recs;  // kSymRec doubles per sorted near pair
   DBuf<int> sym_bounds;
-  int* sym_bounds_host = nullptr;
-  cudaEvent_t sym_ev = nullptr;
   DBuf<double> bundles;
   DBuf<double2> gws;
   PinnedBuf<int> h_jp, h_steps;  // pivoted-QR readbacks
@@ -382,8 +380,6 @@ class Problem {
   DBuf<int>& sym_vals_;             // 2 x pairs (in, out)
   DBuf<double>& sym_recs_;          // sorted pair records (geometry, outputs)
   DBuf<int>& sym_bounds_;
-  int*& sym_bounds_host_;  // pinned
-  cudaEvent_t& sym_ev_;
   DBuf<double>& bundles;
   DBuf<double2>& gws;
   DBuf<int> bad;
@@ -532,6 +528,17 @@ class Fds {
     cudaGraph_t graph[3] = {nullptr, nullptr, nullptr};  // up, top, down
     cudaGraphExec_t exec[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    SolvePlan() = default;
+    SolvePlan(const SolvePlan&) = delete;
+    SolvePlan& operator=(const SolvePlan&) = delete;
+    ~SolvePlan() {  // a re-recorded plan releases its graphs and events
+      for (int ph = 0; ph < 3; ++ph) {
+        if (exec[ph]) cudaGraphExecDestroy(exec[ph]);
+        if (graph[ph]) cudaGraphDestroy(graph[ph]);
+      }
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+    }
   };
   std::unique_ptr<SolvePlan> plan_;
 
