@@ -1523,12 +1523,14 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     size_t smem = 0;
     for (const QrTask& t : tasks)
       if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
-    double fl = 0.0;  // complex Householder QR: 8 m n^2 - 8 n^3 / 3
+    double fl = 0.0;
     double by = 0.0;  // the block read once, its reduced rows written once
     for (const auto* v : {&tasks, &stream16, &stream8, &stream4})
       for (const QrTask& t : *v) {
         const double mm = t.rows, nn = std::min(t.rows, t.n);
-        fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
+        // complex Householder QR with k = min(m, n) reflectors:
+        // 16 m n k - 8 (m + n) k^2 + 16 k^3 / 3 real flops (8 m n^2 - 8 n^3 / 3 at k = n)
+        fl += 16.0 * mm * t.n * nn - 8.0 * (mm + t.n) * nn * nn + 16.0 / 3.0 * nn * nn * nn;
         by += 16.0 * (mm + nn) * t.n;
       }
     g_prof.begin(st);
@@ -1635,7 +1637,8 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     double by = 0.0;  // the (reduced) block read once, R written once
     for (const CpqrTask& t : ct) {
       const double mm = t.rows, nn = std::min(t.rows, t.n);
-      fl += 8.0 * mm * t.n * nn - 4.0 * (mm + t.n) * nn * nn + 8.0 / 3.0 * nn * nn * nn;
+      // full-rank bound of the pivoted QR: 16 m n k - 8 (m + n) k^2 + 16 k^3 / 3
+      fl += 16.0 * mm * t.n * nn - 8.0 * (mm + t.n) * nn * nn + 16.0 / 3.0 * nn * nn * nn;
       by += 16.0 * (mm + nn) * t.n;
     }
     g_prof.begin(st_);

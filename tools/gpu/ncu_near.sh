@@ -1,0 +1,2 @@
+ncu --set full --import-source on --clock-control none -k regex:k_near_sym -s 40 -c 1 -o gpurun_out/near_sym_r2 python tools/repeat_probe.py 262144 1 > gpurun_out/ncu_near.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:k_qr_reduce -s 2 -c 1 -o gpurun_out/tsqr_r2 python tools/repeat_probe.py 262144 1 > gpurun_out/ncu_tsqr.log 2>&1
