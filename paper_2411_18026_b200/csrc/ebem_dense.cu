@@ -751,23 +751,90 @@ k_gemv(const GemmTask* __restrict__ tasks, const int* __restrict__ block_off, in
   }
 }
 
-// --------------------------------------------------------------------- copy
+// Warp-per-tile variant (the default): CTA = 8 independent warps, warp =
+// one 32-row tile of one task running over all of K (no K split, no
+// shared-memory sum, no CTA barrier), 8 columns of A in flight per lane;
+// the right-hand-side entries are read 32 at a time by the lanes and
+// broadcast by shuffles.  8x fewer CTAs than k_gemv for the same tiles:
+// the solve's per-cell products are a few KB each, so per-CTA overhead, not
+// HBM, bounded k_gemv.
+template <int NR>
 __global__ void __launch_bounds__(kThreads)
-k_copy(const CopyTask* __restrict__ tasks, const int* __restrict__ block_off,
-       int n_tasks) {
+k_gemv_w(const GemmTask* __restrict__ tasks, const int* __restrict__ tile_off, int n_tasks,
+         int n_tiles) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int tile = blockIdx.x * kWarps + w;
+  if (tile >= n_tiles) return;
   int lo = 0, hi = n_tasks - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (block_off[mid] <= (int)blockIdx.x) lo = mid;
+    if (__ldg(tile_off + mid) <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmTask& T = tasks[lo];
+  const int m = T.m, kdim = T.k, ncol = T.n;
+  const size_t lda = T.lda, ldb = T.ldb;
+  const int r = (tile - __ldg(tile_off + lo)) * 32 + l;
+  const bool live = r < m;
+  const double2* __restrict__ A = reinterpret_cast<const double2*>(T.a) + (live ? r : 0);
+  const double2* __restrict__ B = reinterpret_cast<const double2*>(T.b);
+  double2 acc[NR];
+#pragma unroll
+  for (int c = 0; c < NR; ++c) acc[c] = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < kdim; k0 += 32) {
+    const int kk = min(32, kdim - k0);
+    double2 xb[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c)
+      xb[c] = (c < ncol && l < kk) ? __ldg(B + (size_t)c * ldb + k0 + l) : make_double2(0.0, 0.0);
+#pragma unroll 8
+    for (int j = 0; j < kk; ++j) {
+      const double2 a = live ? __ldg(A + (size_t)(k0 + j) * lda) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < NR; ++c) {
+        const double2 x = make_double2(__shfl_sync(0xffffffffu, xb[c].x, j),
+                                       __shfl_sync(0xffffffffu, xb[c].y, j));
+        acc[c] = zfma(acc[c], a, x);
+      }
+    }
+  }
+  if (!live) return;
+  const double2 alpha = make_double2(T.alpha_re, T.alpha_im);
+  const double2 beta = make_double2(T.beta_re, T.beta_im);
+  double2* C = reinterpret_cast<double2*>(T.c);
+#pragma unroll
+  for (int c = 0; c < NR; ++c) {
+    if (c >= ncol) break;
+    double2* cp = C + (size_t)c * T.ldc + r;
+    double2 v = zmul(alpha, acc[c]);
+    if (beta.x != 0.0 || beta.y != 0.0) v = zfma(v, beta, *cp);
+    *cp = v;
+  }
+}
+
+// --------------------------------------------------------------------- copy
+constexpr int kCopyUnit = 128;  // elements per warp
+__global__ void __launch_bounds__(kThreads)
+k_copy(const CopyTask* __restrict__ tasks, const int* __restrict__ unit_off,
+       int n_tasks, int n_units) {
+  // one warp per unit of kCopyUnit elements (most solve copies are a few
+  // dozen elements: a CTA per task would idle 7 of its 8 warps)
+  const int unit = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (unit >= n_units) return;
+  const int l = threadIdx.x & 31;
+  int lo = 0, hi = n_tasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(unit_off + mid) <= unit) lo = mid;
     else hi = mid - 1;
   }
   const CopyTask T = tasks[lo];
-  const long long base = (long long)(blockIdx.x - block_off[lo]) * kThreads * 4;
+  const long long base = (long long)(unit - __ldg(unit_off + lo)) * kCopyUnit;
   const double2* S = reinterpret_cast<const double2*>(T.src);
   double2* D = reinterpret_cast<double2*>(T.dst);
   const long long total = (long long)T.rows * T.cols;
-  for (int q = 0; q < 4; ++q) {
-    const long long idx = base + q * kThreads + threadIdx.x;
+  for (int q = 0; q < kCopyUnit / 32; ++q) {
+    const long long idx = base + q * 32 + l;
     if (idx >= total) break;
     const int j = int(idx / T.rows), i = int(idx - (long long)j * T.rows);
     double2 v = T.src ? S[(size_t)j * T.src_ld + i] : make_double2(0.0, 0.0);
@@ -1518,19 +1585,36 @@ int gemm_blocks(const GemmTask& g, int narrow) {
 void launch_gemm(const GemmTask* tasks, const int* block_off, int n_tasks,
                  int n_blocks, cudaStream_t st, int narrow) {
   if (n_blocks <= 0) return;
-  if (narrow == 1) k_gemv<1><<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+  static const bool warp_gemv = [] {  // EBEM_GEMV_WARP=0: the K-split k_gemv (A/B)
+    const char* e = std::getenv("EBEM_GEMV_WARP");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  // few tiles (the upper levels): the K-split kernel keeps more loads in
+  // flight per tile than one warp running down K
+  static const int warp_min = [] {
+    const char* e = std::getenv("EBEM_GEMV_WARP_MIN");
+    return e ? std::atoi(e) : 4096;
+  }();
+  const int wgrid = (n_blocks + kWarps - 1) / kWarps;
+  if (narrow && warp_gemv && n_blocks >= warp_min) {
+    if (narrow == 1)
+      k_gemv_w<1><<<wgrid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
+    else
+      k_gemv_w<kNarrow><<<wgrid, kThreads, 0, st>>>(tasks, block_off, n_tasks, n_blocks);
+  } else if (narrow == 1) k_gemv<1><<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
   else if (narrow) k_gemv<kNarrow><<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
   else if (gemm_use_mma()) k_gemm_mma<<<n_blocks, kMmaThreads, 0, st>>>(tasks, block_off, n_tasks);
   else k_gemm<<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
 }
-int copy_blocks(int rows, int cols) {
+int copy_blocks(int rows, int cols) {  // warp units
   const long long t = (long long)rows * cols;
-  return int((t + kThreads * 4 - 1) / (kThreads * 4));
+  return int((t + kCopyUnit - 1) / kCopyUnit);
 }
 void launch_copy(const CopyTask* tasks, const int* block_off, int n_tasks,
                  int n_blocks, cudaStream_t st) {
   if (n_blocks <= 0) return;
-  k_copy<<<n_blocks, kThreads, 0, st>>>(tasks, block_off, n_tasks);
+  k_copy<<<(n_blocks + kWarps - 1) / kWarps, kThreads, 0, st>>>(tasks, block_off, n_tasks,
+                                                                 n_blocks);
 }
 
 }  // namespace ebem_gpu

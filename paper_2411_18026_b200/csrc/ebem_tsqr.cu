@@ -152,8 +152,13 @@ __device__ __forceinline__ void make_reflector(double2 (&B)[kRpt], bool mine, in
 // phase: a warp that skipped reflector t - D (no column right of it) may get
 // here before t - D was even produced, and a parity test would then mistake
 // phase t/D - 2 for t/D.
+#ifndef EBEM_TSQR_SLEEP
+#define EBEM_TSQR_SLEEP 20
+#endif
 __device__ __forceinline__ void wait_seq(const volatile int* seq, int slot, int t) {
-  while (seq[slot] != t) __nanosleep(20);
+  while (seq[slot] != t) {
+    if (EBEM_TSQR_SLEEP > 0) __nanosleep(EBEM_TSQR_SLEEP);
+  }
   __threadfence_block();
 }
 
