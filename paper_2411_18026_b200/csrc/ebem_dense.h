@@ -83,6 +83,8 @@ void launch_qr_reduce(const QrTask* tasks, int n, size_t smem, double2* gws,
                       cudaStream_t st);
 void launch_cpqr(const CpqrTask* tasks, int n, size_t smem, double2* gws,
                  cudaStream_t st);
+// blocks of at most 32 x 32: one warp per matrix (k_cpqr_warp)
+void launch_cpqr_warp(const CpqrTask* tasks, int n, cudaStream_t st);
 // Team-layout Householder kernels (ebem_qr.cu), same task descriptors.
 void launch_qr_team(const QrTask* tasks, int n, size_t smem, double2* gws,
                     cudaStream_t st);

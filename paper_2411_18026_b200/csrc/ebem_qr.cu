@@ -323,6 +323,170 @@ void launch_qr_team(const QrTask* tasks, int n, size_t smem, double2* gws,
   k_qr_team<<<n, kTeamThreads, smem, st>>>(tasks, gws);
 }
 
+// Warp-per-matrix pivoted QR for blocks of at most 32 x 32 (the leaf
+// level's reduced ID inputs): lane j holds column j in registers, so a step
+// needs no barrier -- the pivot is a shuffle argmax, the column swap and the
+// reflector broadcast are shuffles, and every lane updates its own column.
+// Same zlaqp2 decisions and zlarfg arithmetic as cpqr_team_body (the sums
+// run in row order here, so partial norms may differ in the last bit).
+constexpr int kCpqrWarps = 4;  // matrices per CTA
+__global__ void __launch_bounds__(kCpqrWarps * 32)
+k_cpqr_warp(const CpqrTask* __restrict__ tasks, int n_tasks) {
+  const int task = blockIdx.x * kCpqrWarps + (threadIdx.x >> 5);
+  if (task >= n_tasks) return;
+  const int l = threadIdx.x & 31;
+  const CpqrTask T = tasks[task];
+  const int m = T.rows, n = T.n;
+  const bool own = l < n;
+  const double2* src = reinterpret_cast<const double2*>(T.src) + (size_t)l * T.ld;
+  double2 c[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) c[r] = (own && r < m) ? src[r] : make_double2(0.0, 0.0);
+  double vn1 = 0.0;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) vn1 = fma(c[r].x, c[r].x, fma(c[r].y, c[r].y, vn1));
+  vn1 = own ? sqrt(vn1) : -1.0;
+  double vn2 = vn1;
+  int jp = l;
+  const double tol3z = 1.0536712127723509e-08;  // sqrt(2^-53)
+  const int mn = m < n ? m : n;
+  int steps = mn;
+  double r00 = 0.0;
+  for (int i = 0; i < mn; ++i) {
+    // pivot: first index of the largest partial norm among columns >= i
+    double best = l >= i ? vn1 : -2.0;
+    int bi = l;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const int pvt = bi;
+    if (pvt != i) {  // swap columns i and pvt; vn of pvt takes i's (zlaqp2)
+      const int from = l == i ? pvt : (l == pvt ? i : l);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        c[r].x = __shfl_sync(0xffffffffu, c[r].x, from);
+        c[r].y = __shfl_sync(0xffffffffu, c[r].y, from);
+      }
+      jp = __shfl_sync(0xffffffffu, jp, from);
+      const double a1 = __shfl_sync(0xffffffffu, vn1, i);
+      const double a2 = __shfl_sync(0xffffffffu, vn2, i);
+      if (l == pvt) { vn1 = a1; vn2 = a2; }
+    }
+    // reflector of column i (zlarfg, the arithmetic of team_reflector)
+    double2 tau = make_double2(0.0, 0.0);
+    double beta = 0.0;
+    if (l == i) {
+      double xn2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (r > i && r < m) xn2 = fma(c[r].x, c[r].x, fma(c[r].y, c[r].y, xn2));
+      double2 alpha = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (r == i) alpha = c[r];
+      if (xn2 == 0.0 && alpha.y == 0.0) {
+        beta = alpha.x;
+      } else {
+        const double x2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, xn2));
+        const double sr = rsqrt(x2);
+        const bool pos = alpha.x >= 0.0;
+        beta = pos ? -(x2 * sr) : x2 * sr;
+        const double ib = pos ? -sr : sr;
+        tau = make_double2((beta - alpha.x) * ib, -alpha.y * ib);
+        const double arn = fma(alpha.x, sr, pos ? 1.0 : -1.0);
+        const double ain = alpha.y * sr;
+        const double id = sr / fma(arn, arn, ain * ain);
+        const double2 scal = make_double2(arn * id, -ain * id);
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+          if (r > i && r < m) c[r] = zmul(scal, c[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (r == i) c[r] = make_double2(beta, 0.0);
+    }
+    beta = __shfl_sync(0xffffffffu, beta, i);
+    tau.x = __shfl_sync(0xffffffffu, tau.x, i);
+    tau.y = __shfl_sync(0xffffffffu, tau.y, i);
+    const double rii = fabs(beta);
+    if (l == 0) T.rdiag[i] = rii;
+    if (i == 0) r00 = rii;
+    if (r00 == 0.0 || rii <= T.stop_rel * r00) {
+      steps = i;
+      break;
+    }
+    // apply H^H = I - conj(tau) v v^H to the columns right of i
+    // v (lane i's column below the diagonal) is broadcast row by row in
+    // both passes; lane i's registers are not modified by this step
+    const double2 ctau = make_double2(tau.x, -tau.y);
+    const bool apply = ctau.x != 0.0 || ctau.y != 0.0;  // warp-uniform
+    if (apply) {
+      double sx = 0.0, sy = 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        if (r < i || r >= m) continue;
+        double2 vr = make_double2(__shfl_sync(0xffffffffu, c[r].x, i),
+                                  __shfl_sync(0xffffffffu, c[r].y, i));
+        if (r == i) vr = make_double2(1.0, 0.0);
+        sx = fma(vr.x, c[r].x, fma(vr.y, c[r].y, sx));
+        sy = fma(vr.x, c[r].y, fma(-vr.y, c[r].x, sy));
+      }
+      const double2 f = zmul(ctau, make_double2(sx, sy));
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        if (r < i || r >= m) continue;
+        double2 vr = make_double2(__shfl_sync(0xffffffffu, c[r].x, i),
+                                  __shfl_sync(0xffffffffu, c[r].y, i));
+        if (r == i) vr = make_double2(1.0, 0.0);
+        if (own && l > i) {
+          c[r].x = fma(-vr.x, f.x, fma(vr.y, f.y, c[r].x));
+          c[r].y = fma(-vr.x, f.y, fma(-vr.y, f.x, c[r].y));
+        }
+      }
+    }
+    if (own && l > i) {
+      // partial norm downdate (zlaqp2)
+      if (vn1 != 0.0) {
+        double2 aij = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+          if (r == i) aij = c[r];
+        const double iv1 = 1.0 / vn1;
+        double temp = hypot(aij.x, aij.y) * iv1;
+        temp = 1.0 - temp * temp;
+        temp = temp > 0.0 ? temp : 0.0;
+        const double ratio = vn1 * (1.0 / vn2);
+        const double temp2 = temp * ratio * ratio;
+        if (temp2 <= tol3z) {
+          double s2 = 0.0;
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            if (r > i && r < m) s2 = fma(c[r].x, c[r].x, fma(c[r].y, c[r].y, s2));
+          vn1 = vn2 = (i + 1 < m) ? sqrt(s2) : 0.0;
+        } else {
+          vn1 = vn1 * sqrt(temp);
+        }
+      }
+    }
+  }
+  if (own) T.jpvt[l] = jp;
+  if (l == 0) *T.steps = steps;
+  if (own) {
+    double2* R = reinterpret_cast<double2*>(T.r_out) + (size_t)l * T.r_ld;
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r < steps) R[r] = (r <= l) ? c[r] : make_double2(0.0, 0.0);
+  }
+}
+
+void launch_cpqr_warp(const CpqrTask* tasks, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_cpqr_warp<<<(n + kCpqrWarps - 1) / kCpqrWarps, kCpqrWarps * 32, 0, st>>>(tasks, n);
+}
+
 void launch_cpqr_team(const CpqrTask* tasks, int n, size_t smem, double2* gws,
                       cudaStream_t st) {
   if (n <= 0) return;

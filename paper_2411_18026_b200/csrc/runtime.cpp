@@ -1630,8 +1630,18 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
   }
   gws.ensure(ws_total + 1);
   {
+    // blocks of at most 32 x 32 run one warp per matrix (EBEM_CPQR_WARP=0: all
+    // through the team kernel, A/B)
+    static const bool warp_cpqr = [] {
+      const char* e = std::getenv("EBEM_CPQR_WARP");
+      return e == nullptr || std::atoi(e) != 0;
+    }();
+    std::vector<CpqrTask> ct_w, ct_t;
+    for (const CpqrTask& t : ct)
+      ((warp_cpqr && t.n <= 32 && t.rows <= 32) ? ct_w : ct_t).push_back(t);
     Pack pk;
-    const size_t o = pk.add(ct);
+    const size_t o = pk.add(ct_t);
+    const size_t ow = pk.add(ct_w);
     char* tb = staging.put(pk, st_);
     double fl = 0.0;  // full-rank bound of the pivoted QR flops
     double by = 0.0;  // the (reduced) block read once, R written once
@@ -1642,7 +1652,8 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
       by += 16.0 * (mm + nn) * t.n;
     }
     g_prof.begin(st_);
-    launch_cpqr_team(Pack::at<CpqrTask>(tb, o), int(nq), smem, gws.get(), st_);
+    launch_cpqr_team(Pack::at<CpqrTask>(tb, o), int(ct_t.size()), smem, gws.get(), st_);
+    launch_cpqr_warp(Pack::at<CpqrTask>(tb, ow), int(ct_w.size()), st_);
     g_prof.end(KP_CPQR, st_, fl, by);
     CK(cudaGetLastError());
     staging.fence(st_);
