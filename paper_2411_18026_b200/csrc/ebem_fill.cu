@@ -14,6 +14,7 @@
 //   k_gather          ordered scatter of bundles into output blocks
 //                     (proj/src/assembly.cpp:373-407, :493-506)
 #include <stdexcept>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -747,6 +748,191 @@ __device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const 
   }
 }
 
+// Thread-per-pair variant of near_body: one thread owns one element pair and
+// sweeps all n x n points (test point s_i outer, trial point t_j inner), so
+// no shared-memory reduction over i and no CTA barrier between evaluation
+// and output.  After each test point the thread folds its trial sums into
+// its bundle accumulators, acc[x][y][e] += w_i phi_x(s_i) r[y][e], kept in
+// the thread's own shared-memory column (thread-major, conflict-free); the
+// arithmetic (fma(w_i phi, r, acc) from i = 0 upward, Q summed the same way)
+// is that of the reduction in near_body, so both variants give the same bits.
+// The bundle is written from the thread's column at the end of the pair.
+#ifndef EBEM_PP_THREADS
+#define EBEM_PP_THREADS 64
+#endif
+#ifndef EBEM_PP_MINB
+#define EBEM_PP_MINB 4
+#endif
+constexpr int kPpRecPitch = kSymRec + 2;  // 144-byte record rows: conflict-free LDS.128
+// thread per pair only for launches that fill the grid several times over:
+// its unit of work is a whole pair, so a small launch would idle most SMs
+#ifndef EBEM_PP_MIN_ROUNDS
+#define EBEM_PP_MIN_ROUNDS 3
+#endif
+constexpr int kPpMinRounds = EBEM_PP_MIN_ROUNDS;
+template <bool BOTH, bool PROXY>
+__device__ __forceinline__ void near_body_pp(const DevCtx* __restrict__ ctx,
+                                             const FillConst& fc,
+                                             const double* __restrict__ recs, int first,
+                                             int count, int n, double* __restrict__ bundles,
+                                             long long nb) {
+  constexpr int kOrient = BOTH ? 2 : 1;
+  constexpr int kAcc = 16 * kOrient;  // complex accumulators per thread
+  // dynamic: [kAcc][T] accumulators, then one record buffer [T][pitch]
+  extern __shared__ double2 sh[];
+  __shared__ SerSm S;
+  __shared__ double sgx[kMaxGauss], sgw[kMaxGauss];
+  const int T = blockDim.x;
+  const int tid = threadIdx.x;
+  if ((int)blockIdx.x * T >= count) return;  // uniform per CTA
+  double2* const acc = sh + tid;              // acc[k * T]
+  double* const s_rec = reinterpret_cast<double*>(sh + kAcc * T);
+  const double* __restrict__ crec = recs + (long long)first * kSymRec;
+  auto stage = [&](int g) {
+    const int np = min(T, count - g);
+    const double* src = crec + (long long)g * kSymRec;
+    for (int c = tid; c < np * (kSymRec / 2); c += T) {
+      const int p = c / (kSymRec / 2), q = c - p * (kSymRec / 2);
+      cp_async16(s_rec + p * kPpRecPitch + 2 * q, src + 2 * c);
+    }
+    cp_async_commit();
+  };
+  stage(blockIdx.x * T);
+  load_sersm(ctx, S);
+  if (tid < n) {
+    sgx[tid] = ctx->gx[gauss_offset(n) + tid];
+    sgw[tid] = ctx->gw[gauss_offset(n) + tid];
+  }
+  const cplx alpha = mk(fc.med.alpha_re, fc.med.alpha_im);
+  const double qfac = fc.med.qfactor;
+  for (int base = blockIdx.x * T; base < count; base += gridDim.x * T) {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    // the record goes to registers; the buffer then takes the next group
+    const double2* R2 = reinterpret_cast<const double2*>(s_rec + tid * kPpRecPitch);
+    const double2 r0 = R2[0], r1 = R2[1], r2 = R2[2], r3 = R2[3], r4 = R2[4], r5 = R2[5],
+                  r6 = R2[6], r7 = R2[7];
+    __syncthreads();
+    const int nxt = base + gridDim.x * T;
+    if (nxt < count) stage(nxt);
+    const int idx = base + tid;
+    const bool active =
+        idx < count && (!PROXY || __double_as_longlong(r6.x) >= 0);
+    if (active) {
+      const double pax = r0.x, pay = r0.y, dax = r1.x, day = r1.y, nax = r2.x, nay = r2.y;
+      const double pbx = r3.x, pby = r3.y, dbx = r4.x, dby = r4.y, nbx = r5.x, nby = r5.y;
+      const long long vd = __double_as_longlong(r6.x), ud = __double_as_longlong(r6.y);
+      const double hh = r7.x;
+      double qs[3] = {0.0, 0.0, 0.0};
+#pragma unroll 1
+      for (int i = 0; i < n; ++i) {
+        const double s = sgx[i];
+        const double wi = sgw[i];
+        const double xx = pax + s * dax, xy = pay + s * day;
+        const double rmax =
+            fmax(hypot(xx - pbx, xy - pby), hypot(xx - pbx - dbx, xy - pby - dby));
+        const int nt = series_terms(S, rmax);
+        cplx rv[2][4], ru[2][4];
+        double Q[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) rv[b][e] = ru[b][e] = mk(0.0);
+#pragma unroll 1
+        for (int j = 0; j < n; ++j) {
+          const double t = sgx[j];
+          const double wj = sgw[j];
+          const double zx = xx - (pbx + t * dbx);
+          const double zy = xy - (pby + t * dby);
+          const double r = hypot(zx, zy);
+          const double ir = 1.0 / r;
+          const double logr = log(r);
+          const double zhx = ir * zx, zhy = ir * zy;
+          DN dn;
+          dn_eval<!PROXY>(fc, S, r, ir, logr, nt, dn);
+          const double pt[2] = {wj * (1.0 - t), wj * t};
+          CMat2 dm, nm;
+          combine_D(dn, zhx, zhy, nbx, nby, dm);
+          combine_N(dn, zhx, zhy, nax, nay, nbx, nby, nm);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const cplx k = dm.a[e] + alpha * nm.a[e];
+            axpy(rv[0][e], pt[0], k);
+            axpy(rv[1][e], pt[1], k);
+          }
+          if (BOTH) {
+            combine_D(dn, -zhx, -zhy, nax, nay, dm);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const cplx k = dm.a[e] + alpha * nm.a[(e >> 1) | ((e & 1) << 1)];
+              axpy(ru[0][e], pt[0], k);
+              axpy(ru[1][e], pt[1], k);
+            }
+          }
+          if (!PROXY) {
+            const double lq = qfac * logr;
+            Q[0] = fma(wj, lq - qfac * (zhx * zhx), Q[0]);
+            Q[1] = fma(wj, -qfac * (zhx * zhy), Q[1]);
+            Q[2] = fma(wj, lq - qfac * (zhy * zhy), Q[2]);
+          }
+        }
+        // fold: acc[o][x][y][e] (+)= w_i phi_x(s_i) r_o[y][e]
+        const double wsh[2] = {wi * (1.0 - s), wi * s};
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int kv = (x * 2 + y) * 4 + e;
+              double2 a = i ? acc[kv * T] : make_double2(0.0, 0.0);
+              a.x = fma(wsh[x], rv[y][e].re, a.x);
+              a.y = fma(wsh[x], rv[y][e].im, a.y);
+              acc[kv * T] = a;
+              if (BOTH) {
+                double2 b = i ? acc[(16 + kv) * T] : make_double2(0.0, 0.0);
+                b.x = fma(wsh[x], ru[y][e].re, b.x);
+                b.y = fma(wsh[x], ru[y][e].im, b.y);
+                acc[(16 + kv) * T] = b;
+              }
+            }
+        if (!PROXY) {
+#pragma unroll
+          for (int e = 0; e < 3; ++e) qs[e] = fma(wi, Q[e], qs[e]);
+        }
+      }
+      // bundle entries: k = bidx(la, lb, i, j), component e = k & 3
+      double2* const out = reinterpret_cast<double2*>(bundles);
+#pragma unroll
+      for (int o = 0; o < kOrient; ++o) {
+        const long long dst = o == 0 ? vd : ud;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double q = qs[e == 3 ? 2 : (e == 0 ? 0 : 1)];
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            const int la = l >> 1, lb = l & 1;
+            // V: acc[la][lb][e]; U: acc[lb][la][e] (its test shape is lb)
+            const int kv = o == 0 ? (la * 2 + lb) * 4 + e : 16 + (lb * 2 + la) * 4 + e;
+            const double2 a = acc[kv * T];
+            const double sg = (la == lb) ? 1.0 : -1.0;
+            const double re = PROXY ? hh * a.x : fma(hh, a.x, sg * q * alpha.re);
+            const double im = PROXY ? hh * a.y : fma(hh, a.y, sg * q * alpha.im);
+            out[bslot(dst, (l << 2) | e, nb)] = make_double2(re, im);
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(EBEM_PP_THREADS, EBEM_PP_MINB)
+k_proxy_pp(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
+           const double* __restrict__ recs, int n_slots, int ng,
+           double* __restrict__ bundles, long long nb) {
+  near_body_pp<true, true>(ctx, fc, recs, 0, n_slots, ng, bundles, nb);
+}
+
 template <bool BOTH>
 __global__ void __launch_bounds__(EBEM_SYM_THREADS, EBEM_SYM_MINB)
 k_near_sym(const DevCtx* __restrict__ ctx, const __grid_constant__ FillConst fc,
@@ -889,6 +1075,20 @@ k_gather(const GatherJob* __restrict__ jobs, const int* __restrict__ job_block_o
 // ------------------------------------------------------------ host wrappers
 
 
+// Thread-per-pair proxy body (near_body_pp); EBEM_FILL_PP=0 selects the
+// (pair, test point) thread mapping with the shared-memory reduction.  (The
+// near field measured slower with it, 407 -> 436 ms at 2N = 2^19: n = 4
+// points per side leave too little work per pair to hide the fold and the
+// per-thread bundle stores; the proxy blocks, 36 points of full scalars per
+// pair, gain 134 -> 121 ms.)
+static bool fill_pp() {
+  static const bool on = [] {
+    const char* e = std::getenv("EBEM_FILL_PP");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 void launch_sym_bucket(const DevCtx* ctx, const SymJob* jobs, const long long* job_off,
                        int n_jobs, const int* elems, long long n_pairs,
                        unsigned char* keys, int* pair_job, int* bounds, double* recs,
@@ -968,6 +1168,20 @@ void launch_proxy_pairs(const DevCtx* ctx, const FillConst& fc, int n_gauss,
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v > 0 ? v : 148;
   }();
+  if (fill_pp() && n_slots >= (long long)kPpMinRounds * EBEM_PP_MINB * n_sm * EBEM_PP_THREADS) {
+    const int T = EBEM_PP_THREADS;
+    const size_t smem_pp = size_t(T) * 32 * sizeof(double2) +
+                           size_t(T) * kPpRecPitch * sizeof(double);
+    static bool attr_pp = [smem_pp] {
+      cudaFuncSetAttribute(k_proxy_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_pp));
+      return true;
+    }();
+    (void)attr_pp;
+    const long long need_pp = (n_slots + T - 1) / T;
+    const int grid_pp = int(std::min<long long>(need_pp, (long long)EBEM_PP_MINB * n_sm));
+    k_proxy_pp<<<grid_pp, T, smem_pp, st>>>(ctx, fc, recs, int(n_slots), n_gauss, bundles, nb);
+    return;
+  }
   const int P = EBEM_PRX_THREADS / n_gauss;
   const int threads = P * n_gauss;
   const size_t smem = size_t(threads) * 18 * sizeof(double2) +
