@@ -599,9 +599,14 @@ __device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const 
   stage(blockIdx.x * P, 0);
   cp_async_commit();
   load_sersm(ctx, S);
+  __shared__ double sws[2 * kMaxGauss];  // w_i (1 - s_i), w_i s_i
   if (threadIdx.x < n) {
-    sgx[threadIdx.x] = ctx->gx[gauss_offset(n) + threadIdx.x];
-    sgw[threadIdx.x] = ctx->gw[gauss_offset(n) + threadIdx.x];
+    const double x = ctx->gx[gauss_offset(n) + threadIdx.x];
+    const double w = ctx->gw[gauss_offset(n) + threadIdx.x];
+    sgx[threadIdx.x] = x;
+    sgw[threadIdx.x] = w;
+    sws[threadIdx.x] = w * (1.0 - x);
+    sws[kMaxGauss + threadIdx.x] = w * x;
   }
   const int lp = threadIdx.x / n;
   const int i = threadIdx.x - lp * n;
@@ -706,43 +711,43 @@ __device__ __forceinline__ void near_body(const DevCtx* __restrict__ ctx, const 
     }
   }
   __syncthreads();
-  // reduction over i; each pair's first thread handles nothing special:
-  // threads stride over (pair, orientation, 16 outputs)
+  // reduction over i: threads stride over (pair, orientation, 16 outputs),
+  // consecutive threads on consecutive shape entries of one component plane
+  // (64-byte store runs).  Output (la, lb, e) of orientation o sums
+  // fma(w_i phi_x(s_i), row_i[slot], .) over i in order, x = la (V) or lb (U),
+  // with the shape weights from the per-CTA table sws.
   const cplx alpha = mk(fc.med.alpha_re, fc.med.alpha_im);
   constexpr int kOrient = BOTH ? 2 : 1;
   for (int o = threadIdx.x; o < P * kOrient * kBundle; o += blockDim.x) {
     const int lp2 = o / (kOrient * kBundle);
-    const int rem = o - lp2 * kOrient * kBundle;
-    const int orient = rem / kBundle;
-    const int kk = rem - orient * kBundle;
-    const int k = ((kk & 3) << 2) | (kk >> 2);  // bidx(la, lb, i, j); kk: plane-major
+    const int rem = o - lp2 * (kOrient * kBundle);
+    const int orient = rem >> 4;
+    const int kk = rem & 15;
+    const int e = kk >> 2, l = kk & 3;  // plane-major: kk = e * 4 + (la, lb)
     const int idx2 = base + lp2;
     if (idx2 >= count) continue;
     const double* R2 = rec_all + lp2 * kSymRec;
     if (PROXY && __double_as_longlong(R2[SR_VD]) < 0) continue;
-    const int la = k >> 3, lb = (k >> 2) & 1, e = k & 3;
+    const int la = l >> 1, lb = l & 1;
+    const int slot = orient == 0 ? (lb * 4 + e) : (8 + la * 4 + e);
+    const double* wsh = sws + (orient == 0 ? la : lb) * kMaxGauss;
+    const double2* row = sh + (lp2 * n) * 18;
+    const double* qrow = reinterpret_cast<const double*>(sh + (lp2 * n) * 18 + 16) + e;
     double ar = 0.0, ai = 0.0, qs = 0.0;
+#pragma unroll 4
     for (int ii = 0; ii < n; ++ii) {
-      const double sv = gx[ii];
-      const double wi = gw[ii];
-      const double shape = orient == 0 ? (la == 0 ? 1.0 - sv : sv)
-                                       : (lb == 0 ? 1.0 - sv : sv);
-      const int slot = orient == 0 ? (lb * 4 + e) : (8 + la * 4 + e);
-      const double2* row = sh + (lp2 * n + ii) * 18;
-      const double2 v = row[slot];
-      ar = fma(wi * shape, v.x, ar);
-      ai = fma(wi * shape, v.y, ai);
-      if (!PROXY) {
-        const double2 qq = row[16 + (e >> 1)];
-        qs = fma(wi, (e & 1) ? qq.y : qq.x, qs);
-      }
+      const double2 v = row[ii * 18 + slot];
+      const double w = wsh[ii];
+      ar = fma(w, v.x, ar);
+      ai = fma(w, v.y, ai);
+      if (!PROXY) qs = fma(sgw[ii], qrow[ii * 36], qs);
     }
     const double hh = R2[SR_HH];
     const double sg = (la == lb) ? 1.0 : -1.0;  // slope_la * slope_lb
     const double re = PROXY ? hh * ar : fma(hh, ar, sg * qs * alpha.re);
     const double im = PROXY ? hh * ai : fma(hh, ai, sg * qs * alpha.im);
     const long long dst = __double_as_longlong(orient == 0 ? R2[SR_VD] : R2[SR_UD]);
-    reinterpret_cast<double2*>(bundles)[bslot(dst, k, nb)] = make_double2(re, im);
+    reinterpret_cast<double2*>(bundles)[bslot(dst, (l << 2) | e, nb)] = make_double2(re, im);
   }
   __syncthreads();  // shared row sums and pair records are reused
   }
