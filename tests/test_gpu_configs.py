@@ -65,7 +65,11 @@ def check_solution(meta, fx, x):
     s = meta["stride"]
     tol = solution_tol(meta)
     cols = fx.get("x_sample_cols", np.arange(x.shape[1]))
-    assert rel(x[::s][:, cols], fx["x_sample"]) < tol
+    err = rel(x[::s][:, cols], fx["x_sample"])
+    REPORT.mkdir(exist_ok=True)
+    (REPORT / f"solution_{meta['config']}.json").write_text(
+        json.dumps({"config": meta["config"], "n": meta["n"], "rel_sample": err, "tol": tol}) + "\n")
+    assert err < tol
     np.testing.assert_allclose(np.linalg.norm(x, axis=0), fx["x_norm"], rtol=tol)
     # g^H (x - x_ref) for complex Gaussian g (E|g_i|^2 = 2) estimates
     # sqrt(2) ||x - x_ref|| over ALL 2N entries
