@@ -80,7 +80,7 @@ const char* kernel_name(int id) {
   static const char* names[KP_COUNT] = {
       "k_proxy_pairs", "k_near_onesided", "k_near_singular", "k_gather",
       "k_qr_reduce", "k_cpqr", "k_interp", "k_getrf", "k_getrs", "k_gemm",
-      "k_copy", "k_rhs_plane", "k_near_sym"};
+      "k_copy", "k_rhs_plane", "k_near_sym", "k_sym_bucket"};
   return (id >= 0 && id < KP_COUNT) ? names[id] : "?";
 }
 
@@ -183,17 +183,24 @@ void cuda_check(cudaError_t e, const char* what) {
 Staging::~Staging() {
   for (Slot& x : s_) {
     if (x.ev) cudaEventSynchronize(x.ev);
+    if (x.up) cudaEventSynchronize(x.up);
     if (x.host) cudaFreeHost(x.host);
     if (x.dev) cudaFree(x.dev);
     if (x.ev) cudaEventDestroy(x.ev);
+    if (x.up) cudaEventDestroy(x.up);
   }
+  if (copy_) cudaStreamDestroy(copy_);
 }
 
+static double g_staged_bytes = 0.0;  // timeline statistics
+static long g_staged_copies = 0;
 char* Staging::put(const Pack& pk, cudaStream_t st) {
   cur_ = (cur_ + 1) % int(s_.size());
   Slot& x = s_[cur_];
   if (!x.ev) CK(cudaEventCreateWithFlags(&x.ev, cudaEventDisableTiming));
-  if (x.pending) {
+  if (!x.up) CK(cudaEventCreateWithFlags(&x.up, cudaEventDisableTiming));
+  if (!copy_) CK(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+  if (x.pending) {  // the slot's previous kernels (and so its upload) are done
     CK(cudaEventSynchronize(x.ev));
     x.pending = false;
   }
@@ -208,7 +215,11 @@ char* Staging::put(const Pack& pk, cudaStream_t st) {
   }
   if (bytes) {
     std::memcpy(x.host, pk.data(), bytes);
-    CK(cudaMemcpyAsync(x.dev, x.host, bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x.dev, x.host, bytes, cudaMemcpyHostToDevice, copy_));
+    CK(cudaEventRecord(x.up, copy_));
+    CK(cudaStreamWaitEvent(st, x.up, 0));
+    g_staged_bytes += double(bytes);
+    ++g_staged_copies;
   }
   return x.dev;
 }
@@ -297,6 +308,84 @@ void NodeBoxTree::enclosed(const double* xy, double cx, double cy,
       stack[sp++] = b.left;
     }
   }
+}
+
+// ------------------------------------------------------------- timeline
+// EBEM_TIMELINE=1 (development aid): events + host clocks at the level
+// loop's hand-off points; printed after the build as (GPU ms, host ms, lag).
+// A lag near zero means the GPU had drained its queue when the host got
+// there: device idle waiting for host planning.
+namespace {
+struct Timeline {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  double h0 = 0.0;
+  cudaEvent_t e0 = nullptr;
+  std::vector<std::string> names;
+  std::vector<cudaEvent_t> ev;
+  std::vector<double> host;
+};
+Timeline& tl() {
+  static Timeline t;
+  return t;
+}
+bool tl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("EBEM_TIMELINE");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+}  // namespace
+void tl_begin(cudaStream_t st) {
+  Timeline& t = tl();
+  t.on = tl_enabled();
+  if (!t.on) return;
+  t.st = st;
+  t.names.clear();
+  t.ev.clear();
+  t.host.clear();
+  g_staged_bytes = 0.0;
+  g_staged_copies = 0;
+  if (!t.e0) cudaEventCreate(&t.e0);
+  cudaEventRecord(t.e0, st);
+  cudaEventSynchronize(t.e0);
+  t.h0 = now();
+}
+void tl_mark(const std::string& name) {
+  Timeline& t = tl();
+  if (!t.on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, t.st);
+  t.names.push_back(name);
+  t.ev.push_back(e);
+  t.host.push_back(now() - t.h0);
+}
+void tl_dump() {
+  Timeline& t = tl();
+  if (!t.on) return;
+  cudaStreamSynchronize(t.st);
+  double idle = 0.0, prev_g = 0.0;
+  for (size_t i = 0; i < t.ev.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.e0, t.ev[i]);
+    const double h = 1e3 * t.host[i];
+    // the GPU reached this mark no earlier than the host recorded it: when
+    // it got there within 20 us of the host, it waited (since the previous
+    // mark at the latest) for the host
+    const double lag = ms - h;
+    if (lag < 0.02) idle += std::max(0.0, ms - std::max(prev_g, 0.0)) ;
+    std::fprintf(stderr, "[tl] %-28s gpu %9.3f ms  host %9.3f ms  lag %8.3f\n", t.names[i].c_str(), ms, h, lag);
+    prev_g = ms;
+    cudaEventDestroy(t.ev[i]);
+  }
+  std::fprintf(stderr, "[tl] upper bound of host-bound device time: %.1f ms; staged %.1f MB in %ld copies\n",
+               idle, g_staged_bytes / 1e6, g_staged_copies);
+  g_staged_bytes = 0.0;
+  g_staged_copies = 0;
+  t.ev.clear();
+  t.on = false;
 }
 
 // ---------------------------------------------------------------- Problem
@@ -1279,8 +1368,10 @@ void Problem::execute(FillPlan& plan) {
     sym_vals_.ensure(size_t(nsym));  // job of each pair
     if (!sym_bounds_.get()) sym_bounds_.alloc(size_t(sym_bounds_ints()));
     sym_recs_.ensure(size_t(kSymRec) * (nsym + proxy_slots));
+    g_prof.begin(st_);
     launch_sym_bucket(dctx(), sj, so, int(plan.sym_.size()), el, nsym, sym_keys_.get(),
                       sym_vals_.get(), sym_bounds_.get(), sym_recs_.get(), st_);
+    g_prof.end(KP_BUCKET, st_, double(nsym));
     g_launches += 2;
   }
   if (!plan.proxy_.empty()) {
@@ -1394,6 +1485,7 @@ void Problem::interaction(const std::vector<BasisReq>& req,
         plan.append_many(parts, k0, k + 1);
         for (int q = k0; q <= k; ++q) parts[q] = FillPlan(n_, m, pcfg_.n_gauss);
       }
+      tl_mark("  wave planned");
       execute(plan);
       k0 = k + 1;
       acc = 0;
@@ -1562,7 +1654,9 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
   std::vector<int> n_out;
   DBuf<double>& tbuf = tbuf_;
   const double t0 = now();
+  tl_mark("  bases start");
   interaction(req, geom, tv_off, tu_off, n_out, tbuf);
+  tl_mark("  fill enq");
   if (fill_seconds) {
     CK(cudaStreamSynchronize(st_));
     *fill_seconds = now() - t0;
@@ -1664,7 +1758,9 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
   CK(cudaMemcpyAsync(h_jp, d_jp.get(), jp_total * 4, cudaMemcpyDeviceToHost, st_));
   CK(cudaMemcpyAsync(h_steps, d_steps.get(), nq * 4, cudaMemcpyDeviceToHost, st_));
   CK(cudaMemcpyAsync(h_rd, d_rd.get(), jp_total * 8, cudaMemcpyDeviceToHost, st_));
+  tl_mark("  id enq");
   CK(cudaStreamSynchronize(st_));
+  tl_mark("  readback");
   check_domain();  // the fill's element-length guard, read after the sync
 
   // ---- shared rank (basis_from_interactions, compression.cpp:92-99)
@@ -2117,6 +2213,7 @@ void Fds::build() {
   CK(cudaEventCreate(&ev0));
   CK(cudaEventCreate(&ev1));
   CK(cudaEventRecord(ev0, P_.stream()));
+  tl_begin(P_.stream());
   const int n = P_.n();
   const int ncells = (2 << depth_) - 1;
   cells_.assign(ncells, Cell{});
@@ -2233,7 +2330,9 @@ void Fds::build() {
       run_getrf(P_, lt);
     }
     };
+    tl_mark("L" + std::to_string(level) + " start");
     if (!hs_) diagonal_and_lu();
+    tl_mark("L" + std::to_string(level) + " diag+lu enq");
     // ---- bases of every cell of the level
     std::vector<BasisReq> req(nlev);
     for (int c = f; c <= L; ++c)
@@ -2244,6 +2343,7 @@ void Fds::build() {
     if (hs_) host_bases(level, br, S.v, ubuf);
     else P_.bases(req, cfg_.epsilon, br, S.v, ubuf);
     PhaseTimer t_after("level_after_bases", nullptr);
+    tl_mark("L" + std::to_string(level) + " bases done");
     basis_seconds += now() - tb;
     if (hs_) diagonal_and_lu();
     size_t au_total = 0, at_total = 0;
@@ -2343,6 +2443,8 @@ void Fds::build() {
       Pc.nloc = c1.k + c2.k;
     }
   }
+  tl_mark("upward enq");
+  tl_dump();
   CK(cudaStreamSynchronize(P_.stream()));
   stats_.upward_seconds = now() - t_start;
   stats_.basis_cpu_seconds = basis_seconds;

@@ -40,7 +40,7 @@ extern std::atomic<long long> g_launches;
 // kernels, bytes or flops for the rest); enabled by ebem_gpu_prof_enable.
 enum KernelId {
   KP_PROXY = 0, KP_NEAR_1S, KP_NEAR_SING, KP_GATHER, KP_QR, KP_CPQR,
-  KP_INTERP, KP_GETRF, KP_GETRS, KP_GEMM, KP_COPY, KP_RHS, KP_NEAR_SYM, KP_COUNT
+  KP_INTERP, KP_GETRF, KP_GETRS, KP_GEMM, KP_COPY, KP_RHS, KP_NEAR_SYM, KP_BUCKET, KP_COUNT
 };
 const char* kernel_name(int id);
 
@@ -207,11 +207,15 @@ class Staging {
     char* host = nullptr;
     char* dev = nullptr;
     size_t cap = 0;
-    cudaEvent_t ev = nullptr;
+    cudaEvent_t ev = nullptr;  // the kernels reading the slot are done
+    cudaEvent_t up = nullptr;  // the slot's upload is done
     bool pending = false;
   };
   std::vector<Slot> s_;
   int cur_ = -1;
+  // uploads run on their own stream, so a wave's task arrays cross PCIe
+  // while the previous wave computes; the compute stream waits on `up`
+  cudaStream_t copy_ = nullptr;
 };
 
 // ------------------------------------------------------------ segment tree
