@@ -11,7 +11,7 @@ commit=${1:-unknown}
 mkdir -p gpurun_out
 python tools/calibrate_flops.py 262144 > gpurun_out/cal_points.log
 ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-    --clock-control none -k regex:'k_near_sym|k_proxy_pairs' --csv \
+    --clock-control none -k regex:'k_near_sym|k_proxy_pairs|k_proxy_pp' --csv \
     python tools/calibrate_flops.py 262144 > gpurun_out/cal_fill.csv 2> gpurun_out/cal_fill.err
 ncu --metrics gpu__time_duration.sum,sm__inst_executed_pipe_tensor_subpipe_dmma.sum,smsp__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active \
     --clock-control none -k regex:k_gemm_mma --csv \

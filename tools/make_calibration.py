@@ -17,6 +17,8 @@ def rows_of(path):
 
 def kname(full):
     name = re.sub(r"^void ", "", full).split("(")[0].split("<")[0].replace("ebem_gpu::", "")
+    if name == "k_proxy_pp":
+        name = "k_proxy_pairs"  # the thread-per-pair body of the proxy blocks (profiler name)
     if name == "k_near_sym" and re.search(r"k_near_sym<(\(bool\))?(0|false)>", full):
         name = "k_near_onesided"  # the one-sided instantiation (profiler name)
     return name
