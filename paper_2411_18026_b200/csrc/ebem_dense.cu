@@ -1231,6 +1231,58 @@ k_getrs_cta(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
 // reads coalesced across the 64 row lanes).  Orders up to 64 Q.
 constexpr int kBlkRhs = 16;
 constexpr int kBlkPanel = 32;
+#ifndef EBEM_GETRS_MMA
+#define EBEM_GETRS_MMA 1
+#endif
+// Trailing update of a panel on the FP64 tensor cores:
+//   X[r][0..16) -= A[r][k0 .. k0 + pw) X[k0 .. k0 + pw)[0..16),  ra <= r < rb,
+// A the LU (column-major, lda), X the CTA's right-hand sides ([col][row],
+// ld n).  Warps take 8-row tiles; per tile 8 k-steps of 4 x 2 column tiles
+// x 4 real m8n8k4 products (complex as four real MMAs), the tile's A
+// fragments loaded from global memory up front, X's from shared memory.
+__device__ __forceinline__ void blk_update_mma(const double2* __restrict__ A, size_t lda,
+                                               double2* X, int n, int k0, int pw, int ra,
+                                               int rb, int w, int l) {
+  const int fr = l >> 2, fk = l & 3;
+  const int mtiles = (rb - ra + 7) >> 3;
+  for (int mt = w; mt < mtiles; mt += kWarps) {
+    const int r = ra + 8 * mt + fr;
+    double2 a[kBlkPanel / 4];
+#pragma unroll
+    for (int ks = 0; ks < kBlkPanel / 4; ++ks) {
+      const int kk = 4 * ks + fk;
+      a[ks] = (r < rb && kk < pw) ? __ldg(A + (size_t)(k0 + kk) * lda + r)
+                                  : make_double2(0.0, 0.0);
+    }
+    double acc[2][2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) acc[nt][c][0] = acc[nt][c][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < kBlkPanel / 4; ++ks) {
+      const int kk = 4 * ks + fk;
+      if (4 * ks >= pw) break;  // warp-uniform
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const double2 b = kk < pw ? X[(size_t)(8 * nt + fr) * n + k0 + kk] : make_double2(0.0, 0.0);
+        dmma(acc[nt][0][0], acc[nt][0][1], a[ks].x, b.x);
+        dmma(acc[nt][0][0], acc[nt][0][1], -a[ks].y, b.y);
+        dmma(acc[nt][1][0], acc[nt][1][1], a[ks].x, b.y);
+        dmma(acc[nt][1][0], acc[nt][1][1], a[ks].y, b.x);
+      }
+    }
+    const int row = ra + 8 * mt + fr;
+    if (row < rb)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double2& xr = X[(size_t)(8 * nt + 2 * fk + h) * n + row];
+          xr = make_double2(xr.x - acc[nt][0][h], xr.y - acc[nt][1][h]);
+        }
+  }
+}
 template <int Q>
 __global__ void __launch_bounds__(kThreads)
 k_getrs_blk(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block_off,
@@ -1292,7 +1344,9 @@ k_getrs_blk(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
       if (l < pw) xc[l] = x;
     }
     __syncthreads();
-    if (k1 < n) {
+    if (EBEM_GETRS_MMA && k1 < n) {
+      blk_update_mma(A, lda, X, n, k0, pw, k1, n, w, l);
+    } else if (k1 < n) {
       double2 acc[Q][4];
 #pragma unroll
       for (int q = 0; q < Q; ++q)
@@ -1349,7 +1403,9 @@ k_getrs_blk(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
       if (l < pw) xc[l] = x;
     }
     __syncthreads();
-    if (k0 > 0) {
+    if (EBEM_GETRS_MMA && k0 > 0) {
+      blk_update_mma(A, lda, X, n, k0, pw, 0, k0, w, l);
+    } else if (k0 > 0) {
       double2 acc[Q][4];
 #pragma unroll
       for (int q = 0; q < Q; ++q)

@@ -1,0 +1,3 @@
+python -m pytest tests/test_gpu_solve_kernels.py tests/test_gpu_fds.py -q -x 2>&1 | tail -n 2
+for l in base ""; do echo "== $l"; EBEM_GPU_LIB=${l:+abx/$l.so} python tools/solve180_profile.py 2>&1 | tail -n 1; EBEM_GPU_LIB=${l:+abx/$l.so} python tools/kernel_table.py 262144 2 2>&1 | grep -E "factorize|k_getrs"; done
+python -m pytest tests/test_gpu_configs.py -q -x 2>&1 | tail -n 2; cat gpurun_out/solution_*.json
