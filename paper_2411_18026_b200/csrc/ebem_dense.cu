@@ -37,6 +37,9 @@ constexpr int kWarps = kThreads / 32;
 #define EBEM_QR_THREADS 512
 #endif
 constexpr int kQrThreads = EBEM_QR_THREADS;  // QR / CPQR / LU CTAs
+#ifndef EBEM_GETRF_LA
+#define EBEM_GETRF_LA 1  // look-ahead k_getrf (one barrier per column); 0: the unblocked sequence
+#endif
 
 __device__ __forceinline__ double2 zmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -362,6 +365,79 @@ k_getrf(const LuTask* __restrict__ tasks, double2* __restrict__ gws) {
   if (threadIdx.x == 0) s_info = 0;
   __syncthreads();
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#if EBEM_GETRF_LA
+  // Look-ahead elimination, one CTA barrier per column: in step k warp 0
+  // finishes column k + 1 (interchange and update by column k, then its
+  // pivot search, interchange and scaling) while the other warps interchange
+  // and update the columns right of it and interchange the L columns left of
+  // k.  Every element sees the same operations in the same order as the
+  // unblocked sequence below (bitwise-identical factors).
+  const int nw = blockDim.x >> 5;
+  auto pivot_col = [&](int k) {  // warp 0: pivot of column k, interchange + scale it
+    double best = -1.0;
+    int bi = k;
+    for (int r = k + l; r < n; r += 32) {
+      const double v = cabs1(A[(size_t)k * n + r]);
+      if (v > best) { best = v; bi = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (l == 0) {
+      s_p = bi;
+      T.ipiv[k] = bi;
+      if (best == 0.0 && s_info == 0) s_info = k + 1;
+    }
+    if (bi != k && l == 0) {
+      const double2 t = A[(size_t)k * n + k];
+      A[(size_t)k * n + k] = A[(size_t)k * n + bi];
+      A[(size_t)k * n + bi] = t;
+    }
+    __syncwarp();
+    const double2 piv = A[(size_t)k * n + k];
+    if (piv.x != 0.0 || piv.y != 0.0) {
+      const double2 rp = zdiv(make_double2(1.0, 0.0), piv);
+      for (int r = k + 1 + l; r < n; r += 32)
+        A[(size_t)k * n + r] = zmul(A[(size_t)k * n + r], rp);
+    }
+  };
+  if (w == 0) pivot_col(0);
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    const int p = s_p;  // pivot of column k (applied to column k, which is scaled)
+    __syncthreads();    // everyone read s_p before warp 0 overwrites it
+    auto swap_update = [&](int j) {  // column j > k: interchange rows k, p; update
+      if (p != k && l == 0) {
+        const double2 t = A[(size_t)j * n + k];
+        A[(size_t)j * n + k] = A[(size_t)j * n + p];
+        A[(size_t)j * n + p] = t;
+      }
+      __syncwarp();
+      const double2 akj = A[(size_t)j * n + k];
+      for (int r = k + 1 + l; r < n; r += 32)
+        A[(size_t)j * n + r] = zfms(A[(size_t)j * n + r], A[(size_t)k * n + r], akj);
+      __syncwarp();
+    };
+    if (w == 0) {
+      if (k + 1 < n) {
+        swap_update(k + 1);
+        pivot_col(k + 1);
+      }
+    } else {
+      for (int j = k + 2 + (w - 1); j < n; j += nw - 1) swap_update(j);
+      if (p != k)
+        for (int j = (w - 1) * 32 + l; j < k; j += (nw - 1) * 32) {
+          const double2 t = A[(size_t)j * n + k];
+          A[(size_t)j * n + k] = A[(size_t)j * n + p];
+          A[(size_t)j * n + p] = t;
+        }
+    }
+    __syncthreads();
+  }
+#else
   for (int k = 0; k < n; ++k) {
     if (w == 0) {
       double best = -1.0;
@@ -407,6 +483,7 @@ k_getrf(const LuTask* __restrict__ tasks, double2* __restrict__ gws) {
     }
     __syncthreads();
   }
+#endif
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
     const int j = idx / n, i = idx - j * n;
     G[(size_t)j * T.ld + i] = A[idx];
@@ -1540,6 +1617,8 @@ void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st) {
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st) {
   if (n <= 0) return;
+  k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
+}
   k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
 int getrs_cpw(int max_nrhs, int max_n) {

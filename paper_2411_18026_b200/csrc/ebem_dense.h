@@ -113,7 +113,7 @@ constexpr int kGetrsWarpMaxN = 128;
 constexpr int kGetrsCtaMaxN = 2048;
 // -2: blocked panels for many columns (ebem_dense.cu k_getrs_blk)
 #ifndef EBEM_BLK_MIN_N
-#define EBEM_BLK_MIN_N 96
+#define EBEM_BLK_MIN_N 64
 #endif
 constexpr int kBlkMinRhs = 16;
 constexpr int kBlkMinN = EBEM_BLK_MIN_N;
