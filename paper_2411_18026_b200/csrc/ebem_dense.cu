@@ -1619,8 +1619,6 @@ void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
   if (n <= 0) return;
   k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
 }
-  k_getrf<<<n, kQrThreads, smem, st>>>(tasks, gws);
-}
 int getrs_cpw(int max_nrhs, int max_n) {
   if (max_nrhs >= kBlkMinRhs && max_n >= kBlkMinN && max_n <= kGetrsBlkMaxN) return -2;
   if (max_n > 256 && max_n <= kGetrsCtaMaxN) return -1;  // one CTA per column
