@@ -20,6 +20,14 @@ namespace ebem_gpu {
 namespace {
 
 constexpr int kNb = 32;
+#ifndef EBEM_LU_MMA
+#define EBEM_LU_MMA 1  // trailing update on the FP64 tensor cores (0: SIMT register tiles)
+#endif
+__device__ __forceinline__ void mma_f64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 constexpr int kPanelThreads = 512;
 constexpr int kTile = 64;
 
@@ -171,6 +179,15 @@ k_lu_update(const LuTask* __restrict__ tasks, int j0) {
   const size_t ld = T.ld;
   const int r0 = s + tr * kTile, c0 = s + tc * kTile;
   const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;  // rows ty + 16 a, cols tx + 16 b
+#if EBEM_LU_MMA
+  double macc[8][2][2];  // [column tile][re, im][2]
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) macc[t][c][0] = macc[t][c][1] = 0.0;
+  (void)ty;
+  (void)tx;
+#endif
   double2 acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -186,6 +203,27 @@ k_lu_update(const LuTask* __restrict__ tasks, int j0) {
       Us[k][i] = (c0 + i < n) ? A[(size_t)(c0 + i) * ld + j0 + k0 + k] : make_double2(0.0, 0.0);
     }
     __syncthreads();
+#if EBEM_LU_MMA
+    {
+      // FP64 tensor cores: warp w owns output rows 8w .. 8w + 7 of the tile,
+      // all 8 column tiles; per k-step one A fragment, eight B fragments,
+      // 8 x 4 real m8n8k4 products (complex as four real MMAs)
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31, fr = l >> 2, fk = l & 3;
+#pragma unroll
+      for (int k = 0; k < kK; k += 4) {
+        const double2 a = Ls[k + fk][8 * w + fr];
+        const double an = -a.y;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const double2 b = Us[k + fk][8 * t + fr];
+          mma_f64(macc[t][0][0], macc[t][0][1], a.x, b.x);
+          mma_f64(macc[t][0][0], macc[t][0][1], an, b.y);
+          mma_f64(macc[t][1][0], macc[t][1][1], a.x, b.y);
+          mma_f64(macc[t][1][0], macc[t][1][1], a.y, b.x);
+        }
+      }
+    }
+#else
 #pragma unroll 4
     for (int k = 0; k < kK; ++k) {
       double2 lv[4], uv[4];
@@ -201,8 +239,26 @@ k_lu_update(const LuTask* __restrict__ tasks, int j0) {
           acc[a][b].y = fma(lv[a].x, uv[b].y, fma(lv[a].y, uv[b].x, acc[a][b].y));
         }
     }
+#endif
     __syncthreads();
   }
+#if EBEM_LU_MMA
+  {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, fr = l >> 2, fk = l & 3;
+    const int r = r0 + 8 * w + fr;
+    if (r < n)
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = c0 + 8 * t + 2 * fk + h;
+          if (c >= n) continue;
+          double2* e = A + (size_t)c * ld + r;
+          *e = make_double2(e->x - macc[t][0][h], e->y - macc[t][1][h]);
+        }
+  }
+  return;
+#endif
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
     const int c = c0 + tx + 16 * b;
