@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <stdexcept>
 #include <cstdlib>
 
 #include "ebem_dense.h"
@@ -321,17 +322,25 @@ k_interp(const InterpTask* __restrict__ tasks) {
   const double2* R = reinterpret_cast<const double2*>(T.r);
   double2* out = reinterpret_cast<double2*>(T.out);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  // one warp per column j >= k of R12: back substitution, lanes over rows
-  extern __shared__ double2 col[];  // kWarps * k
-  double2* x = col + w * k;
+  // R11 (k x k upper triangle) staged in shared memory once per task, so
+  // the back substitutions' dependent steps read ~30-cycle shared memory,
+  // not L2; then one warp per column j >= k of R12, lanes over rows
+  extern __shared__ double2 col[];  // R11 [k][k] | kWarps * k
+  double2* Rs = col;
+  double2* x = col + (size_t)k * k + w * k;
+  for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
+    const int c = idx / k, r = idx - c * k;
+    Rs[idx] = r <= c ? R[(size_t)c * T.r_ld + r] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
   for (int j = k + w; j < n; j += kWarps) {
     for (int r = l; r < k; r += 32) x[r] = R[(size_t)j * T.r_ld + r];
     __syncwarp();
     for (int r = k - 1; r >= 0; --r) {
-      if (l == 0) x[r] = zdiv(x[r], R[(size_t)r * T.r_ld + r]);
+      if (l == 0) x[r] = zdiv(x[r], Rs[(size_t)r * k + r]);
       __syncwarp();
       const double2 xr = x[r];
-      for (int q = l; q < r; q += 32) x[q] = zfms(x[q], R[(size_t)r * T.r_ld + q], xr);
+      for (int q = l; q < r; q += 32) x[q] = zfms(x[q], Rs[(size_t)r * k + q], xr);
       __syncwarp();
     }
     const int dc = T.jpvt[j];
@@ -1611,8 +1620,15 @@ void launch_cpqr(const CpqrTask* tasks, int n, size_t smem, double2* gws,
 }
 void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st) {
   if (n <= 0) return;
-  k_interp<<<n, kThreads, size_t(kWarps) * (max_k > 0 ? max_k : 1) * sizeof(double2),
-             st>>>(tasks);
+  const int kk = max_k > 0 ? max_k : 1;
+  const size_t smem = (size_t(kk) * kk + size_t(kWarps) * kk) * sizeof(double2);
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
+    return true;
+  }();
+  (void)attr;
+  if (smem > size_t(kSmemCap)) throw std::length_error("interpolation: rank too large");
+  k_interp<<<n, kThreads, smem, st>>>(tasks);
 }
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st) {
