@@ -438,6 +438,7 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
       pcfg_(p) {
   if (n < 4) throw Error(EBEM_INVALID_ARGUMENT, "Mesh: needs at least 4 nodes");
   if (n < 8) throw Error(EBEM_INVALID_ARGUMENT, "PairIntegrator: mesh too coarse");
+  const double tc0 = now();
   xy_.assign(xy, xy + 2 * size_t(n));
   elem_.resize(size_t(kElemFields) * n);
   try {
@@ -452,6 +453,7 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
     throw Error(EBEM_INVALID_ARGUMENT, e.what());
   }
   auto scaled = [&](int q) { return int(q * a.refine + 0.5); };
+  const double tc1 = now();
   hctx_.med = med;
   hctx_.n_nodes = n;
   try {
@@ -576,6 +578,7 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw Error(EBEM_CUDA_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
+  const double tc2 = now();
   st_ = scratch().st;
   delem_.alloc(elem_.size());
   dxy_.alloc(xy_.size());
@@ -599,7 +602,11 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   CK(cudaMemsetAsync(bad.get(), 0, sizeof(int), st_));
   CK(cudaStreamSynchronize(st_));
   dense_init();
+  const double tc3 = now();
   tree_.build(xy_.data(), n);
+  if (verbose_level())
+    std::fprintf(stderr, "[ebem] problem setup: geometry %.1f ms, tables %.1f ms, upload %.1f ms, box tree %.1f ms\n",
+                 1e3 * (tc1 - tc0), 1e3 * (tc2 - tc1), 1e3 * (tc3 - tc2), 1e3 * (now() - tc3));
 }
 
 Problem::Problem(int n)
@@ -2655,6 +2662,7 @@ void Fds::cell_info(int cell, int* sizes, int* skel) const {
 }
 
 void Fds::record_solve(int m) {
+  const double tr0 = now();
   plan_.reset(new SolvePlan());
   SolvePlan& S = *plan_;
   S.m = m;
@@ -2781,7 +2789,9 @@ void Fds::record_solve(int m) {
   }
   S.rec.mark();
   P_.recorder = nullptr;
+  const double tr1 = now();
   S.rec.finalize(P_.stream());
+  const double tr2 = now();
   for (int q = 0; q < 4; ++q) CK(cudaEventCreate(&S.ev[q]));
   // one graph per phase (upward, top, downward); timing events go between
   for (int ph = 0; ph < 3; ++ph) {
@@ -2790,6 +2800,9 @@ void Fds::record_solve(int m) {
     CK(cudaStreamEndCapture(P_.stream(), &S.graph[ph]));
     CK(cudaGraphInstantiate(&S.exec[ph], S.graph[ph], 0));
   }
+  if (verbose_level())
+    std::fprintf(stderr, "[ebem] record_solve(%d): tasks %.1f ms, upload %.1f ms, graphs %.1f ms (%zu launches)\n",
+                 m, 1e3 * (tr1 - tr0), 1e3 * (tr2 - tr1), 1e3 * (now() - tr2), S.rec.n_launches());
 }
 
 Fds::~Fds() = default;  // SolvePlan releases its graphs
