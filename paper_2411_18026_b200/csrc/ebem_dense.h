@@ -95,11 +95,6 @@ void launch_cpqr_team(const CpqrTask* tasks, int n, size_t smem, double2* gws,
 // smem = tsqr_smem_bytes(n) for the largest n of a launch.
 constexpr int kTsqrMaxCols = 128;
 int tsqr_variant(int n);  // -1: not supported (n > kTsqrMaxCols)
-// Compact-WY streaming TSQR (ebem_tsqr_wy.cu): panels of 8 columns, block
-// reflectors applied on DMMA; orders up to tsqr_wy_max_n().
-size_t tsqr_wy_smem_bytes(int n);
-int tsqr_wy_max_n();
-void launch_tsqr_wy(const QrTask* tasks, int n_tasks, size_t smem, cudaStream_t st);
 int tsqr_block_rows(int n);
 int tsqr_ctas_per_sm(int n);
 size_t tsqr_smem_bytes(int n);

@@ -1522,22 +1522,9 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     const char* e = std::getenv("EBEM_TSQR_PIECES");
     return e ? std::atoi(e) : 0;
   }();
-  // EBEM_TSQR_WY=0: the reflector-at-a-time wavefront kernel for the wide
-  // inputs too (A/B); else orders 65 .. tsqr_wy_max_n() take the compact-WY
-  // kernel with DMMA block updates
-  static const bool wy = [] {  // experiment, off by default (slower: 152 -> 240 ms)
-    const char* e = std::getenv("EBEM_TSQR_WY");
-    return e != nullptr && std::atoi(e) != 0;
-  }();
-  static const int wy_max = tsqr_wy_max_n();
-  static const int wy_min = [] {  // experiments: EBEM_TSQR_WY_MIN (default: the wide variant's orders)
-    const char* e = std::getenv("EBEM_TSQR_WY_MIN");
-    return e ? std::atoi(e) : 65;
-  }();
   size_t round = 0;
   for (;;) {
-    std::vector<QrTask> tasks, stream16, stream8, stream4, streamwy;
-    size_t smemwy = 0;
+    std::vector<QrTask> tasks, stream16, stream8, stream4;
     std::vector<size_t> out_off(q.size(), 0);
     size_t out_total = 0, ws_total = 0;
     std::vector<int> pieces(q.size(), 0);
@@ -1606,11 +1593,6 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
         t.n = x.n;
         t.ld = x.ld;
         t.dst_ld = ld_out;
-        if (streamed[i] && wy && x.n >= wy_min && x.n <= wy_max) {
-          streamwy.push_back(t);
-          smemwy = std::max(smemwy, tsqr_wy_smem_bytes(x.n));
-          continue;
-        }
         if (streamed[i]) {
           if (tsqr_variant(x.n) == 2) {
             stream4.push_back(t);
@@ -1636,14 +1618,13 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     const size_t o16 = pk.add(stream16);
     const size_t o8 = pk.add(stream8);
     const size_t o4 = pk.add(stream4);
-    const size_t owy = pk.add(streamwy);
     char* tb = staging.put(pk, st);
     size_t smem = 0;
     for (const QrTask& t : tasks)
       if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
     double fl = 0.0;
     double by = 0.0;  // the block read once, its reduced rows written once
-    for (const auto* v : {&tasks, &stream16, &stream8, &stream4, &streamwy})
+    for (const auto* v : {&tasks, &stream16, &stream8, &stream4})
       for (const QrTask& t : *v) {
         const double mm = t.rows, nn = std::min(t.rows, t.n);
         // complex Householder QR with k = min(m, n) reflectors:
@@ -1657,7 +1638,6 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     launch_tsqr(Pack::at<QrTask>(tb, o16), int(stream16.size()), 0, smem16, st);
     launch_tsqr(Pack::at<QrTask>(tb, o8), int(stream8.size()), 1, smem8, st);
     launch_tsqr(Pack::at<QrTask>(tb, o4), int(stream4.size()), 2, smem4, st);
-    launch_tsqr_wy(Pack::at<QrTask>(tb, owy), int(streamwy.size()), smemwy, st);
     g_prof.end(KP_QR, st, fl, by);
     CK(cudaGetLastError());
     staging.fence(st);
