@@ -257,8 +257,7 @@ k_lu_update(const LuTask* __restrict__ tasks, int j0) {
           *e = make_double2(e->x - macc[t][0][h], e->y - macc[t][1][h]);
         }
   }
-  return;
-#endif
+#else
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
     const int c = c0 + tx + 16 * b;
@@ -271,6 +270,7 @@ k_lu_update(const LuTask* __restrict__ tasks, int j0) {
       *e = make_double2(e->x - acc[a][b].x, e->y - acc[a][b].y);
     }
   }
+#endif
 }
 
 }  // namespace
