@@ -723,6 +723,8 @@ k_gemm_mma(const GemmTask* __restrict__ tasks, const int* __restrict__ block_off
       for (int c = 0; c < 2; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
   const int wr = (w & 1) * 16, wc = (w >> 1) * 16;
   const int fr = lane >> 2, fk = lane & 3;
+  const bool live_r[2] = {r0 + wr < m, r0 + wr + 8 < m};
+  const bool live_c[2] = {c0 + wc < n, c0 + wc + 8 < n};
   const double sa = ta == 2 ? -1.0 : 1.0, sb = tb == 2 ? -1.0 : 1.0;  // conjugation
   const int nck = (kdim + kMmaKc - 1) / kMmaKc;
   issue(0, 0);
@@ -754,6 +756,9 @@ k_gemm_mma(const GemmTask* __restrict__ tasks, const int* __restrict__ block_off
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
+          // 8 x 8 sub-tiles wholly outside m x n (the padding of m = k, n = 2k
+          // to 32 x 32 tiles) issue no MMAs (warp-uniform)
+          if (!live_r[i] || !live_c[j]) continue;
           dmma(acc[i][j][0][0], acc[i][j][0][1], ar[i], br[j]);
           dmma(acc[i][j][0][0], acc[i][j][0][1], an[i], bi[j]);
           dmma(acc[i][j][1][0], acc[i][j][1][1], ar[i], bi[j]);

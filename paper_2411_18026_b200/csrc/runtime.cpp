@@ -204,6 +204,10 @@ char* Staging::put(const Pack& pk, cudaStream_t st) {
     CK(cudaEventSynchronize(x.ev));
     x.pending = false;
   }
+  if (x.uploading) {  // a put without a fence: its copy may still read x.host
+    CK(cudaEventSynchronize(x.up));
+    x.uploading = false;
+  }
   const size_t bytes = pk.bytes();
   if (bytes > x.cap) {
     const size_t cap = std::max(std::max(bytes + bytes / 2, 2 * x.cap), size_t(32) << 20);
@@ -218,6 +222,7 @@ char* Staging::put(const Pack& pk, cudaStream_t st) {
     CK(cudaMemcpyAsync(x.dev, x.host, bytes, cudaMemcpyHostToDevice, copy_));
     CK(cudaEventRecord(x.up, copy_));
     CK(cudaStreamWaitEvent(st, x.up, 0));
+    x.uploading = true;
     g_staged_bytes += double(bytes);
     ++g_staged_copies;
   }

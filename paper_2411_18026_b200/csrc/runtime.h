@@ -210,6 +210,7 @@ class Staging {
     cudaEvent_t ev = nullptr;  // the kernels reading the slot are done
     cudaEvent_t up = nullptr;  // the slot's upload is done
     bool pending = false;
+    bool uploading = false;    // `up` recorded since the last host rewrite
   };
   std::vector<Slot> s_;
   int cur_ = -1;
