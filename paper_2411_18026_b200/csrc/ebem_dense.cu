@@ -325,19 +325,41 @@ k_interp(const InterpTask* __restrict__ tasks) {
   // R11 (k x k upper triangle) staged in shared memory once per task, so
   // the back substitutions' dependent steps read ~30-cycle shared memory,
   // not L2; then one warp per column j >= k of R12, lanes over rows
-  extern __shared__ double2 col[];  // R11 [k][k] | kWarps * k
+  extern __shared__ double2 col[];  // R11 [k][k] | Smith terms [k] | kWarps * k | branch [k]
   double2* Rs = col;
-  double2* x = col + (size_t)k * k + w * k;
+  double2* sd = col + (size_t)k * k;  // (ratio, denominator) of zdiv by R_rr
+  double2* x = col + (size_t)k * k + k + w * k;
+  int* br = reinterpret_cast<int*>(col + (size_t)k * k + k + kWarps * k);
   for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
     const int c = idx / k, r = idx - c * k;
     Rs[idx] = r <= c ? R[(size_t)c * T.r_ld + r] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  // the divisor-only half of Smith's algorithm (zdiv), once per diagonal
+  // entry, so each substitution step keeps two independent divisions
+  for (int r = threadIdx.x; r < k; r += blockDim.x) {
+    const double2 b = Rs[(size_t)r * k + r];
+    br[r] = fabs(b.x) >= fabs(b.y);
+    if (br[r]) {
+      const double q = b.y / b.x;
+      sd[r] = make_double2(q, b.x + b.y * q);
+    } else {
+      const double q = b.x / b.y;
+      sd[r] = make_double2(q, b.y + b.x * q);
+    }
   }
   __syncthreads();
   for (int j = k + w; j < n; j += kWarps) {
     for (int r = l; r < k; r += 32) x[r] = R[(size_t)j * T.r_ld + r];
     __syncwarp();
     for (int r = k - 1; r >= 0; --r) {
-      if (l == 0) x[r] = zdiv(x[r], Rs[(size_t)r * k + r]);
+      if (l == 0) {  // x[r] / R_rr, Smith's algorithm (as zdiv)
+        const double2 a = x[r], q = sd[r];
+        if (br[r])
+          x[r] = make_double2((a.x + a.y * q.x) / q.y, (a.y - a.x * q.x) / q.y);
+        else
+          x[r] = make_double2((a.x * q.x + a.y) / q.y, (a.y * q.x - a.x) / q.y);
+      }
       __syncwarp();
       const double2 xr = x[r];
       for (int q = l; q < r; q += 32) x[q] = zfms(x[q], Rs[(size_t)r * k + q], xr);
@@ -1626,7 +1648,8 @@ void launch_cpqr(const CpqrTask* tasks, int n, size_t smem, double2* gws,
 void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st) {
   if (n <= 0) return;
   const int kk = max_k > 0 ? max_k : 1;
-  const size_t smem = (size_t(kk) * kk + size_t(kWarps) * kk) * sizeof(double2);
+  const size_t smem = (size_t(kk) * kk + kk + size_t(kWarps) * kk) * sizeof(double2) +
+                      size_t(kk) * sizeof(int);
   static bool attr = [] {
     cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap);
     return true;
