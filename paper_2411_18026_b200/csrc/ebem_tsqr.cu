@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "ebem_dense.h"
@@ -277,17 +278,251 @@ k_tsqr(const QrTask* __restrict__ tasks) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-private TSQR (variants 3 and 4): one warp per row piece, lane = column.
+//
+// The wavefront kernel above couples the warps of a CTA through the reflector
+// ring, so its chain (one hand-off per reflector per row block) sets the
+// time.  Here every warp streams its own piece into its own R and nothing
+// crosses warps: lane l owns column l (variant 3, n <= 32; rows in blocks of
+// 32) or columns l and n - 32 + l ... see col_of (variant 4, n <= 64; blocks
+// of 16 rows), the block's rows of its columns live in the lane's registers
+// and R (packed upper triangle, row-major, so R(i, .) of consecutive lanes is
+// contiguous) lives in the warp's slice of shared memory.  Column c of R is
+// only ever touched by the lane that owns column c, so the only exchange is
+// the reflector itself: the owner of column i writes v and tau into a
+// double-buffered warp slot, one __syncwarp, every lane reads it as a
+// broadcast.  Same zlarfg / zlarf arithmetic as make_reflector / k_tsqr:
+//   x = [R_ii; B(:, i)], beta = -sign(Re R_ii) ||x||, tau = (beta - R_ii) / beta,
+//   v = B(:, i) / (R_ii - beta);  s = R_ij + v^H B(:, j), f = conj(tau) s,
+//   R_ij -= f, B(:, j) -= v f.
+// Latency is hidden across warps (10-12 independent chains per SM) instead
+// of inside one chain; the pieces' R factors are stacked and reduced again
+// by the next round of reduce_tall.
+template <int SLOTS>
+struct LaneCfg;
+template <>
+struct LaneCfg<1> {
+  static constexpr int kBr = 16, kWpc = 4, kMinB = 3;
+};
+template <>
+struct LaneCfg<2> {
+  static constexpr int kBr = 16, kWpc = 2, kMinB = 4;
+};
+
+__device__ __forceinline__ int roff(int i, int n) { return i * n - ((i * (i - 1)) >> 1); }
+
+template <int BR>
+__device__ __forceinline__ void lane_reflector(double2 (&B)[BR], double2* Rs, int i, int n,
+                                               double2* vb, double2* tb) {
+  double p[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < BR; ++k) p[k & 3] = fma(B[k].x, B[k].x, fma(B[k].y, B[k].y, p[k & 3]));
+  const double xnorm2 = (p[0] + p[1]) + (p[2] + p[3]);
+  double2 alpha = Rs[roff(i, n)];
+  double2 tau = make_double2(0.0, 0.0);
+  if (!(xnorm2 == 0.0 && alpha.y == 0.0)) {
+    double x2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, xnorm2));
+    // Stacked R factors drive later columns through cascades of rounding
+    // residues whose squares leave the normal range; the approximate rsqrt
+    // flushes those, so such columns are scaled by 2^600 first (exact).
+    double sc = 1.0;
+    if (x2 < 0x1p-960) {
+      sc = 0x1p600;
+      double q[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < BR; ++k) {
+        const double bx = B[k].x * sc, by = B[k].y * sc;
+        q[k & 3] = fma(bx, bx, fma(by, by, q[k & 3]));
+      }
+      alpha = make_double2(alpha.x * sc, alpha.y * sc);
+      x2 = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, (q[0] + q[1]) + (q[2] + q[3])));
+    }
+    // rsqrt and the reciprocal below by the hardware approximations and
+    // Newton steps (x2 normal, den in [1, 2]): the library versions carry
+    // slow-path calls that spill the lane's block registers
+    double s;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(s) : "d"(x2));
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+      const double e = fma(-x2 * s, s, 1.0);
+      s = fma(0.5 * s, e, s);
+    }
+    const double nrm = x2 * s;
+    const bool pos = alpha.x >= 0.0;
+    const double beta = pos ? -nrm : nrm;
+    const double ib = pos ? -s : s;
+    tau = make_double2((beta - alpha.x) * ib, -alpha.y * ib);
+    const double arn = fma(alpha.x, s, pos ? 1.0 : -1.0);
+    const double ain = alpha.y * s;
+    const double den = fma(arn, arn, ain * ain);
+    double rc;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+      const double e = fma(-den, rc, 1.0);
+      rc = fma(rc, e, rc);
+    }
+    const double id = s * rc * sc;
+    const double2 scal = make_double2(arn * id, -ain * id);
+#pragma unroll
+    for (int k = 0; k < BR; ++k)
+      vb[k] = make_double2(scal.x * B[k].x - scal.y * B[k].y, scal.x * B[k].y + scal.y * B[k].x);
+    Rs[roff(i, n)] = make_double2(beta * (1.0 / sc), 0.0);
+  } else {
+#pragma unroll
+    for (int k = 0; k < BR; ++k) vb[k] = B[k];
+  }
+  *tb = tau;
+}
+
+// s = R_ij + v^H B(:, j) for one column slot, then R_ij -= f, B -= v f
+// (dots of both slots first so their chains overlap; see k_tsqr_lane)
+template <int BR>
+__device__ __forceinline__ void lane_update(double2 (&B)[BR], const double2* v, double2 tau,
+                                            double sr, double si, double2* rij) {
+  const double2 r = *rij;
+  sr += r.x;
+  si += r.y;
+  const double fr = tau.x * sr + tau.y * si;
+  const double fi = tau.x * si - tau.y * sr;
+#pragma unroll
+  for (int k = 0; k < BR; ++k) {
+    const double2 a = v[k];
+    B[k].x = fma(-a.x, fr, fma(a.y, fi, B[k].x));
+    B[k].y = fma(-a.x, fi, fma(-a.y, fr, B[k].y));
+  }
+  *rij = make_double2(r.x - fr, r.y - fi);
+}
+
+template <int BR>
+__device__ __forceinline__ void lane_dot(const double2 (&B)[BR], const double2* v, double& sr,
+                                         double& si) {
+  double ar[2] = {0.0, 0.0}, ai[2] = {0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < BR; ++k) {
+    const double2 a = v[k], bb = B[k];
+    ar[k & 1] = fma(a.x, bb.x, fma(a.y, bb.y, ar[k & 1]));
+    ai[k & 1] = fma(a.x, bb.y, fma(-a.y, bb.x, ai[k & 1]));
+  }
+  sr = ar[0] + ar[1];
+  si = ai[0] + ai[1];
+}
+
+template <int SLOTS>
+__global__ void __launch_bounds__(LaneCfg<SLOTS>::kWpc * 32, LaneCfg<SLOTS>::kMinB)
+k_tsqr_lane(const QrTask* __restrict__ tasks, int n_tasks, int wstride) {
+  constexpr int BR = LaneCfg<SLOTS>::kBr;
+  extern __shared__ double2 sm_lane[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = blockIdx.x * LaneCfg<SLOTS>::kWpc + warp;
+  if (task >= n_tasks) return;  // warps are independent: no CTA barrier below
+  const QrTask T = tasks[task];
+  const int n = T.n, rows = T.rows, ld = T.ld;
+  const int nr = (n * (n + 1)) >> 1;
+  double2* Rs = sm_lane + size_t(warp) * wstride;
+  double2* vbuf = Rs + nr;  // 2 x BR
+  double2* tbuf = vbuf + 2 * BR;
+  // slot 0: column n2 + lane; slot 1 (variant 4): column lane < n2.  The low
+  // columns sit in slot 1 so that slot retires after n2 reflectors.
+  const int n2 = SLOTS == 2 ? n - 32 : 0;
+  const int c0 = n2 + lane;
+  const bool v0 = c0 < n;
+  const bool v1 = SLOTS == 2 && lane < n2;
+  for (int q = lane; q < nr; q += 32) Rs[q] = make_double2(0.0, 0.0);
+  __syncwarp();
+  const double2* src = reinterpret_cast<const double2*>(T.src);
+  const double2* s0 = src + size_t(v0 ? c0 : 0) * ld;
+  const double2* s1 = src + size_t(v1 ? lane : 0) * ld;
+  for (int r0 = 0; r0 < rows; r0 += BR) {
+    double2 B0[BR], B1[BR];  // B1 unused (eliminated) for SLOTS == 1
+#pragma unroll
+    for (int k = 0; k < BR; ++k) {
+      const int r = r0 + k;
+      B0[k] = (v0 && r < rows) ? __ldg(s0 + r) : make_double2(0.0, 0.0);
+      B1[k] = (SLOTS == 2 && v1 && r < rows) ? __ldg(s1 + r) : make_double2(0.0, 0.0);
+    }
+    if (r0 + BR < rows) {  // warm L2 for the next block of this lane's columns
+      if (v0) asm volatile("prefetch.global.L2 [%0];" ::"l"(s0 + r0 + BR));
+      if (SLOTS == 2 && v1) asm volatile("prefetch.global.L2 [%0];" ::"l"(s1 + r0 + BR));
+    }
+    for (int i = 0; i < n; ++i) {
+      double2* vb = vbuf + (i & 1) * BR;
+      double2* tb = tbuf + (i & 1);
+      if constexpr (SLOTS == 2) {
+        if (i < n2) {
+          if (lane == i) lane_reflector<BR>(B1, Rs, i, n, vb, tb);
+        } else if (lane == i - n2) {
+          lane_reflector<BR>(B0, Rs, i, n, vb, tb);
+        }
+      } else {
+        if (lane == i) lane_reflector<BR>(B0, Rs, i, n, vb, tb);
+      }
+      __syncwarp();
+      if (i + 1 >= n) break;
+      const double2 tau = *tb;
+      const int ro = roff(i, n) - i;  // R(i, c) = Rs[ro + c]
+      if constexpr (SLOTS == 2) {
+        if (i + 1 < n2) {  // both slots have columns right of i (every slot-0 column)
+          double sr0, si0, sr1, si1;
+          lane_dot<BR>(B0, vb, sr0, si0);
+          lane_dot<BR>(B1, vb, sr1, si1);
+          if (v0) lane_update<BR>(B0, vb, tau, sr0, si0, Rs + ro + c0);
+          if (v1 && lane > i) lane_update<BR>(B1, vb, tau, sr1, si1, Rs + ro + lane);
+          continue;
+        }
+      }
+      double sr0, si0;
+      lane_dot<BR>(B0, vb, sr0, si0);
+      if (v0 && c0 > i) lane_update<BR>(B0, vb, tau, sr0, si0, Rs + ro + c0);
+    }
+  }
+  // R (n x n, column-major, zeros below the diagonal); each lane its columns
+  double2* out = reinterpret_cast<double2*>(T.dst);
+  if (v0)
+    for (int r = 0; r < n; ++r)
+      out[size_t(c0) * T.dst_ld + r] = r <= c0 ? Rs[roff(r, n) + c0 - r] : make_double2(0.0, 0.0);
+  if (SLOTS == 2 && v1)
+    for (int r = 0; r < n; ++r)
+      out[size_t(lane) * T.dst_ld + r] = r <= lane ? Rs[roff(r, n) + lane - r] : make_double2(0.0, 0.0);
+}
+
 }  // namespace
+
+static bool lane_tsqr_enabled() {  // EBEM_TSQR_LANE=0: the wavefront kernel (A/B)
+  static const bool on = [] {
+    const char* e = std::getenv("EBEM_TSQR_LANE");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+static int lane_wstride(int n, int slots) {
+  const int br = slots == 1 ? LaneCfg<1>::kBr : LaneCfg<2>::kBr;
+  return (n * (n + 1)) / 2 + 2 * br + 2;
+}
 
 // variant 2: n <= 32 (the leaf blocks), 128 threads, so more independent
 // reflector chains share an SM
 constexpr int kTinyThreads = 128;
 static int tsqr_slots(int n) { return n <= 64 ? EBEM_TSQR_S_SLOTS : EBEM_TSQR_M_SLOTS; }
-int tsqr_variant(int n) { return n <= 32 ? 2 : n <= 64 ? 0 : n <= kTsqrMaxCols ? 1 : -1; }
+int tsqr_variant(int n) {
+  if (lane_tsqr_enabled() && n <= 64) return n <= 32 ? 3 : 4;
+  return n <= 32 ? 2 : n <= 64 ? 0 : n <= kTsqrMaxCols ? 1 : -1;
+}
 int tsqr_block_rows(int n) {
+  if (tsqr_variant(n) == 3) return LaneCfg<1>::kBr;
+  if (tsqr_variant(n) == 4) return LaneCfg<2>::kBr;
   return tsqr_variant(n) == 1 ? EBEM_TSQR_M_LANES * kRpt : EBEM_TSQR_S_LANES * kRpt;
 }
 int tsqr_ctas_per_sm(int n) {
+  if (tsqr_variant(n) >= 3) {  // resident warps (= tasks) per SM
+    const int slots = tsqr_variant(n) == 3 ? 1 : 2;
+    const int wpc = slots == 1 ? LaneCfg<1>::kWpc : LaneCfg<2>::kWpc;
+    const int minb = slots == 1 ? LaneCfg<1>::kMinB : LaneCfg<2>::kMinB;
+    const int by_smem = int((227 * 1024) / (tsqr_smem_bytes(n) + 1024));
+    return wpc * std::max(1, std::min(minb, by_smem));
+  }
   const bool small = tsqr_variant(n) != 1;
   const int t = tsqr_variant(n) == 2 ? kTinyThreads : small ? EBEM_TSQR_S_THREADS : EBEM_TSQR_M_THREADS;
   const int by_regs = std::max(1, 65536 / (t * (small ? EBEM_TSQR_REGS : EBEM_TSQR_M_REGS)));
@@ -295,6 +530,11 @@ int tsqr_ctas_per_sm(int n) {
   return std::min(std::min(by_regs, by_smem), 2048 / t);
 }
 size_t tsqr_smem_bytes(int n) {
+  if (tsqr_variant(n) >= 3) {
+    const int slots = tsqr_variant(n) == 3 ? 1 : 2;
+    const int wpc = slots == 1 ? LaneCfg<1>::kWpc : LaneCfg<2>::kWpc;
+    return sizeof(double2) * size_t(wpc) * lane_wstride(n, slots);
+  }
   return sizeof(double2) *
          (size_t(n) * (n + 1) / 2 + size_t(tsqr_slots(n)) * (tsqr_block_rows(n) + 1));
 }
@@ -312,6 +552,24 @@ static void launch_variant(const QrTask* tasks, int n_tasks, size_t smem, cudaSt
 void launch_tsqr(const QrTask* tasks, int n_tasks, int variant, size_t smem,
                  cudaStream_t st) {
   if (n_tasks <= 0) return;
+  if (variant == 3 || variant == 4) {
+    // smem was sized for the launch's largest n: recover that n's stride
+    const int slots = variant == 3 ? 1 : 2;
+    const int wpc = slots == 1 ? LaneCfg<1>::kWpc : LaneCfg<2>::kWpc;
+    const int wstride = int(smem / (sizeof(double2) * wpc));
+    const int grid = (n_tasks + wpc - 1) / wpc;
+    static bool once = [] {
+      cudaFuncSetAttribute(k_tsqr_lane<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_tsqr_lane<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      return true;
+    }();
+    (void)once;
+    if (slots == 1)
+      k_tsqr_lane<1><<<grid, wpc * 32, smem, st>>>(tasks, n_tasks, wstride);
+    else
+      k_tsqr_lane<2><<<grid, wpc * 32, smem, st>>>(tasks, n_tasks, wstride);
+    return;
+  }
   if (variant == 2)
     launch_variant<EBEM_TSQR_S_LANES, kTinyThreads, EBEM_TSQR_S_SLOTS, EBEM_TSQR_REGS>(tasks, n_tasks, smem, st);
   else if (variant == 0)

@@ -1529,7 +1529,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
   }();
   size_t round = 0;
   for (;;) {
-    std::vector<QrTask> tasks, stream16, stream8, stream4;
+    std::vector<QrTask> tasks, streamv[5];
     std::vector<size_t> out_off(q.size(), 0);
     size_t out_total = 0, ws_total = 0;
     std::vector<int> pieces(q.size(), 0);
@@ -1582,7 +1582,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     qr_rounds_[round].ensure(2 * out_total);
     double* ob = qr_rounds_[round].get();
     ++round;
-    size_t smem16 = 0, smem8 = 0, smem4 = 0;
+    size_t smemv[5] = {0, 0, 0, 0, 0};
     for (size_t i = 0; i < q.size(); ++i) {
       if (!pieces[i]) continue;
       const TallBlock& x = q[i];
@@ -1599,16 +1599,9 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
         t.ld = x.ld;
         t.dst_ld = ld_out;
         if (streamed[i]) {
-          if (tsqr_variant(x.n) == 2) {
-            stream4.push_back(t);
-            smem4 = std::max(smem4, tsqr_smem_bytes(x.n));
-          } else if (tsqr_variant(x.n) == 0) {
-            stream16.push_back(t);
-            smem16 = std::max(smem16, tsqr_smem_bytes(x.n));
-          } else {
-            stream8.push_back(t);
-            smem8 = std::max(smem8, tsqr_smem_bytes(x.n));
-          }
+          const int v = tsqr_variant(x.n);
+          streamv[v].push_back(t);
+          smemv[v] = std::max(smemv[v], tsqr_smem_bytes(x.n));
           continue;
         }
         t.in_smem = size_t(rr) * x.n * 16 <= size_t(kSmemCap);
@@ -1620,16 +1613,15 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     gws.ensure(ws_total + 1);
     Pack pk;
     const size_t o = pk.add(tasks);
-    const size_t o16 = pk.add(stream16);
-    const size_t o8 = pk.add(stream8);
-    const size_t o4 = pk.add(stream4);
+    size_t ov[5];
+    for (int v = 0; v < 5; ++v) ov[v] = pk.add(streamv[v]);
     char* tb = staging.put(pk, st);
     size_t smem = 0;
     for (const QrTask& t : tasks)
       if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
     double fl = 0.0;
     double by = 0.0;  // the block read once, its reduced rows written once
-    for (const auto* v : {&tasks, &stream16, &stream8, &stream4})
+    for (const auto* v : {&tasks, &streamv[0], &streamv[1], &streamv[2], &streamv[3], &streamv[4]})
       for (const QrTask& t : *v) {
         const double mm = t.rows, nn = std::min(t.rows, t.n);
         // complex Householder QR with k = min(m, n) reflectors:
@@ -1640,9 +1632,8 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     g_prof.begin(st);
     // (the team-layout k_qr_team measured slower on these shapes: 485 vs 404 ms)
     launch_qr_reduce(Pack::at<QrTask>(tb, o), int(tasks.size()), smem, gws.get(), st);
-    launch_tsqr(Pack::at<QrTask>(tb, o16), int(stream16.size()), 0, smem16, st);
-    launch_tsqr(Pack::at<QrTask>(tb, o8), int(stream8.size()), 1, smem8, st);
-    launch_tsqr(Pack::at<QrTask>(tb, o4), int(stream4.size()), 2, smem4, st);
+    for (int v = 0; v < 5; ++v)
+      launch_tsqr(Pack::at<QrTask>(tb, ov[v]), int(streamv[v].size()), v, smemv[v], st);
     g_prof.end(KP_QR, st, fl, by);
     CK(cudaGetLastError());
     staging.fence(st);
