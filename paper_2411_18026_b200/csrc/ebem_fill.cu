@@ -1097,7 +1097,42 @@ k_gather(const GatherJob* __restrict__ jobs, const int* __restrict__ job_block_o
   else D[cd.dest * (long long)J.ld + rd.dest] = make_double2(re, im);
 }
 
+// ------------------------------------------------------------ cross-level reuse
+// One warp per (task, column): the column's listed enclosed rows, both
+// components, from the child's matrix to the cell's.  Row pairs are runs of
+// consecutive positions in both matrices, so the lanes read and write
+// consecutive addresses.
+__global__ void __launch_bounds__(32 * kReuseCols)
+k_reuse_copy(const ReuseTask* __restrict__ tasks, const int* __restrict__ task_block_off,
+             int n_tasks, const int2* __restrict__ row_pairs,
+             const int2* __restrict__ col_pairs) {
+  __shared__ int s_t;
+  if (threadIdx.x == 0) s_t = find_job(task_block_off, n_tasks, int(blockIdx.x));
+  __syncthreads();
+  const ReuseTask T = tasks[s_t];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = (int(blockIdx.x) - __ldg(task_block_off + s_t)) * kReuseCols + warp;
+  if (c >= T.n_cols) return;
+  const int2 cp = __ldg(col_pairs + T.col_off + c);
+  const double2* src = reinterpret_cast<const double2*>(T.src) + (long long)cp.x * T.src_ld;
+  double2* dst = reinterpret_cast<double2*>(T.dst) + (long long)cp.y * T.dst_ld;
+  const int2* rp = row_pairs + T.row_off;
+  for (int r = lane; r < T.n_rows; r += 32) {
+    const int2 q = __ldg(rp + r);
+    dst[T.dst_row0 + q.y] = __ldg(src + T.src_row0 + q.x);
+    dst[T.dst_row0 + T.dst_ne + q.y] = __ldg(src + T.src_row0 + T.src_ne + q.x);
+  }
+}
+
 // ------------------------------------------------------------ host wrappers
+
+void launch_reuse_copy(const ReuseTask* tasks, const int* task_block_off, int n_tasks,
+                       int n_blocks, const int2* row_pairs, const int2* col_pairs,
+                       cudaStream_t st) {
+  if (n_blocks <= 0) return;
+  k_reuse_copy<<<n_blocks, 32 * kReuseCols, 0, st>>>(tasks, task_block_off, n_tasks, row_pairs,
+                                                     col_pairs);
+}
 
 
 // Thread-per-pair proxy body (near_body_pp); EBEM_FILL_PP=0 selects the

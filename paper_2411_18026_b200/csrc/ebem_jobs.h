@@ -74,4 +74,19 @@ struct GatherJob {
   double* dest;  // interleaved complex, column-major
 };
 
+// Entries of a cell's interaction matrix that its child already holds: for
+// every listed (child column, cell column) and (child enclosed position,
+// cell enclosed position) pair, both displacement components of the enclosed
+// node are copied from the child's matrix (previous level) into the cell's.
+struct ReuseTask {
+  const double* src;  // child matrix, interleaved complex, column-major
+  double* dst;        // cell matrix
+  int src_ld, dst_ld;
+  int src_row0, src_ne;  // enclosed rows of component p start at row0 + p * ne
+  int dst_row0, dst_ne;
+  int n_rows, n_cols;    // listed pairs
+  long long row_off;     // first (child, cell) enclosed position pair
+  long long col_off;     // first (child, cell) column pair
+};
+
 }  // namespace ebem_gpu

@@ -41,6 +41,12 @@ constexpr int kGatherTile = 256;  // output entries per gather CTA
 void launch_gather(const GatherJob* jobs, const int* job_block_off, int n_jobs,
                    int n_blocks, const NodeDesc* desc, const double* bundles,
                    long long nb, cudaStream_t st);
+// Cross-level reuse: copies the listed entries of the children's interaction
+// matrices into the cells' (kReuseCols columns per CTA, one warp each).
+constexpr int kReuseCols = 4;
+void launch_reuse_copy(const ReuseTask* tasks, const int* task_block_off, int n_tasks,
+                       int n_blocks, const int2* row_pairs, const int2* col_pairs,
+                       cudaStream_t st);
 
 // ---- incident-field right-hand sides (ebem_rhs.cu)
 // Post-processing (proj/src/postprocess.cpp): distance of m points to the

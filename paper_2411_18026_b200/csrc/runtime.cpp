@@ -80,7 +80,7 @@ const char* kernel_name(int id) {
   static const char* names[KP_COUNT] = {
       "k_proxy_pairs", "k_near_onesided", "k_near_singular", "k_gather",
       "k_qr_reduce", "k_cpqr", "k_interp", "k_getrf", "k_getrs", "k_gemm",
-      "k_copy", "k_rhs_plane", "k_near_sym", "k_sym_bucket"};
+      "k_copy", "k_rhs_plane", "k_near_sym", "k_sym_bucket", "k_reuse_copy"};
   return (id >= 0 && id < KP_COUNT) ? names[id] : "?";
 }
 
@@ -987,8 +987,8 @@ void FillPlan::elements_of(const Lists& nodes, std::vector<int>& out) const {
 }
 
 void FillPlan::node_descs(const Lists& nodes, const std::vector<int>& elems,
-                          const int dest_off[2],
-                          std::vector<NodeDesc>& out) const {
+                          const int dest_off[2], std::vector<NodeDesc>& out,
+                          const std::vector<int>* pos) const {
   auto idx = [&](int e) {
     return int(std::lower_bound(elems.begin(), elems.end(), e) - elems.begin());
   };
@@ -1000,7 +1000,7 @@ void FillPlan::node_descs(const Lists& nodes, const std::vector<int>& elems,
     for (size_t k = 0; k < v.size(); ++k) {
       const int g = v[k];
       NodeDesc d;
-      d.dest = dest_off[p] + int(k);
+      d.dest = dest_off[p] + (pos ? (*pos)[k] : int(k));
       int la1, la2;
       if (g == 0) {  // elements 0 (shape 0) and N-1 (shape 1)
         d.e1 = idx(0);
@@ -1092,7 +1092,20 @@ void FillPlan::add_true_block(const Lists& rows, const Lists& cols,
 void FillPlan::add_sym_near(const std::vector<int>& enc, const Lists& rows,
                             const Lists& cols, double* tv, int ld_v, double* tu,
                             int ld_u) {
+  const int rdest[2] = {0, int(rows[0].size())};
+  const int cdest[2] = {0, int(cols[0].size())};
+  add_sym_near_part(enc, nullptr, int(enc.size()), rows, rdest, cols, cdest, tv, ld_v, tu,
+                    ld_u);
+}
+
+void FillPlan::add_sym_near_part(const std::vector<int>& enc, const std::vector<int>* enc_pos,
+                                 int ne_total, const Lists& rows, const int rdest[2],
+                                 const Lists& cols, const int cdest[2], double* tv,
+                                 int ld_v, double* tu, int ld_u) {
   if (enc.empty()) return;
+  const int nr = int(rows[0].size() + rows[1].size());
+  const int nc = int(cols[0].size() + cols[1].size());
+  if (nr == 0 && nc == 0) return;
   const Lists encl{enc, enc};
   std::vector<int> A, E;
   elements_of(encl, A);
@@ -1138,20 +1151,17 @@ void FillPlan::add_sym_near(const std::vector<int>& enc, const Lists& rows,
     }
   }
   const int ne = int(enc.size());
-  const int nr = int(rows[0].size() + rows[1].size());
-  const int nc = int(cols[0].size() + cols[1].size());
+  const int denc[2] = {2 * m_, 2 * m_ + ne_total};  // enclosed rows per component
   if (nc > 0) {  // T_V rows 2m'.. : true_block(enc x 2, cols)
     GatherJob G;
     G.pair_off = J.v_off;
     G.entry_off = entries_;
     G.nces = J.nE;
     G.rdesc_off = int(desc_.size());
-    const int drow[2] = {2 * m_, 2 * m_ + ne};
-    node_descs(encl, A, drow, desc_);
+    node_descs(encl, A, denc, desc_, enc_pos);
     G.nrows = 2 * ne;
     G.cdesc_off = int(desc_.size());
-    const int dcol[2] = {0, int(cols[0].size())};
-    node_descs(cols, E, dcol, desc_);
+    node_descs(cols, E, cdest, desc_);
     G.ncols = nc;
     G.trans = 0;
     G.ld = ld_v;
@@ -1166,12 +1176,10 @@ void FillPlan::add_sym_near(const std::vector<int>& enc, const Lists& rows,
     G.entry_off = entries_;
     G.nces = J.nA;
     G.rdesc_off = int(desc_.size());
-    const int drow[2] = {0, int(rows[0].size())};
-    node_descs(rows, E, drow, desc_);
+    node_descs(rows, E, rdest, desc_);
     G.nrows = nr;
     G.cdesc_off = int(desc_.size());
-    const int dcol[2] = {2 * m_, 2 * m_ + ne};
-    node_descs(encl, A, dcol, desc_);
+    node_descs(encl, A, denc, desc_, enc_pos);
     G.ncols = 2 * ne;
     G.trans = 1;
     G.ld = ld_u;
@@ -1433,11 +1441,55 @@ void Problem::execute(FillPlan& plan) {
   plan.clear();
 }
 
+namespace {
+
+// Common nodes of a cell's enclosed list P and its child's C, as (position in
+// C, position in P) pairs in P order, and the positions of P not in C.
+void intersect_enclosed(const std::vector<int>& P, const std::vector<int>& C,
+                        std::vector<int2>& common, std::vector<int>& rest) {
+  common.clear();
+  rest.clear();
+  if (std::is_sorted(P.begin(), P.end()) && std::is_sorted(C.begin(), C.end())) {
+    size_t j = 0;
+    for (size_t i = 0; i < P.size(); ++i) {
+      while (j < C.size() && C[j] < P[i]) ++j;
+      if (j < C.size() && C[j] == P[i]) common.push_back(make_int2(int(j), int(i)));
+      else rest.push_back(int(i));
+    }
+    return;
+  }
+  std::vector<std::pair<int, int>> idx(C.size());
+  for (size_t j = 0; j < C.size(); ++j) idx[j] = {C[j], int(j)};
+  std::sort(idx.begin(), idx.end());
+  for (size_t i = 0; i < P.size(); ++i) {
+    auto it = std::lower_bound(idx.begin(), idx.end(), std::make_pair(P[i], -1));
+    if (it != idx.end() && it->first == P[i]) common.push_back(make_int2(it->second, int(i)));
+    else rest.push_back(int(i));
+  }
+}
+
+// Reuse copies planned by one planning thread (offsets local to the part).
+struct ReusePart {
+  std::vector<ReuseTask> tasks;
+  std::vector<int2> rows, cols;
+  long long entries = 0;
+};
+
+bool reuse_enabled() {  // EBEM_REUSE=0: every level computes all its entries (A/B)
+  static const bool on = [] {
+    const char* e = std::getenv("EBEM_REUSE");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+}  // namespace
+
 void Problem::interaction(const std::vector<BasisReq>& req,
                           std::vector<ProxyGeom>& geom,
                           std::vector<size_t>& tv_off,
                           std::vector<size_t>& tu_off, std::vector<int>& n_out,
-                          DBuf<double>& tbuf) {
+                          DBuf<double>& tbuf, const PrevLevel* prev) {
   const int m = pcfg_.m_prime;
   const size_t nc_ = req.size();
   geom.resize(nc_);
@@ -1462,12 +1514,105 @@ void Problem::interaction(const std::vector<BasisReq>& req,
     PhaseTimer t_alloc("alloc_tbuf", nullptr);
     tbuf.ensure(2 * run + 2);
   }
+  if (prev && !(prev->valid && reuse_enabled())) prev = nullptr;
+  const double* pbase = nullptr;
+  if (prev) pbase = (prev->buf ? scratch().tbuf_alt : scratch().tbuf).get();
   // Cells are planned in contiguous chunks on the planning threads and the
   // chunk plans appended in cell order: the same jobs, offsets and gather
   // order as a serial pass.
   double* base = tbuf.get();
   const int nchunk = int(std::min<size_t>(nc_, size_t(4 * planning_threads())));
   std::vector<FillPlan> parts(nchunk, FillPlan(n_, m, pcfg_.n_gauss));
+  std::vector<ReusePart> rparts(nchunk);
+  // Cross-level reuse (chained calls): the entry (enclosed node b, skeleton a
+  // of child ch) of this cell's near blocks is the entry (b, a) of the
+  // child's, whenever b was enclosed by the child's proxy circle too -- the
+  // same element-pair bundles summed in the same order.  Those entries are
+  // copied from the child's matrices (previous level, other buffer); the
+  // near-field fill of the cell covers the remaining enclosed nodes only,
+  // one job per child.
+  auto plan_near = [&](FillPlan& fp, ReusePart& rp, size_t c, double* tv, double* tu) {
+    const Lists& rows = *req[c].rows;
+    const Lists& cols = *req[c].cols;
+    const int no = n_out[c];
+    const std::vector<int>& enc = geom[c].enclosed;
+    const int ne = int(enc.size());
+    bool ok = prev != nullptr && ne > 0;
+    int ch[2] = {-1, -1}, kc[2] = {0, 0};
+    for (int x = 0; ok && x < 2; ++x) {
+      ch[x] = req[c].child[x];
+      ok = ch[x] >= 0 && ch[x] < int(prev->geom.size());
+      if (ok) kc[x] = int(prev->spos[ch[x]][0].size());
+    }
+    // the cell's lists must be the children's skeletons, child 0 first
+    for (int a = 0; ok && a < 4; ++a) {
+      const std::vector<int>& L = a < 2 ? cols[a] : rows[a - 2];
+      ok = int(L.size()) == kc[0] + kc[1];
+      for (int x = 0; ok && x < 2; ++x) {
+        const std::vector<int>& sn = prev->snode[ch[x]][a];
+        ok = int(sn.size()) == kc[x] &&
+             std::equal(sn.begin(), sn.end(), L.begin() + (x ? kc[0] : 0));
+      }
+    }
+    std::vector<int2> common[2];
+    std::vector<int> rest[2];
+    if (ok) {
+      for (int x = 0; x < 2; ++x)
+        intersect_enclosed(enc, prev->geom[ch[x]].enclosed, common[x], rest[x]);
+      ok = !common[0].empty() || !common[1].empty();
+    }
+    if (!ok) {
+      fp.add_sym_near(enc, rows, cols, tv, no, tu, no);
+      return;
+    }
+    const int nc0 = int(cols[0].size()), nr0 = int(rows[0].size());
+    for (int x = 0; x < 2; ++x) {
+      const int j0 = x ? kc[0] : 0, k = kc[x];
+      if (k == 0) continue;
+      Lists rs, cs;
+      for (int p = 0; p < 2; ++p) {
+        rs[p].assign(rows[p].begin() + j0, rows[p].begin() + j0 + k);
+        cs[p].assign(cols[p].begin() + j0, cols[p].begin() + j0 + k);
+      }
+      const int rdest[2] = {j0, nr0 + j0}, cdest[2] = {j0, nc0 + j0};
+      if (common[x].empty()) {
+        fp.add_sym_near_part(enc, nullptr, ne, rs, rdest, cs, cdest, tv, no, tu, no);
+        continue;
+      }
+      std::vector<int> sub(rest[x].size());
+      for (size_t i = 0; i < sub.size(); ++i) sub[i] = enc[rest[x][i]];
+      fp.add_sym_near_part(sub, &rest[x], ne, rs, rdest, cs, cdest, tv, no, tu, no);
+      // copies: T_V columns from the child's cols skeletons, T_U from rows
+      const int cc = ch[x];
+      const int cne = int(prev->geom[cc].enclosed.size());
+      const long long row_off = (long long)rp.rows.size();
+      rp.rows.insert(rp.rows.end(), common[x].begin(), common[x].end());
+      for (int w = 0; w < 2; ++w) {  // 0: T_V, 1: T_U
+        ReuseTask T{};
+        T.src = pbase + 2 * (w ? prev->tu_off[cc] : prev->tv_off[cc]);
+        T.dst = w ? tu : tv;
+        T.src_ld = prev->n_out[cc];
+        T.dst_ld = no;
+        T.src_row0 = 2 * m;
+        T.src_ne = cne;
+        T.dst_row0 = 2 * m;
+        T.dst_ne = ne;
+        T.n_rows = int(common[x].size());
+        T.n_cols = 2 * k;
+        T.row_off = row_off;
+        T.col_off = (long long)rp.cols.size();
+        const int shalf = w ? prev->nr0[cc] : prev->nc0[cc];
+        const int dhalf = w ? nr0 : nc0;
+        for (int p = 0; p < 2; ++p) {
+          const std::vector<int>& sp = prev->spos[cc][2 * w + p];
+          for (int j = 0; j < k; ++j)
+            rp.cols.push_back(make_int2(p * shalf + sp[j], p * dhalf + j0 + j));
+        }
+        rp.tasks.push_back(T);
+        rp.entries += 2ll * T.n_rows * T.n_cols;
+      }
+    }
+  };
   {
     PhaseTimer t_plan("fill_plan", nullptr);
     parallel_for(nchunk, [&](int k) {
@@ -1480,7 +1625,7 @@ void Problem::interaction(const std::vector<BasisReq>& req,
         const int no = n_out[c];
         parts[k].add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv,
                            no, tu, no);
-        parts[k].add_sym_near(geom[c].enclosed, rows, cols, tv, no, tu, no);
+        plan_near(parts[k], rparts[k], c, tv, tu);
       }
     });
   }
@@ -1502,6 +1647,40 @@ void Problem::interaction(const std::vector<BasisReq>& req,
       k0 = k + 1;
       acc = 0;
     }
+  }
+  // the reuse copies of the level: one launch
+  std::vector<ReuseTask> rtasks;
+  std::vector<int2> rrows, rcols;
+  long long rentries = 0;
+  for (ReusePart& rp : rparts) {
+    for (ReuseTask T : rp.tasks) {
+      T.row_off += (long long)rrows.size();
+      T.col_off += (long long)rcols.size();
+      rtasks.push_back(T);
+    }
+    rrows.insert(rrows.end(), rp.rows.begin(), rp.rows.end());
+    rcols.insert(rcols.end(), rp.cols.begin(), rp.cols.end());
+    rentries += rp.entries;
+  }
+  if (!rtasks.empty()) {
+    std::vector<int> boff(rtasks.size());
+    int nblk = 0;
+    for (size_t i = 0; i < rtasks.size(); ++i) {
+      boff[i] = nblk;
+      nblk += (rtasks[i].n_cols + kReuseCols - 1) / kReuseCols;
+    }
+    Pack pk;
+    const size_t o_t = pk.add(rtasks);
+    const size_t o_b = pk.add(boff);
+    const size_t o_r = pk.add(rrows);
+    const size_t o_c = pk.add(rcols);
+    char* tb = staging.put(pk, st_);
+    g_prof.begin(st_);
+    launch_reuse_copy(Pack::at<ReuseTask>(tb, o_t), Pack::at<int>(tb, o_b), int(rtasks.size()),
+                      nblk, Pack::at<int2>(tb, o_r), Pack::at<int2>(tb, o_c), st_);
+    g_prof.end(KP_REUSE, st_, double(rentries), 32.0 * double(rentries));
+    CK(cudaGetLastError());
+    staging.fence(st_);
   }
 }
 
@@ -1648,17 +1827,21 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
 
 void Problem::bases(const std::vector<BasisReq>& req, double eps,
                     std::vector<BasisRes>& res, DBuf<double>& vbuf,
-                    DBuf<double>& ubuf, double* fill_seconds) {
+                    DBuf<double>& ubuf, double* fill_seconds, bool chain) {
   const size_t ncell = req.size();
   res.assign(ncell, BasisRes{});
   if (ncell == 0) return;
   std::vector<ProxyGeom> geom;
   std::vector<size_t> tv_off, tu_off;
   std::vector<int> n_out;
-  DBuf<double>& tbuf = tbuf_;
+  // chained calls alternate between the two interaction buffers, so the
+  // previous level's matrices outlive this level's fill (cross-level reuse)
+  if (!chain) prev_.valid = false;
+  const int cur_buf = prev_.valid ? 1 - prev_.buf : 0;
+  DBuf<double>& tbuf = cur_buf ? scratch().tbuf_alt : tbuf_;
   const double t0 = now();
   tl_mark("  bases start");
-  interaction(req, geom, tv_off, tu_off, n_out, tbuf);
+  interaction(req, geom, tv_off, tu_off, n_out, tbuf, chain ? &prev_ : nullptr);
   tl_mark("  fill enq");
   if (fill_seconds) {
     CK(cudaStreamSynchronize(st_));
@@ -1806,6 +1989,29 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     v_total += size_t(k) * (cols[0].size() + cols[1].size());
     r.u_off = u_total;
     u_total += size_t(k) * (rows[0].size() + rows[1].size());
+  }
+  if (chain) {  // what the next level's reuse needs of this one
+    prev_.valid = true;
+    prev_.buf = cur_buf;
+    prev_.geom = std::move(geom);
+    prev_.tv_off = tv_off;
+    prev_.tu_off = tu_off;
+    prev_.n_out = n_out;
+    prev_.nc0.resize(ncell);
+    prev_.nr0.resize(ncell);
+    prev_.spos.assign(ncell, {});
+    prev_.snode.assign(ncell, {});
+    for (size_t c = 0; c < ncell; ++c) {
+      prev_.nc0[c] = int((*req[c].cols)[0].size());
+      prev_.nr0[c] = int((*req[c].rows)[0].size());
+      const int k = res[c].k;
+      for (int a = 0; a < 4; ++a) {
+        const int* jp = h_jp + jp_off[4 * c + a];
+        prev_.spos[c][a].assign(jp, jp + k);
+        prev_.snode[c][a] = a == 0 ? res[c].scol[0] : a == 1 ? res[c].scol[1]
+                            : a == 2 ? res[c].srow[0] : res[c].srow[1];
+      }
+    }
   }
   // ---- interpolation coefficients
   vbuf.ensure(2 * v_total + 2);
@@ -2241,6 +2447,7 @@ void Fds::build() {
     C.nloc = leaf;
   }
   double basis_seconds = 0.0;
+  P_.reset_chain();
   const int m = P_.proxy_cfg().m_prime;
   (void)m;
   for (int level = depth_; level > cfg_.ell0; --level) {
@@ -2340,11 +2547,16 @@ void Fds::build() {
     std::vector<BasisReq> req(nlev);
     for (int c = f; c <= L; ++c)
       req[c - f] = BasisReq{&cells_[c].jrow, &cells_[c].jcol, cells_[c].begin, cells_[c].end};
+    if (level < depth_)  // children 2c+1, 2c+2: consecutive cells of the level below
+      for (int i = 0; i < nlev; ++i) {
+        req[i].child[0] = 2 * i;
+        req[i].child[1] = 2 * i + 1;
+      }
     std::vector<BasisRes> br;
     DBuf<double>& ubuf = ubuf_;
     const double tb = now();
     if (hs_) host_bases(level, br, S.v, ubuf);
-    else P_.bases(req, cfg_.epsilon, br, S.v, ubuf);
+    else P_.bases(req, cfg_.epsilon, br, S.v, ubuf, nullptr, true);
     PhaseTimer t_after("level_after_bases", nullptr);
     tl_mark("L" + std::to_string(level) + " bases done");
     basis_seconds += now() - tb;

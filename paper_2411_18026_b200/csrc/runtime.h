@@ -40,7 +40,7 @@ extern std::atomic<long long> g_launches;
 // kernels, bytes or flops for the rest); enabled by ebem_gpu_prof_enable.
 enum KernelId {
   KP_PROXY = 0, KP_NEAR_1S, KP_NEAR_SING, KP_GATHER, KP_QR, KP_CPQR,
-  KP_INTERP, KP_GETRF, KP_GETRS, KP_GEMM, KP_COPY, KP_RHS, KP_NEAR_SYM, KP_BUCKET, KP_COUNT
+  KP_INTERP, KP_GETRF, KP_GETRS, KP_GEMM, KP_COPY, KP_RHS, KP_NEAR_SYM, KP_BUCKET, KP_REUSE, KP_COUNT
 };
 const char* kernel_name(int id);
 
@@ -246,6 +246,24 @@ struct BasisReq {  // one cell_basis call
   const Lists* rows;
   const Lists* cols;
   int begin, end;
+  // Chained level-by-level calls (Fds::build): indices of the cell's two
+  // children in the previous chained call, whose interaction matrices still
+  // hold the entries (enclosed node of both, child skeleton) this cell needs
+  // again; -1: none (leaf cells, single cell_basis calls).
+  int child[2] = {-1, -1};
+};
+
+// What a chained bases() call leaves for the next level: where each cell's
+// interaction matrices are and which of their columns its skeletons were.
+struct PrevLevel {
+  bool valid = false;
+  int buf = 0;  // which of the two interaction buffers holds the matrices
+  std::vector<ProxyGeom> geom;
+  std::vector<size_t> tv_off, tu_off;
+  std::vector<int> n_out, nc0, nr0;
+  // per cell: column positions (within the component's half) and nodes of
+  // the k skeletons of cols[0], cols[1], rows[0], rows[1]
+  std::vector<std::array<std::vector<int>, 4>> spos, snode;
 };
 
 struct BasisRes {
@@ -304,7 +322,7 @@ class Recorder {
 struct Scratch {
   cudaStream_t st = nullptr;
   Staging staging;
-  DBuf<double> tbuf;
+  DBuf<double> tbuf, tbuf_alt;  // interaction matrices (two: level l and l+1)
   std::vector<DBuf<double>> qr_rounds;
   DBuf<int> id_jp, id_steps;
   DBuf<double> id_rd, id_r;
@@ -358,13 +376,15 @@ class Problem {
   // V/U coefficient blocks land in vbuf/ubuf (device), offsets in res.
   void bases(const std::vector<BasisReq>& req, double eps,
              std::vector<BasisRes>& res, DBuf<double>& vbuf,
-             DBuf<double>& ubuf, double* fill_seconds = nullptr);
+             DBuf<double>& ubuf, double* fill_seconds = nullptr, bool chain = false);
+  // Forget the previous chained level (start of a factorization).
+  void reset_chain() { prev_.valid = false; }
   // Interaction matrices (device, column-major) of a batch of cells:
   // T_V = M_V (n_out x ncols) and T_U = M_U^H (n_out x nrows).
   void interaction(const std::vector<BasisReq>& req,
                    std::vector<ProxyGeom>& geom, std::vector<size_t>& tv_off,
                    std::vector<size_t>& tu_off, std::vector<int>& n_out,
-                   DBuf<double>& tbuf);
+                   DBuf<double>& tbuf, const PrevLevel* prev = nullptr);
   void true_block_host(const Lists& rows, const Lists& cols, double* out);
   void rhs_plane(int kind, const double* angles, int m, double amp,
                  double* out_host);
@@ -402,6 +422,7 @@ class Problem {
   DBuf<double> delem_, delem8_, dxy_;
   cudaStream_t st_ = nullptr;
   NodeBoxTree tree_;
+  PrevLevel prev_;
 };
 
 // Work planner for one batch of Galerkin fills.
@@ -423,6 +444,13 @@ class FillPlan {
   void add_sym_near(const std::vector<int>& enc, const Lists& rows,
                     const Lists& cols, double* tv, int ld_v, double* tu,
                     int ld_u);
+  // The same for a part of the cell's blocks: the enclosed nodes enc (row
+  // position enc_pos[k] of the cell's ne_total enclosed nodes) against the
+  // row / column sub-lists, whose first entries sit at rdest / cdest.
+  void add_sym_near_part(const std::vector<int>& enc, const std::vector<int>* enc_pos,
+                         int ne_total, const Lists& rows, const int rdest[2],
+                         const Lists& cols, const int cdest[2], double* tv, int ld_v,
+                         double* tu, int ld_u);
   // true_block(J, J) for an ascending node list J (the leaf diagonal) from
   // the upper triangle of element pairs, both orientations per evaluation.
   void add_sym_diag(const std::vector<int>& nodes, double* dest, int ld);
@@ -441,7 +469,8 @@ class FillPlan {
   friend class Problem;
   void elements_of(const Lists& nodes, std::vector<int>& out) const;
   void node_descs(const Lists& nodes, const std::vector<int>& elems,
-                  const int dest_off[2], std::vector<NodeDesc>& out) const;
+                  const int dest_off[2], std::vector<NodeDesc>& out,
+                  const std::vector<int>* pos = nullptr) const;
   int poly_descs();
   int N_, m_, ng_;
   long long bundles_ = 0;
