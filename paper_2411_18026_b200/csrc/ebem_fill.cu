@@ -1124,7 +1124,37 @@ k_reuse_copy(const ReuseTask* __restrict__ tasks, const int* __restrict__ task_b
   }
 }
 
+// One CTA per task; consecutive threads on consecutive destination rows.
+__global__ void __launch_bounds__(128)
+k_map_copy(const MapTask* __restrict__ tasks, const int2* __restrict__ row_pairs,
+           const int2* __restrict__ col_pairs) {
+  const MapTask T = tasks[blockIdx.x];
+  const double2* src = reinterpret_cast<const double2*>(T.src);
+  double2* dst = reinterpret_cast<double2*>(T.dst);
+  const int2* rp = row_pairs + T.row_off;
+  const int2* cp = col_pairs + T.col_off;
+  const int total = T.n_rows * T.n_cols;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int c = idx / T.n_rows, r = idx - c * T.n_rows;
+    const int2 rr = __ldg(rp + r), cc = __ldg(cp + c);
+    double2 v;
+    if (T.swap) {
+      v = __ldg(src + (long long)rr.x * T.src_ld + cc.x);
+      v.y = -v.y;
+    } else {
+      v = __ldg(src + (long long)cc.x * T.src_ld + rr.x);
+    }
+    dst[(long long)cc.y * T.dst_ld + rr.y] = v;
+  }
+}
+
 // ------------------------------------------------------------ host wrappers
+
+void launch_map_copy(const MapTask* tasks, int n_tasks, const int2* row_pairs,
+                     const int2* col_pairs, cudaStream_t st) {
+  if (n_tasks <= 0) return;
+  k_map_copy<<<n_tasks, 128, 0, st>>>(tasks, row_pairs, col_pairs);
+}
 
 void launch_reuse_copy(const ReuseTask* tasks, const int* task_block_off, int n_tasks,
                        int n_blocks, const int2* row_pairs, const int2* col_pairs,

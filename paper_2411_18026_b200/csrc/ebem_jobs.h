@@ -89,4 +89,16 @@ struct ReuseTask {
   long long col_off;     // first (child, cell) column pair
 };
 
+// Generic entry copy between two column-major complex matrices: entry
+// (row pair r, column pair c) goes to dst(rows[r].y, cols[c].y) from
+// src(rows[r].x, cols[c].x), or, with swap, from conj(src(cols[c].x, rows[r].x)).
+struct MapTask {
+  const double* src;
+  double* dst;
+  int src_ld, dst_ld;
+  int n_rows, n_cols;
+  int swap, pad;
+  long long row_off, col_off;
+};
+
 }  // namespace ebem_gpu

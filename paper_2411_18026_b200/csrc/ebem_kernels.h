@@ -47,6 +47,9 @@ constexpr int kReuseCols = 4;
 void launch_reuse_copy(const ReuseTask* tasks, const int* task_block_off, int n_tasks,
                        int n_blocks, const int2* row_pairs, const int2* col_pairs,
                        cudaStream_t st);
+// Entry copies of the sibling blocks (one CTA per task).
+void launch_map_copy(const MapTask* tasks, int n_tasks, const int2* row_pairs,
+                     const int2* col_pairs, cudaStream_t st);
 
 // ---- incident-field right-hand sides (ebem_rhs.cu)
 // Post-processing (proj/src/postprocess.cpp): distance of m points to the

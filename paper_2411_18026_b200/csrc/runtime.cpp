@@ -988,7 +988,7 @@ void FillPlan::elements_of(const Lists& nodes, std::vector<int>& out) const {
 
 void FillPlan::node_descs(const Lists& nodes, const std::vector<int>& elems,
                           const int dest_off[2], std::vector<NodeDesc>& out,
-                          const std::vector<int>* pos) const {
+                          const std::vector<int>* const* pos) const {
   auto idx = [&](int e) {
     return int(std::lower_bound(elems.begin(), elems.end(), e) - elems.begin());
   };
@@ -1000,7 +1000,7 @@ void FillPlan::node_descs(const Lists& nodes, const std::vector<int>& elems,
     for (size_t k = 0; k < v.size(); ++k) {
       const int g = v[k];
       NodeDesc d;
-      d.dest = dest_off[p] + (pos ? (*pos)[k] : int(k));
+      d.dest = dest_off[p] + (pos ? (*pos[p])[k] : int(k));
       int la1, la2;
       if (g == 0) {  // elements 0 (shape 0) and N-1 (shape 1)
         d.e1 = idx(0);
@@ -1026,7 +1026,9 @@ void FillPlan::node_descs(const Lists& nodes, const std::vector<int>& elems,
 
 void FillPlan::add_true_block(const Lists& rows, const Lists& cols,
                               double* dest, int ld, const int drow[2],
-                              const int dcol[2], int trans) {
+                              const int dcol[2], int trans,
+                              const std::vector<int>* const* rpos,
+                              const std::vector<int>* const* cpos) {
   const int nr = int(rows[0].size() + rows[1].size());
   const int nc = int(cols[0].size() + cols[1].size());
   if (nr == 0 || nc == 0) return;
@@ -1075,10 +1077,10 @@ void FillPlan::add_true_block(const Lists& rows, const Lists& cols,
   G.entry_off = entries_;
   G.nces = J.nE;
   G.rdesc_off = int(desc_.size());
-  node_descs(rows, res, drow, desc_);
+  node_descs(rows, res, drow, desc_, rpos);
   G.nrows = nr;
   G.cdesc_off = int(desc_.size());
-  node_descs(cols, ces, dcol, desc_);
+  node_descs(cols, ces, dcol, desc_, cpos);
   G.ncols = nc;
   G.trans = trans;
   G.ld = ld;
@@ -1152,13 +1154,15 @@ void FillPlan::add_sym_near_part(const std::vector<int>& enc, const std::vector<
   }
   const int ne = int(enc.size());
   const int denc[2] = {2 * m_, 2 * m_ + ne_total};  // enclosed rows per component
+  const std::vector<int>* const epos2[2] = {enc_pos, enc_pos};
+  const std::vector<int>* const* epos = enc_pos ? epos2 : nullptr;
   if (nc > 0) {  // T_V rows 2m'.. : true_block(enc x 2, cols)
     GatherJob G;
     G.pair_off = J.v_off;
     G.entry_off = entries_;
     G.nces = J.nE;
     G.rdesc_off = int(desc_.size());
-    node_descs(encl, A, denc, desc_, enc_pos);
+    node_descs(encl, A, denc, desc_, epos);
     G.nrows = 2 * ne;
     G.cdesc_off = int(desc_.size());
     node_descs(cols, E, cdest, desc_);
@@ -1179,7 +1183,7 @@ void FillPlan::add_sym_near_part(const std::vector<int>& enc, const std::vector<
     node_descs(rows, E, rdest, desc_);
     G.nrows = nr;
     G.cdesc_off = int(desc_.size());
-    node_descs(encl, A, denc, desc_, enc_pos);
+    node_descs(encl, A, denc, desc_, epos);
     G.ncols = 2 * ne;
     G.trans = 1;
     G.ld = ld_u;
@@ -1475,13 +1479,18 @@ struct ReusePart {
   long long entries = 0;
 };
 
-bool reuse_enabled() {  // EBEM_REUSE=0: every level computes all its entries (A/B)
-  static const bool on = [] {
+// EBEM_REUSE: 0 = every level computes all its entries (A/B); 1 = only the
+// copies that reproduce the computed entries bit for bit (same bundles, same
+// summation order); 2 (default) = also the sibling-block entries taken from
+// the other orientation of a symmetric evaluation (equal up to rounding).
+int reuse_level() {
+  static const int lv = [] {
     const char* e = std::getenv("EBEM_REUSE");
-    return e == nullptr || std::atoi(e) != 0;
+    return e == nullptr ? 2 : std::atoi(e);
   }();
-  return on;
+  return lv;
 }
+bool reuse_enabled() { return reuse_level() >= 1; }
 
 }  // namespace
 
@@ -1613,39 +1622,47 @@ void Problem::interaction(const std::vector<BasisReq>& req,
       }
     }
   };
-  {
-    PhaseTimer t_plan("fill_plan", nullptr);
-    parallel_for(nchunk, [&](int k) {
-      const size_t c0 = nc_ * size_t(k) / nchunk, c1 = nc_ * size_t(k + 1) / nchunk;
-      for (size_t c = c0; c < c1; ++c) {
-        const Lists& rows = *req[c].rows;
-        const Lists& cols = *req[c].cols;
-        double* tv = base + 2 * tv_off[c];
-        double* tu = base + 2 * tu_off[c];
-        const int no = n_out[c];
-        parts[k].add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv,
-                           no, tu, no);
-        plan_near(parts[k], rparts[k], c, tv, tu);
-      }
-    });
-  }
+  // Chunks are planned a batch (one chunk per planning thread) at a time and
+  // every wave is executed as soon as its chunks are planned, so the device
+  // starts on the first wave while the host plans the rest.
   // waves: consecutive chunks until the bundle count passes the cap (the
   // chunk that crosses it closes the wave), concatenated in parallel
   FillPlan plan(n_, m, pcfg_.n_gauss);
   int k0 = 0;
   long long acc = 0;
-  for (int k = 0; k < nchunk; ++k) {
-    acc += parts[k].bundles();
-    if (acc > kMaxBundlesPerWave || k == nchunk - 1) {
-      {
-        PhaseTimer t_app("fill_plan_append", nullptr);
-        plan.append_many(parts, k0, k + 1);
-        for (int q = k0; q <= k; ++q) parts[q] = FillPlan(n_, m, pcfg_.n_gauss);
+  const int batch = std::max(1, planning_threads());
+  for (int kb = 0; kb < nchunk; kb += batch) {
+    const int ke = std::min(nchunk, kb + batch);
+    {
+      PhaseTimer t_plan("fill_plan", nullptr);
+      parallel_for(ke - kb, [&](int kk) {
+        const int k = kb + kk;
+        const size_t c0 = nc_ * size_t(k) / nchunk, c1 = nc_ * size_t(k + 1) / nchunk;
+        for (size_t c = c0; c < c1; ++c) {
+          const Lists& rows = *req[c].rows;
+          const Lists& cols = *req[c].cols;
+          double* tv = base + 2 * tv_off[c];
+          double* tu = base + 2 * tu_off[c];
+          const int no = n_out[c];
+          parts[k].add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv,
+                             no, tu, no);
+          plan_near(parts[k], rparts[k], c, tv, tu);
+        }
+      });
+    }
+    for (int k = kb; k < ke; ++k) {
+      acc += parts[k].bundles();
+      if (acc > kMaxBundlesPerWave || k == nchunk - 1) {
+        {
+          PhaseTimer t_app("fill_plan_append", nullptr);
+          plan.append_many(parts, k0, k + 1);
+          for (int q = k0; q <= k; ++q) parts[q] = FillPlan(n_, m, pcfg_.n_gauss);
+        }
+        tl_mark("  wave planned");
+        execute(plan);
+        k0 = k + 1;
+        acc = 0;
       }
-      tl_mark("  wave planned");
-      execute(plan);
-      k0 = k + 1;
-      acc = 0;
     }
   }
   // the reuse copies of the level: one launch
@@ -1682,6 +1699,125 @@ void Problem::interaction(const std::vector<BasisReq>& req,
     CK(cudaGetLastError());
     staging.fence(st_);
   }
+}
+
+void Problem::plan_sibling_block(FillPlan& plan, MapPart& mp, int ca, int cb,
+                                 const Lists& rows, const Lists& cols, double* dest, int ld,
+                                 const int drow[2], const int dcol[2]) {
+  const int m = pcfg_.m_prime;
+  bool ok = prev_.valid && reuse_enabled() && ca >= 0 && cb >= 0 &&
+            ca < int(prev_.geom.size()) && cb < int(prev_.geom.size());
+  for (int p = 0; ok && p < 2; ++p)
+    ok = rows[p] == prev_.snode[ca][2 + p] && cols[p] == prev_.snode[cb][p];
+  if (!ok) {
+    plan.add_true_block(rows, cols, dest, ld, drow, dcol, 0);
+    return;
+  }
+  const std::vector<int>& encA = prev_.geom[ca].enclosed;
+  const std::vector<int>& encB = prev_.geom[cb].enclosed;
+  const bool sa = std::is_sorted(encA.begin(), encA.end());
+  const bool sb = std::is_sorted(encB.begin(), encB.end());
+  auto find = [](const std::vector<int>& enc, bool sorted, int node) {
+    if (sorted) {
+      auto it = std::lower_bound(enc.begin(), enc.end(), node);
+      return (it != enc.end() && *it == node) ? int(it - enc.begin()) : -1;
+    }
+    auto it = std::find(enc.begin(), enc.end(), node);
+    return it != enc.end() ? int(it - enc.begin()) : -1;
+  };
+  const int neA = int(encA.size()), neB = int(encB.size());
+  const double* pbase = (prev_.buf ? scratch().tbuf_alt : scratch().tbuf).get();
+  // rows whose node lies inside cb's circle: whole rows from cb's T_V
+  Lists rest_r, rest_c;
+  std::vector<int> rpos[2], cpos[2];
+  std::vector<int2> rows_v, cols_all, rows_u, cols_u;
+  for (int p = 0; p < 2; ++p)
+    for (int ia = 0; ia < int(rows[p].size()); ++ia) {
+      const int ib = find(encB, sb, rows[p][ia]);
+      if (ib >= 0) {
+        rows_v.push_back(make_int2(2 * m + p * neB + ib, drow[p] + ia));
+      } else {
+        rest_r[p].push_back(rows[p][ia]);
+        rpos[p].push_back(ia);
+        rows_u.push_back(make_int2(p * prev_.nr0[ca] + prev_.spos[ca][2 + p][ia], drow[p] + ia));
+      }
+    }
+  const bool other = reuse_level() >= 2;
+  for (int q = 0; q < 2; ++q)
+    for (int jb = 0; jb < int(cols[q].size()); ++jb) {
+      cols_all.push_back(make_int2(q * prev_.nc0[cb] + prev_.spos[cb][q][jb], dcol[q] + jb));
+      const int ja = other ? find(encA, sa, cols[q][jb]) : -1;
+      if (ja >= 0) {
+        cols_u.push_back(make_int2(2 * m + q * neA + ja, dcol[q] + jb));
+      } else {
+        rest_c[q].push_back(cols[q][jb]);
+        cpos[q].push_back(jb);
+      }
+    }
+  if (!rows_v.empty()) {
+    MapTask T{};
+    T.src = pbase + 2 * prev_.tv_off[cb];
+    T.dst = dest;
+    T.src_ld = prev_.n_out[cb];
+    T.dst_ld = ld;
+    T.n_rows = int(rows_v.size());
+    T.n_cols = int(cols_all.size());
+    T.swap = 0;
+    T.row_off = (long long)mp.rows.size();
+    T.col_off = (long long)mp.cols.size();
+    mp.rows.insert(mp.rows.end(), rows_v.begin(), rows_v.end());
+    mp.cols.insert(mp.cols.end(), cols_all.begin(), cols_all.end());
+    mp.tasks.push_back(T);
+  }
+  if (!rows_u.empty() && !cols_u.empty()) {
+    // the remaining rows against the columns inside ca's circle: ca's
+    // T_U = M_U^H holds conj(K(row, enclosed)) at (enclosed, row)
+    MapTask T{};
+    T.src = pbase + 2 * prev_.tu_off[ca];
+    T.dst = dest;
+    T.src_ld = prev_.n_out[ca];
+    T.dst_ld = ld;
+    T.n_rows = int(rows_u.size());
+    T.n_cols = int(cols_u.size());
+    T.swap = 1;
+    T.row_off = (long long)mp.rows.size();
+    T.col_off = (long long)mp.cols.size();
+    mp.rows.insert(mp.rows.end(), rows_u.begin(), rows_u.end());
+    mp.cols.insert(mp.cols.end(), cols_u.begin(), cols_u.end());
+    mp.tasks.push_back(T);
+  }
+  const std::vector<int>* const rp[2] = {&rpos[0], &rpos[1]};
+  const std::vector<int>* const cp[2] = {&cpos[0], &cpos[1]};
+  plan.add_true_block(rest_r, rest_c, dest, ld, drow, dcol, 0, rp, cp);
+}
+
+void Problem::run_map_copies(std::vector<MapPart>& parts) {
+  std::vector<MapTask> tasks;
+  std::vector<int2> rows, cols;
+  double entries = 0.0;
+  for (MapPart& mp : parts) {
+    for (MapTask T : mp.tasks) {
+      T.row_off += (long long)rows.size();
+      T.col_off += (long long)cols.size();
+      entries += double(T.n_rows) * T.n_cols;
+      tasks.push_back(T);
+    }
+    rows.insert(rows.end(), mp.rows.begin(), mp.rows.end());
+    cols.insert(cols.end(), mp.cols.begin(), mp.cols.end());
+    mp = MapPart{};
+  }
+  if (tasks.empty()) return;
+  Pack pk;
+  const size_t o_t = pk.add(tasks);
+  const size_t o_r = pk.add(rows);
+  const size_t o_c = pk.add(cols);
+  char* tb = staging.put(pk, st_);
+  g_prof.begin(st_);
+  launch_map_copy(Pack::at<MapTask>(tb, o_t), int(tasks.size()), Pack::at<int2>(tb, o_r),
+                  Pack::at<int2>(tb, o_c), st_);
+  g_prof.end(KP_REUSE, st_, entries, 32.0 * entries);
+  CK(cudaGetLastError());
+  staging.fence(st_);
 }
 
 // TSQR rounds until each block is an n x n R or fits one CTA's shared memory
@@ -1827,7 +1963,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
 
 void Problem::bases(const std::vector<BasisReq>& req, double eps,
                     std::vector<BasisRes>& res, DBuf<double>& vbuf,
-                    DBuf<double>& ubuf, double* fill_seconds, bool chain) {
+                    DBuf<double>& ubuf, double* fill_seconds, bool chain, bool defer_lists) {
   const size_t ncell = req.size();
   res.assign(ncell, BasisRes{});
   if (ncell == 0) return;
@@ -1978,41 +2114,13 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     r.k = k;
     r.saturated = k >= std::min(std::min(cols[0].size(), cols[1].size()),
                                 std::min(rows[0].size(), rows[1].size()));
-    for (int a = 0; a < 4; ++a) {
-      const int* jp = h_jp + jp_off[4 * c + a];
-      const std::vector<int>& src = a == 0 ? cols[0] : a == 1 ? cols[1] : a == 2 ? rows[0] : rows[1];
-      std::vector<int>& dst = a == 0 ? r.scol[0] : a == 1 ? r.scol[1] : a == 2 ? r.srow[0] : r.srow[1];
-      dst.resize(k);
-      for (int j = 0; j < k; ++j) dst[j] = src[jp[j]];
-    }
     r.v_off = v_total;
     v_total += size_t(k) * (cols[0].size() + cols[1].size());
     r.u_off = u_total;
     u_total += size_t(k) * (rows[0].size() + rows[1].size());
   }
-  if (chain) {  // what the next level's reuse needs of this one
-    prev_.valid = true;
-    prev_.buf = cur_buf;
-    prev_.geom = std::move(geom);
-    prev_.tv_off = tv_off;
-    prev_.tu_off = tu_off;
-    prev_.n_out = n_out;
-    prev_.nc0.resize(ncell);
-    prev_.nr0.resize(ncell);
-    prev_.spos.assign(ncell, {});
-    prev_.snode.assign(ncell, {});
-    for (size_t c = 0; c < ncell; ++c) {
-      prev_.nc0[c] = int((*req[c].cols)[0].size());
-      prev_.nr0[c] = int((*req[c].rows)[0].size());
-      const int k = res[c].k;
-      for (int a = 0; a < 4; ++a) {
-        const int* jp = h_jp + jp_off[4 * c + a];
-        prev_.spos[c][a].assign(jp, jp + k);
-        prev_.snode[c][a] = a == 0 ? res[c].scol[0] : a == 1 ? res[c].scol[1]
-                            : a == 2 ? res[c].srow[0] : res[c].srow[1];
-      }
-    }
-  }
+  // (the skeleton lists are filled in after the interpolation launch below:
+  // the device needs only the ranks)
   // ---- interpolation coefficients
   vbuf.ensure(2 * v_total + 2);
   ubuf.ensure(2 * u_total + 2);
@@ -2059,6 +2167,69 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
     CK(cudaGetLastError());
     staging.fence(st_);
   }
+  // ---- skeleton lists in pivot order and, for chained calls, what the next
+  // level's reuse needs of this one: finish_bases (deferred by the level
+  // loop until its merges are enqueued -- the device needs only the ranks)
+  pend_.active = true;
+  pend_.chain = chain;
+  pend_.cur_buf = cur_buf;
+  pend_.req = &req;
+  pend_.res = &res;
+  pend_.h_jp = h_jp;
+  pend_.jp_off = std::move(jp_off);
+  pend_.geom = std::move(geom);
+  pend_.tv_off = std::move(tv_off);
+  pend_.tu_off = std::move(tu_off);
+  pend_.n_out = std::move(n_out);
+  if (!defer_lists) finish_bases();
+}
+
+void Problem::finish_bases() {
+  if (!pend_.active) return;
+  pend_.active = false;
+  const std::vector<BasisReq>& req = *pend_.req;
+  std::vector<BasisRes>& res = *pend_.res;
+  const size_t ncell = req.size();
+  const bool chain = pend_.chain;
+  const int* h_jp = pend_.h_jp;
+  const std::vector<size_t>& jp_off = pend_.jp_off;
+  if (chain) {
+    prev_.valid = true;
+    prev_.buf = pend_.cur_buf;
+    prev_.geom = std::move(pend_.geom);
+    prev_.tv_off = std::move(pend_.tv_off);
+    prev_.tu_off = std::move(pend_.tu_off);
+    prev_.n_out = std::move(pend_.n_out);
+    prev_.nc0.resize(ncell);
+    prev_.nr0.resize(ncell);
+    prev_.spos.resize(ncell);  // (the per-cell vectors are reassigned below)
+    prev_.snode.resize(ncell);
+  }
+  const int nchunk = int(std::min<size_t>(ncell, size_t(4 * planning_threads())));
+  parallel_for(nchunk, [&](int kq) {
+    const size_t c0 = ncell * size_t(kq) / nchunk, c1 = ncell * size_t(kq + 1) / nchunk;
+    for (size_t c = c0; c < c1; ++c) {
+      const Lists& rows = *req[c].rows;
+      const Lists& cols = *req[c].cols;
+      BasisRes& r = res[c];
+      const int k = r.k;
+      for (int a = 0; a < 4; ++a) {
+        const int* jp = h_jp + jp_off[4 * c + a];
+        const std::vector<int>& src = a == 0 ? cols[0] : a == 1 ? cols[1] : a == 2 ? rows[0] : rows[1];
+        std::vector<int>& dst = a == 0 ? r.scol[0] : a == 1 ? r.scol[1] : a == 2 ? r.srow[0] : r.srow[1];
+        dst.resize(k);
+        for (int j = 0; j < k; ++j) dst[j] = src[jp[j]];
+        if (chain) {
+          prev_.spos[c][a].assign(jp, jp + k);
+          prev_.snode[c][a] = dst;
+        }
+      }
+      if (chain) {
+        prev_.nc0[c] = int(cols[0].size());
+        prev_.nr0[c] = int(rows[0].size());
+      }
+    }
+  });
 }
 
 void Problem::true_block_host(const Lists& rows, const Lists& cols, double* out) {
@@ -2391,7 +2562,7 @@ int* Fds::lu_info(int n) {
 }
 
 void Fds::reduced_diagonal(FillPlan& plan, std::vector<CopyTask>& copies,
-                           int cell, double* dest, int ld, int off) {
+                           int cell, double* dest, int ld, int off, MapPart* mp) {
   // proj/src/fds.cpp:33-54
   const Cell& c1 = cells_[2 * cell + 1];
   const Cell& c2 = cells_[2 * cell + 2];
@@ -2411,8 +2582,18 @@ void Fds::reduced_diagonal(FillPlan& plan, std::vector<CopyTask>& copies,
     }
   double* base = dest + 2 * (size_t(off) * ld + off);
   const int drow12[2] = {0, np}, dcol12[2] = {k1, np + k1};
-  plan.add_true_block(c1.srow, c2.scol, base, ld, drow12, dcol12, 0);
   const int drow21[2] = {k1, np + k1}, dcol21[2] = {0, np};
+  if (mp) {
+    // the children are consecutive cells of the level below (the previous
+    // chained bases call): entries they already hold are copied
+    int lv = 0;
+    while (last(lv) < cell) ++lv;
+    const int i1 = 2 * cell + 1 - first(lv + 1);
+    P_.plan_sibling_block(plan, *mp, i1, i1 + 1, c1.srow, c2.scol, base, ld, drow12, dcol12);
+    P_.plan_sibling_block(plan, *mp, i1 + 1, i1, c2.srow, c1.scol, base, ld, drow21, dcol21);
+    return;
+  }
+  plan.add_true_block(c1.srow, c2.scol, base, ld, drow12, dcol12, 0);
   plan.add_true_block(c2.srow, c1.scol, base, ld, drow21, dcol21, 0);
 }
 
@@ -2482,6 +2663,7 @@ void Fds::build() {
       PhaseTimer tp("fill_diagonal", P_.stream());
       FillPlan plan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
       std::vector<CopyTask> copies;
+      std::vector<MapPart> mparts;
       for (int i = 0; hs_ && i < nlev; ++i) {  // host source: assemble on host
         Cell& C = cells_[f + i];
         const int d = 2 * C.nloc;
@@ -2501,27 +2683,45 @@ void Fds::build() {
         std::vector<FillPlan> parts(nchunk, FillPlan(n, P_.proxy_cfg().m_prime,
                                                      P_.proxy_cfg().n_gauss));
         std::vector<std::vector<CopyTask>> pcopies(nchunk);
-        parallel_for(nchunk, [&](int k) {
-          const int i0 = int(size_t(nlev) * k / nchunk), i1 = int(size_t(nlev) * (k + 1) / nchunk);
-          for (int i = i0; i < i1; ++i) {
-            Cell& C = cells_[f + i];
-            const int d = 2 * C.nloc;
-            if (level == depth_) {
-              parts[k].add_sym_diag(C.jrow[0], C.lu, d);  // leaf: jrow == jcol, ascending
-            } else {
-              reduced_diagonal(parts[k], pcopies[k], f + i, C.lu, d, 0);
+        mparts.assign(nchunk, MapPart{});
+        // a batch of chunks (one per planning thread) at a time, each wave
+        // executed as soon as its chunks are planned
+        const int batch = std::max(1, planning_threads());
+        int k0 = 0;
+        long long acc = 0;
+        for (int kb = 0; kb < nchunk; kb += batch) {
+          const int ke = std::min(nchunk, kb + batch);
+          parallel_for(ke - kb, [&](int kk) {
+            const int k = kb + kk;
+            const int i0 = int(size_t(nlev) * k / nchunk), i1 = int(size_t(nlev) * (k + 1) / nchunk);
+            for (int i = i0; i < i1; ++i) {
+              Cell& C = cells_[f + i];
+              const int d = 2 * C.nloc;
+              if (level == depth_) {
+                parts[k].add_sym_diag(C.jrow[0], C.lu, d);  // leaf: jrow == jcol, ascending
+              } else {
+                reduced_diagonal(parts[k], pcopies[k], f + i, C.lu, d, 0, &mparts[k]);
+              }
+            }
+          });
+          for (int k = kb; k < ke; ++k) {
+            copies.insert(copies.end(), pcopies[k].begin(), pcopies[k].end());
+            acc += parts[k].bundles();
+            if (acc > kMaxBundlesPerWave || k == nchunk - 1) {
+              plan.append_many(parts, k0, k + 1);
+              for (int q = k0; q <= k; ++q)
+                parts[q] = FillPlan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
+              tl_mark("  diag wave planned");
+              P_.execute(plan);
+              k0 = k + 1;
+              acc = 0;
             }
           }
-        });
-        for (int k = 0; k < nchunk; ++k) {
-          plan.append(parts[k]);
-          parts[k] = FillPlan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
-          copies.insert(copies.end(), pcopies[k].begin(), pcopies[k].end());
-          if (plan.bundles() > kMaxBundlesPerWave) P_.execute(plan);
         }
       }
       P_.execute(plan);
       run_copies(P_, copies);
+      P_.run_map_copies(mparts);
       // element-length guard: read at the bases' synchronisation below
     }
     {
@@ -2556,7 +2756,7 @@ void Fds::build() {
     DBuf<double>& ubuf = ubuf_;
     const double tb = now();
     if (hs_) host_bases(level, br, S.v, ubuf);
-    else P_.bases(req, cfg_.epsilon, br, S.v, ubuf, nullptr, true);
+    else P_.bases(req, cfg_.epsilon, br, S.v, ubuf, nullptr, true, true);
     PhaseTimer t_after("level_after_bases", nullptr);
     tl_mark("L" + std::to_string(level) + " bases done");
     basis_seconds += now() - tb;
@@ -2566,8 +2766,6 @@ void Fds::build() {
     for (int i = 0; i < nlev; ++i) {
       Cell& C = cells_[f + i];
       C.k = br[i].k;
-      C.srow = br[i].srow;
-      C.scol = br[i].scol;
       au_off[i] = au_total;
       au_total += size_t(2 * C.nloc) * (2 * C.k);
       at_off[i] = at_total;
@@ -2583,6 +2781,7 @@ void Fds::build() {
       C.atilde = S.atilde.get() + 2 * at_off[i];
       C.v = S.v.get() + 2 * br[i].v_off;
     }
+    tl_mark("  merge alloc");
     // ---- A^-1 U with U = blockdiag(u0, u1)
     {
       PhaseTimer tp("merge_ainv_u", P_.stream());
@@ -2605,6 +2804,7 @@ void Fds::build() {
       run_copies(P_, ct);
       run_getrs(P_, st);
     }
+    tl_mark("  ainv_u enq");
     // ---- W = [v0 A^-1U_top ; v1 A^-1U_bottom], atilde = W^-1
     {
       PhaseTimer tp("merge_atilde", P_.stream());
@@ -2644,18 +2844,33 @@ void Fds::build() {
       run_copies(P_, ct);
       run_getrs(P_, st);
     }
+    tl_mark("  merges enq");
+    // ---- skeleton lists (deferred: the merges above needed only the ranks)
+    if (!hs_) P_.finish_bases();
+    tl_mark("  lists");
     // ---- parent sequences: concatenated child skeletons per component
-    for (int c = first(level - 1); c <= last(level - 1); ++c) {
-      Cell& Pc = cells_[c];
-      const Cell& c1 = cells_[2 * c + 1];
-      const Cell& c2 = cells_[2 * c + 2];
-      for (int comp = 0; comp < 2; ++comp) {
-        Pc.jrow[comp] = c1.srow[comp];
-        Pc.jrow[comp].insert(Pc.jrow[comp].end(), c2.srow[comp].begin(), c2.srow[comp].end());
-        Pc.jcol[comp] = c1.scol[comp];
-        Pc.jcol[comp].insert(Pc.jcol[comp].end(), c2.scol[comp].begin(), c2.scol[comp].end());
-      }
-      Pc.nloc = c1.k + c2.k;
+    {
+      const int pf = first(level - 1), np = last(level - 1) - pf + 1;
+      const int nch = std::min(np, 4 * planning_threads());
+      parallel_for(nch, [&](int kq) {
+        const int p0 = int(size_t(np) * kq / nch), p1 = int(size_t(np) * (kq + 1) / nch);
+        for (int c = pf + p0; c < pf + p1; ++c) {
+          Cell& Pc = cells_[c];
+          Cell& c1 = cells_[2 * c + 1];
+          Cell& c2 = cells_[2 * c + 2];
+          c1.srow = std::move(br[2 * c + 1 - f].srow);
+          c1.scol = std::move(br[2 * c + 1 - f].scol);
+          c2.srow = std::move(br[2 * c + 2 - f].srow);
+          c2.scol = std::move(br[2 * c + 2 - f].scol);
+          for (int comp = 0; comp < 2; ++comp) {
+            Pc.jrow[comp] = c1.srow[comp];
+            Pc.jrow[comp].insert(Pc.jrow[comp].end(), c2.srow[comp].begin(), c2.srow[comp].end());
+            Pc.jcol[comp] = c1.scol[comp];
+            Pc.jcol[comp].insert(Pc.jcol[comp].end(), c2.scol[comp].begin(), c2.scol[comp].end());
+          }
+          Pc.nloc = c1.k + c2.k;
+        }
+      });
     }
   }
   tl_mark("upward enq");
@@ -2699,12 +2914,14 @@ void Fds::build() {
   {
     FillPlan plan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
     std::vector<CopyTask> copies;
+    std::vector<MapPart> mparts(1);
     for (int i = 0; !hs_ && i <= tl - tf; ++i) {
       const Cell& ci = cells_[tf + i];
       for (int j = 0; j <= tl - tf; ++j) {
         const Cell& cj = cells_[tf + j];
         if (i == j) {
-          reduced_diagonal(plan, copies, tf + i, top_lu_.get(), top_dim_, top_off_[i]);
+          reduced_diagonal(plan, copies, tf + i, top_lu_.get(), top_dim_, top_off_[i],
+                           &mparts[0]);
         } else {
           const int drow[2] = {top_off_[i], top_off_[i] + ci.nloc};
           const int dcol[2] = {top_off_[j], top_off_[j] + cj.nloc};
@@ -2714,6 +2931,7 @@ void Fds::build() {
     }
     P_.execute(plan);
     run_copies(P_, copies);
+    P_.run_map_copies(mparts);
     P_.check_domain();
     if (top_dim_ > 0) {
       LuTask t{};

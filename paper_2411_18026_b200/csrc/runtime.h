@@ -276,6 +276,12 @@ struct BasisRes {
 
 class FillPlan;
 
+// Entry copies planned by one planning thread (offsets local to the part).
+struct MapPart {
+  std::vector<MapTask> tasks;
+  std::vector<int2> rows, cols;
+};
+
 // Records batched LA launches (copies, GEMMs, LU solves) instead of issuing
 // them: the task arrays of a whole solve are uploaded once and the launch
 // sequence is captured into a CUDA graph that each solve replays.
@@ -376,9 +382,25 @@ class Problem {
   // V/U coefficient blocks land in vbuf/ubuf (device), offsets in res.
   void bases(const std::vector<BasisReq>& req, double eps,
              std::vector<BasisRes>& res, DBuf<double>& vbuf,
-             DBuf<double>& ubuf, double* fill_seconds = nullptr, bool chain = false);
+             DBuf<double>& ubuf, double* fill_seconds = nullptr, bool chain = false,
+             bool defer_lists = false);
+  // Fills in the skeleton lists of the last bases() call made with
+  // defer_lists (req and res must still be alive), and records the level
+  // for the next chained call.
+  void finish_bases();
   // Forget the previous chained level (start of a factorization).
   void reset_chain() { prev_.valid = false; }
+  // true_block(rows, cols) of two sibling cells' skeletons (the off-diagonal
+  // blocks of a reduced diagonal, fds.cpp:33-54): rows = srow of the child
+  // with index ca in the previous chained level, cols = scol of child cb.
+  // Entries whose row node lies inside cb's proxy circle are copied from cb's
+  // T_V, those whose column node lies inside ca's circle from ca's T_U
+  // (conjugate-transposed); the rest is planned as a true block.
+  void plan_sibling_block(FillPlan& plan, MapPart& mp, int ca, int cb, const Lists& rows,
+                          const Lists& cols, double* dest, int ld, const int drow[2],
+                          const int dcol[2]);
+  // Runs the entry copies planned by plan_sibling_block (one launch).
+  void run_map_copies(std::vector<MapPart>& parts);
   // Interaction matrices (device, column-major) of a batch of cells:
   // T_V = M_V (n_out x ncols) and T_U = M_U^H (n_out x nrows).
   void interaction(const std::vector<BasisReq>& req,
@@ -423,6 +445,16 @@ class Problem {
   cudaStream_t st_ = nullptr;
   NodeBoxTree tree_;
   PrevLevel prev_;
+  struct PendingBases {
+    bool active = false, chain = false;
+    int cur_buf = 0;
+    const std::vector<BasisReq>* req = nullptr;
+    std::vector<BasisRes>* res = nullptr;
+    const int* h_jp = nullptr;
+    std::vector<size_t> jp_off, tv_off, tu_off;
+    std::vector<ProxyGeom> geom;
+    std::vector<int> n_out;
+  } pend_;
 };
 
 // Work planner for one batch of Galerkin fills.
@@ -432,8 +464,12 @@ class FillPlan {
       : N_(n_nodes), m_(m_prime), ng_(n_gauss) {}
   // true_block(rows, cols) into dest with per-component destination offsets;
   // trans writes conj(v) at (col, row).
+  // rpos / cpos (optional, per component): destination position of each
+  // listed node relative to drow / dcol instead of its index in the list.
   void add_true_block(const Lists& rows, const Lists& cols, double* dest,
-                      int ld, const int drow[2], const int dcol[2], int trans);
+                      int ld, const int drow[2], const int dcol[2], int trans,
+                      const std::vector<int>* const* rpos = nullptr,
+                      const std::vector<int>* const* cpos = nullptr);
   // Both proxy blocks of one cell: polygon rows -> T_V rows [0, 2m'),
   // polygon cols of M_U -> T_U rows [0, 2m') (conj-transposed).
   void add_proxy(double cx, double cy, double radius, const Lists& rows,
@@ -470,7 +506,7 @@ class FillPlan {
   void elements_of(const Lists& nodes, std::vector<int>& out) const;
   void node_descs(const Lists& nodes, const std::vector<int>& elems,
                   const int dest_off[2], std::vector<NodeDesc>& out,
-                  const std::vector<int>* pos = nullptr) const;
+                  const std::vector<int>* const* pos = nullptr) const;
   int poly_descs();
   int N_, m_, ng_;
   long long bundles_ = 0;
@@ -532,7 +568,7 @@ class Fds {
   void host_reduced_diagonal(int cell, double* out, int ld);
   const HostSource* hs_ = nullptr;
   void reduced_diagonal(FillPlan& plan, std::vector<CopyTask>& copies, int cell,
-                        double* dest, int ld, int off);
+                        double* dest, int ld, int off, MapPart* mp = nullptr);
   int first(int l) const { return (1 << l) - 1; }
   int last(int l) const { return (2 << l) - 2; }
 
