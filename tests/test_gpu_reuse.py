@@ -1,0 +1,69 @@
+"""Cross-level reuse (runtime.cpp, Problem::interaction / plan_sibling_block):
+entries of a cell's interaction matrices and sibling blocks that a child
+already holds are copied instead of evaluated again.  The reference evaluates
+every block afresh (AssemblerSource::cell_basis, compression.cpp:132-169;
+reduced_diagonal, fds.cpp:33-54), so the factorization with the copies must
+give the same ranks, the same skeleton sets and the same solution as the one
+without (EBEM_REUSE=0): the near-field copies reproduce the evaluated entries
+bit for bit, the sibling-block copies up to rounding (another summation order
+of the same quadrature).  The switch is read once per process, so each level
+runs in its own interpreter."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+WORKER = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %r)
+import paper_2411_18026_b200 as eb
+kind, n, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+if kind == "circle":
+    mesh = eb.Mesh.star(n, eb.StarShape(1.0, 0.0, 3))
+    med = eb.Medium.from_lame(1.0, 1.0, 1.0, 1.0)
+else:
+    mesh = eb.Mesh.star(n, eb.StarShape(1.0, 0.3, 5))
+    med = eb.Medium.from_lame(1.5, 1.0, 1.0, 6.0)
+asm = eb.BlockAssembler(mesh, med, med.default_coupling())
+src = eb.AssemblerSource(asm)
+tree = eb.ClusterTree(n, eb.ClusterTree.depth_for(n, 32))
+fds = eb.FdsSolver(src, tree, eb.FdsConfig(1e-10, 1))
+x = fds.solve(asm.rhs(eb.PlanePWave(med, 1.0, 0.0)))
+skel = []
+for lv in range(2, tree.depth() + 1):
+    for c in range(tree.first_cell(lv), tree.first_cell(lv) + (1 << lv)):
+        info = fds.cell(c)
+        skel.append([info["k"]] + [s.tolist() for s in (*info["row_skeleton"], *info["col_skeleton"])])
+np.save(out + ".npy", x)
+json.dump(dict(max_rank=list(fds.stats().max_rank), skel=skel), open(out + ".json", "w"))
+""" % str(ROOT)
+
+
+def run(level, kind, n, tmp_path):
+    out = tmp_path / f"reuse{level}_{kind}_{n}"
+    env = dict(os.environ, EBEM_REUSE=str(level))
+    subprocess.run([sys.executable, "-c", WORKER, kind, str(n), str(out)], check=True, env=env,
+                   timeout=600)
+    return np.load(str(out) + ".npy"), json.load(open(str(out) + ".json"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n", [("circle", 4096), ("star", 8192)])
+def test_reuse_matches_fresh_evaluation(kind, n, tmp_path):
+    x0, s0 = run(0, kind, n, tmp_path)
+    x1, s1 = run(1, kind, n, tmp_path)
+    x2, s2 = run(2, kind, n, tmp_path)
+    nrm = np.linalg.norm(x0)
+    # same ranks and skeleton sets, in the same pivot order
+    assert s1 == s0
+    assert s2 == s0
+    # copies of entries evaluated by the same kernel path: rounding level
+    assert np.linalg.norm(x1 - x0) / nrm < 1e-11
+    assert np.linalg.norm(x2 - x0) / nrm < 1e-10
