@@ -433,4 +433,29 @@ void build_elements(const double* xy, int n, double* elem, double* hmin,
   *hmax = hi;
 }
 
+// Elements [e0, e1) of the mesh: the field-major array elem (as
+// build_elements) and the packed 8-double rows elem8 (px, py, dx, dy, nx, ny,
+// h, 0) in one pass.  Returns false on a zero-length element.
+bool build_elements_range(const double* xy, int n, int e0, int e1, double* elem,
+                          double* elem8, double* hmin, double* hmax) {
+  double lo = 1e300, hi = 0.0;
+  for (int e = e0; e < e1; ++e) {
+    const int nx = (e + 1) % n;
+    const double sx = xy[2 * e], sy = xy[2 * e + 1];
+    const double ex = xy[2 * nx] - sx, ey = xy[2 * nx + 1] - sy;
+    const double len = std::hypot(ex, ey);
+    if (!(len > 0.0)) return false;
+    const double ux = ex / len, uy = ey / len;
+    const double vals[kElemFields] = {sx, sy, ex, ey, ux, uy, -uy, ux, len};
+    for (int f = 0; f < kElemFields; ++f) elem[size_t(f) * n + e] = vals[f];
+    double* r = elem8 + 8 * size_t(e);
+    r[0] = sx; r[1] = sy; r[2] = ex; r[3] = ey; r[4] = -uy; r[5] = ux; r[6] = len; r[7] = 0.0;
+    lo = std::min(lo, len);
+    hi = std::max(hi, len);
+  }
+  *hmin = lo;
+  *hmax = hi;
+  return true;
+}
+
 }  // namespace ebem_gpu

@@ -19,5 +19,7 @@ void gauss_rule(int n, double* x, double* w);
 // Element table (ElemField planes) of the closed polygon through xy.
 void build_elements(const double* xy, int n, double* elem, double* hmin,
                     double* hmax);
+bool build_elements_range(const double* xy, int n, int e0, int e1, double* elem,
+                          double* elem8, double* hmin, double* hmax);
 
 }  // namespace ebem_gpu

@@ -445,11 +445,29 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   if (n < 8) throw Error(EBEM_INVALID_ARGUMENT, "PairIntegrator: mesh too coarse");
   const double tc0 = now();
   xy_.assign(xy, xy + 2 * size_t(n));
-  elem_.resize(size_t(kElemFields) * n);
-  try {
-    build_elements(xy_.data(), n, elem_.data(), &hmin_, &hmax_);
-  } catch (const std::invalid_argument& e) {
-    throw Error(EBEM_INVALID_ARGUMENT, e.what());
+  // element geometry straight into pinned staging memory (process-wide,
+  // grow-only), built on the planning threads: field-major array, packed
+  // 8-double rows and the node coordinates, uploaded below
+  const size_t n9 = size_t(kElemFields) * n;
+  double* const h_elem = scratch().h_geom.ensure(n9 + 10 * size_t(n));
+  double* const h_e8 = h_elem + n9;
+  double* const h_xy = h_e8 + 8 * size_t(n);
+  {
+    const int nch = std::max(1, std::min(n / 4096, 4 * planning_threads()));
+    std::vector<double> lo(nch, 1e300), hi(nch, 0.0);
+    std::vector<char> okv(nch, 1);
+    parallel_for(nch, [&](int k) {
+      const int e0 = int(size_t(n) * k / nch), e1 = int(size_t(n) * (k + 1) / nch);
+      okv[k] = build_elements_range(xy_.data(), n, e0, e1, h_elem, h_e8, &lo[k], &hi[k]);
+      std::memcpy(h_xy + 2 * size_t(e0), xy_.data() + 2 * size_t(e0), 16 * size_t(e1 - e0));
+    });
+    hmin_ = 1e300;
+    hmax_ = 0.0;
+    for (int k = 0; k < nch; ++k) {
+      if (!okv[k]) throw Error(EBEM_INVALID_ARGUMENT, "Mesh: zero-length element");
+      hmin_ = std::min(hmin_, lo[k]);
+      hmax_ = std::max(hmax_, hi[k]);
+    }
   }
   DevMedium med;
   try {
@@ -461,10 +479,28 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   const double tc1 = now();
   hctx_.med = med;
   hctx_.n_nodes = n;
+  // the series tables depend on the medium only: kept for the next problem
+  // with the same medium (API calls are serialised by the API mutex)
+  struct SeriesCache {
+    bool valid = false;
+    double key[6];
+    int maxq;
+    unsigned char series[sizeof(hctx_.series)];
+    ParSeries pser;
+  };
+  static SeriesCache scache;
+  const double skey[6] = {lam, mu, rho, omega, are, aim};
+  const bool cached = scache.valid && std::memcmp(scache.key, skey, sizeof(skey)) == 0;
+  fc_.med = med;
+  if (cached) {
+    hctx_.series_maxq = scache.maxq;
+    std::memcpy(hctx_.series, scache.series, sizeof(hctx_.series));
+    hctx_.pser = scache.pser;
+  }
   try {
+    if (!cached) {
     hctx_.series_maxq = build_series(med, hctx_.series, kMaxSeriesPow);
     build_parity_series(hctx_.series, kMaxSeriesPow, hctx_.pser);
-    fc_.med = med;
     for (int k = 2; k < 10; ++k)  // series_joint drops the imaginary log chain
       for (int p = 0; p < kParTerms; ++p)
         if (hctx_.pser.b[k][p].y != 0.0)
@@ -544,6 +580,13 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
         for (int t = 1; t < ntmax; ++t)
           fprintf(stderr, "series: r > %.3e needs > %d terms\n", ps.rcut[t], t);
     }
+    scache.valid = false;
+    std::memcpy(scache.key, skey, sizeof(skey));
+    scache.maxq = hctx_.series_maxq;
+    std::memcpy(scache.series, hctx_.series, sizeof(hctx_.series));
+    scache.pser = hctx_.pser;
+    scache.valid = true;
+    }
   } catch (const std::logic_error& e) {
     throw Error(EBEM_LOGIC_ERROR, e.what());
   }
@@ -585,21 +628,15 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
     throw Error(EBEM_CUDA_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
   const double tc2 = now();
   st_ = scratch().st;
-  delem_.alloc(elem_.size());
+  delem_.alloc(n9);
   dxy_.alloc(xy_.size());
-  CK(cudaMemcpyAsync(delem_.get(), elem_.data(), elem_.size() * 8, cudaMemcpyHostToDevice, st_));
-  CK(cudaMemcpyAsync(dxy_.get(), xy_.data(), xy_.size() * 8, cudaMemcpyHostToDevice, st_));
+  delem8_.alloc(8 * size_t(n));
+  CK(cudaMemcpyAsync(delem_.get(), h_elem, n9 * 8, cudaMemcpyHostToDevice, st_));
+  CK(cudaMemcpyAsync(dxy_.get(), h_xy, xy_.size() * 8, cudaMemcpyHostToDevice, st_));
+  CK(cudaMemcpyAsync(delem8_.get(), h_e8, 64 * size_t(n), cudaMemcpyHostToDevice, st_));
   hctx_.elem = delem_.get();
-  {
-    std::vector<double> e8(8 * size_t(n), 0.0);
-    const int f[7] = {EPX, EPY, EDX, EDY, ENX, ENY, EH};
-    for (int e = 0; e < n; ++e)
-      for (int k = 0; k < 7; ++k) e8[8 * size_t(e) + k] = elem_[size_t(f[k]) * n + e];
-    delem8_.alloc(e8.size());
-    CK(cudaMemcpyAsync(delem8_.get(), e8.data(), e8.size() * 8, cudaMemcpyHostToDevice, st_));
-    CK(cudaStreamSynchronize(st_));  // e8 is pageable and goes out of scope
-    hctx_.elem8 = delem8_.get();
-  }
+  hctx_.elem8 = delem8_.get();
+  // (the stream is synchronised below, before the staging memory can be reused)
   hctx_.node_xy = dxy_.get();
   dctx_.alloc(1);
   CK(cudaMemcpyAsync(dctx_.get(), &hctx_, sizeof(DevCtx), cudaMemcpyHostToDevice, st_));

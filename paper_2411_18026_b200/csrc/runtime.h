@@ -338,6 +338,7 @@ struct Scratch {
   DBuf<int> sym_bounds;
   DBuf<double> bundles;
   DBuf<double2> gws;
+  PinnedBuf<double> h_geom;      // element geometry staging of a problem setup
   PinnedBuf<int> h_jp, h_steps;  // pivoted-QR readbacks
   PinnedBuf<double> h_rd;
 };
