@@ -251,6 +251,9 @@ double now() {
 }
 
 constexpr long long kMaxBundlesPerWave = 8ll << 20;  // 2 GiB of bundles
+// The first wave of a plan is closed at the end of the first planning batch
+// that brings it to this size: the device starts while the host plans on.
+constexpr long long kFirstWaveBundles = 1ll << 20;
 
 }  // namespace
 
@@ -596,8 +599,19 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
       fc_.sa[p][k] = in ? hctx_.pser.a[k + 2][p] : double2{0.0, 0.0};
       fc_.sb[p][k] = in ? hctx_.pser.b[k + 2][p] : double2{0.0, 0.0};
     }
-  for (int q = 1; q <= kMaxGauss; ++q)
-    gauss_rule(q, hctx_.gx + gauss_offset(q), hctx_.gw + gauss_offset(q));
+  {
+    // Gauss-Legendre rules 1 .. kMaxGauss: computed once per process
+    static const std::vector<double> rules = [] {
+      const size_t len = size_t(gauss_offset(kMaxGauss)) + kMaxGauss;
+      std::vector<double> r(2 * len);
+      for (int q = 1; q <= kMaxGauss; ++q)
+        gauss_rule(q, r.data() + gauss_offset(q), r.data() + len + gauss_offset(q));
+      return r;
+    }();
+    const size_t len = rules.size() / 2;
+    std::memcpy(hctx_.gx, rules.data(), len * sizeof(double));
+    std::memcpy(hctx_.gw, rules.data() + len, len * sizeof(double));
+  }
   hctx_.far_nodes = a.far_nodes;
   hctx_.refine = a.refine;
   hctx_.corner_n = scaled(a.corner_nodes);
@@ -1567,7 +1581,7 @@ void Problem::interaction(const std::vector<BasisReq>& req,
   // chunk plans appended in cell order: the same jobs, offsets and gather
   // order as a serial pass.
   double* base = tbuf.get();
-  const int nchunk = int(std::min<size_t>(nc_, size_t(4 * planning_threads())));
+  const int nchunk = int(std::min<size_t>(nc_, size_t(8 * planning_threads())));
   std::vector<FillPlan> parts(nchunk, FillPlan(n_, m, pcfg_.n_gauss));
   std::vector<ReusePart> rparts(nchunk);
   // Cross-level reuse (chained calls): the entry (enclosed node b, skeleton a
@@ -1689,7 +1703,8 @@ void Problem::interaction(const std::vector<BasisReq>& req,
     }
     for (int k = kb; k < ke; ++k) {
       acc += parts[k].bundles();
-      if (acc > kMaxBundlesPerWave || k == nchunk - 1) {
+      const bool first_early = k0 == 0 && k == ke - 1 && acc >= kFirstWaveBundles;
+      if (acc > kMaxBundlesPerWave || k == nchunk - 1 || first_early) {
         {
           PhaseTimer t_app("fill_plan_append", nullptr);
           plan.append_many(parts, k0, k + 1);
@@ -2397,11 +2412,21 @@ void run_blocked(Problem& P, const std::vector<T>& t, F blocks_of,
 }
 }  // namespace
 
+namespace {
+std::vector<char>& recorder_pool() {  // host task buffer of the last recording (API mutex held)
+  static std::vector<char> pool;
+  return pool;
+}
+}  // namespace
+
+void Recorder::begin() { pk_.adopt(std::move(recorder_pool())); }
+
 void Recorder::finalize(cudaStream_t st) {
   if (!pk_.bytes()) return;
   dev_.alloc(pk_.bytes());
   CK(cudaMemcpyAsync(dev_.get(), pk_.data(), pk_.bytes(), cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
+  recorder_pool() = pk_.take();  // the host copy is not needed again
 }
 
 void Recorder::replay(cudaStream_t st, int phase) {
@@ -2716,7 +2741,7 @@ void Fds::build() {
       if (!hs_) {
         // planned in contiguous chunks on the planning threads, appended in
         // cell order (same jobs and order as a serial pass)
-        const int nchunk = std::min(nlev, 4 * planning_threads());
+        const int nchunk = std::min(nlev, 8 * planning_threads());
         std::vector<FillPlan> parts(nchunk, FillPlan(n, P_.proxy_cfg().m_prime,
                                                      P_.proxy_cfg().n_gauss));
         std::vector<std::vector<CopyTask>> pcopies(nchunk);
@@ -2744,7 +2769,8 @@ void Fds::build() {
           for (int k = kb; k < ke; ++k) {
             copies.insert(copies.end(), pcopies[k].begin(), pcopies[k].end());
             acc += parts[k].bundles();
-            if (acc > kMaxBundlesPerWave || k == nchunk - 1) {
+            const bool first_early = k0 == 0 && k == ke - 1 && acc >= kFirstWaveBundles;
+            if (acc > kMaxBundlesPerWave || k == nchunk - 1 || first_early) {
               plan.append_many(parts, k0, k + 1);
               for (int q = k0; q <= k; ++q)
                 parts[q] = FillPlan(n, P_.proxy_cfg().m_prime, P_.proxy_cfg().n_gauss);
@@ -3152,11 +3178,19 @@ void Fds::record_solve(int m) {
   auto F = [&](int c) { return ws_f_.get() + 2 * fo[c] * m; };
   auto FT = [&](int c) { return ws_ft_.get() + 2 * ko[c] * m; };
   auto TT = [&](int c) { return ws_t_.get() + 2 * ko[c] * m; };
+  const double tr_alloc = now();
   P_.recorder = &S.rec;
+  S.rec.begin();
   S.rec.mark();
+  // task lists recycled across recordings (fresh vectors of this size cost
+  // thousands of page faults; API calls are serialised)
+  static std::vector<CopyTask> s_ct, s_back;
+  static std::vector<LuSolveTask> s_st;
+  static std::vector<GemmTask> s_g1, s_g2;
   // leaves: f = [rhs[a:a+s]; rhs[N+a:N+a+s]]
   {
-    std::vector<CopyTask> ct;
+    std::vector<CopyTask>& ct = s_ct;
+    ct.clear();
     for (int c = first(depth_); c <= last(depth_); ++c) {
       const int a = cells_[c].begin;
       ct.push_back(copy_task(rhs + 2 * size_t(a), 2 * n, F(c), 2 * leaf, leaf, m));
@@ -3165,8 +3199,11 @@ void Fds::record_solve(int m) {
     run_copies(P_, ct);
   }
   for (int level = depth_; level > cfg_.ell0; --level) {
-    std::vector<LuSolveTask> st;
-    std::vector<GemmTask> g1, g2;
+    std::vector<LuSolveTask>& st = s_st;
+    std::vector<GemmTask>&g1 = s_g1, &g2 = s_g2;
+    st.clear();
+    g1.clear();
+    g2.clear();
     for (int c = first(level); c <= last(level); ++c) {
       const Cell& C = cells_[c];
       const int nl = C.nloc, d = 2 * nl, k = C.k, kk = 2 * k;
@@ -3181,7 +3218,8 @@ void Fds::record_solve(int m) {
     run_gemms(P_, g1);
     run_gemms(P_, g2);
     // parent f = [ft1 top; ft2 top; ft1 bottom; ft2 bottom]
-    std::vector<CopyTask> ct;
+    std::vector<CopyTask>& ct = s_ct;
+    ct.clear();
     for (int c = first(level - 1); c <= last(level - 1); ++c) {
       const int c1 = 2 * c + 1, c2 = 2 * c + 2;
       const int k1 = cells_[c1].k, k2 = cells_[c2].k, np = k1 + k2;
@@ -3202,7 +3240,9 @@ void Fds::record_solve(int m) {
   // top: stack, solve, unstack (x of the top cells lives in their f blocks)
   {
     const int tf = first(cfg_.ell0), tl = last(cfg_.ell0);
-    std::vector<CopyTask> ct, back;
+    std::vector<CopyTask>&ct = s_ct, &back = s_back;
+    ct.clear();
+    back.clear();
     for (int i = 0; i <= tl - tf; ++i) {
       const int c = tf + i;
       const int d = 2 * cells_[c].nloc;
@@ -3219,8 +3259,11 @@ void Fds::record_solve(int m) {
   S.rec.mark();
   // downward: x_child = ainvf + ainv_u (atilde y - ftilde)
   for (int level = cfg_.ell0; level < depth_; ++level) {
-    std::vector<CopyTask> ct;
-    std::vector<GemmTask> g1, g2;
+    std::vector<CopyTask>& ct = s_ct;
+    std::vector<GemmTask>&g1 = s_g1, &g2 = s_g2;
+    ct.clear();
+    g1.clear();
+    g2.clear();
     for (int c = first(level); c <= last(level); ++c) {
       const int c1 = 2 * c + 1, c2 = 2 * c + 2;
       const int k1 = cells_[c1].k, k2 = cells_[c2].k, np = k1 + k2;
@@ -3242,7 +3285,8 @@ void Fds::record_solve(int m) {
     run_gemms(P_, g2);
   }
   {
-    std::vector<CopyTask> ct;
+    std::vector<CopyTask>& ct = s_ct;
+    ct.clear();
     for (int c = first(depth_); c <= last(depth_); ++c) {
       const int a = cells_[c].begin;
       ct.push_back(copy_task(F(c), 2 * leaf, x + 2 * size_t(a), 2 * n, leaf, m));
@@ -3264,8 +3308,8 @@ void Fds::record_solve(int m) {
     CK(cudaGraphInstantiate(&S.exec[ph], S.graph[ph], 0));
   }
   if (verbose_level())
-    std::fprintf(stderr, "[ebem] record_solve(%d): tasks %.1f ms, upload %.1f ms, graphs %.1f ms (%zu launches)\n",
-                 m, 1e3 * (tr1 - tr0), 1e3 * (tr2 - tr1), 1e3 * (now() - tr2), S.rec.n_launches());
+    std::fprintf(stderr, "[ebem] record_solve(%d): workspaces %.1f ms, tasks %.1f ms, upload %.1f ms, graphs %.1f ms (%zu launches)\n",
+                 m, 1e3 * (tr_alloc - tr0), 1e3 * (tr1 - tr_alloc), 1e3 * (tr2 - tr1), 1e3 * (now() - tr2), S.rec.n_launches());
 }
 
 Fds::~Fds() = default;  // SolvePlan releases its graphs

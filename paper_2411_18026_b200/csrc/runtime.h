@@ -186,6 +186,13 @@ class Pack {
   }
   size_t bytes() const { return buf_.size(); }
   const char* data() const { return buf_.data(); }
+  // Buffer recycling (a fresh 10 MB vector costs thousands of page faults):
+  // start from a used buffer's capacity / hand the buffer back.
+  void adopt(std::vector<char>&& b) {
+    buf_ = std::move(b);
+    buf_.clear();
+  }
+  std::vector<char> take() { return std::move(buf_); }
 
  private:
   std::vector<char> buf_;
@@ -301,6 +308,8 @@ class Recorder {
     launches_.push_back(l);
   }
   void mark() { marks_.push_back(int(launches_.size())); }
+  // Starts a recording on the process-wide recycled host buffer.
+  void begin();
   void finalize(cudaStream_t st);
   // launches between marks a and b (phase a of the recording)
   void replay(cudaStream_t st, int phase);
