@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <stdint.h>
 
@@ -94,11 +95,19 @@ __device__ __forceinline__ void wait_slot(const volatile int* prog, int need) {
 
 // Reflector of column i from the owning group's registers (warp-uniform call;
 // only the `mine` lanes write).  Waits for the ring slot to be free first.
+#ifdef EBEM_TSQR_TIMING
+#define TSQR_T0(v) const long long v = clock64()
+#define TSQR_ACC(acc, v) acc += clock64() - v
+#else
+#define TSQR_T0(v)
+#define TSQR_ACC(acc, v)
+#endif
 template <int LANES, int D, int W>
 __device__ __forceinline__ void make_reflector(double2 (&B)[kRpt], bool mine, int i,
                                                int g, double2* R, int t,
                                                double2* vring, double2* tring,
-                                               volatile int* seq, const volatile int* prog) {
+                                               volatile int* seq, const volatile int* prog,
+                                               long long& t_slot) {
   constexpr int kRows = LANES * kRpt;
   double p[4] = {0.0, 0.0, 0.0, 0.0};
   double2 alpha = make_double2(0.0, 0.0);
@@ -134,7 +143,11 @@ __device__ __forceinline__ void make_reflector(double2 (&B)[kRpt], bool mine, in
                           scal.x * B[k].y + scal.y * B[k].x);
     if (g == 0) R[pidx(i, i)] = make_double2(beta, 0.0);
   }
-  if (t >= D) wait_slot<W>(prog, t - D + 1);
+  {
+    TSQR_T0(c0);
+    if (t >= D) wait_slot<W>(prog, t - D + 1);
+    TSQR_ACC(t_slot, c0);
+  }
   const int slot = t % D;
   if (mine) {
     double2* v = vring + slot * kRows;
@@ -205,28 +218,42 @@ k_tsqr(const QrTask* __restrict__ tasks) {
   __syncthreads();
   volatile int* vprog = prog;
   volatile int* seq = seq_s;
+  long long t_slot = 0, t_seq = 0, t_make = 0, t_load = 0;
+  TSQR_T0(c_all);
   if (wfirst >= n) {  // no columns: never holds the ring back
     if (lane == 0) vprog[warp] = 0x7fffffff;
   } else {
     for (int r0 = 0, b = 0; r0 < rows; r0 += kRows, ++b) {
       const int t0 = b * n;  // global index of reflector 0 of this block
       double2 B[kRpt];
+      TSQR_T0(c_ld);
 #pragma unroll
       for (int k = 0; k < kRpt; ++k) {
         const int r = r0 + g + LANES * k;
         B[k] = (own && r < rows) ? src[r] : make_double2(0.0, 0.0);
       }
+#ifdef EBEM_TSQR_TIMING
+      if (B[0].x == 1.2345e300) t_load += 1;  // (forces the loads to complete here)
+#endif
+      TSQR_ACC(t_load, c_ld);
       if (own && r0 + kRows < rows) {  // warm L2 for the next block
         const int r = r0 + kRows + g * kRpt;
         if (r < rows) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + r));
       }
-      if (wfirst == 0)
+      if (wfirst == 0) {
+        TSQR_T0(c_mk);
         make_reflector<LANES, D, kWarpsPerCta>(B, j == 0, 0, g, R, t0, vring, tring, seq,
-                                               vprog);
+                                               vprog, t_slot);
+        TSQR_ACC(t_make, c_mk);
+      }
       for (int i = 0; i < wlast; ++i) {
         const int t = t0 + i;
         const int slot = t % D;
-        wait_seq(seq, slot, t);
+        {
+          TSQR_T0(c_sq);
+          wait_seq(seq, slot, t);
+          TSQR_ACC(t_seq, c_sq);
+        }
         const bool act = own && j > i;
         const double2* v = vring + slot * kRows;
         double2 rij = make_double2(0.0, 0.0);
@@ -260,9 +287,12 @@ k_tsqr(const QrTask* __restrict__ tasks) {
           __threadfence_block();
           vprog[warp] = t + 1;
         }
-        if (i + 1 >= wfirst)  // the warp owns column i + 1 (i + 1 <= wlast)
+        if (i + 1 >= wfirst) {  // the warp owns column i + 1 (i + 1 <= wlast)
+          TSQR_T0(c_mk);
           make_reflector<LANES, D, kWarpsPerCta>(B, j == i + 1, i + 1, g, R, t + 1, vring,
-                                                 tring, seq, vprog);
+                                                 tring, seq, vprog, t_slot);
+          TSQR_ACC(t_make, c_mk);
+        }
       }
       if (lane == 0) {  // nothing else of this block is read by this warp
         __threadfence_block();
@@ -270,6 +300,11 @@ k_tsqr(const QrTask* __restrict__ tasks) {
       }
     }
   }
+#ifdef EBEM_TSQR_TIMING
+  if (lane == 0 && blockIdx.x == gridDim.x / 2 && wfirst < n)
+    printf("tsqr n=%d rows=%d warp=%d all=%lld load=%lld seq=%lld make=%lld (slot=%lld)\n", n, rows,
+           warp, clock64() - c_all, t_load, t_seq, t_make, t_slot);
+#endif
   __syncthreads();
   double2* out = reinterpret_cast<double2*>(T.dst);
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
