@@ -1273,6 +1273,14 @@ k_getrs_cta(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
     const int r = t + kThreads * s;
     b[s] = r < n ? xs[r] : make_double2(0.0, 0.0);
   }
+  // 1 / U_rr of the thread's own rows, formed here so that the division is
+  // off the substitution chain of the U phase (same operations, same bits)
+  double2 rinv[kS];
+#pragma unroll
+  for (int s = 0; s < kS; ++s) {
+    const int r = t + kThreads * s;
+    rinv[s] = r < n ? zrcp(__ldg(A + (size_t)r * lda + r)) : make_double2(0.0, 0.0);
+  }
   // L y = b: x_0 is b_0; the owner of row k + 1 publishes it after step k
   if (t == 0) bc[0] = b[0];
   __syncthreads();
@@ -1302,7 +1310,7 @@ k_getrs_cta(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
 #pragma unroll
   for (int s = 0; s < kS; ++s)
     if (t + kThreads * s == n - 1) {
-      b[s] = zmul(b[s], zrcp(slot(0, s)));
+      b[s] = zmul(b[s], rinv[s]);
       bc[(n - 1) & 1] = b[s];
     }
   __syncthreads();
@@ -1320,7 +1328,7 @@ k_getrs_cta(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
           const int r = t + kThreads * s;
           if (r < k) b[s] = zfms(b[s], slot(q, s), xk);
           if (r == k - 1) {
-            b[s] = zmul(b[s], zrcp(slot((q + 1) % PF, s)));
+            b[s] = zmul(b[s], rinv[s]);
             bc[(k - 1) & 1] = b[s];
           }
         }
