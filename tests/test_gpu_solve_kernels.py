@@ -20,6 +20,8 @@ def rel(a, b):
     (100, 1), (100, 5),    # n = 200: one CTA per column
     (100, 16), (100, 37),  # n = 200: blocked panels (full and ragged column tiles)
     (60, 33),              # n = 120: blocked panels, order not a multiple of 32
+    (65, 1), (128, 2),     # n = 130, 256: column blocks of 16 (ragged / exact last block)
+    (129, 1), (250, 3),    # n = 258, 500: two rows per thread, column blocks of 8
     (200, 2),              # n = 400: CTA per column, two rows per thread
     (200, 20),             # n = 400: blocked panels, eight rows per lane group
     (700, 1),              # n = 1400: CTA per column, eight rows per thread
