@@ -1200,6 +1200,38 @@ k_getrs_warp(const LuSolveTask* __restrict__ tasks, const int* __restrict__ warp
   }
 }
 
+// The row interchanges of an LU composed into one permutation: perm[r] is the
+// row of b that ends up in row r (swaps applied in order to the identity).
+// One warp per task; the serial part runs on shared memory.
+constexpr int kPermWarps = 4;
+__global__ void __launch_bounds__(32 * kPermWarps)
+k_pivots_to_perm(const LuTask* __restrict__ tasks, int n_tasks) {
+  __shared__ int sm[kPermWarps][2 * kPermMaxN];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = blockIdx.x * kPermWarps + warp;
+  if (task >= n_tasks) return;
+  const LuTask T = tasks[task];
+  if (T.perm == nullptr || T.n > kPermMaxN) return;
+  int* idx = sm[warp];
+  int* piv = idx + kPermMaxN;
+  for (int r = lane; r < T.n; r += 32) {
+    idx[r] = r;
+    piv[r] = T.ipiv[r];
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int k = 0; k < T.n; ++k) {
+      const int p = piv[k];
+      if (p != k) {
+        const int v = idx[k];
+        idx[k] = idx[p];
+        idx[p] = v;
+      }
+    }
+  __syncwarp();
+  for (int r = lane; r < T.n; r += 32) T.perm[r] = idx[r];
+}
+
 // ------------------------------------------------ LU solve, one CTA each
 // One CTA (kThreads) per (task, right-hand side) for orders up to
 // kThreads * kS: thread t keeps rows t, t + kThreads, ... in registers and
@@ -1250,14 +1282,19 @@ k_getrs_cta(const LuSolveTask* __restrict__ tasks, const int* __restrict__ block
     asm volatile("cp.async.commit_group;\n" ::);
   };
   auto wait_oldest = [] { asm volatile("cp.async.wait_group %0;\n" ::"n"(PF - 1) : "memory"); };
+  const bool permuted = T.perm != nullptr;  // CTA-uniform
   for (int r = t; r < n; r += kThreads) {
-    xs[r] = bg[r];
-    sp[r] = __ldg(T.ipiv + r);
+    if (permuted) {
+      xs[r] = bg[__ldg(T.perm + r)];
+    } else {
+      xs[r] = bg[r];
+      sp[r] = __ldg(T.ipiv + r);
+    }
   }
 #pragma unroll
   for (int q = 0; q < PF; ++q) fetch(q < n - 1 ? q : -1, q);
   __syncthreads();
-  if (t == 0)
+  if (t == 0 && !permuted)
     for (int k = 0; k < n; ++k) {
       const int p = sp[k];
       if (p != k) {
@@ -1665,6 +1702,10 @@ void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st) {
   (void)attr;
   if (smem > size_t(kSmemCap)) throw std::length_error("interpolation: rank too large");
   k_interp<<<n, kThreads, smem, st>>>(tasks);
+}
+void launch_pivots_to_perm(const LuTask* tasks, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_pivots_to_perm<<<(n + kPermWarps - 1) / kPermWarps, 32 * kPermWarps, 0, st>>>(tasks, n);
 }
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st) {

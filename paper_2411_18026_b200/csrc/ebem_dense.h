@@ -50,13 +50,19 @@ struct LuTask {
   int in_smem;
   int pad;
   long long ws_off;
+  int* perm;  // optional (n <= kPermMaxN): the interchanges composed into one permutation
 };
+constexpr int kPermMaxN = 1024;
 
 struct LuSolveTask {
   const double* lu;
   const int* ipiv;
   double* b;
   int n, ld, nrhs, ldb;
+  // optional: row r of the permuted right-hand side is row perm[r] of b (the
+  // interchanges ipiv applied in order); spares the few-column solves their
+  // serial interchange loop
+  const int* perm;
 };
 
 // trans: 0 = N, 1 = T, 2 = C (conjugate transpose)
@@ -100,6 +106,8 @@ int tsqr_ctas_per_sm(int n);
 size_t tsqr_smem_bytes(int n);
 void launch_tsqr(const QrTask* tasks, int n_tasks, int variant, size_t smem,
                  cudaStream_t st);
+// perm of every task that asks for one, from its ipiv (one warp per task).
+void launch_pivots_to_perm(const LuTask* tasks, int n, cudaStream_t st);
 void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st);
 void launch_getrf(const LuTask* tasks, int n, size_t smem, double2* gws,
                   cudaStream_t st);

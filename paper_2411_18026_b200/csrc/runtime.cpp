@@ -2550,6 +2550,12 @@ void run_getrf(Problem& P, std::vector<LuTask> t) {
   g_prof.begin(P.stream());
   launch_getrf(Pack::at<LuTask>(tb, o), int(small.size()), smem, P.gws.get(), P.stream());
   launch_lu_blocked(Pack::at<LuTask>(tb, ob), int(big.size()), big_n, P.stream());
+  bool any_perm = false;
+  for (const LuTask& x : t) any_perm = any_perm || x.perm != nullptr;
+  if (any_perm) {  // the interchanges composed for the few-column solves
+    launch_pivots_to_perm(Pack::at<LuTask>(tb, o), int(small.size()), P.stream());
+    launch_pivots_to_perm(Pack::at<LuTask>(tb, ob), int(big.size()), P.stream());
+  }
   g_prof.end(KP_GETRF, P.stream(), fl, by);
   P.staging.fence(P.stream());
   CK(cudaGetLastError());
@@ -2711,11 +2717,12 @@ void Fds::build() {
       piv_total += 2 * C.nloc;
     }
     S.lu.alloc(2 * lu_total + 2);
-    S.ipiv.alloc(piv_total + 1);
+    S.ipiv.alloc(2 * piv_total + 2);  // interchanges, then the composed permutations
     for (int i = 0; i < nlev; ++i) {
       Cell& C = cells_[f + i];
       C.lu = S.lu.get() + 2 * lu_off[i];
       C.ipiv = S.ipiv.get() + piv_off[i];
+      C.perm = 2 * C.nloc <= kPermMaxN ? S.ipiv.get() + piv_total + 1 + piv_off[i] : nullptr;
     }
     // A host BlockSource sees the reference's callback order (cell_basis of
     // a cell before its diagonal block, fds.cpp:77-89), so for it this
@@ -2795,6 +2802,7 @@ void Fds::build() {
         LuTask t{};
         t.a = C.lu;
         t.ipiv = C.ipiv;
+        t.perm = C.perm;
         t.n = 2 * C.nloc;
         t.ld = 2 * C.nloc;
         lt.push_back(t);
@@ -2951,7 +2959,7 @@ void Fds::build() {
   top_dim_ = top_off_.back();
   stats_.top_dim = top_dim_;
   top_lu_.alloc(2 * size_t(top_dim_) * top_dim_ + 2);
-  top_ipiv_.alloc(top_dim_ + 1);
+  top_ipiv_.alloc(2 * size_t(top_dim_) + 2);  // interchanges, then the composed permutation
   if (hs_ && top_dim_ > 0) {  // host source: the dense top system on the host
     std::vector<double> h(2 * size_t(top_dim_) * top_dim_, 0.0);
     for (int i = 0; i <= tl - tf; ++i) {
@@ -3000,6 +3008,7 @@ void Fds::build() {
       LuTask t{};
       t.a = top_lu_.get();
       t.ipiv = top_ipiv_.get();
+      t.perm = top_dim_ <= kPermMaxN ? top_ipiv_.get() + top_dim_ + 1 : nullptr;
       t.n = top_dim_;
       t.ld = top_dim_;
       t.info = lu_info(top_dim_);
@@ -3207,7 +3216,7 @@ void Fds::record_solve(int m) {
     for (int c = first(level); c <= last(level); ++c) {
       const Cell& C = cells_[c];
       const int nl = C.nloc, d = 2 * nl, k = C.k, kk = 2 * k;
-      st.push_back(LuSolveTask{C.lu, C.ipiv, F(c), d, d, m, d});  // ainvf in place
+      st.push_back(LuSolveTask{C.lu, C.ipiv, F(c), d, d, m, d, C.perm});  // ainvf in place
       if (k == 0) continue;
       g1.push_back(gemm_task(C.v, k, F(c), d, TT(c), kk, k, m, nl, 0.0));
       g1.push_back(gemm_task(C.v + 2 * size_t(k) * nl, k, F(c) + 2 * size_t(nl), d,
@@ -3253,7 +3262,8 @@ void Fds::record_solve(int m) {
     run_copies(P_, ct);
     if (top_dim_ > 0)
       run_getrs(P_, {LuSolveTask{top_lu_.get(), top_ipiv_.get(), ws_x_.get(), top_dim_,
-                                 top_dim_, m, top_dim_}});
+                                 top_dim_, m, top_dim_,
+                                 top_dim_ <= kPermMaxN ? top_ipiv_.get() + top_dim_ + 1 : nullptr}});
     run_copies(P_, back);
   }
   S.rec.mark();

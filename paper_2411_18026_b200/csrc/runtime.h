@@ -562,6 +562,7 @@ class Fds {
     // device factors
     double* lu = nullptr;
     int* ipiv = nullptr;
+    int* perm = nullptr;  // the interchanges composed (single-RHS solves)
     double* ainv_u = nullptr;  // 2n x 2k
     double* v = nullptr;       // V0 (k x n) then V1 (k x n)
     double* atilde = nullptr;  // 2k x 2k
