@@ -1703,6 +1703,21 @@ void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st) {
   if (smem > size_t(kSmemCap)) throw std::length_error("interpolation: rank too large");
   k_interp<<<n, kThreads, smem, st>>>(tasks);
 }
+__global__ void __launch_bounds__(256)
+k_prefetch_l2(const PrefetchTask* __restrict__ tasks, int n) {
+  const unsigned long long tid = blockIdx.x * 256ull + threadIdx.x;
+  const unsigned long long nth = gridDim.x * 256ull;
+  for (int i = 0; i < n; ++i) {
+    const char* p = static_cast<const char*>(tasks[i].p);
+    const unsigned long long lines = (tasks[i].bytes + 127) >> 7;
+    for (unsigned long long q = tid; q < lines; q += nth)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p + (q << 7)));
+  }
+}
+void launch_prefetch_l2(const PrefetchTask* tasks, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_prefetch_l2<<<148 * 4, 256, 0, st>>>(tasks, n);
+}
 void launch_pivots_to_perm(const LuTask* tasks, int n, cudaStream_t st) {
   if (n <= 0) return;
   k_pivots_to_perm<<<(n + kPermWarps - 1) / kPermWarps, 32 * kPermWarps, 0, st>>>(tasks, n);

@@ -106,6 +106,14 @@ int tsqr_ctas_per_sm(int n);
 size_t tsqr_smem_bytes(int n);
 void launch_tsqr(const QrTask* tasks, int n_tasks, int variant, size_t smem,
                  cudaStream_t st);
+// L2 warm-up of byte ranges (prefetch.global.L2, one line per thread step):
+// the solve's upper tree levels are few, latency-bound launches whose
+// factors fit the L2.
+struct PrefetchTask {
+  const void* p;
+  unsigned long long bytes;
+};
+void launch_prefetch_l2(const PrefetchTask* tasks, int n, cudaStream_t st);
 // perm of every task that asks for one, from its ipiv (one warp per task).
 void launch_pivots_to_perm(const LuTask* tasks, int n, cudaStream_t st);
 void launch_interp(const InterpTask* tasks, int n, int max_k, cudaStream_t st);

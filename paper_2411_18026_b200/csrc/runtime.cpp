@@ -2424,6 +2424,11 @@ void Recorder::begin() { pk_.adopt(std::move(recorder_pool())); }
 void Recorder::finalize(cudaStream_t st) {
   if (!pk_.bytes()) return;
   dev_.alloc(pk_.bytes());
+  for (const Launch& l : launches_)  // the warm-ups cover the task arrays too
+    if (l.kind == kPrefetchKind) {
+      PrefetchTask* pt = reinterpret_cast<PrefetchTask*>(pk_.mutable_data() + l.task_off);
+      pt[l.n_tasks - 1] = PrefetchTask{dev_.get(), pk_.bytes()};
+    }
   CK(cudaMemcpyAsync(dev_.get(), pk_.data(), pk_.bytes(), cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
   recorder_pool() = pk_.take();  // the host copy is not needed again
@@ -2445,6 +2450,9 @@ void Recorder::replay(cudaStream_t st, int phase) {
       case KP_GETRS:
         launch_getrs(Pack::at<LuSolveTask>(base, l.task_off), boff, l.n_tasks, l.n_blocks, st,
                      l.aux, l.aux2 & 0xffff, (l.aux2 >> 16) - 2);
+        break;
+      case kPrefetchKind:
+        launch_prefetch_l2(Pack::at<PrefetchTask>(base, l.task_off), l.n_tasks, st);
         break;
       default:
         throw Error(EBEM_LOGIC_ERROR, "Recorder: unexpected kernel kind");
@@ -3207,7 +3215,42 @@ void Fds::record_solve(int m) {
     }
     run_copies(P_, ct);
   }
+  // The upper levels are few-CTA, latency-bound launches: warm the L2 with
+  // their factors (and the task arrays) right before the first of them.
+  // lp = the lowest level such that the factors of levels ell0+1 .. lp and
+  // the top LU fit half the L2 (EBEM_SOLVE_PREFETCH_MB, 0 = off).
+  int lp = -1;
+  std::vector<PrefetchTask> warm;
+  {
+    static const double cap_mb = [] {
+      const char* e = std::getenv("EBEM_SOLVE_PREFETCH_MB");
+      return e ? std::atof(e) : 64.0;
+    }();
+    auto bytes_of = [&](const Store& s) {
+      return 8.0 * (s.lu.size() + s.ainv_u.size() + s.v.size() + s.atilde.size()) +
+             4.0 * s.ipiv.size();
+    };
+    double acc = 8.0 * top_lu_.size();
+    for (int l = cfg_.ell0 + 1; l <= depth_; ++l) {
+      acc += bytes_of(store_[l]);
+      if (acc > cap_mb * 1048576.0) break;
+      lp = l;
+    }
+    if (lp > cfg_.ell0) {
+      warm.push_back(PrefetchTask{top_lu_.get(), 8ull * top_lu_.size()});
+      warm.push_back(PrefetchTask{top_ipiv_.get(), 4ull * top_ipiv_.size()});
+      for (int l = cfg_.ell0 + 1; l <= lp; ++l) {
+        const Store& s = store_[l];
+        warm.push_back(PrefetchTask{s.lu.get(), 8ull * s.lu.size()});
+        warm.push_back(PrefetchTask{s.ipiv.get(), 4ull * s.ipiv.size()});
+        warm.push_back(PrefetchTask{s.ainv_u.get(), 8ull * s.ainv_u.size()});
+        warm.push_back(PrefetchTask{s.v.get(), 8ull * s.v.size()});
+        warm.push_back(PrefetchTask{s.atilde.get(), 8ull * s.atilde.size()});
+      }
+    }
+  }
   for (int level = depth_; level > cfg_.ell0; --level) {
+    if (level == lp) S.rec.add_prefetch(warm);
     std::vector<LuSolveTask>& st = s_st;
     std::vector<GemmTask>&g1 = s_g1, &g2 = s_g2;
     st.clear();

@@ -186,6 +186,7 @@ class Pack {
   }
   size_t bytes() const { return buf_.size(); }
   const char* data() const { return buf_.data(); }
+  char* mutable_data() { return buf_.data(); }
   // Buffer recycling (a fresh 10 MB vector costs thousands of page faults):
   // start from a used buffer's capacity / hand the buffer back.
   void adopt(std::vector<char>&& b) {
@@ -308,6 +309,17 @@ class Recorder {
     launches_.push_back(l);
   }
   void mark() { marks_.push_back(int(launches_.size())); }
+  // An L2 warm-up of the given ranges plus this recording's own task arrays
+  // (their range is filled in by finalize).
+  void add_prefetch(std::vector<PrefetchTask> ranges) {
+    ranges.push_back(PrefetchTask{nullptr, 0});
+    Launch l{};
+    l.kind = kPrefetchKind;
+    l.task_off = pk_.add(ranges);
+    l.n_tasks = int(ranges.size());
+    launches_.push_back(l);
+  }
+  static constexpr int kPrefetchKind = 1000;
   // Starts a recording on the process-wide recycled host buffer.
   void begin();
   void finalize(cudaStream_t st);
