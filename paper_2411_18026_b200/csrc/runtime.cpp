@@ -1679,6 +1679,27 @@ void Problem::interaction(const std::vector<BasisReq>& req,
   // waves: consecutive chunks until the bundle count passes the cap (the
   // chunk that crosses it closes the wave), concatenated in parallel
   FillPlan plan(n_, m, pcfg_.n_gauss);
+  // Upper levels (few cells, each with a near field of 10^4 .. 10^5 enclosed
+  // nodes that takes milliseconds to plan): the proxy blocks, quick to plan,
+  // go first as a wave of their own, so the device works on them while the
+  // host plans the near field.
+  const bool proxy_first = nc_ <= 512 && nc_ > 0;
+  if (proxy_first) {
+    {
+      PhaseTimer t_plan("fill_plan", nullptr);
+      parallel_for(nchunk, [&](int k) {
+        const size_t c0 = nc_ * size_t(k) / nchunk, c1 = nc_ * size_t(k + 1) / nchunk;
+        for (size_t c = c0; c < c1; ++c)
+          parts[k].add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, *req[c].rows,
+                             *req[c].cols, base + 2 * tv_off[c], n_out[c],
+                             base + 2 * tu_off[c], n_out[c]);
+      });
+    }
+    plan.append_many(parts, 0, nchunk);
+    for (int q = 0; q < nchunk; ++q) parts[q] = FillPlan(n_, m, pcfg_.n_gauss);
+    tl_mark("  proxy wave planned");
+    execute(plan);
+  }
   int k0 = 0;
   long long acc = 0;
   const int batch = std::max(1, planning_threads());
@@ -1695,8 +1716,9 @@ void Problem::interaction(const std::vector<BasisReq>& req,
           double* tv = base + 2 * tv_off[c];
           double* tu = base + 2 * tu_off[c];
           const int no = n_out[c];
-          parts[k].add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv,
-                             no, tu, no);
+          if (!proxy_first)
+            parts[k].add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv,
+                               no, tu, no);
           plan_near(parts[k], rparts[k], c, tv, tu);
         }
       });
