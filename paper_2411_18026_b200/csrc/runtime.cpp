@@ -1591,14 +1591,25 @@ void Problem::interaction(const std::vector<BasisReq>& req,
   // copied from the child's matrices (previous level, other buffer); the
   // near-field fill of the cell covers the remaining enclosed nodes only,
   // one job per child.
-  auto plan_near = [&](FillPlan& fp, ReusePart& rp, size_t c, double* tv, double* tu) {
+  // What the near-field jobs of one cell look like: whether its enclosed
+  // nodes split per child (reuse), and which of them each child's job keeps.
+  struct NearPrep {
+    bool split = false;
+    int kc[2] = {0, 0};
+    std::vector<int> rest[2];
+    bool whole[2] = {true, true};  // child x keeps every enclosed node
+  };
+  auto prep_near = [&](NearPrep& np, ReusePart& rp, size_t c) {
+    double* tv = base + 2 * tv_off[c];
+    double* tu = base + 2 * tu_off[c];
     const Lists& rows = *req[c].rows;
     const Lists& cols = *req[c].cols;
     const int no = n_out[c];
     const std::vector<int>& enc = geom[c].enclosed;
     const int ne = int(enc.size());
     bool ok = prev != nullptr && ne > 0;
-    int ch[2] = {-1, -1}, kc[2] = {0, 0};
+    int ch[2] = {-1, -1};
+    int (&kc)[2] = np.kc;
     for (int x = 0; ok && x < 2; ++x) {
       ch[x] = req[c].child[x];
       ok = ch[x] >= 0 && ch[x] < int(prev->geom.size());
@@ -1615,33 +1626,18 @@ void Problem::interaction(const std::vector<BasisReq>& req,
       }
     }
     std::vector<int2> common[2];
-    std::vector<int> rest[2];
     if (ok) {
       for (int x = 0; x < 2; ++x)
-        intersect_enclosed(enc, prev->geom[ch[x]].enclosed, common[x], rest[x]);
+        intersect_enclosed(enc, prev->geom[ch[x]].enclosed, common[x], np.rest[x]);
       ok = !common[0].empty() || !common[1].empty();
     }
-    if (!ok) {
-      fp.add_sym_near(enc, rows, cols, tv, no, tu, no);
-      return;
-    }
+    np.split = ok;
+    if (!ok) return;
     const int nc0 = int(cols[0].size()), nr0 = int(rows[0].size());
     for (int x = 0; x < 2; ++x) {
       const int j0 = x ? kc[0] : 0, k = kc[x];
-      if (k == 0) continue;
-      Lists rs, cs;
-      for (int p = 0; p < 2; ++p) {
-        rs[p].assign(rows[p].begin() + j0, rows[p].begin() + j0 + k);
-        cs[p].assign(cols[p].begin() + j0, cols[p].begin() + j0 + k);
-      }
-      const int rdest[2] = {j0, nr0 + j0}, cdest[2] = {j0, nc0 + j0};
-      if (common[x].empty()) {
-        fp.add_sym_near_part(enc, nullptr, ne, rs, rdest, cs, cdest, tv, no, tu, no);
-        continue;
-      }
-      std::vector<int> sub(rest[x].size());
-      for (size_t i = 0; i < sub.size(); ++i) sub[i] = enc[rest[x][i]];
-      fp.add_sym_near_part(sub, &rest[x], ne, rs, rdest, cs, cdest, tv, no, tu, no);
+      np.whole[x] = common[x].empty();
+      if (k == 0 || common[x].empty()) continue;
       // copies: T_V columns from the child's cols skeletons, T_U from rows
       const int cc = ch[x];
       const int cne = int(prev->geom[cc].enclosed.size());
@@ -1673,6 +1669,59 @@ void Problem::interaction(const std::vector<BasisReq>& req,
       }
     }
   };
+  // Number of enclosed nodes the job of child x (x = -1: the unsplit cell) keeps.
+  auto near_count = [&](const NearPrep& np, size_t c, int x) {
+    if (x < 0 || np.whole[x]) return int(geom[c].enclosed.size());
+    return int(np.rest[x].size());
+  };
+  // The near-field job of child x of cell c over the kept enclosed nodes
+  // [lo, hi) (all of them: the job the unsplit planner makes).
+  auto plan_piece = [&](FillPlan& fp, const NearPrep& np, size_t c, int x, int lo, int hi) {
+    double* tv = base + 2 * tv_off[c];
+    double* tu = base + 2 * tu_off[c];
+    const Lists& rows = *req[c].rows;
+    const Lists& cols = *req[c].cols;
+    const int no = n_out[c];
+    const std::vector<int>& enc = geom[c].enclosed;
+    const int ne = int(enc.size());
+    const int nc0 = int(cols[0].size()), nr0 = int(rows[0].size());
+    const bool all = lo == 0 && hi == near_count(np, c, x);
+    const bool identity = x < 0 || np.whole[x];
+    std::vector<int> sub, pos;
+    if (!(all && identity)) {
+      sub.resize(hi - lo);
+      pos.resize(hi - lo);
+      for (int i = lo; i < hi; ++i) {
+        pos[i - lo] = identity ? i : np.rest[x][i];
+        sub[i - lo] = enc[pos[i - lo]];
+      }
+    }
+    const std::vector<int>& nodes = (all && identity) ? enc : sub;
+    const std::vector<int>* pp = (all && identity) ? nullptr : &pos;
+    if (x < 0) {
+      const int rdest[2] = {0, nr0}, cdest[2] = {0, nc0};
+      fp.add_sym_near_part(nodes, pp, ne, rows, rdest, cols, cdest, tv, no, tu, no);
+      return;
+    }
+    const int j0 = x ? np.kc[0] : 0, k = np.kc[x];
+    if (k == 0) return;
+    Lists rs, cs;
+    for (int p = 0; p < 2; ++p) {
+      rs[p].assign(rows[p].begin() + j0, rows[p].begin() + j0 + k);
+      cs[p].assign(cols[p].begin() + j0, cols[p].begin() + j0 + k);
+    }
+    const int rdest[2] = {j0, nr0 + j0}, cdest[2] = {j0, nc0 + j0};
+    fp.add_sym_near_part(nodes, pp, ne, rs, rdest, cs, cdest, tv, no, tu, no);
+  };
+  auto plan_near = [&](FillPlan& fp, ReusePart& rp, size_t c) {
+    NearPrep np;
+    prep_near(np, rp, c);
+    if (!np.split) {
+      plan_piece(fp, np, c, -1, 0, near_count(np, c, -1));
+      return;
+    }
+    for (int x = 0; x < 2; ++x) plan_piece(fp, np, c, x, 0, near_count(np, c, x));
+  };
   // Chunks are planned a batch (one chunk per planning thread) at a time and
   // every wave is executed as soon as its chunks are planned, so the device
   // starts on the first wave while the host plans the rest.
@@ -1699,11 +1748,62 @@ void Problem::interaction(const std::vector<BasisReq>& req,
     for (int q = 0; q < nchunk; ++q) parts[q] = FillPlan(n_, m, pcfg_.n_gauss);
     tl_mark("  proxy wave planned");
     execute(plan);
+    // The near fields in pieces of kPiece enclosed nodes per job: a cell's
+    // near field is planned by many threads at once and the first wave is
+    // ready after one piece per thread, not after whole cells.
+    constexpr int kPiece = 8192;
+    std::vector<NearPrep> preps(nc_);
+    rparts.assign(nc_, ReusePart{});
+    {
+      PhaseTimer t_plan("fill_plan", nullptr);
+      parallel_for(int(nc_), [&](int c) { prep_near(preps[c], rparts[c], size_t(c)); });
+    }
+    struct Item {
+      int c, x, lo, hi;
+    };
+    std::vector<Item> items;
+    for (size_t c = 0; c < nc_; ++c)
+      for (int x = preps[c].split ? 0 : -1; x < (preps[c].split ? 2 : 0); ++x) {
+        if (x >= 0 && preps[c].kc[x] == 0) continue;
+        const int cnt = near_count(preps[c], c, x);
+        for (int lo = 0; lo < cnt; lo += kPiece)
+          items.push_back(Item{int(c), x, lo, std::min(cnt, lo + kPiece)});
+      }
+    const int nitems = int(items.size());
+    std::vector<FillPlan> iparts(nitems, FillPlan(n_, m, pcfg_.n_gauss));
+    const int ibatch = std::max(1, planning_threads());
+    int i0 = 0;
+    long long iacc = 0;
+    for (int ib = 0; ib < nitems; ib += ibatch) {
+      const int ie = std::min(nitems, ib + ibatch);
+      {
+        PhaseTimer t_plan("fill_plan", nullptr);
+        parallel_for(ie - ib, [&](int kk) {
+          const Item& it = items[ib + kk];
+          plan_piece(iparts[ib + kk], preps[it.c], size_t(it.c), it.x, it.lo, it.hi);
+        });
+      }
+      for (int k = ib; k < ie; ++k) {
+        iacc += iparts[k].bundles();
+        const bool first_early = i0 == 0 && k == ie - 1 && iacc >= kFirstWaveBundles;
+        if (iacc > kMaxBundlesPerWave || k == nitems - 1 || first_early) {
+          {
+            PhaseTimer t_app("fill_plan_append", nullptr);
+            plan.append_many(iparts, i0, k + 1);
+            for (int q = i0; q <= k; ++q) iparts[q] = FillPlan(n_, m, pcfg_.n_gauss);
+          }
+          tl_mark("  wave planned");
+          execute(plan);
+          i0 = k + 1;
+          iacc = 0;
+        }
+      }
+    }
   }
   int k0 = 0;
   long long acc = 0;
   const int batch = std::max(1, planning_threads());
-  for (int kb = 0; kb < nchunk; kb += batch) {
+  for (int kb = 0; !proxy_first && kb < nchunk; kb += batch) {
     const int ke = std::min(nchunk, kb + batch);
     {
       PhaseTimer t_plan("fill_plan", nullptr);
@@ -1719,7 +1819,7 @@ void Problem::interaction(const std::vector<BasisReq>& req,
           if (!proxy_first)
             parts[k].add_proxy(geom[c].cx, geom[c].cy, geom[c].radius, rows, cols, tv,
                                no, tu, no);
-          plan_near(parts[k], rparts[k], c, tv, tu);
+          plan_near(parts[k], rparts[k], c);
         }
       });
     }
