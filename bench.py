@@ -98,7 +98,7 @@ class ClockSampler:
                  "clocks_event_reasons.sw_thermal_slowdown,"
                  "clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-i", os.environ.get("LOCAL_RANK", "0"),
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("EBEM_BENCH_SMI_MS", "200")], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self._p = None
