@@ -210,7 +210,11 @@ char* Staging::put(const Pack& pk, cudaStream_t st) {
   }
   const size_t bytes = pk.bytes();
   if (bytes > x.cap) {
-    const size_t cap = std::max(std::max(bytes + bytes / 2, 2 * x.cap), size_t(32) << 20);
+    // grow to the largest size any slot has needed so far: the slots rotate,
+    // and each regrowth frees device memory (a device-wide synchronisation)
+    static size_t high_water = 0;
+    high_water = std::max(high_water, std::max(std::max(bytes + bytes / 2, 2 * x.cap), size_t(32) << 20));
+    const size_t cap = high_water;
     if (x.host) CK(cudaFreeHost(x.host));
     if (x.dev) CK(cudaFree(x.dev));
     CK(cudaMallocHost(reinterpret_cast<void**>(&x.host), cap));
