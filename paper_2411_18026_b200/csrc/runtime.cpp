@@ -2263,39 +2263,51 @@ void Problem::bases(const std::vector<BasisReq>& req, double eps,
   tl_mark("  readback");
   check_domain();  // the fill's element-length guard, read after the sync
 
-  // ---- shared rank (basis_from_interactions, compression.cpp:92-99)
+  // ---- shared rank (basis_from_interactions, compression.cpp:92-99), on the
+  // planning threads; the offsets follow serially
+  {
+    const int nch = int(std::min<size_t>(ncell, size_t(4 * planning_threads())));
+    parallel_for(nch, [&](int kq) {
+      const size_t c0 = ncell * size_t(kq) / nch, c1 = ncell * size_t(kq + 1) / nch;
+      for (size_t c = c0; c < c1; ++c) {
+        int k = 0, cap = std::numeric_limits<int>::max();
+        for (int a = 0; a < 4; ++a) {
+          const size_t i = 4 * c + a;
+          const double* rd = h_rd + jp_off[i];
+          const int steps = h_steps[i];
+          const int mn = std::min(q[i].rows, q[i].n);
+          // eps_rank(eps): first j with |R_jj| <= eps |R_00| (0 if R_00 == 0)
+          int er;
+          if (steps == 0 && mn > 0 && rd[0] == 0.0) {
+            er = 0;
+          } else {
+            er = std::min(steps, mn);
+            const int lim = std::min(steps + 1, mn);
+            for (int j = 0; j < lim; ++j)
+              if (rd[j] <= eps * rd[0]) { er = j; break; }
+          }
+          k = std::max(k, er);
+          cap = std::min(cap, steps);
+        }
+        k = std::min(k, cap);
+        const Lists& rows = *req[c].rows;
+        const Lists& cols = *req[c].cols;
+        BasisRes& r = res[c];
+        r.k = k;
+        r.saturated = k >= std::min(std::min(cols[0].size(), cols[1].size()),
+                                    std::min(rows[0].size(), rows[1].size()));
+      }
+    });
+  }
   size_t v_total = 0, u_total = 0;
   for (size_t c = 0; c < ncell; ++c) {
-    int k = 0, cap = std::numeric_limits<int>::max();
-    for (int a = 0; a < 4; ++a) {
-      const size_t i = 4 * c + a;
-      const double* rd = h_rd + jp_off[i];
-      const int steps = h_steps[i];
-      const int mn = std::min(q[i].rows, q[i].n);
-      // eps_rank(eps): first j with |R_jj| <= eps |R_00| (0 if R_00 == 0)
-      int er;
-      if (steps == 0 && mn > 0 && rd[0] == 0.0) {
-        er = 0;
-      } else {
-        er = std::min(steps, mn);
-        const int lim = std::min(steps + 1, mn);
-        for (int j = 0; j < lim; ++j)
-          if (rd[j] <= eps * rd[0]) { er = j; break; }
-      }
-      k = std::max(k, er);
-      cap = std::min(cap, steps);
-    }
-    k = std::min(k, cap);
     const Lists& rows = *req[c].rows;
     const Lists& cols = *req[c].cols;
     BasisRes& r = res[c];
-    r.k = k;
-    r.saturated = k >= std::min(std::min(cols[0].size(), cols[1].size()),
-                                std::min(rows[0].size(), rows[1].size()));
     r.v_off = v_total;
-    v_total += size_t(k) * (cols[0].size() + cols[1].size());
+    v_total += size_t(r.k) * (cols[0].size() + cols[1].size());
     r.u_off = u_total;
-    u_total += size_t(k) * (rows[0].size() + rows[1].size());
+    u_total += size_t(r.k) * (rows[0].size() + rows[1].size());
   }
   // (the skeleton lists are filled in after the interpolation launch below:
   // the device needs only the ranks)
