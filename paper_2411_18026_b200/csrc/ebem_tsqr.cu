@@ -283,7 +283,9 @@ k_tsqr(const QrTask* __restrict__ tasks) {
           if (g == 0) R[pidx(i, j)] = make_double2(rij.x - fr, rij.y - fi);
         }
         __syncwarp();
-        if (lane == 0) {  // slot t read by this warp
+        // progress (slot reuse) published every fourth reflector and before
+        // the warp's own reflectors: a fence and a store less per step
+        if (lane == 0 && ((i & 3) == 3 || i + 1 >= wfirst)) {  // slots <= t read by this warp
           __threadfence_block();
           vprog[warp] = t + 1;
         }
