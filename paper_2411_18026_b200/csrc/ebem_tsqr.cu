@@ -102,19 +102,19 @@ __device__ __forceinline__ void wait_slot(const volatile int* prog, int need) {
 #define TSQR_T0(v)
 #define TSQR_ACC(acc, v)
 #endif
-template <int LANES, int D, int W>
-__device__ __forceinline__ void make_reflector(double2 (&B)[kRpt], bool mine, int i,
+template <int LANES, int RPT, int D, int W>
+__device__ __forceinline__ void make_reflector(double2 (&B)[RPT], bool mine, int i,
                                                int g, double2* R, int t,
                                                double2* vring, double2* tring,
                                                volatile int* seq, const volatile int* prog,
                                                long long& t_slot) {
-  constexpr int kRows = LANES * kRpt;
+  constexpr int kRows = LANES * RPT;
   double p[4] = {0.0, 0.0, 0.0, 0.0};
   double2 alpha = make_double2(0.0, 0.0);
   if (mine) {
     alpha = R[pidx(i, i)];
 #pragma unroll
-    for (int k = 0; k < kRpt; ++k)
+    for (int k = 0; k < RPT; ++k)
       p[k & 3] = fma(B[k].x, B[k].x, fma(B[k].y, B[k].y, p[k & 3]));
   }
   const double xnorm2 = group_sum<LANES>((p[0] + p[1]) + (p[2] + p[3]));
@@ -138,7 +138,7 @@ __device__ __forceinline__ void make_reflector(double2 (&B)[kRpt], bool mine, in
     const double id = s / fma(arn, arn, ain * ain);
     const double2 scal = make_double2(arn * id, -ain * id);
 #pragma unroll
-    for (int k = 0; k < kRpt; ++k)
+    for (int k = 0; k < RPT; ++k)
       B[k] = make_double2(scal.x * B[k].x - scal.y * B[k].y,
                           scal.x * B[k].y + scal.y * B[k].x);
     if (g == 0) R[pidx(i, i)] = make_double2(beta, 0.0);
@@ -152,7 +152,7 @@ __device__ __forceinline__ void make_reflector(double2 (&B)[kRpt], bool mine, in
   if (mine) {
     double2* v = vring + slot * kRows;
 #pragma unroll
-    for (int k = 0; k < kRpt; ++k) v[g + LANES * k] = B[k];
+    for (int k = 0; k < RPT; ++k) v[g + LANES * k] = B[k];
     if (g == 0) tring[slot] = tau;
   }
   __syncwarp();
@@ -190,11 +190,11 @@ __device__ __forceinline__ void wait_seq(const volatile int* seq, int slot, int 
 // owner), so a warp whose columns are done moves on to the next block at
 // once: the reflector chains of consecutive blocks overlap instead of the
 // whole CTA stepping through n reflectors per block in lock step.
-template <int LANES, int THREADS, int D, int REGS>
+template <int LANES, int RPT, int THREADS, int D, int REGS>
 __global__ void __launch_bounds__(THREADS, (65536 / (THREADS * REGS)) > 0 ? 65536 / (THREADS * REGS) : 1)
 k_tsqr(const QrTask* __restrict__ tasks) {
   constexpr int kWarpsPerCta = THREADS / 32;
-  constexpr int kRows = LANES * kRpt;
+  constexpr int kRows = LANES * RPT;
   constexpr int kGroupsPerWarp = 32 / LANES;
   extern __shared__ double2 R[];  // packed upper triangle | v ring | tau ring
   __shared__ int seq_s[D];
@@ -225,10 +225,10 @@ k_tsqr(const QrTask* __restrict__ tasks) {
   } else {
     for (int r0 = 0, b = 0; r0 < rows; r0 += kRows, ++b) {
       const int t0 = b * n;  // global index of reflector 0 of this block
-      double2 B[kRpt];
+      double2 B[RPT];
       TSQR_T0(c_ld);
 #pragma unroll
-      for (int k = 0; k < kRpt; ++k) {
+      for (int k = 0; k < RPT; ++k) {
         const int r = r0 + g + LANES * k;
         B[k] = (own && r < rows) ? src[r] : make_double2(0.0, 0.0);
       }
@@ -237,12 +237,12 @@ k_tsqr(const QrTask* __restrict__ tasks) {
 #endif
       TSQR_ACC(t_load, c_ld);
       if (own && r0 + kRows < rows) {  // warm L2 for the next block
-        const int r = r0 + kRows + g * kRpt;
+        const int r = r0 + kRows + g * RPT;
         if (r < rows) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + r));
       }
       if (wfirst == 0) {
         TSQR_T0(c_mk);
-        make_reflector<LANES, D, kWarpsPerCta>(B, j == 0, 0, g, R, t0, vring, tring, seq,
+        make_reflector<LANES, RPT, D, kWarpsPerCta>(B, j == 0, 0, g, R, t0, vring, tring, seq,
                                                vprog, t_slot);
         TSQR_ACC(t_make, c_mk);
       }
@@ -260,7 +260,7 @@ k_tsqr(const QrTask* __restrict__ tasks) {
         if (act) rij = R[pidx(i, j)];
         double ar[4] = {0.0, 0.0, 0.0, 0.0}, ai[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int k = 0; k < kRpt; ++k) {
+        for (int k = 0; k < RPT; ++k) {
           const double2 a = v[g + LANES * k], bb = B[k];
           ar[k & 3] = fma(a.x, bb.x, fma(a.y, bb.y, ar[k & 3]));
           ai[k & 3] = fma(a.x, bb.y, fma(-a.y, bb.x, ai[k & 3]));
@@ -275,7 +275,7 @@ k_tsqr(const QrTask* __restrict__ tasks) {
           const double fr = tau.x * sr + tau.y * si;
           const double fi = tau.x * si - tau.y * sr;
 #pragma unroll
-          for (int k = 0; k < kRpt; ++k) {
+          for (int k = 0; k < RPT; ++k) {
             const double2 a = v[g + LANES * k];
             B[k].x = fma(-a.x, fr, fma(a.y, fi, B[k].x));
             B[k].y = fma(-a.x, fi, fma(-a.y, fr, B[k].y));
@@ -291,7 +291,7 @@ k_tsqr(const QrTask* __restrict__ tasks) {
         }
         if (i + 1 >= wfirst) {  // the warp owns column i + 1 (i + 1 <= wlast)
           TSQR_T0(c_mk);
-          make_reflector<LANES, D, kWarpsPerCta>(B, j == i + 1, i + 1, g, R, t + 1, vring,
+          make_reflector<LANES, RPT, D, kWarpsPerCta>(B, j == i + 1, i + 1, g, R, t + 1, vring,
                                                  tring, seq, vprog, t_slot);
           TSQR_ACC(t_make, c_mk);
         }
@@ -542,24 +542,43 @@ static int lane_wstride(int n, int slots) {
 // variant 2: n <= 32 (the leaf blocks), 128 threads, so more independent
 // reflector chains share an SM
 constexpr int kTinyThreads = 128;
-static int tsqr_slots(int n) { return n <= 64 ? EBEM_TSQR_S_SLOTS : EBEM_TSQR_M_SLOTS; }
+// variant 5: 64 < n <= 96 on 384-thread CTAs (12 warps x 8 columns) with
+// 16 rows per lane (64-row blocks): the kernel's time is (row blocks) x
+// (reflectors) x (the last warp's ~800 cycles per consumed reflector), and
+// 170 registers per thread hold a block twice as tall, so the same chain
+// covers twice the rows (EBEM_TSQR_TALL=0: variant 1 for these, A/B).
+constexpr int kTallCols = 96, kTallThreads = 384, kTallRpt = 16, kTallSlots = 128;
+static bool tall_tsqr_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("EBEM_TSQR_TALL");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+static int tsqr_slots(int n) {
+  if (tsqr_variant(n) == 5) return kTallSlots;
+  return n <= 64 ? EBEM_TSQR_S_SLOTS : EBEM_TSQR_M_SLOTS;
+}
 int tsqr_variant(int n) {
   if (lane_tsqr_enabled() && n <= 64) return n <= 32 ? 3 : 4;
+  if (tall_tsqr_enabled() && n > 64 && n <= kTallCols) return 5;
   return n <= 32 ? 2 : n <= 64 ? 0 : n <= kTsqrMaxCols ? 1 : -1;
 }
 int tsqr_block_rows(int n) {
   if (tsqr_variant(n) == 3) return LaneCfg<1>::kBr;
   if (tsqr_variant(n) == 4) return LaneCfg<2>::kBr;
+  if (tsqr_variant(n) == 5) return EBEM_TSQR_M_LANES * kTallRpt;
   return tsqr_variant(n) == 1 ? EBEM_TSQR_M_LANES * kRpt : EBEM_TSQR_S_LANES * kRpt;
 }
 int tsqr_ctas_per_sm(int n) {
-  if (tsqr_variant(n) >= 3) {  // resident warps (= tasks) per SM
+  if (tsqr_variant(n) == 3 || tsqr_variant(n) == 4) {  // resident warps (= tasks) per SM
     const int slots = tsqr_variant(n) == 3 ? 1 : 2;
     const int wpc = slots == 1 ? LaneCfg<1>::kWpc : LaneCfg<2>::kWpc;
     const int minb = slots == 1 ? LaneCfg<1>::kMinB : LaneCfg<2>::kMinB;
     const int by_smem = int((227 * 1024) / (tsqr_smem_bytes(n) + 1024));
     return wpc * std::max(1, std::min(minb, by_smem));
   }
+  if (tsqr_variant(n) == 5) return 1;
   const bool small = tsqr_variant(n) != 1;
   const int t = tsqr_variant(n) == 2 ? kTinyThreads : small ? EBEM_TSQR_S_THREADS : EBEM_TSQR_M_THREADS;
   const int by_regs = std::max(1, 65536 / (t * (small ? EBEM_TSQR_REGS : EBEM_TSQR_M_REGS)));
@@ -567,7 +586,7 @@ int tsqr_ctas_per_sm(int n) {
   return std::min(std::min(by_regs, by_smem), 2048 / t);
 }
 size_t tsqr_smem_bytes(int n) {
-  if (tsqr_variant(n) >= 3) {
+  if (tsqr_variant(n) == 3 || tsqr_variant(n) == 4) {
     const int slots = tsqr_variant(n) == 3 ? 1 : 2;
     const int wpc = slots == 1 ? LaneCfg<1>::kWpc : LaneCfg<2>::kWpc;
     return sizeof(double2) * size_t(wpc) * lane_wstride(n, slots);
@@ -576,14 +595,15 @@ size_t tsqr_smem_bytes(int n) {
          (size_t(n) * (n + 1) / 2 + size_t(tsqr_slots(n)) * (tsqr_block_rows(n) + 1));
 }
 
-template <int L, int T, int D, int G>
+template <int L, int RPT, int T, int D, int G>
 static void launch_variant(const QrTask* tasks, int n_tasks, size_t smem, cudaStream_t st) {
   static bool once = [] {
-    cudaFuncSetAttribute(k_tsqr<L, T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tsqr<L, RPT, T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         216 * 1024);
     return true;
   }();
   (void)once;
-  k_tsqr<L, T, D, G><<<n_tasks, T, smem, st>>>(tasks);
+  k_tsqr<L, RPT, T, D, G><<<n_tasks, T, smem, st>>>(tasks);
 }
 
 void launch_tsqr(const QrTask* tasks, int n_tasks, int variant, size_t smem,
@@ -608,11 +628,13 @@ void launch_tsqr(const QrTask* tasks, int n_tasks, int variant, size_t smem,
     return;
   }
   if (variant == 2)
-    launch_variant<EBEM_TSQR_S_LANES, kTinyThreads, EBEM_TSQR_S_SLOTS, EBEM_TSQR_REGS>(tasks, n_tasks, smem, st);
+    launch_variant<EBEM_TSQR_S_LANES, kRpt, kTinyThreads, EBEM_TSQR_S_SLOTS, EBEM_TSQR_REGS>(tasks, n_tasks, smem, st);
   else if (variant == 0)
-    launch_variant<EBEM_TSQR_S_LANES, EBEM_TSQR_S_THREADS, EBEM_TSQR_S_SLOTS, EBEM_TSQR_REGS>(tasks, n_tasks, smem, st);
+    launch_variant<EBEM_TSQR_S_LANES, kRpt, EBEM_TSQR_S_THREADS, EBEM_TSQR_S_SLOTS, EBEM_TSQR_REGS>(tasks, n_tasks, smem, st);
+  else if (variant == 5)
+    launch_variant<EBEM_TSQR_M_LANES, kTallRpt, kTallThreads, kTallSlots, 170>(tasks, n_tasks, smem, st);
   else
-    launch_variant<EBEM_TSQR_M_LANES, EBEM_TSQR_M_THREADS, EBEM_TSQR_M_SLOTS, EBEM_TSQR_M_REGS>(tasks, n_tasks, smem, st);
+    launch_variant<EBEM_TSQR_M_LANES, kRpt, EBEM_TSQR_M_THREADS, EBEM_TSQR_M_SLOTS, EBEM_TSQR_M_REGS>(tasks, n_tasks, smem, st);
 }
 
 }  // namespace ebem_gpu
