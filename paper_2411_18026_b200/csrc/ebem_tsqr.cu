@@ -548,6 +548,17 @@ constexpr int kTinyThreads = 128;
 // 170 registers per thread hold a block twice as tall, so the same chain
 // covers twice the rows (EBEM_TSQR_TALL=0: variant 1 for these, A/B).
 constexpr int kTallCols = 96, kTallThreads = 384, kTallRpt = 16, kTallSlots = 128;
+// variant 7: 96 < n <= 112 (the two top levels at the bench size) on 512
+// threads with 12 rows per lane (48-row blocks; 128 registers, a few spilled
+// bytes), R (<= 101 KB) beside a 128-slot ring (EBEM_TSQR_TALL7=0: variant 1).
+constexpr int kTall7Cols = 112, kTall7Threads = 512, kTall7Rpt = 12, kTall7Slots = 128;
+static bool tall7_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("EBEM_TSQR_TALL7");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
 static bool tall_tsqr_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("EBEM_TSQR_TALL");
@@ -557,17 +568,20 @@ static bool tall_tsqr_enabled() {
 }
 static int tsqr_slots(int n) {
   if (tsqr_variant(n) == 5) return kTallSlots;
+  if (tsqr_variant(n) == 7) return kTall7Slots;
   return n <= 64 ? EBEM_TSQR_S_SLOTS : EBEM_TSQR_M_SLOTS;
 }
 int tsqr_variant(int n) {
   if (lane_tsqr_enabled() && n <= 64) return n <= 32 ? 3 : 4;
   if (tall_tsqr_enabled() && n > 64 && n <= kTallCols) return 5;
+  if (tall_tsqr_enabled() && tall7_enabled() && n > kTallCols && n <= kTall7Cols) return 7;
   return n <= 32 ? 2 : n <= 64 ? 0 : n <= kTsqrMaxCols ? 1 : -1;
 }
 int tsqr_block_rows(int n) {
   if (tsqr_variant(n) == 3) return LaneCfg<1>::kBr;
   if (tsqr_variant(n) == 4) return LaneCfg<2>::kBr;
   if (tsqr_variant(n) == 5) return EBEM_TSQR_M_LANES * kTallRpt;
+  if (tsqr_variant(n) == 7) return EBEM_TSQR_M_LANES * kTall7Rpt;
   return tsqr_variant(n) == 1 ? EBEM_TSQR_M_LANES * kRpt : EBEM_TSQR_S_LANES * kRpt;
 }
 int tsqr_ctas_per_sm(int n) {
@@ -578,7 +592,7 @@ int tsqr_ctas_per_sm(int n) {
     const int by_smem = int((227 * 1024) / (tsqr_smem_bytes(n) + 1024));
     return wpc * std::max(1, std::min(minb, by_smem));
   }
-  if (tsqr_variant(n) == 5) return 1;
+  if (tsqr_variant(n) >= 5) return 1;
   const bool small = tsqr_variant(n) != 1;
   const int t = tsqr_variant(n) == 2 ? kTinyThreads : small ? EBEM_TSQR_S_THREADS : EBEM_TSQR_M_THREADS;
   const int by_regs = std::max(1, 65536 / (t * (small ? EBEM_TSQR_REGS : EBEM_TSQR_M_REGS)));
@@ -633,6 +647,8 @@ void launch_tsqr(const QrTask* tasks, int n_tasks, int variant, size_t smem,
     launch_variant<EBEM_TSQR_S_LANES, kRpt, EBEM_TSQR_S_THREADS, EBEM_TSQR_S_SLOTS, EBEM_TSQR_REGS>(tasks, n_tasks, smem, st);
   else if (variant == 5)
     launch_variant<EBEM_TSQR_M_LANES, kTallRpt, kTallThreads, kTallSlots, 170>(tasks, n_tasks, smem, st);
+  else if (variant == 7)
+    launch_variant<EBEM_TSQR_M_LANES, kTall7Rpt, kTall7Threads, kTall7Slots, 128>(tasks, n_tasks, smem, st);
   else
     launch_variant<EBEM_TSQR_M_LANES, kRpt, EBEM_TSQR_M_THREADS, EBEM_TSQR_M_SLOTS, EBEM_TSQR_M_REGS>(tasks, n_tasks, smem, st);
 }

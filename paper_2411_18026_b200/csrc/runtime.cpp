@@ -2022,7 +2022,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
   }();
   size_t round = 0;
   for (;;) {
-    std::vector<QrTask> tasks, streamv[6];
+    std::vector<QrTask> tasks, streamv[8];
     std::vector<size_t> out_off(q.size(), 0);
     size_t out_total = 0, ws_total = 0;
     std::vector<int> pieces(q.size(), 0);
@@ -2075,7 +2075,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     qr_rounds_[round].ensure(2 * out_total);
     double* ob = qr_rounds_[round].get();
     ++round;
-    size_t smemv[6] = {0, 0, 0, 0, 0, 0};
+    size_t smemv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (size_t i = 0; i < q.size(); ++i) {
       if (!pieces[i]) continue;
       const TallBlock& x = q[i];
@@ -2106,15 +2106,15 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     gws.ensure(ws_total + 1);
     Pack pk;
     const size_t o = pk.add(tasks);
-    size_t ov[6];
-    for (int v = 0; v < 6; ++v) ov[v] = pk.add(streamv[v]);
+    size_t ov[8];
+    for (int v = 0; v < 8; ++v) ov[v] = pk.add(streamv[v]);
     char* tb = staging.put(pk, st);
     size_t smem = 0;
     for (const QrTask& t : tasks)
       if (t.in_smem) smem = std::max(smem, size_t(t.rows) * t.n * 16);
     double fl = 0.0;
     double by = 0.0;  // the block read once, its reduced rows written once
-    for (const auto* v : {&tasks, &streamv[0], &streamv[1], &streamv[2], &streamv[3], &streamv[4], &streamv[5]})
+    for (const auto* v : {&tasks, &streamv[0], &streamv[1], &streamv[2], &streamv[3], &streamv[4], &streamv[5], &streamv[6], &streamv[7]})
       for (const QrTask& t : *v) {
         const double mm = t.rows, nn = std::min(t.rows, t.n);
         // complex Householder QR with k = min(m, n) reflectors:
@@ -2125,7 +2125,7 @@ void reduce_tall(std::vector<TallBlock>& q, cudaStream_t st, bool force) {
     g_prof.begin(st);
     // (the team-layout k_qr_team measured slower on these shapes: 485 vs 404 ms)
     launch_qr_reduce(Pack::at<QrTask>(tb, o), int(tasks.size()), smem, gws.get(), st);
-    for (int v = 0; v < 6; ++v)
+    for (int v = 0; v < 8; ++v)
       launch_tsqr(Pack::at<QrTask>(tb, ov[v]), int(streamv[v].size()), v, smemv[v], st);
     g_prof.end(KP_QR, st, fl, by);
     CK(cudaGetLastError());
