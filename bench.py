@@ -476,7 +476,9 @@ def extra_configs(eb, fp64_peak, hbm):
     s3 = eb.AssemblerSource(a3)
     t3 = eb.ClusterTree(n3, eb.ClusterTree.depth_for(n3, LEAF))
     F = a3.rhs_batch(med3, [2 * np.pi * j / 180 for j in range(180)], 1.0)
-    f3 = eb.FdsSolver(s3, t3, eb.FdsConfig(EPS, 1))
+    f3 = eb.FdsSolver(s3, t3, eb.FdsConfig(EPS, 1))  # warm-up (as the headline's warm-up steps)
+    del f3
+    f3 = eb.FdsSolver(s3, t3, eb.FdsConfig(EPS, 1))  # a second factorization, warm
     tm1, tm = eb.FdsSolveTiming(), eb.FdsSolveTiming()
     f3.solve(F[:, 0], tm1)  # records the one-column graphs
     f3.solve(F[:, 0], tm1)

@@ -77,6 +77,7 @@ struct DevCtx {
   int proxy_n;    // ProxyConfig::n_gauss
   int m_prime;    // ProxyConfig::m_prime
   double refine;
+  int very_far_tier;  // 1: pairs beyond kVeryFar element lengths take the 3 x 3 rule
   // cos/sin of 2 pi j / m' (host libm), for the proxy polygons.
   double poly_cs[2 * 512];
   // Element geometry (device pointer, kElemFields * n_nodes doubles).

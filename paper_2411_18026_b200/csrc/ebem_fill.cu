@@ -442,11 +442,16 @@ k_sym_count(const DevCtx* __restrict__ ctx, const SymJob* __restrict__ jobs,
       const double cy = (A.py + 0.5 * A.dy) - (B.py + 0.5 * B.dy);
       const double thr = 8.0 * hmax * (1.0 + 1e-9) + 0.5 * (A.h + B.h) * (1.0 + 1e-9);
       int tier = 0;
-      if (fma(cx, cx, cy * cy) < thr * thr) {
+      const double c2 = fma(cx, cx, cy * cy);
+      if (c2 < thr * thr) {
         const double rq = element_distance8(A, B) / hmax;
         tier = rq >= 8.0 ? 0 : rq >= 4.0 ? 1 : rq >= 2.0 ? 2 : 3;
+      } else if (ctx->very_far_tier) {
+        // the same lower bound on the segment distance, against kVeryFar h_max
+        const double vf = kVeryFar * hmax + 0.5 * (A.h + B.h);
+        if (c2 >= vf * vf) tier = 4;
       }
-      key = tier + (J.onesided ? 4 : 0);
+      key = tier + (J.onesided ? kSymTiers : 0);
     }
     keys[p] = key;
     pair_job[p] = jb;  // read back by the scatter pass (no second search)

@@ -52,9 +52,22 @@ struct SymJob {
 };
 
 // Near-pair classes of the bucketing sort: tier (0..3 = far, far+2, far+5,
-// far+9 points) + 4 for one-sided jobs; the last class is "skip" (touching
+// far+9 points; 4 = very far, 3 points) + kSymTiers for one-sided jobs; the
+// last class is "skip" (touching
 // pairs, handled by k_near_singular, and the lower triangle of tri jobs).
-constexpr int kSymClasses = 9;
+constexpr int kSymTiers = 5;  // the reference's four tiers + the very-far 3 x 3 tier
+constexpr int kSymClasses = 2 * kSymTiers + 1;
+// Very-far pairs (segment distance >= kVeryFar x the longer element, default
+// assembly settings only): a 3 x 3 rule instead of the reference's 4 x 4.  For
+// these pairs both rules integrate the same smooth integrand to below
+// rounding: the 3-point Gauss remainder h^7 f(6) / 2016000 of a 1/r^3-type
+// kernel is 0.01 (h/r)^6 of the integral, 4e-17 at h/r = 1/250, a fraction
+// of an ulp (EBEM_FAR3=0: the reference's tiers only).  (A 2 x 2 rule beyond
+// 4000 element lengths, remainder (h/r)^4 / 12 = 3e-16, was measured too:
+// faster still, but the far-pair cancellation of DESIGN.md section 5 turns
+// those ulps into 1.3e-8 of the solution at N = 262144.)
+constexpr double kVeryFar = 250.0;
+constexpr int kVeryFarNodes = 3;
 
 // Sorted near-pair record, 16 doubles (128 B): geometry of the enclosed
 // element a and the cell element b (px, py, dx, dy, nx, ny each), the two

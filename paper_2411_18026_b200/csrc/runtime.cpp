@@ -618,6 +618,15 @@ Problem::Problem(const double* xy, int n, double lam, double mu, double rho,
   }
   hctx_.far_nodes = a.far_nodes;
   hctx_.refine = a.refine;
+  {
+    // the very-far 3 x 3 tier only with the default far rule (4 points, no
+    // refinement), whose value it reproduces to rounding
+    static const bool far2 = [] {
+      const char* e = std::getenv("EBEM_FAR3");
+      return e == nullptr || std::atoi(e) != 0;
+    }();
+    hctx_.very_far_tier = (far2 && a.far_nodes == 4 && a.refine == 1.0) ? 1 : 0;
+  }
   hctx_.corner_n = scaled(a.corner_nodes);
   hctx_.proxy_n = p.n_gauss;
   hctx_.m_prime = p.m_prime;
@@ -1469,10 +1478,11 @@ void Problem::execute(FillPlan& plan) {
     // range from the device-side bounds (no host round trip)
     const int add[4] = {0, 2, 5, 9};
     for (int c = 0; c < kSymClasses - 1; ++c) {  // the last class is "skip"
-      const int tier = c & 3;
-      const bool both = c < 4;  // classes 4..7: one-sided true blocks
+      const int tier = c % kSymTiers;
+      const bool both = c < kSymTiers;  // the upper classes: one-sided true blocks
       if (both ? !plan.has_two_sided_ : !plan.has_one_sided_) continue;
-      const int nq = int((acfg_.far_nodes + add[tier]) * acfg_.refine + 0.5);
+      if (tier == 4 && !hctx_.very_far_tier) continue;
+      const int nq = tier == 4 ? kVeryFarNodes : int((acfg_.far_nodes + add[tier]) * acfg_.refine + 0.5);
       g_prof.begin(st_);
       launch_near_sym(dctx(), fc_, sym_recs_.get(), sym_bounds_.get(), c, nsym, nq, both,
                       bundles.get(), plan.bundles_, st_);
